@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark of the STMG solve path (BASELINE.json metric: space-time DoF/s of
+the operator vmult and the STMG V-cycle, fp64, with the HBM roofline
+fraction).
+
+One step = one preconditioned GMRES iteration's operator work on the slab
+system: one V-cycle (SpaceTimeMultigrid::apply) followed by one vmult
+(SpaceTimeOperator::apply) -- exactly the precond(v) / op(z) pair of
+gmres.cpp:45-47. value = N_fine / t_step over K timed steps (inputs resident
+in HBM, vectors larger than L2). The e2e figure runs the same step through the
+host-buffer C-ABI entry points (H2D of the step's input and D2H of its result
+inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
+  python bench.py --impl reference ...   (the reference's CPU implementation)
+
+Multi-GPU (torchrun, N>1): every rank runs an independent replica of the slab
+system ("replicas only" in round 1); value sums the units
+all ranks processed over the max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time DoF/s: operator vmult & STMG V-cycle, fp64, % of HBM roofline"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(workload: str, budget_s: float = 15.0, refinements: int = 3):
+    """The reference's own C++ (oracle/_ref, single-threaded by construction)
+    on a bounded, oracle-reachable sample of the workload: the same step
+    (V-cycle + vmult) on the same configuration at `refinements`."""
+    import numpy as np
+    from oracle import refbind
+    from paper_2408_04372_b200 import problems
+    cfg = problems.config(workload, refinements)
+    t0 = time.perf_counter()
+    R = refbind.Reference(cfg, with_mg=True)
+    setup = time.perf_counter() - t0
+    r = problems.uniform_vector(R.n_dofs, seed=1)
+    R.apply(R.vcycle(r))  # warm-up
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        R.apply(R.vcycle(r))
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    val = steps * R.n_dofs / el
+    return {"value": val, "unit": "DoF/s", "cores": 1, "kind": "reference",
+            "sample": f"{workload} at {cfg.cells}^{cfg.dim} cells (N={R.n_dofs}), {steps} steps of V-cycle+vmult "
+                      f"in {el:.1f}s, setup {setup:.1f}s excluded; reference proj/src via oracle/_ref, 1 thread"}, cfg
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import refbind
+    from paper_2408_04372_b200 import problems
+    cfg = problems.config(args.workload, args.ref_refinements)
+    R = refbind.Reference(cfg, with_mg=True)
+    r = problems.uniform_vector(R.n_dofs, seed=1)
+    for _ in range(args.warmup):
+        R.apply(R.vcycle(r))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        R.apply(R.vcycle(r))
+    el = time.perf_counter() - t0
+    val = args.steps * R.n_dofs / el
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "DoF/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "sample_cells": cfg.cells, "n_dofs": R.n_dofs,
+                       "note": "reference CPU implementation (single-threaded) on an oracle-reachable size"},
+            "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": 1, "kind": "reference",
+                             "sample": f"{args.workload} at {cfg.cells}^{cfg.dim} cells, {args.steps} steps"},
+            "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2408_04372_b200 import api, native, problems
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = native.load()
+
+    cfg = problems.config(args.workload)
+    t0 = time.perf_counter()
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
+    M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps,
+                               cfg.tau)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    op = M.operator_at(0)
+    N = op.n_dofs
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    r = torch.rand(N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    z = torch.empty_like(r)
+    y = torch.empty_like(r)
+
+    def step():
+        M.apply(r, z)
+        op.apply(z, y)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    def timed(fn, reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps  # ms
+
+    # per-kernel times (same stream as the launches), for the roofline
+    t_vmult = timed(lambda: op.apply(r, y), 10)
+    zz = torch.zeros_like(r)
+    t_asm = timed(lambda: M.asm_add_correction(0, r, zz), 5)
+    t_vcycle = timed(lambda: M.apply(r, z), 5)
+
+    # timed region
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.stmg_kernel_launches()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        e1.synchronize()
+    torch.cuda.synchronize()
+    launches = lib.stmg_kernel_launches() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = world * N / (ms * 1e-3)
+
+    # end to end through the host-buffer C ABI (pinned host memory)
+    rh = torch.empty(N, dtype=torch.float64).pin_memory()
+    rh.copy_(r.cpu())
+    zh = torch.empty(N, dtype=torch.float64).pin_memory()
+    yh = torch.empty(N, dtype=torch.float64).pin_memory()
+    rn, zn, yn = rh.numpy(), zh.numpy(), yh.numpy()
+    M.apply_host(rn, zn)
+    op.apply_host(zn, yn)
+    e2e_steps = max(2, min(args.steps, 5))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tw = time.perf_counter()
+    for _ in range(e2e_steps):
+        M.apply_host(rn, zn)
+        op.apply_host(zn, yn)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - tw) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": world * N / e2e_s, "unit": "DoF/s", "h2d_bytes_per_step": 2 * 8 * N,
+           "d2h_bytes_per_step": 2 * 8 * N}
+
+    # roofline of the dominant kernel
+    peak, peak_kind = measured_peaks()
+    cells = cfg.cells ** cfg.dim
+    m = (cfg.p + 1) ** cfg.dim
+    n_verts = (cfg.cells + 1) ** cfg.dim
+    vmult_bytes = 16 * N + (24 * n_verts if cfg.perturb > 0 else 0)
+    asm_bytes = cells * m * m * 8 + cells * m * 8 + 8 * N + 16 * N
+    # fine-level launches per step: vmult 3 (2 residuals in the V-cycle + the
+    # outer op), ASM 2 (pre- and post-smoothing)
+    share_vmult = 3 * t_vmult / ms
+    share_asm = 2 * t_asm / ms
+    if share_asm >= share_vmult:
+        dom = {"kernel": "asm_apply_kernel (fine-level exact cell-block smoother)", "ms": t_asm,
+               "bytes": asm_bytes, "share_of_step": share_asm}
+    else:
+        dom = {"kernel": "st_apply_kernel (fused space-time vmult)", "ms": t_vmult, "bytes": vmult_bytes,
+               "share_of_step": share_vmult}
+    achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": peak_kind, "kernel": dom["kernel"],
+                "algorithmic_bytes_per_launch": dom["bytes"], "launch_ms": dom["ms"],
+                "share_of_step": dom["share_of_step"]}
+    vm_ach = vmult_bytes / (t_vmult * 1e-3) / 1e9
+
+    line = {"metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, **cfg.describe(), "parallelism": f"replicas x{world}",
+                       "step": "1 V-cycle + 1 vmult (one preconditioned GMRES iteration's operator work)",
+                       "l2": "vectors (8N = %.0f MB) larger than L2; no flush" % (8 * N / 1e6)},
+            "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
+            "kernels": {"vmult_ms": t_vmult, "vmult_dofs_per_s": N / (t_vmult * 1e-3),
+                        "vmult_hbm_frac": vm_ach / peak, "vcycle_ms": t_vcycle,
+                        "vcycle_dofs_per_s": N / (t_vcycle * 1e-3), "asm_fine_ms": t_asm},
+            "setup_s": setup_s, "mg_levels": M.n_levels, "device_bytes": M.device_bytes()}
+    line["clocks"] = clk.summary()
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb, _ = cpu_baseline(args.workload, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = cb
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--ref-refinements", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

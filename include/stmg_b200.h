@@ -1,0 +1,159 @@
+/*
+ * stmg_b200.h -- C ABI of the B200-native space-time multigrid (STMG) solve
+ * path (arXiv 2408.04372). Plain pointers and sizes only; every compute entry
+ * point takes DEVICE pointers plus a cudaStream_t passed as void* (NULL = the
+ * legacy default stream), except the *_host variants, which take host buffers
+ * and do the host<->device copies themselves. All vectors use the reference's
+ * layout: index (s*n_t + i)*n_space + g, spatial lattice x fastest
+ * (include/stmg/space_time_operator.hpp:23-29,43-45 of the reference).
+ *
+ * Every function returns 0 on success and a negative code on failure; the
+ * message is available from stmg_last_error() (the reference throws
+ * std::invalid_argument / std::runtime_error instead).
+ * Codes: -1 invalid argument, -2 runtime/numerical failure, -3 CUDA error.
+ *
+ * Each entry point names the reference interface it replaces; paths are
+ * relative to /root/reference/proj.
+ */
+#ifndef STMG_B200_H
+#define STMG_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct stmg_mesh stmg_mesh;
+typedef struct stmg_st_operator stmg_st_operator;
+typedef struct stmg_asm stmg_asm;
+typedef struct stmg_transfer stmg_transfer;
+typedef struct stmg_multigrid stmg_multigrid;
+
+enum { STMG_HEAT = 0, STMG_WAVE = 1 };                 /* Equation, space_time_operator.hpp:12 */
+enum { STMG_DG = 0, STMG_CGP = 1 };                    /* TimeScheme, temporal_weights.hpp:9 */
+enum { STMG_SPACE_H = 0, STMG_SPACE_P = 1, STMG_TIME_TAU = 2, STMG_TIME_K = 3 }; /* Coarsening, multigrid.hpp:14 */
+
+const char* stmg_last_error(void);
+const char* stmg_version(void);
+/* number of sm_100a kernels this library has launched since it was loaded */
+long long stmg_kernel_launches(void);
+
+/* Host-side discretisation tables (no GPU needed), for parity checks:
+ * quadrature rules on [0,1] (src/quadrature.cpp:98-166; kind 0 Gauss,
+ * 1 Gauss-Lobatto, 2 right Gauss-Radau), temporal weights
+ * (src/temporal_weights.cpp:29-106; n_t x n_t row-major) and the slab block
+ * coefficients CM, CA ((S n_t)^2 row-major, src/space_time_operator.cpp:269-317). */
+int stmg_quadrature(int kind, int n, double* points, double* weights);
+int stmg_temporal_weights(int scheme, int k, double* m_tau, double* a_tau, double* alpha, double* beta,
+                          double* unknown_nodes);
+int stmg_block_coefficients(int equation, int scheme, int k, double tau, int n_steps, double* CM, double* CA);
+
+/* MeshHierarchy: make_cartesian (src/mesh.cpp:148-187). finest_vertices
+ * (n_verts*3 doubles, x fastest) may be NULL for the exact Cartesian lattice;
+ * otherwise they replace the finest level's vertices and coarser levels take
+ * the shared positions (src/mesh.cpp:221-236). */
+int stmg_mesh_create(int dim, const double lo[3], const double hi[3], long long base_cells, int refinements,
+                     const double* finest_vertices, stmg_mesh** out);
+void stmg_mesh_destroy(stmg_mesh* mesh);
+
+/* SpaceTimeOperator ctor (include/stmg/space_time_operator.hpp:34-36) with its
+ * SpatialOperator pair built on mesh level `mesh_level` with degree p; the
+ * coefficient is coarse_cell_scale[level-0 ancestor] (CoefficientField,
+ * include/stmg/mesh.hpp:76-83), NULL = 1. */
+int stmg_st_operator_create(const stmg_mesh* mesh, int mesh_level, int p, int equation, int scheme, int k, double tau,
+                            int n_steps, const double* coarse_cell_scale, stmg_st_operator** out);
+void stmg_st_operator_destroy(stmg_st_operator* op);
+long long stmg_st_operator_n_dofs(const stmg_st_operator* op);  /* n_dofs(), space_time_operator.hpp:42 */
+long long stmg_st_operator_n_space(const stmg_st_operator* op); /* n_space(), :41 */
+int stmg_st_operator_n_t(const stmg_st_operator* op);           /* n_t(), :40 */
+/* SpaceTimeOperator::apply (space_time_operator.cpp:45-130): y = S u, overwrite */
+int stmg_st_operator_apply(const stmg_st_operator* op, const double* d_u, double* d_y, void* stream);
+int stmg_st_operator_apply_host(const stmg_st_operator* op, const double* h_u, double* h_y);
+/* SpatialOperator::apply (spatial_operator.cpp:292-315), kind 0 mass / 1 stiffness */
+int stmg_spatial_apply(const stmg_st_operator* op, int kind, const double* d_u, double* d_y, void* stream);
+
+/* ASMSmoother (include/stmg/asm_smoother.hpp:16-30) */
+int stmg_asm_create(const stmg_st_operator* op, stmg_asm** out);
+void stmg_asm_destroy(stmg_asm* a);
+/* add_correction (asm_smoother.cpp:60-78): d_z += W sum_T R_T^T B_T^-1 R_T d_r (accumulate) */
+int stmg_asm_add_correction(const stmg_asm* a, const double* d_r, double* d_z, void* stream);
+
+/* Transfer (include/stmg/transfer.hpp:22-24) between two operators that
+ * differ in exactly one attribute */
+int stmg_transfer_create(const stmg_st_operator* fine, const stmg_st_operator* coarse, stmg_transfer** out);
+void stmg_transfer_destroy(stmg_transfer* t);
+int stmg_transfer_prolong(const stmg_transfer* t, const double* d_coarse, double* d_fine, void* stream);
+int stmg_transfer_restrict(const stmg_transfer* t, const double* d_fine, double* d_coarse, void* stream);
+
+/* MultigridOptions (include/stmg/multigrid.hpp:39-46) */
+typedef struct {
+  int n_smooth;
+  long long direct_coarse_max;
+  double coarse_rel_tol;
+  int coarse_max_iters;
+  int eig_iters;
+  unsigned long long seed;
+} stmg_mg_options;
+void stmg_mg_options_default(stmg_mg_options* o);
+
+/* SpaceTimeMultigrid ctor (multigrid.cpp:83-125) for the plan
+ * build_level_plan(finest, scheme, strategy) (multigrid.cpp:34-81);
+ * n_strategy < 0 selects default_strategy. */
+int stmg_multigrid_create(int equation, int scheme, const stmg_mesh* mesh, const double* coarse_cell_scale,
+                          int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
+                          const int* strategy, const stmg_mg_options* options, stmg_multigrid** out);
+void stmg_multigrid_destroy(stmg_multigrid* mg);
+int stmg_multigrid_n_levels(const stmg_multigrid* mg);
+/* level_info (multigrid.cpp:236-247): ints = {mesh_level, p, k, n_steps, coarsening(-1 finest)} */
+int stmg_multigrid_level_info(const stmg_multigrid* mg, int level, int ints[5], long long* n_dofs, double* omega);
+int stmg_multigrid_set_omega(stmg_multigrid* mg, int level, double omega);
+const stmg_st_operator* stmg_multigrid_operator_at(const stmg_multigrid* mg, int level);
+/* apply (multigrid.cpp:228-234): one V-cycle, zero initial guess, overwrite d_z */
+int stmg_multigrid_apply(const stmg_multigrid* mg, const double* d_r, double* d_z, void* stream);
+int stmg_multigrid_apply_host(const stmg_multigrid* mg, const double* h_r, double* h_z);
+/* smooth (multigrid.cpp:174-185): d_u += omega_l ASM_l(d_f - S_l d_u) */
+int stmg_multigrid_smooth(const stmg_multigrid* mg, int level, const double* d_f, double* d_u, void* stream);
+/* the level-l smoother and the level-l -> l+1 transfer of the hierarchy */
+int stmg_multigrid_asm_add_correction(const stmg_multigrid* mg, int level, const double* d_r, double* d_z, void* stream);
+int stmg_multigrid_prolong(const stmg_multigrid* mg, int level, const double* d_coarse, double* d_fine, void* stream);
+int stmg_multigrid_restrict(const stmg_multigrid* mg, int level, const double* d_fine, double* d_coarse, void* stream);
+long long stmg_multigrid_device_bytes(const stmg_multigrid* mg);
+
+/* GmresOptions / GmresResult (include/stmg/gmres.hpp:12-25) */
+typedef struct {
+  int max_iters;
+  int restart;
+  double rel_tol;
+  double abs_tol;
+} stmg_gmres_options;
+typedef struct {
+  int converged;
+  int iterations;
+  double initial_residual;
+  double final_residual;
+  int history_len;
+} stmg_gmres_result;
+void stmg_gmres_options_default(stmg_gmres_options* o);
+
+/* LinearMap (include/stmg/gmres.hpp:9-10) on device vectors: out = A in */
+typedef int (*stmg_linear_map)(void* ctx, const double* d_in, double* d_out, void* stream);
+
+/* gmres (gmres.cpp:8-115): restarted right-preconditioned GMRES on device
+ * vectors; precond may be NULL (identity). history (may be NULL) receives up
+ * to history_cap residual norms including the initial one. */
+int stmg_gmres(long long n, stmg_linear_map op, void* op_ctx, stmg_linear_map precond, void* precond_ctx,
+               const double* d_b, double* d_x, const stmg_gmres_options* options, stmg_gmres_result* result,
+               double* history, int history_cap, void* stream);
+/* The slab solve as march() plugs it (driver.cpp:193-203): op = the finest
+ * SpaceTimeOperator of mg, precond = one V-cycle (precondition != 0). */
+int stmg_solve(const stmg_multigrid* mg, int precondition, const double* d_b, double* d_x,
+               const stmg_gmres_options* options, stmg_gmres_result* result, double* history, int history_cap,
+               void* stream);
+/* same with host buffers (b in, x in/out): copies inside */
+int stmg_solve_host(const stmg_multigrid* mg, int precondition, const double* h_b, double* h_x,
+                    const stmg_gmres_options* options, stmg_gmres_result* result, double* history, int history_cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STMG_B200_H */

@@ -1,0 +1,327 @@
+"""Python mirror of the reference's operator-level interfaces over the C ABI
+(include/stmg_b200.h). Vectors are CUDA torch tensors (float64) in the
+reference layout; torch is used only for device memory and streams.
+
+  Mesh                ~ stmg::MeshHierarchy   (include/stmg/mesh.hpp:38-60)
+  SpaceTimeOperator   ~ stmg::SpaceTimeOperator (space_time_operator.hpp:34-105)
+  ASMSmoother         ~ stmg::ASMSmoother      (asm_smoother.hpp:16-45)
+  Transfer            ~ stmg::Transfer         (transfer.hpp:22-40)
+  SpaceTimeMultigrid  ~ stmg::SpaceTimeMultigrid (multigrid.hpp:61-113)
+  gmres / solve       ~ stmg::gmres            (gmres.hpp:9-33)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import native as N
+
+HEAT, WAVE = 0, 1
+DG, CGP = 0, 1
+SPACE_H, SPACE_P, TIME_TAU, TIME_K = 0, 1, 2, 3
+COARSENING_NAMES = {0: "space-h", 1: "space-p", 2: "time-tau", 3: "time-k", -1: "finest"}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream():
+    return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> C.c_void_p:
+    if not t.is_cuda or t.dtype != _torch().float64 or not t.is_contiguous():
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _dbl(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(N.c_double_p)
+
+
+class Mesh:
+    def __init__(self, dim: int, lo, hi, base_cells: int, refinements: int, vertices: Optional[np.ndarray] = None):
+        lib = N.load()
+        self.dim, self.base_cells, self.refinements = dim, base_cells, refinements
+        lo_a, lo_p = _dbl(np.asarray(lo, dtype=np.float64))
+        hi_a, hi_p = _dbl(np.asarray(hi, dtype=np.float64))
+        v = _dbl(vertices)
+        h = C.c_void_p()
+        N.check(lib.stmg_mesh_create(dim, lo_p, hi_p, base_cells, refinements, v[1] if v else None, C.byref(h)))
+        self._h = h
+
+    def cells(self, level: int) -> int:
+        return (self.base_cells << level) ** self.dim
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.load().stmg_mesh_destroy(self._h)
+            self._h = None
+
+
+class SpaceTimeOperator:
+    def __init__(self, mesh: Mesh, mesh_level: int, p: int, equation: int, scheme: int, k: int, tau: float,
+                 n_steps: int, rho: Optional[np.ndarray] = None, _handle=None, _owner=None):
+        lib = N.load()
+        self.mesh = mesh
+        if _handle is not None:
+            self._h, self._owned, self._owner = C.c_void_p(_handle), False, _owner
+        else:
+            r = _dbl(rho)
+            h = C.c_void_p()
+            N.check(lib.stmg_st_operator_create(mesh._h, mesh_level, p, equation, scheme, k, tau, n_steps,
+                                                r[1] if r else None, C.byref(h)))
+            self._h, self._owned = h, True
+        self.n_dofs = lib.stmg_st_operator_n_dofs(self._h)
+        self.n_space = lib.stmg_st_operator_n_space(self._h)
+        self.n_t = lib.stmg_st_operator_n_t(self._h)
+
+    def apply(self, u, y=None):
+        """y = S u (overwrite)."""
+        torch = _torch()
+        if u.numel() != self.n_dofs:
+            raise N.StmgInvalidArgument("SpaceTimeOperator::apply: size mismatch")
+        if y is None:
+            y = torch.empty_like(u)
+        N.check(N.load().stmg_st_operator_apply(self._h, _ptr(u), _ptr(y), _stream()))
+        return y
+
+    def apply_host(self, u: np.ndarray, y: Optional[np.ndarray] = None) -> np.ndarray:
+        """y = S u on host buffers (H2D/D2H inside the C ABI call)."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if u.size != self.n_dofs:
+            raise N.StmgInvalidArgument("SpaceTimeOperator::apply: size mismatch")
+        if y is None:
+            y = np.empty_like(u)
+        N.check(N.load().stmg_st_operator_apply_host(self._h, u.ctypes.data_as(N.c_double_p),
+                                                     y.ctypes.data_as(N.c_double_p)))
+        return y
+
+    def spatial_apply(self, kind: int, u, y=None):
+        torch = _torch()
+        if y is None:
+            y = torch.empty_like(u)
+        N.check(N.load().stmg_spatial_apply(self._h, kind, _ptr(u), _ptr(y), _stream()))
+        return y
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and self._h:
+            N.load().stmg_st_operator_destroy(self._h)
+            self._h = None
+
+
+class ASMSmoother:
+    def __init__(self, op: SpaceTimeOperator):
+        h = C.c_void_p()
+        N.check(N.load().stmg_asm_create(op._h, C.byref(h)))
+        self._h, self.op = h, op
+
+    def add_correction(self, r, z):
+        """z += W sum_T R_T^T B_T^-1 R_T r (accumulate)."""
+        N.check(N.load().stmg_asm_add_correction(self._h, _ptr(r), _ptr(z), _stream()))
+        return z
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.load().stmg_asm_destroy(self._h)
+            self._h = None
+
+
+class Transfer:
+    def __init__(self, fine: SpaceTimeOperator, coarse: SpaceTimeOperator):
+        h = C.c_void_p()
+        N.check(N.load().stmg_transfer_create(fine._h, coarse._h, C.byref(h)))
+        self._h, self.fine, self.coarse = h, fine, coarse
+
+    def prolong(self, c, f=None):
+        if f is None:
+            f = _torch().empty(self.fine.n_dofs, dtype=c.dtype, device=c.device)
+        N.check(N.load().stmg_transfer_prolong(self._h, _ptr(c), _ptr(f), _stream()))
+        return f
+
+    def restrict_(self, f, c=None):
+        if c is None:
+            c = _torch().empty(self.coarse.n_dofs, dtype=f.dtype, device=f.device)
+        N.check(N.load().stmg_transfer_restrict(self._h, _ptr(f), _ptr(c), _stream()))
+        return c
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.load().stmg_transfer_destroy(self._h)
+            self._h = None
+
+
+def mg_options(**kw) -> N.MgOptions:
+    o = N.MgOptions()
+    N.load().stmg_mg_options_default(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def gmres_options(**kw) -> N.GmresOptions:
+    o = N.GmresOptions()
+    N.load().stmg_gmres_options_default(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+class SpaceTimeMultigrid:
+    def __init__(self, equation: int, scheme: int, mesh: Mesh, rho: Optional[np.ndarray], fine_level: int, p: int,
+                 k: int, n_steps: int, tau: float, strategy: Optional[Sequence[int]] = None, **options):
+        lib = N.load()
+        r = _dbl(rho)
+        strat = None
+        ns = -1
+        if strategy is not None:
+            ns = len(strategy)
+            strat = (C.c_int * max(ns, 1))(*strategy)
+        o = mg_options(**options)
+        h = C.c_void_p()
+        N.check(lib.stmg_multigrid_create(equation, scheme, mesh._h, r[1] if r else None, fine_level, p, k, n_steps,
+                                          tau, ns, strat, C.byref(o), C.byref(h)))
+        self._h, self.mesh = h, mesh
+        self.n_levels = lib.stmg_multigrid_n_levels(h)
+        self._ops = [SpaceTimeOperator(mesh, 0, 1, 0, 0, 0, 1.0, 1, _handle=lib.stmg_multigrid_operator_at(h, l),
+                                       _owner=self) for l in range(self.n_levels)]
+
+    def operator_at(self, l: int) -> SpaceTimeOperator:
+        return self._ops[l]
+
+    def level_info(self):
+        out = []
+        for l in range(self.n_levels):
+            ints = (C.c_int * 5)()
+            n = C.c_longlong()
+            w = C.c_double()
+            N.check(N.load().stmg_multigrid_level_info(self._h, l, ints, C.byref(n), C.byref(w)))
+            out.append({"coarsening": COARSENING_NAMES[ints[4]], "mesh_level": ints[0], "p": ints[1], "k": ints[2],
+                        "n_steps": ints[3], "n_dofs": n.value, "omega": w.value})
+        return out
+
+    def omega_at(self, l: int) -> float:
+        return self.level_info()[l]["omega"]
+
+    def set_omega(self, l: int, w: float):
+        N.check(N.load().stmg_multigrid_set_omega(self._h, l, w))
+
+    def apply(self, r, z=None):
+        if z is None:
+            z = _torch().empty_like(r)
+        N.check(N.load().stmg_multigrid_apply(self._h, _ptr(r), _ptr(z), _stream()))
+        return z
+
+    def apply_host(self, r: np.ndarray, z: np.ndarray) -> np.ndarray:
+        """One V-cycle on host buffers (H2D/D2H inside the C ABI call)."""
+        N.check(N.load().stmg_multigrid_apply_host(self._h, r.ctypes.data_as(N.c_double_p),
+                                                   z.ctypes.data_as(N.c_double_p)))
+        return z
+
+    def smooth(self, l: int, f, u):
+        N.check(N.load().stmg_multigrid_smooth(self._h, l, _ptr(f), _ptr(u), _stream()))
+        return u
+
+    def asm_add_correction(self, l: int, r, z):
+        N.check(N.load().stmg_multigrid_asm_add_correction(self._h, l, _ptr(r), _ptr(z), _stream()))
+        return z
+
+    def prolong(self, l: int, c, f=None):
+        if f is None:
+            f = _torch().empty(self._ops[l].n_dofs, dtype=c.dtype, device=c.device)
+        N.check(N.load().stmg_multigrid_prolong(self._h, l, _ptr(c), _ptr(f), _stream()))
+        return f
+
+    def restrict_(self, l: int, f, c=None):
+        if c is None:
+            c = _torch().empty(self._ops[l + 1].n_dofs, dtype=f.dtype, device=f.device)
+        N.check(N.load().stmg_multigrid_restrict(self._h, l, _ptr(f), _ptr(c), _stream()))
+        return c
+
+    def device_bytes(self) -> int:
+        return N.load().stmg_multigrid_device_bytes(self._h)
+
+    def solve(self, b, x, precondition: bool = True, history_cap: int = 1100, **opts):
+        """GMRES(op = finest operator, precond = one V-cycle) as march() plugs
+        them (driver.cpp:193-203); x is the initial guess and the result."""
+        o = gmres_options(**opts)
+        res = N.GmresResult()
+        hist = np.zeros(history_cap)
+        N.check(N.load().stmg_solve(self._h, 1 if precondition else 0, _ptr(b), _ptr(x), C.byref(o), C.byref(res),
+                                    hist.ctypes.data_as(N.c_double_p), history_cap, _stream()))
+        return _result(res, hist)
+
+    def solve_host(self, b: np.ndarray, x: np.ndarray, precondition: bool = True, history_cap: int = 1100, **opts):
+        o = gmres_options(**opts)
+        res = N.GmresResult()
+        hist = np.zeros(history_cap)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        N.check(N.load().stmg_solve_host(self._h, 1 if precondition else 0, b.ctypes.data_as(N.c_double_p),
+                                         x.ctypes.data_as(N.c_double_p), C.byref(o), C.byref(res),
+                                         hist.ctypes.data_as(N.c_double_p), history_cap))
+        return _result(res, hist)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._ops = []
+            N.load().stmg_multigrid_destroy(self._h)
+            self._h = None
+
+
+def _result(res: N.GmresResult, hist: np.ndarray) -> dict:
+    n = min(res.history_len, hist.size)
+    return {"converged": bool(res.converged), "iterations": res.iterations,
+            "initial_residual": res.initial_residual, "final_residual": res.final_residual,
+            "residual_history": hist[:n].tolist()}
+
+
+def gmres(op: Callable, b, x, precond: Optional[Callable] = None, history_cap: int = 1100, **opts) -> dict:
+    """stmg::gmres with Python callables op(in, out) / precond(in, out) on CUDA
+    tensors of length n (include/stmg/gmres.hpp:31-33)."""
+    torch = _torch()
+    n = b.numel()
+
+    def wrap(fn):
+        def cb(ctx, din, dout, stream):
+            try:
+                # zero-copy views of the device buffers
+                tin = _view(din, n)
+                tout = _view(dout, n)
+                fn(tin, tout)
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a failed callback
+                return -1
+        return N.LINEAR_MAP(cb)
+
+    cop = wrap(op)
+    cpc = wrap(precond) if precond is not None else N.LINEAR_MAP()
+    o = gmres_options(**opts)
+    res = N.GmresResult()
+    hist = np.zeros(history_cap)
+    torch.cuda.synchronize()
+    N.check(N.load().stmg_gmres(n, cop, None, cpc, None, _ptr(b), _ptr(x), C.byref(o), C.byref(res),
+                                hist.ctypes.data_as(N.c_double_p), history_cap, _stream()))
+    return _result(res, hist)
+
+
+_VIEW_CACHE: dict = {}
+
+
+def _view(ptr, n):
+    """float64 CUDA tensor aliasing device memory at ptr (no copy)."""
+    torch = _torch()
+    key = (ptr, n)
+    t = _VIEW_CACHE.get(key)
+    if t is None:
+        class _Cai:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+        t = torch.as_tensor(_Cai(), device="cuda")
+        _VIEW_CACHE[key] = t
+    return t

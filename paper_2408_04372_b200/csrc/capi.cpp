@@ -1,0 +1,420 @@
+// C ABI over the host C++ layer (declarations: include/stmg_b200.h). No
+// exception crosses this boundary; failures become negative return codes and
+// stmg_last_error().
+#include "../../include/stmg_b200.h"
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "stmg.hpp"
+
+using namespace stmgb;
+
+struct stmg_mesh {
+  MeshHierarchy h;
+};
+struct stmg_st_operator {
+  std::unique_ptr<SpaceTimeOperator> owned;
+  const SpaceTimeOperator* op = nullptr;  // owned.get() or a multigrid level
+  TemporalWeights w;
+  mutable DeviceBuffer hu, hy;  // staging for the host-buffer entry point
+};
+struct stmg_asm {
+  std::unique_ptr<ASMSmoother> s;
+};
+struct stmg_transfer {
+  std::unique_ptr<Transfer> t;
+};
+struct stmg_multigrid {
+  std::unique_ptr<SpaceTimeMultigrid> mg;
+  std::vector<std::unique_ptr<stmg_st_operator>> views;  // non-owning wrappers for operator_at
+  mutable GmresWorkspace ws;
+  mutable DeviceBuffer hr, hz;  // staging for the host-buffer entry points
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      g_err = std::string("CUDA: ") + cudaGetErrorString(e);
+      return -3;
+    }
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+// host-only entry points: no CUDA state is touched
+template <typename F>
+int guard_host(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+cudaStream_t st(void* s) { return static_cast<cudaStream_t>(s); }
+Coefficient coeff(const MeshHierarchy& h, const double* scale) {
+  Coefficient c;
+  if (scale) c.coarse_cell_scale.assign(scale, scale + h.levels.front().n_cells());
+  return c;
+}
+}  // namespace
+
+extern "C" {
+
+const char* stmg_last_error(void) { return g_err.c_str(); }
+const char* stmg_version(void) { return "stmg-b200 0.1 (sm_100a)"; }
+long long stmg_kernel_launches(void) { return kernel_launches(); }
+
+int stmg_quadrature(int kind, int n, double* points, double* weights) {
+  return guard_host([&] {
+    const Rule r = kind == 0 ? gauss(n) : (kind == 1 ? gauss_lobatto(n) : gauss_radau_right(n));
+    for (size_t i = 0; i < r.x.size(); ++i) {
+      points[i] = r.x[i];
+      weights[i] = r.w[i];
+    }
+  });
+}
+int stmg_temporal_weights(int scheme, int k, double* m_tau, double* a_tau, double* alpha, double* beta,
+                          double* unknown_nodes) {
+  return guard_host([&] {
+    const TemporalWeights w = scheme == STMG_DG ? dg_weights(k) : cgp_weights(k);
+    std::copy(w.m.begin(), w.m.end(), m_tau);
+    std::copy(w.a.begin(), w.a.end(), a_tau);
+    std::copy(w.alpha.begin(), w.alpha.end(), alpha);
+    std::copy(w.beta.begin(), w.beta.end(), beta);
+    std::copy(w.unknown_nodes.begin(), w.unknown_nodes.end(), unknown_nodes);
+  });
+}
+int stmg_block_coefficients(int equation, int scheme, int k, double tau, int n_steps, double* CM, double* CA) {
+  return guard_host([&] {
+    const TemporalWeights w = scheme == STMG_DG ? dg_weights(k) : cgp_weights(k);
+    std::vector<double> cm, ca;
+    block_coefficient_matrices(static_cast<Equation>(equation), w, tau, n_steps, cm, ca);
+    std::copy(cm.begin(), cm.end(), CM);
+    std::copy(ca.begin(), ca.end(), CA);
+  });
+}
+
+int stmg_mesh_create(int dim, const double lo[3], const double hi[3], long long base_cells, int refinements,
+                     const double* finest_vertices, stmg_mesh** out) {
+  return guard_host([&] {
+    if (!out) throw std::invalid_argument("stmg_mesh_create: null out");
+    auto m = std::make_unique<stmg_mesh>();
+    m->h = make_cartesian(dim, {lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}, base_cells, refinements);
+    if (finest_vertices) set_finest_vertices(m->h, finest_vertices);
+    *out = m.release();
+  });
+}
+void stmg_mesh_destroy(stmg_mesh* mesh) { delete mesh; }
+
+int stmg_st_operator_create(const stmg_mesh* mesh, int mesh_level, int p, int equation, int scheme, int k, double tau,
+                            int n_steps, const double* coarse_cell_scale, stmg_st_operator** out) {
+  return guard([&] {
+    if (!mesh || !out) throw std::invalid_argument("stmg_st_operator_create: null argument");
+    auto o = std::make_unique<stmg_st_operator>();
+    o->w = scheme == STMG_DG ? dg_weights(k) : cgp_weights(k);
+    o->owned = std::make_unique<SpaceTimeOperator>(static_cast<Equation>(equation), o->w, tau, n_steps, mesh->h,
+                                                   mesh_level, p, coeff(mesh->h, coarse_cell_scale));
+    o->op = o->owned.get();
+    *out = o.release();
+  });
+}
+void stmg_st_operator_destroy(stmg_st_operator* op) { delete op; }
+long long stmg_st_operator_n_dofs(const stmg_st_operator* op) { return op ? op->op->n_dofs() : -1; }
+long long stmg_st_operator_n_space(const stmg_st_operator* op) { return op ? op->op->n_space() : -1; }
+int stmg_st_operator_n_t(const stmg_st_operator* op) { return op ? op->op->n_t() : -1; }
+
+int stmg_st_operator_apply(const stmg_st_operator* op, const double* d_u, double* d_y, void* stream) {
+  return guard([&] {
+    if (!op || !d_u || !d_y) throw std::invalid_argument("stmg_st_operator_apply: null argument");
+    op->op->apply(d_u, d_y, st(stream));
+  });
+}
+
+int stmg_st_operator_apply_host(const stmg_st_operator* op, const double* h_u, double* h_y) {
+  return guard([&] {
+    if (!op || !h_u || !h_y) throw std::invalid_argument("stmg_st_operator_apply_host: null argument");
+    const size_t bytes = sizeof(double) * op->op->n_dofs();
+    if (op->hu.bytes() != bytes) {
+      op->hu.allocate(bytes);
+      op->hy.allocate(bytes);
+    }
+    cuda_check(cudaMemcpy(op->hu.raw(), h_u, bytes, cudaMemcpyHostToDevice), "H2D");
+    op->op->apply(op->hu.d(), op->hy.d(), nullptr);
+    cuda_check(cudaMemcpy(h_y, op->hy.raw(), bytes, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int stmg_spatial_apply(const stmg_st_operator* op, int kind, const double* d_u, double* d_y, void* stream) {
+  return guard([&] {
+    if (!op || !d_u || !d_y || (kind != 0 && kind != 1)) throw std::invalid_argument("stmg_spatial_apply: bad argument");
+    op->op->spatial_apply(kind, d_u, d_y, st(stream));
+  });
+}
+
+int stmg_asm_create(const stmg_st_operator* op, stmg_asm** out) {
+  return guard([&] {
+    if (!op || !out) throw std::invalid_argument("stmg_asm_create: null argument");
+    auto a = std::make_unique<stmg_asm>();
+    a->s = std::make_unique<ASMSmoother>(*op->op);
+    *out = a.release();
+  });
+}
+void stmg_asm_destroy(stmg_asm* a) { delete a; }
+int stmg_asm_add_correction(const stmg_asm* a, const double* d_r, double* d_z, void* stream) {
+  return guard([&] {
+    if (!a || !d_r || !d_z) throw std::invalid_argument("stmg_asm_add_correction: null argument");
+    a->s->add_correction(d_r, d_z, st(stream));
+  });
+}
+
+int stmg_transfer_create(const stmg_st_operator* fine, const stmg_st_operator* coarse, stmg_transfer** out) {
+  return guard([&] {
+    if (!fine || !coarse || !out) throw std::invalid_argument("stmg_transfer_create: null argument");
+    auto t = std::make_unique<stmg_transfer>();
+    t->t = std::make_unique<Transfer>(*fine->op, *coarse->op);
+    *out = t.release();
+  });
+}
+void stmg_transfer_destroy(stmg_transfer* t) { delete t; }
+int stmg_transfer_prolong(const stmg_transfer* t, const double* d_c, double* d_f, void* stream) {
+  return guard([&] {
+    if (!t || !d_c || !d_f) throw std::invalid_argument("stmg_transfer_prolong: null argument");
+    t->t->prolong(d_c, d_f, st(stream));
+  });
+}
+int stmg_transfer_restrict(const stmg_transfer* t, const double* d_f, double* d_c, void* stream) {
+  return guard([&] {
+    if (!t || !d_f || !d_c) throw std::invalid_argument("stmg_transfer_restrict: null argument");
+    t->t->restrict_(d_f, d_c, st(stream));
+  });
+}
+
+void stmg_mg_options_default(stmg_mg_options* o) {
+  const MultigridOptions d;
+  o->n_smooth = d.n_smooth;
+  o->direct_coarse_max = d.direct_coarse_max;
+  o->coarse_rel_tol = d.coarse_rel_tol;
+  o->coarse_max_iters = d.coarse_max_iters;
+  o->eig_iters = d.eig_iters;
+  o->seed = d.seed;
+}
+
+int stmg_multigrid_create(int equation, int scheme, const stmg_mesh* mesh, const double* coarse_cell_scale,
+                          int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
+                          const int* strategy, const stmg_mg_options* options, stmg_multigrid** out) {
+  return guard([&] {
+    if (!mesh || !out) throw std::invalid_argument("stmg_multigrid_create: null argument");
+    const TimeScheme sch = static_cast<TimeScheme>(scheme);
+    LevelSpec finest{fine_mesh_level, p, k, n_steps, tau, Coarsening::SpaceH};
+    std::vector<Coarsening> strat;
+    if (n_strategy < 0)
+      strat = default_strategy(finest, sch);
+    else
+      for (int i = 0; i < n_strategy; ++i) strat.push_back(static_cast<Coarsening>(strategy[i]));
+    MultigridOptions mo;
+    if (options) {
+      mo.n_smooth = options->n_smooth;
+      mo.direct_coarse_max = options->direct_coarse_max;
+      mo.coarse_rel_tol = options->coarse_rel_tol;
+      mo.coarse_max_iters = options->coarse_max_iters;
+      mo.eig_iters = options->eig_iters;
+      mo.seed = options->seed;
+    }
+    auto m = std::make_unique<stmg_multigrid>();
+    m->mg = std::make_unique<SpaceTimeMultigrid>(static_cast<Equation>(equation), sch, mesh->h,
+                                                 coeff(mesh->h, coarse_cell_scale),
+                                                 build_level_plan(finest, sch, strat), mo);
+    *out = m.release();
+  });
+}
+void stmg_multigrid_destroy(stmg_multigrid* mg) { delete mg; }
+int stmg_multigrid_n_levels(const stmg_multigrid* mg) { return mg ? mg->mg->n_levels() : -1; }
+
+int stmg_multigrid_level_info(const stmg_multigrid* mg, int level, int ints[5], long long* n_dofs, double* omega) {
+  return guard([&] {
+    if (!mg || level < 0 || level >= mg->mg->n_levels()) throw std::invalid_argument("level_info: bad level");
+    const LevelInfo li = mg->mg->level_info()[static_cast<size_t>(level)];
+    ints[0] = li.mesh_level;
+    ints[1] = li.p;
+    ints[2] = li.k;
+    ints[3] = li.n_steps;
+    int c = -1;
+    if (li.coarsening == "space-h") c = 0;
+    if (li.coarsening == "space-p") c = 1;
+    if (li.coarsening == "time-tau") c = 2;
+    if (li.coarsening == "time-k") c = 3;
+    ints[4] = c;
+    *n_dofs = li.n_dofs;
+    *omega = li.omega;
+  });
+}
+int stmg_multigrid_set_omega(stmg_multigrid* mg, int level, double omega) {
+  return guard([&] {
+    if (!mg || level < 0 || level >= mg->mg->n_levels()) throw std::invalid_argument("set_omega: bad level");
+    mg->mg->set_omega(level, omega);
+  });
+}
+const stmg_st_operator* stmg_multigrid_operator_at(const stmg_multigrid* mg, int level) {
+  if (!mg || level < 0 || level >= mg->mg->n_levels()) return nullptr;
+  // wrapper objects that alias the multigrid's operators (never deleted by callers)
+  auto* self = const_cast<stmg_multigrid*>(mg);
+  if (self->views.empty()) {
+    for (int l = 0; l < mg->mg->n_levels(); ++l) {
+      auto v = std::make_unique<stmg_st_operator>();
+      v->op = &mg->mg->operator_at(l);
+      self->views.push_back(std::move(v));
+    }
+  }
+  return self->views[static_cast<size_t>(level)].get();
+}
+int stmg_multigrid_apply(const stmg_multigrid* mg, const double* d_r, double* d_z, void* stream) {
+  return guard([&] {
+    if (!mg || !d_r || !d_z) throw std::invalid_argument("stmg_multigrid_apply: null argument");
+    mg->mg->apply(d_r, d_z, st(stream));
+  });
+}
+int stmg_multigrid_apply_host(const stmg_multigrid* mg, const double* h_r, double* h_z) {
+  return guard([&] {
+    if (!mg || !h_r || !h_z) throw std::invalid_argument("stmg_multigrid_apply_host: null argument");
+    const size_t bytes = sizeof(double) * mg->mg->fine_operator().n_dofs();
+    if (mg->hr.bytes() != bytes) {
+      mg->hr.allocate(bytes);
+      mg->hz.allocate(bytes);
+    }
+    cuda_check(cudaMemcpy(mg->hr.raw(), h_r, bytes, cudaMemcpyHostToDevice), "H2D");
+    mg->mg->apply(mg->hr.d(), mg->hz.d(), nullptr);
+    cuda_check(cudaMemcpy(h_z, mg->hz.raw(), bytes, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+int stmg_multigrid_smooth(const stmg_multigrid* mg, int level, const double* d_f, double* d_u, void* stream) {
+  return guard([&] {
+    if (!mg || level < 0 || level + 1 >= mg->mg->n_levels() + (mg->mg->n_levels() == 1 ? 1 : 0))
+      throw std::invalid_argument("stmg_multigrid_smooth: bad level");
+    mg->mg->smooth(level, d_f, d_u, st(stream));
+  });
+}
+int stmg_multigrid_asm_add_correction(const stmg_multigrid* mg, int level, const double* d_r, double* d_z,
+                                      void* stream) {
+  return guard([&] {
+    if (!mg || level < 0 || level >= mg->mg->n_levels()) throw std::invalid_argument("asm_add_correction: bad level");
+    mg->mg->smoother_at(level).add_correction(d_r, d_z, st(stream));
+  });
+}
+int stmg_multigrid_prolong(const stmg_multigrid* mg, int level, const double* d_c, double* d_f, void* stream) {
+  return guard([&] {
+    if (!mg || level < 0 || level + 1 >= mg->mg->n_levels()) throw std::invalid_argument("prolong: bad level");
+    mg->mg->transfer_at(level).prolong(d_c, d_f, st(stream));
+  });
+}
+int stmg_multigrid_restrict(const stmg_multigrid* mg, int level, const double* d_f, double* d_c, void* stream) {
+  return guard([&] {
+    if (!mg || level < 0 || level + 1 >= mg->mg->n_levels()) throw std::invalid_argument("restrict: bad level");
+    mg->mg->transfer_at(level).restrict_(d_f, d_c, st(stream));
+  });
+}
+long long stmg_multigrid_device_bytes(const stmg_multigrid* mg) {
+  return mg ? static_cast<long long>(mg->mg->device_bytes()) : -1;
+}
+
+void stmg_gmres_options_default(stmg_gmres_options* o) {
+  const GmresOptions d;
+  o->max_iters = d.max_iters;
+  o->restart = d.restart;
+  o->rel_tol = d.rel_tol;
+  o->abs_tol = d.abs_tol;
+}
+
+namespace {
+GmresOptions gopts(const stmg_gmres_options* o) {
+  GmresOptions g;
+  if (o) {
+    g.max_iters = o->max_iters;
+    g.restart = o->restart;
+    g.rel_tol = o->rel_tol;
+    g.abs_tol = o->abs_tol;
+  }
+  return g;
+}
+void fill_result(const GmresResult& r, stmg_gmres_result* out, double* history, int cap) {
+  if (out) {
+    out->converged = r.converged ? 1 : 0;
+    out->iterations = r.iterations;
+    out->initial_residual = r.initial_residual;
+    out->final_residual = r.final_residual;
+    out->history_len = static_cast<int>(r.residual_history.size());
+  }
+  if (history)
+    for (int i = 0; i < cap && i < static_cast<int>(r.residual_history.size()); ++i)
+      history[i] = r.residual_history[static_cast<size_t>(i)];
+}
+thread_local GmresWorkspace g_ws;
+}  // namespace
+
+int stmg_gmres(long long n, stmg_linear_map op, void* op_ctx, stmg_linear_map precond, void* precond_ctx,
+               const double* d_b, double* d_x, const stmg_gmres_options* options, stmg_gmres_result* result,
+               double* history, int history_cap, void* stream) {
+  return guard([&] {
+    if (!op || !d_b || !d_x || n <= 0) throw std::invalid_argument("stmg_gmres: bad argument");
+    DeviceMap A = [op, op_ctx](const double* in, double* out, cudaStream_t s) {
+      if (op(op_ctx, in, out, s) != 0) throw std::runtime_error("stmg_gmres: operator callback failed");
+    };
+    DeviceMap M;
+    if (precond)
+      M = [precond, precond_ctx](const double* in, double* out, cudaStream_t s) {
+        if (precond(precond_ctx, in, out, s) != 0) throw std::runtime_error("stmg_gmres: preconditioner failed");
+      };
+    const GmresResult r = gmres(A, d_b, d_x, n, gopts(options), M, g_ws, st(stream));
+    fill_result(r, result, history, history_cap);
+  });
+}
+
+int stmg_solve(const stmg_multigrid* mg, int precondition, const double* d_b, double* d_x,
+               const stmg_gmres_options* options, stmg_gmres_result* result, double* history, int history_cap,
+               void* stream) {
+  return guard([&] {
+    if (!mg || !d_b || !d_x) throw std::invalid_argument("stmg_solve: null argument");
+    const SpaceTimeOperator& op = mg->mg->fine_operator();
+    const SpaceTimeMultigrid* m = mg->mg.get();
+    DeviceMap A = [&op](const double* in, double* out, cudaStream_t s) { op.apply(in, out, s); };
+    DeviceMap M;
+    if (precondition) M = [m](const double* in, double* out, cudaStream_t s) { m->apply(in, out, s); };
+    const GmresResult r = gmres(A, d_b, d_x, op.n_dofs(), gopts(options), M, mg->ws, st(stream));
+    fill_result(r, result, history, history_cap);
+  });
+}
+
+int stmg_solve_host(const stmg_multigrid* mg, int precondition, const double* h_b, double* h_x,
+                    const stmg_gmres_options* options, stmg_gmres_result* result, double* history, int history_cap) {
+  return guard([&] {
+    if (!mg || !h_b || !h_x) throw std::invalid_argument("stmg_solve_host: null argument");
+    const size_t bytes = sizeof(double) * mg->mg->fine_operator().n_dofs();
+    DeviceBuffer b(bytes), x(bytes);
+    cuda_check(cudaMemcpy(b.raw(), h_b, bytes, cudaMemcpyHostToDevice), "H2D b");
+    cuda_check(cudaMemcpy(x.raw(), h_x, bytes, cudaMemcpyHostToDevice), "H2D x");
+    const int rc = stmg_solve(mg, precondition, b.d(), x.d(), options, result, history, history_cap, nullptr);
+    if (rc != 0) throw std::runtime_error(g_err);
+    cuda_check(cudaMemcpy(h_x, x.raw(), bytes, cudaMemcpyDeviceToHost), "D2H x");
+  });
+}
+
+}  // extern "C"

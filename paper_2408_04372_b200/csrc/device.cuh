@@ -1,0 +1,46 @@
+// Device-side level descriptor shared by the sm_100a kernels. One descriptor
+// describes one multigrid level: the spatial Q_p lattice, its geometry
+// (exact Cartesian lattice or d-linear cells from vertex coordinates), the
+// coefficient, the 1D shape tables at the Gauss points, and the space-time
+// block coefficients CM/CA of the batched slab system.
+//
+// HBM layout of every space-time vector (identical to the reference's,
+// include/stmg/space_time_operator.hpp:23-29,43-45): index
+// (s*n_t + i)*n_space + g with the spatial lattice index
+// g = ix + dofs_x*(iy + dofs_y*iz), ix = cx*p + local (spatial_operator.cpp:70-114).
+#pragma once
+
+#include <cstdint>
+
+namespace stmgb {
+
+constexpr int kMaxN = 5;   // p <= 4
+constexpr int kMaxF = 8;   // S * n_t <= 8
+
+struct DevLevel {
+  int dim;
+  int p;
+  int n;           // p + 1 (= number of Gauss points per axis)
+  int S, nt, F;    // steps, temporal unknowns per step, F = S*nt fields
+  long long cells[3];
+  long long dofs[3];  // per axis: cells*p + 1 (1 for unused axes)
+  long long n_space;  // prod dofs
+  long long n_dofs;   // F * n_space
+  // geometry: verts == nullptr -> Cartesian lattice with spacing h
+  const double* verts;  // (cells+1)^dim * 3 doubles, x fastest
+  double h[3];
+  // coefficient: rho(cell) = rho0[ancestor on level 0] (1 if rho0 == nullptr)
+  const double* rho0;
+  int rho_shift;          // refinement levels between this level and level 0
+  long long cells0[3];
+  // 1D tables at the q = n Gauss points of [0,1]
+  double B[kMaxN][kMaxN];   // B[q][j] = phi_j(x_q)      (spatial_operator.cpp:141-147)
+  double Dq[kMaxN][kMaxN];  // collocation derivative at the Gauss points
+  double w[kMaxN];          // Gauss weights
+  double xq[kMaxN];         // Gauss points on [0,1]
+  // space-time block coefficients, row-major F x F (space_time_operator.cpp:269-317)
+  double CM[kMaxF * kMaxF];
+  double CA[kMaxF * kMaxF];
+};
+
+}  // namespace stmgb

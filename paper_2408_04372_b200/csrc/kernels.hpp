@@ -1,0 +1,81 @@
+// Launch entry points of the sm_100a kernels (host-callable).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace stmgb {
+
+// y = S u (overwrite), fused space-time operator -- st_operator.cu
+void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream);
+
+// ---- vector kernels (vector_ops.cu)
+void vec_copy(double* y, const double* x, long long n, cudaStream_t s);
+void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s);         // y += a x
+void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t s);  // y = a x + b y
+void vec_scale_into(double* y, double a, const double* x, long long n, cudaStream_t s);   // y = a x
+void vec_sub_into(double* r, const double* f, const double* y, long long n, cudaStream_t s);  // r = f - y
+// out[i] = <V_i, w>, i < k; V = device array of k vector pointers; out is a
+// device buffer of k doubles; scratch holds kDotBlocks * k doubles
+void vec_multidot(const double* const* V, int k, const double* w, long long n, double* out, double* scratch,
+                  cudaStream_t s);
+// w += sign * sum_i h_i V_i (h on device)
+void vec_multi_axpy(double* w, const double* const* V, int k, const double* h, double sign, long long n,
+                    cudaStream_t s);
+constexpr int kDotBlocks = 296;
+void vec_fill(double* y, double v, long long n, cudaStream_t s);
+void vec_set_element(double* y, long long i, double v, cudaStream_t s);
+// y[g] = 1 where every lattice coordinate of g is congruent to colour (mod period)
+void vec_colour_indicator(double* y, const long long* dofs, int dim, int period, int cx, int cy, int cz,
+                          cudaStream_t s);
+// dense matvec y = A x, A row-major n x n (coarse-grid inverse)
+void dense_matvec(const double* A, const double* x, double* y, int n, cudaStream_t s);
+
+// ---- grid transfers (transfer.cu)
+struct DevAxisTransfer {
+  // prolongation rows: fine index i -> first coarse index start[i], weights
+  // wts[i*(nc_loc)+j], j < nc_loc (spatial h/p, transfer.cpp:32-54)
+  const int* row_start;
+  const double* row_w;
+  int row_nnz;
+  // restriction columns (CSR of P^T): coarse index J -> fine rows
+  const int* col_ptr;
+  const int* col_idx;
+  const double* col_w;
+  long long nf, nc;
+};
+void spatial_prolong(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
+                     const double* coarse, double* fine, cudaStream_t s);
+void spatial_restrict(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
+                      const double* fine, double* coarse, cudaStream_t s);
+// temporal: fine block r = sum_c T[r][c] coarse block c (T row-major Ff x Fc)
+void temporal_prolong(const double* T_dev, int Ff, int Fc, long long n_space, const long long* dofs, int dim,
+                      const double* coarse, double* fine, cudaStream_t s);
+void temporal_restrict(const double* T_dev, int Ff, int Fc, long long n_space, const long long* dofs, int dim,
+                       const double* fine, double* coarse, cudaStream_t s);
+
+// ---- additive Schwarz (asm_smoother.cu)
+struct DevASM {
+  int dim, p, n, m;       // m = n^dim local dofs per cell
+  int S, nt;
+  long long cells[3], dofs[3], n_space;
+  const double* X;        // per cell m x m (row-major [a][e]), M_T-orthonormal eigenvectors
+  const double* lam;      // per cell m eigenvalues (0 on Dirichlet dofs)
+  double TM[16], TA[16];  // diagonal (s,s) temporal blocks, n_t x n_t
+};
+void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_t s);
+// probing-based extraction of restricted cell matrices (setup)
+void asm_extract_probe(const DevASM& A, int colour_x, int colour_y, int colour_z, int period, const double* probe,
+                       double* cellmat, cudaStream_t s);
+void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s);  // At <- L^-1 At L^-T, Mt <- L^-1
+void asm_back_transform(int m, long long n_cells, const double* Linv, const double* V, double* X, cudaStream_t s);
+
+}  // namespace stmgb
+
+namespace stmgb {
+// number of kernels launched by this library since load (the bench's
+// gpu_launches evidence); incremented at every launch site
+void count_launch();
+long long kernel_launches();
+}  // namespace stmgb

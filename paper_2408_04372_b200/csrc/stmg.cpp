@@ -1,0 +1,885 @@
+// Host C++ layer of the B200 STMG path (see stmg.hpp for the interface map).
+#include "stmg.hpp"
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+namespace stmgb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+void solver_check(cusolverStatus_t s, const char* what) {
+  if (s != CUSOLVER_STATUS_SUCCESS) throw std::runtime_error(std::string(what) + ": cusolver status " + std::to_string(s));
+}
+template <typename T>
+DeviceBuffer upload(const std::vector<T>& v) {
+  DeviceBuffer b(sizeof(T) * std::max<size_t>(v.size(), 1));
+  if (!v.empty()) cuda_check(cudaMemcpy(b.raw(), v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
+  return b;
+}
+double host_dot(const double* a, const double* b, Index n, cudaStream_t s, DeviceBuffer& ptrs, DeviceBuffer& scratch,
+                DeviceBuffer& out) {
+  const double* hp[1] = {a};
+  cuda_check(cudaMemcpyAsync(ptrs.raw(), hp, sizeof(hp), cudaMemcpyHostToDevice, s), "dot ptrs");
+  vec_multidot(static_cast<const double* const*>(ptrs.raw()), 1, b, n, out.d(), scratch.d(), s);
+  double r = 0.0;
+  cuda_check(cudaMemcpyAsync(&r, out.d(), sizeof(double), cudaMemcpyDeviceToHost, s), "dot result");
+  cuda_check(cudaStreamSynchronize(s), "dot sync");
+  return r;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ buffers
+DeviceBuffer::DeviceBuffer(size_t bytes) { allocate(bytes); }
+DeviceBuffer::~DeviceBuffer() { release(); }
+DeviceBuffer::DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), bytes_(o.bytes_) {
+  o.p_ = nullptr;
+  o.bytes_ = 0;
+}
+DeviceBuffer& DeviceBuffer::operator=(DeviceBuffer&& o) noexcept {
+  if (this != &o) {
+    release();
+    p_ = o.p_;
+    bytes_ = o.bytes_;
+    o.p_ = nullptr;
+    o.bytes_ = 0;
+  }
+  return *this;
+}
+void DeviceBuffer::allocate(size_t bytes) {
+  release();
+  if (bytes == 0) bytes = 8;
+  cuda_check(cudaMalloc(&p_, bytes), "cudaMalloc");
+  bytes_ = bytes;
+}
+void DeviceBuffer::release() {
+  if (p_) cudaFree(p_);
+  p_ = nullptr;
+  bytes_ = 0;
+}
+
+// ------------------------------------------------------ SpaceTimeOperator
+SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& weights, double tau, int n_steps,
+                                     const MeshHierarchy& mesh, int mesh_level, int p, const Coefficient& rho)
+    : equation_(equation), weights_(weights), tau_(tau), n_steps_(n_steps), mesh_level_(mesh_level), p_(p) {
+  if (tau <= 0.0 || n_steps < 1) throw std::invalid_argument("SpaceTimeOperator: bad tau or n_steps");
+  if (mesh_level < 0 || mesh_level >= mesh.n_levels()) throw std::invalid_argument("SpaceTimeOperator: bad level");
+  if (p < 1 || p + 1 > kMaxN) throw std::invalid_argument("SpaceTimeOperator: p must be in [1, 4]");
+  const int F = n_steps * weights.n_t;
+  if (F > kMaxF) throw std::invalid_argument("SpaceTimeOperator: n_steps * n_t must be <= 8");
+  const MeshLevel& m = mesh.levels[static_cast<size_t>(mesh_level)];
+  mesh_level_ptr_ = &m;
+  if (m.dim < 2 || m.dim > 3) throw std::invalid_argument("SpaceTimeOperator: dim must be 2 or 3");
+  DevLevel& d = desc_;
+  d.dim = m.dim;
+  d.p = p;
+  d.n = p + 1;
+  d.S = n_steps;
+  d.nt = weights.n_t;
+  d.F = F;
+  d.n_space = 1;
+  for (int a = 0; a < 3; ++a) {
+    d.cells[a] = a < m.dim ? m.cells[a] : 1;
+    d.dofs[a] = a < m.dim ? m.cells[a] * p + 1 : 1;
+    d.n_space *= d.dofs[a];
+    d.h[a] = a < m.dim ? (m.hi[a] - m.lo[a]) / static_cast<double>(m.cells[a]) : 1.0;
+  }
+  d.n_dofs = d.n_space * F;
+  if (!m.vertices.empty()) {
+    verts_ = upload(m.vertices);
+    d.verts = verts_.d();
+  } else {
+    d.verts = nullptr;
+  }
+  if (!rho.coarse_cell_scale.empty()) {
+    const MeshLevel& m0 = mesh.levels.front();
+    if (static_cast<Index>(rho.coarse_cell_scale.size()) != m0.n_cells())
+      throw std::invalid_argument("SpaceTimeOperator: coefficient needs one value per level-0 cell");
+    for (double v : rho.coarse_cell_scale)
+      if (!(v > 0.0)) throw std::runtime_error("CoefficientField: non-positive value");
+    rho0_ = upload(rho.coarse_cell_scale);
+    d.rho0 = rho0_.d();
+    d.rho_shift = mesh_level;
+    for (int a = 0; a < 3; ++a) d.cells0[a] = a < m.dim ? m0.cells[a] : 1;
+  } else {
+    d.rho0 = nullptr;
+  }
+  const Rule q = gauss(d.n);
+  const Rule gl = gauss_lobatto(d.n);
+  for (int i = 0; i < kMaxN; ++i)
+    for (int j = 0; j < kMaxN; ++j) {
+      d.B[i][j] = (i < d.n && j < d.n) ? lagrange_eval(gl.x, j, q.x[i]) : 0.0;
+      d.Dq[i][j] = (i < d.n && j < d.n) ? lagrange_deriv(q.x, j, q.x[i]) : 0.0;
+    }
+  for (int i = 0; i < kMaxN; ++i) {
+    d.w[i] = i < d.n ? q.w[i] : 0.0;
+    d.xq[i] = i < d.n ? q.x[i] : 0.0;
+  }
+  std::vector<double> CM, CA;
+  block_coefficient_matrices(equation, weights, tau, n_steps, CM, CA);
+  std::memset(d.CM, 0, sizeof(d.CM));
+  std::memset(d.CA, 0, sizeof(d.CA));
+  std::copy(CM.begin(), CM.end(), d.CM);
+  std::copy(CA.begin(), CA.end(), d.CA);
+  // single-field spatial mass / stiffness (SpatialOperator::apply)
+  mass_desc_ = desc_;
+  mass_desc_.S = mass_desc_.nt = mass_desc_.F = 1;
+  mass_desc_.n_dofs = d.n_space;
+  std::memset(mass_desc_.CM, 0, sizeof(mass_desc_.CM));
+  std::memset(mass_desc_.CA, 0, sizeof(mass_desc_.CA));
+  stiff_desc_ = mass_desc_;
+  mass_desc_.CM[0] = 1.0;
+  stiff_desc_.CA[0] = 1.0;
+}
+
+void SpaceTimeOperator::apply(const double* u, double* y, cudaStream_t stream) const {
+  ++apply_count_;
+  st_apply(desc_, u, y, stream);
+}
+
+void SpaceTimeOperator::spatial_apply(int kind, const double* u, double* y, cudaStream_t stream) const {
+  st_apply(kind == 0 ? mass_desc_ : stiff_desc_, u, y, stream);
+}
+
+// ------------------------------------------------------------ ASMSmoother
+ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
+  const DevLevel& d = op.desc();
+  DevASM& A = asm_;
+  A.dim = d.dim;
+  A.p = d.p;
+  A.n = d.n;
+  A.m = d.dim == 2 ? d.n * d.n : d.n * d.n * d.n;
+  A.S = d.S;
+  A.nt = d.nt;
+  if (A.nt > 4) throw std::invalid_argument("ASMSmoother: n_t must be <= 4");
+  if (A.m > 64)
+    throw std::invalid_argument("ASMSmoother: exact cell blocks need (p+1)^dim <= 64 (3D p <= 3)");
+  for (int a = 0; a < 3; ++a) {
+    A.cells[a] = d.cells[a];
+    A.dofs[a] = d.dofs[a];
+  }
+  A.n_space = d.n_space;
+  for (int i = 0; i < 16; ++i) A.TM[i] = A.TA[i] = 0.0;
+  const int F = d.F;
+  for (int i = 0; i < A.nt; ++i)
+    for (int j = 0; j < A.nt; ++j) {
+      A.TM[i * A.nt + j] = d.CM[i * F + j];
+      A.TA[i * A.nt + j] = d.CA[i * F + j];
+    }
+  const Index n_cells = d.cells[0] * d.cells[1] * d.cells[2];
+  const size_t mat_bytes = sizeof(double) * static_cast<size_t>(n_cells) * A.m * A.m;
+  cudaStream_t s = nullptr;
+  DeviceBuffer cellM(mat_bytes), cellA(mat_bytes), probe(sizeof(double) * d.n_space), ind(sizeof(double) * d.n_space);
+  cuda_check(cudaMemsetAsync(cellM.raw(), 0, mat_bytes, s), "memset");
+  cuda_check(cudaMemsetAsync(cellA.raw(), 0, mat_bytes, s), "memset");
+  // restricted global matrices by probing the matrix-free operators with
+  // colour classes of period 2p+1 (no two same-colour dofs share a cell
+  // neighbourhood, so every probe entry is a single matrix entry)
+  const int P = 2 * d.p + 1;
+  const int cz_max = d.dim == 3 ? P : 1;
+  for (int cz = 0; cz < cz_max; ++cz)
+    for (int cy = 0; cy < P; ++cy)
+      for (int cx = 0; cx < P; ++cx) {
+        vec_colour_indicator(ind.d(), d.dofs, d.dim, P, cx, cy, cz, s);
+        op.spatial_apply(0, ind.d(), probe.d(), s);
+        asm_extract_probe(A, cx, cy, cz, P, probe.d(), cellM.d(), s);
+        op.spatial_apply(1, ind.d(), probe.d(), s);
+        asm_extract_probe(A, cx, cy, cz, P, probe.d(), cellA.d(), s);
+      }
+  // standard form C = L^-1 A L^-T (into cellA), L^-1 (into cellM)
+  asm_reduce_standard(A, cellM.d(), cellA.d(), s);
+  cuda_check(cudaGetLastError(), "asm setup kernels");
+  // batched symmetric eigensolver
+  lam_.allocate(sizeof(double) * static_cast<size_t>(n_cells) * A.m);
+  cusolverDnHandle_t h = nullptr;
+  cusolverDnParams_t prm = nullptr;
+  solver_check(cusolverDnCreate(&h), "cusolverDnCreate");
+  solver_check(cusolverDnCreateParams(&prm), "cusolverDnCreateParams");
+  solver_check(cusolverDnSetStream(h, s), "cusolverDnSetStream");
+  const Index chunk = std::min<Index>(n_cells, 1 << 15);
+  size_t dws = 0, hws = 0;
+  solver_check(cusolverDnXsyevBatched_bufferSize(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, A.m,
+                                                 CUDA_R_64F, cellA.raw(), A.m, CUDA_R_64F, lam_.raw(), CUDA_R_64F,
+                                                 &dws, &hws, chunk),
+               "syevBatched_bufferSize");
+  DeviceBuffer dwork(std::max<size_t>(dws, 8)), info(sizeof(int) * static_cast<size_t>(chunk));
+  std::vector<char> hwork(std::max<size_t>(hws, 8));
+  for (Index c0 = 0; c0 < n_cells; c0 += chunk) {
+    const Index nb = std::min<Index>(chunk, n_cells - c0);
+    solver_check(cusolverDnXsyevBatched(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, A.m, CUDA_R_64F,
+                                        cellA.d() + c0 * A.m * A.m, A.m, CUDA_R_64F, lam_.d() + c0 * A.m, CUDA_R_64F,
+                                        dwork.raw(), dws, hwork.data(), hws, static_cast<int*>(info.raw()), nb),
+                 "syevBatched");
+  }
+  cuda_check(cudaStreamSynchronize(s), "syev sync");
+  std::vector<int> hinfo(static_cast<size_t>(std::min<Index>(chunk, n_cells)));
+  cuda_check(cudaMemcpy(hinfo.data(), info.raw(), sizeof(int) * hinfo.size(), cudaMemcpyDeviceToHost), "info");
+  for (int v : hinfo)
+    if (v != 0) throw std::runtime_error("ASMSmoother: singular block (eigensolver info " + std::to_string(v) + ")");
+  cusolverDnDestroyParams(prm);
+  cusolverDnDestroy(h);
+  X_.allocate(mat_bytes);
+  asm_back_transform(A.m, n_cells, cellM.d(), cellA.d(), X_.d(), s);
+  cuda_check(cudaStreamSynchronize(s), "asm setup");
+  A.X = X_.d();
+  A.lam = lam_.d();
+}
+
+void ASMSmoother::add_correction(const double* residual, double* correction, cudaStream_t stream) const {
+  ++sweep_count_;
+  asm_add_correction(asm_, residual, correction, stream);
+}
+
+// --------------------------------------------------------------- Transfer
+namespace {
+// dense 1D prolongation matrix, nf x nc (transfer.cpp:32-54)
+std::vector<double> axis_prolongation(Index fine_cells, int pf, Index coarse_cells, int pc) {
+  const Index nf = fine_cells * pf + 1, nc = coarse_cells * pc + 1;
+  const bool h = coarse_cells != fine_cells;
+  const std::vector<double> fn = gauss_lobatto(pf + 1).x, cn = gauss_lobatto(pc + 1).x;
+  std::vector<double> P(static_cast<size_t>(nf * nc), 0.0);
+  for (Index cf = 0; cf < fine_cells; ++cf)
+    for (int m = 0; m <= pf; ++m) {
+      const Index row = cf * pf + m;
+      Index cc = cf;
+      double tc = fn[m];
+      if (h) {
+        cc = cf / 2;
+        tc = 0.5 * static_cast<double>(cf % 2) + 0.5 * fn[m];
+      }
+      for (int j = 0; j <= pc; ++j) P[static_cast<size_t>(row * nc + cc * pc + j)] = lagrange_eval(cn, j, tc);
+    }
+  return P;
+}
+}  // namespace
+
+Transfer::Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coarse) : fine_(&fine), coarse_(&coarse) {
+  spatial_ = fine.mesh_level() != coarse.mesh_level() || fine.p() != coarse.p();
+  Ff_ = fine.desc().F;
+  Fc_ = coarse.desc().F;
+  if (spatial_) {
+    if (fine.n_steps() != coarse.n_steps() || fine.weights().k != coarse.weights().k ||
+        fine.weights().scheme != coarse.weights().scheme)
+      throw std::invalid_argument("Transfer: more than one attribute changed");
+    const bool h = fine.mesh_level() != coarse.mesh_level();
+    for (int a = 0; a < fine.dim(); ++a) {
+      const Index cf = fine.desc().cells[a], cc = coarse.desc().cells[a];
+      if (h && cc * 2 != cf) throw std::invalid_argument("Transfer: meshes are not nested");
+      const int pf = fine.p(), pc = coarse.p();
+      const std::vector<double> P = axis_prolongation(cf, pf, cc, pc);
+      const Index nf = cf * pf + 1, nc = cc * pc + 1;
+      const int nnz = pc + 1;
+      std::vector<int> start(static_cast<size_t>(nf));
+      std::vector<double> w(static_cast<size_t>(nf * nnz), 0.0);
+      for (Index i = 0; i < nf; ++i) {
+        Index first = nc, last = -1;
+        for (Index j = 0; j < nc; ++j)
+          if (P[static_cast<size_t>(i * nc + j)] != 0.0) {
+            first = std::min(first, j);
+            last = std::max(last, j);
+          }
+        if (last < 0) first = 0;
+        Index st = std::min<Index>(first, nc - nnz);
+        if (last >= st + nnz) throw std::runtime_error("Transfer: prolongation row wider than a coarse cell");
+        start[static_cast<size_t>(i)] = static_cast<int>(st);
+        for (int k = 0; k < nnz; ++k) w[static_cast<size_t>(i * nnz + k)] = P[static_cast<size_t>(i * nc + st + k)];
+      }
+      std::vector<int> cptr(static_cast<size_t>(nc + 1), 0), cidx;
+      std::vector<double> cw;
+      for (Index j = 0; j < nc; ++j) {
+        for (Index i = 0; i < nf; ++i) {
+          const double v = P[static_cast<size_t>(i * nc + j)];
+          if (v != 0.0) {
+            cidx.push_back(static_cast<int>(i));
+            cw.push_back(v);
+          }
+        }
+        cptr[static_cast<size_t>(j + 1)] = static_cast<int>(cidx.size());
+      }
+      bufs_.push_back(upload(start));
+      ax_[a].row_start = static_cast<const int*>(bufs_.back().raw());
+      bufs_.push_back(upload(w));
+      ax_[a].row_w = bufs_.back().d();
+      ax_[a].row_nnz = nnz;
+      bufs_.push_back(upload(cptr));
+      ax_[a].col_ptr = static_cast<const int*>(bufs_.back().raw());
+      bufs_.push_back(upload(cidx));
+      ax_[a].col_idx = static_cast<const int*>(bufs_.back().raw());
+      bufs_.push_back(upload(cw));
+      ax_[a].col_w = bufs_.back().d();
+      ax_[a].nf = nf;
+      ax_[a].nc = nc;
+    }
+  } else {
+    const TemporalWeights& wf = fine.weights();
+    const TemporalWeights& wc = coarse.weights();
+    const int Sf = fine.n_steps(), Sc = coarse.n_steps();
+    const bool tau_c = Sf != Sc;
+    if (tau_c && (Sf != 2 * Sc || wf.k != wc.k)) throw std::invalid_argument("Transfer: invalid tau coarsening");
+    if (!tau_c && wf.k != wc.k + 1) throw std::invalid_argument("Transfer: invalid k coarsening");
+    // evaluation matrix of the coarse trajectory at the fine unknown nodes,
+    // CGP left value folded in (transfer.cpp:75-105)
+    std::vector<double> T(static_cast<size_t>(Ff_ * Fc_), 0.0);
+    for (int sf = 0; sf < Sf; ++sf)
+      for (int i = 0; i < wf.n_t; ++i) {
+        const int row = sf * wf.n_t + i;
+        const double tf = wf.unknown_nodes[static_cast<size_t>(i)];
+        int sc = sf;
+        double tc = tf;
+        if (tau_c) {
+          sc = sf / 2;
+          tc = 0.5 * static_cast<double>(sf % 2) + 0.5 * tf;
+        }
+        for (int j = 0; j < wc.n_t; ++j) T[static_cast<size_t>(row * Fc_ + sc * wc.n_t + j)] += wc.unknown_weight(j, tc);
+        const double lw = wc.left_weight(tc);
+        if (lw != 0.0 && sc > 0) T[static_cast<size_t>(row * Fc_ + sc * wc.n_t - 1)] += lw;
+      }
+    time_p_ = upload(T);
+  }
+}
+
+void Transfer::prolong(const double* coarse, double* fine, cudaStream_t stream) const {
+  const DevLevel& df = fine_->desc();
+  const DevLevel& dc = coarse_->desc();
+  if (spatial_)
+    spatial_prolong(ax_, df.dim, df.F, dc.dofs, df.dofs, coarse, fine, stream);
+  else
+    temporal_prolong(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, coarse, fine, stream);
+}
+
+void Transfer::restrict_(const double* fine, double* coarse, cudaStream_t stream) const {
+  const DevLevel& df = fine_->desc();
+  const DevLevel& dc = coarse_->desc();
+  if (spatial_)
+    spatial_restrict(ax_, df.dim, df.F, dc.dofs, df.dofs, fine, coarse, stream);
+  else
+    temporal_restrict(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, fine, coarse, stream);
+}
+
+// ------------------------------------------------------------------ GMRES
+void GmresWorkspace::ensure(Index n, int vectors) {
+  if (n != n_) {
+    basis_.clear();
+    n_ = n;
+    r_.allocate(sizeof(double) * n);
+    w_.allocate(sizeof(double) * n);
+    z_.allocate(sizeof(double) * n);
+    ptrs_.allocate(sizeof(double*) * 1030);
+    scratch_.allocate(sizeof(double) * kDotBlocks * 1030);
+    small_.allocate(sizeof(double) * 4 * 1030);
+  }
+  if (static_cast<int>(basis_.size()) < vectors) {
+    if (vectors > 1024) throw std::invalid_argument("gmres: restart must be <= 1023");
+    const size_t old = basis_.size();
+    while (static_cast<int>(basis_.size()) < vectors) basis_.emplace_back(sizeof(double) * n);
+    std::vector<const double*> hp(basis_.size());
+    for (size_t i = 0; i < basis_.size(); ++i) hp[i] = basis_[i].d();
+    cuda_check(cudaMemcpy(static_cast<const double**>(ptrs_.raw()) + old, hp.data() + old,
+                          sizeof(double*) * (hp.size() - old), cudaMemcpyHostToDevice),
+               "gmres ptrs");
+  }
+}
+
+GmresResult gmres(const DeviceMap& op, const double* b, double* x, Index n, const GmresOptions& options,
+                  const DeviceMap& precond, GmresWorkspace& ws, cudaStream_t s) {
+  if (!op) throw std::invalid_argument("gmres: missing operator");
+  const int m = std::max(1, options.restart);
+  ws.ensure(n, 1);
+  // extra pointer slot after the basis for norms of w / r
+  DeviceBuffer one_ptr(sizeof(double*));
+  auto norm_of = [&](const double* v) {
+    const double* hp[1] = {v};
+    cuda_check(cudaMemcpyAsync(one_ptr.raw(), hp, sizeof(hp), cudaMemcpyHostToDevice, s), "ptr");
+    vec_multidot(static_cast<const double* const*>(one_ptr.raw()), 1, v, n, ws.small(), ws.scratch(), s);
+    double r = 0.0;
+    cuda_check(cudaMemcpyAsync(&r, ws.small(), sizeof(double), cudaMemcpyDeviceToHost, s), "nrm");
+    cuda_check(cudaStreamSynchronize(s), "nrm sync");
+    return std::sqrt(r);
+  };
+  GmresResult result;
+  op(x, ws.r(), s);
+  vec_sub_into(ws.r(), b, ws.r(), n, s);
+  double beta = norm_of(ws.r());
+  result.initial_residual = beta;
+  result.residual_history.push_back(beta);
+  const double tol = std::max(options.abs_tol, options.rel_tol * std::max(beta, 1e-300));
+  if (!std::isfinite(beta)) throw std::runtime_error("gmres: non-finite initial residual");
+  if (beta <= tol) {
+    result.converged = true;
+    result.final_residual = beta;
+    return result;
+  }
+  std::vector<double> H(static_cast<size_t>((m + 1) * m), 0.0), cs(m), sn(m), g(m + 1);
+  auto Hs = [&H, m](int i, int j) -> double& { return H[static_cast<size_t>(i * m + j)]; };
+  std::vector<double> hbuf(static_cast<size_t>(2 * (m + 1) + 1));
+  while (result.iterations < options.max_iters) {
+    ws.ensure(n, 1);
+    vec_scale_into(ws.vec(0), 1.0 / beta, ws.r(), n, s);
+    std::fill(g.begin(), g.end(), 0.0);
+    std::fill(H.begin(), H.end(), 0.0);
+    g[0] = beta;
+    int k = 0;
+    for (; k < m && result.iterations < options.max_iters; ++k) {
+      ++result.iterations;
+      ws.ensure(n, k + 2);
+      if (precond) {
+        precond(ws.vec(k), ws.z(), s);
+        op(ws.z(), ws.w(), s);
+      } else {
+        op(ws.vec(k), ws.w(), s);
+      }
+      // classical Gram-Schmidt, two passes (h1 + h2 = the reference's two MGS passes)
+      double* h1 = ws.small();
+      double* h2 = ws.small() + (m + 1);
+      vec_multidot(ws.dev_ptrs(), k + 1, ws.w(), n, h1, ws.scratch(), s);
+      vec_multi_axpy(ws.w(), ws.dev_ptrs(), k + 1, h1, -1.0, n, s);
+      vec_multidot(ws.dev_ptrs(), k + 1, ws.w(), n, h2, ws.scratch(), s);
+      vec_multi_axpy(ws.w(), ws.dev_ptrs(), k + 1, h2, -1.0, n, s);
+      cuda_check(cudaMemcpyAsync(hbuf.data(), ws.small(), sizeof(double) * 2 * (m + 1), cudaMemcpyDeviceToHost, s),
+                 "h");
+      const double hn = norm_of(ws.w());  // synchronises
+      for (int i = 0; i <= k; ++i) Hs(i, k) = hbuf[static_cast<size_t>(i)] + hbuf[static_cast<size_t>(m + 1 + i)];
+      Hs(k + 1, k) = hn;
+      if (!std::isfinite(hn)) throw std::runtime_error("gmres: non-finite Arnoldi coefficient");
+      const bool breakdown = !(hn > 0.0);
+      if (!breakdown) vec_scale_into(ws.vec(k + 1), 1.0 / hn, ws.w(), n, s);
+      for (int i = 0; i < k; ++i) {
+        const double t = cs[i] * Hs(i, k) + sn[i] * Hs(i + 1, k);
+        Hs(i + 1, k) = -sn[i] * Hs(i, k) + cs[i] * Hs(i + 1, k);
+        Hs(i, k) = t;
+      }
+      const double denom = std::hypot(Hs(k, k), Hs(k + 1, k));
+      if (denom == 0.0) {
+        cs[k] = 1.0;
+        sn[k] = 0.0;
+      } else {
+        cs[k] = Hs(k, k) / denom;
+        sn[k] = Hs(k + 1, k) / denom;
+      }
+      Hs(k, k) = denom;
+      Hs(k + 1, k) = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      const double res = std::abs(g[k + 1]);
+      result.residual_history.push_back(res);
+      if (res <= tol || breakdown) {
+        ++k;
+        break;
+      }
+    }
+    // y = H(0:k,0:k)^-1 g(0:k), then x += M^-1 (V y)
+    std::vector<double> y(static_cast<size_t>(k));
+    for (int i = k - 1; i >= 0; --i) {
+      double sum = g[i];
+      for (int j = i + 1; j < k; ++j) sum -= Hs(i, j) * y[static_cast<size_t>(j)];
+      y[static_cast<size_t>(i)] = sum / Hs(i, i);
+    }
+    cuda_check(cudaMemcpyAsync(ws.small(), y.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s), "y");
+    vec_fill(ws.w(), 0.0, n, s);
+    vec_multi_axpy(ws.w(), ws.dev_ptrs(), k, ws.small(), 1.0, n, s);
+    if (precond) {
+      precond(ws.w(), ws.z(), s);
+      vec_axpy(x, 1.0, ws.z(), n, s);
+    } else {
+      vec_axpy(x, 1.0, ws.w(), n, s);
+    }
+    op(x, ws.r(), s);
+    vec_sub_into(ws.r(), b, ws.r(), n, s);
+    beta = norm_of(ws.r());
+    result.final_residual = beta;
+    if (beta <= tol) {
+      result.converged = true;
+      return result;
+    }
+    if (beta == 0.0) break;
+  }
+  result.final_residual = beta;
+  result.converged = beta <= tol;
+  return result;
+}
+
+// ---------------------------------------------------------------- eigen
+std::vector<std::pair<double, double>> eigenvalues_small(std::vector<double> a, int n) {
+  // Householder reduction to upper Hessenberg form
+  auto A = [&a, n](int i, int j) -> double& { return a[static_cast<size_t>(i * n + j)]; };
+  std::vector<double> v(static_cast<size_t>(n));
+  for (int k = 0; k < n - 2; ++k) {
+    double alpha = 0.0;
+    for (int i = k + 1; i < n; ++i) alpha += A(i, k) * A(i, k);
+    alpha = std::sqrt(alpha);
+    if (alpha == 0.0) continue;
+    if (A(k + 1, k) > 0) alpha = -alpha;
+    std::fill(v.begin(), v.end(), 0.0);
+    v[k + 1] = A(k + 1, k) - alpha;
+    for (int i = k + 2; i < n; ++i) v[i] = A(i, k);
+    double vn = 0.0;
+    for (int i = k + 1; i < n; ++i) vn += v[i] * v[i];
+    if (vn == 0.0) continue;
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int i = k + 1; i < n; ++i) s += v[i] * A(i, j);
+      s *= 2.0 / vn;
+      for (int i = k + 1; i < n; ++i) A(i, j) -= s * v[i];
+    }
+    for (int i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int j = k + 1; j < n; ++j) s += A(i, j) * v[j];
+      s *= 2.0 / vn;
+      for (int j = k + 1; j < n; ++j) A(i, j) -= s * v[j];
+    }
+  }
+  // Francis double-shift QR on the Hessenberg matrix (active window [lo, hi])
+  std::vector<std::pair<double, double>> ev(static_cast<size_t>(n));
+  double norm = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int j = std::max(i - 1, 0); j < n; ++j) norm += std::abs(A(i, j));
+  int hi = n - 1;
+  double shift_acc = 0.0;
+  int iter = 0;
+  while (hi >= 0) {
+    int l = hi;
+    for (; l > 0; --l) {
+      double s = std::abs(A(l - 1, l - 1)) + std::abs(A(l, l));
+      if (s == 0.0) s = norm;
+      if (std::abs(A(l, l - 1)) < 1e-16 * s) {
+        A(l, l - 1) = 0.0;
+        break;
+      }
+    }
+    const double x = A(hi, hi);
+    if (l == hi) {  // one real root
+      ev[static_cast<size_t>(hi)] = {x + shift_acc, 0.0};
+      --hi;
+      iter = 0;
+      continue;
+    }
+    const double yv = A(hi - 1, hi - 1), w = A(hi, hi - 1) * A(hi - 1, hi);
+    if (l == hi - 1) {  // 2x2 block
+      const double p = 0.5 * (yv - x), q = p * p + w, zz = std::sqrt(std::abs(q));
+      const double xs = x + shift_acc;
+      if (q >= 0.0) {
+        const double z = p + (p >= 0 ? zz : -zz);
+        ev[static_cast<size_t>(hi - 1)] = {xs + z, 0.0};
+        ev[static_cast<size_t>(hi)] = {z != 0.0 ? xs - w / z : xs + z, 0.0};
+      } else {
+        ev[static_cast<size_t>(hi - 1)] = {xs + p, zz};
+        ev[static_cast<size_t>(hi)] = {xs + p, -zz};
+      }
+      hi -= 2;
+      iter = 0;
+      continue;
+    }
+    if (++iter > 200) throw std::runtime_error("eigenvalues_small: QR iteration did not converge");
+    double sx = x, sy = yv, sw = w;
+    if (iter == 10 || iter == 20) {  // exceptional shift
+      shift_acc += x;
+      for (int i = 0; i <= hi; ++i) A(i, i) -= x;
+      const double s = std::abs(A(hi, hi - 1)) + std::abs(A(hi - 1, hi - 2));
+      sx = sy = 0.75 * s;
+      sw = -0.4375 * s * s;
+    }
+    // find the start row of the bulge
+    int mrow = hi - 2;
+    double p = 0, q = 0, r = 0;
+    for (; mrow >= l; --mrow) {
+      const double z = A(mrow, mrow);
+      const double rr = sx - z, ss = sy - z;
+      p = (rr * ss - sw) / A(mrow + 1, mrow) + A(mrow, mrow + 1);
+      q = A(mrow + 1, mrow + 1) - z - rr - ss;
+      r = A(mrow + 2, mrow + 1);
+      const double s = std::abs(p) + std::abs(q) + std::abs(r);
+      p /= s;
+      q /= s;
+      r /= s;
+      if (mrow == l) break;
+      const double u = std::abs(A(mrow, mrow - 1)) * (std::abs(q) + std::abs(r));
+      const double vv = std::abs(p) * (std::abs(A(mrow - 1, mrow - 1)) + std::abs(z) + std::abs(A(mrow + 1, mrow + 1)));
+      if (u < 1e-16 * vv) break;
+    }
+    for (int i = mrow + 2; i <= hi; ++i) {
+      A(i, i - 2) = 0.0;
+      if (i != mrow + 2) A(i, i - 3) = 0.0;
+    }
+    for (int k = mrow; k <= hi - 1; ++k) {
+      double xk = 0.0;
+      if (k != mrow) {
+        p = A(k, k - 1);
+        q = A(k + 1, k - 1);
+        r = (k != hi - 1) ? A(k + 2, k - 1) : 0.0;
+        xk = std::abs(p) + std::abs(q) + std::abs(r);
+        if (xk != 0.0) {
+          p /= xk;
+          q /= xk;
+          r /= xk;
+        }
+      }
+      double s = std::sqrt(p * p + q * q + r * r);
+      if (p < 0) s = -s;
+      if (s == 0.0) continue;
+      if (k == mrow) {
+        if (l != mrow) A(k, k - 1) = -A(k, k - 1);
+      } else {
+        A(k, k - 1) = -s * xk;
+      }
+      p += s;
+      const double xx = p / s, yy = q / s, zz = r / s;
+      q /= p;
+      r /= p;
+      for (int j = k; j <= hi; ++j) {
+        double t = A(k, j) + q * A(k + 1, j);
+        if (k != hi - 1) {
+          t += r * A(k + 2, j);
+          A(k + 2, j) -= t * zz;
+        }
+        A(k + 1, j) -= t * yy;
+        A(k, j) -= t * xx;
+      }
+      const int mmin = std::min(hi, k + 3);
+      for (int i = l; i <= mmin; ++i) {
+        double t = xx * A(i, k) + yy * A(i, k + 1);
+        if (k != hi - 1) {
+          t += zz * A(i, k + 2);
+          A(i, k + 2) -= t * r;
+        }
+        A(i, k + 1) -= t * q;
+        A(i, k) -= t;
+      }
+    }
+  }
+  return ev;
+}
+
+// ---------------------------------------------------- SpaceTimeMultigrid
+namespace {
+std::string coarsening_name(Coarsening c) {
+  switch (c) {
+    case Coarsening::SpaceH: return "space-h";
+    case Coarsening::SpaceP: return "space-p";
+    case Coarsening::TimeTau: return "time-tau";
+    case Coarsening::TimeK: return "time-k";
+  }
+  return "?";
+}
+}  // namespace
+
+SpaceTimeMultigrid::SpaceTimeMultigrid(Equation equation, TimeScheme scheme, const MeshHierarchy& mesh,
+                                       const Coefficient& rho, const std::vector<LevelSpec>& plan,
+                                       const MultigridOptions& options)
+    : options_(options) {
+  if (plan.empty()) throw std::invalid_argument("SpaceTimeMultigrid: empty plan");
+  levels_.resize(plan.size());
+  for (size_t l = 0; l < plan.size(); ++l) {
+    Level& lv = levels_[l];
+    lv.spec = plan[l];
+    lv.weights = scheme == TimeScheme::DG ? dg_weights(lv.spec.k) : cgp_weights(lv.spec.k);
+    lv.op = std::make_unique<SpaceTimeOperator>(equation, lv.weights, lv.spec.tau, lv.spec.n_steps, mesh,
+                                                lv.spec.mesh_level, lv.spec.p, rho);
+    const Index n = lv.op->n_dofs();
+    lv.r.allocate(sizeof(double) * n);
+    lv.z.allocate(sizeof(double) * n);
+    lv.e.allocate(sizeof(double) * n);
+    const bool coarsest = l + 1 == plan.size();
+    if (!coarsest || levels_.size() == 1) {
+      lv.smoother = std::make_unique<ASMSmoother>(*lv.op);
+      lv.omega = estimate_relaxation(lv, options_.seed + l);
+    }
+    if (coarsest && n <= options_.direct_coarse_max) build_coarse_inverse(lv);
+  }
+  for (size_t l = 0; l + 1 < levels_.size(); ++l) {
+    levels_[l].to_coarser = std::make_unique<Transfer>(*levels_[l].op, *levels_[l + 1].op);
+    const Index nc = levels_[l + 1].op->n_dofs();
+    levels_[l].rc.allocate(sizeof(double) * nc);
+    levels_[l].ec.allocate(sizeof(double) * nc);
+  }
+}
+
+double SpaceTimeMultigrid::estimate_relaxation(const Level& lv, std::uint64_t seed) const {
+  // extremal Ritz values of P^-1 S from a short seeded Arnoldi run
+  // (multigrid.cpp:127-172), modified Gram-Schmidt in the reference order
+  const Index n = lv.op->n_dofs();
+  const int m = static_cast<int>(std::min<Index>(options_.eig_iters, n));
+  Xoshiro256pp rng(seed);
+  std::vector<double> hv(static_cast<size_t>(n));
+  double nrm2 = 0.0;
+  for (Index i = 0; i < n; ++i) {
+    hv[static_cast<size_t>(i)] = rng.normal();
+    nrm2 += hv[static_cast<size_t>(i)] * hv[static_cast<size_t>(i)];
+  }
+  if (nrm2 == 0.0) return 1.0;
+  const double inv = 1.0 / std::sqrt(nrm2);
+  for (double& x : hv) x *= inv;
+  cudaStream_t s = nullptr;
+  std::vector<DeviceBuffer> V;
+  V.emplace_back(sizeof(double) * n);
+  cuda_check(cudaMemcpy(V[0].raw(), hv.data(), sizeof(double) * n, cudaMemcpyHostToDevice), "arnoldi v0");
+  DeviceBuffer w(sizeof(double) * n), z(sizeof(double) * n), ptrs(sizeof(double*)),
+      scratch(sizeof(double) * kDotBlocks), out(sizeof(double));
+  std::vector<double> H(static_cast<size_t>((m + 1) * m), 0.0);
+  int kdim = 0;
+  for (int j = 0; j < m; ++j) {
+    lv.op->apply(V[j].d(), w.d(), s);
+    vec_fill(z.d(), 0.0, n, s);
+    lv.smoother->add_correction(w.d(), z.d(), s);
+    for (int i = 0; i <= j; ++i) {
+      const double h = host_dot(V[i].d(), z.d(), n, s, ptrs, scratch, out);
+      H[static_cast<size_t>(i * m + j)] = h;
+      vec_axpy(z.d(), -h, V[i].d(), n, s);
+    }
+    const double hn = std::sqrt(host_dot(z.d(), z.d(), n, s, ptrs, scratch, out));
+    H[static_cast<size_t>((j + 1) * m + j)] = hn;
+    kdim = j + 1;
+    if (hn < 1e-13) break;
+    V.emplace_back(sizeof(double) * n);
+    vec_scale_into(V.back().d(), 1.0 / hn, z.d(), n, s);
+  }
+  if (kdim == 0) return 1.0;
+  std::vector<double> Hk(static_cast<size_t>(kdim * kdim));
+  for (int i = 0; i < kdim; ++i)
+    for (int j = 0; j < kdim; ++j) Hk[static_cast<size_t>(i * kdim + j)] = H[static_cast<size_t>(i * m + j)];
+  std::vector<std::pair<double, double>> ev;
+  try {
+    ev = eigenvalues_small(Hk, kdim);
+  } catch (const std::exception&) {
+    return 1.0;
+  }
+  double lmax = -1e300, lmin = 1e300;
+  for (const auto& e : ev) {
+    lmax = std::max(lmax, e.first);
+    lmin = std::min(lmin, e.first);
+  }
+  lmin = std::max(0.0, lmin);
+  const double omega = 2.0 / (lmax + lmin);
+  if (!std::isfinite(omega) || omega <= 0.0) return 1.0;
+  return std::min(omega, 1.0);
+}
+
+void SpaceTimeMultigrid::build_coarse_inverse(Level& lv) {
+  // dense coarse matrix = matrix-free operator applied to the unit vectors,
+  // inverted once with cuSOLVER (multigrid.cpp:112-120 uses SparseLU)
+  const Index n = lv.op->n_dofs();
+  cudaStream_t s = nullptr;
+  DeviceBuffer Acm(sizeof(double) * n * n), e(sizeof(double) * n);
+  vec_fill(e.d(), 0.0, n, s);
+  for (Index j = 0; j < n; ++j) {
+    vec_set_element(e.d(), j, 1.0, s);
+    lv.op->apply(e.d(), Acm.d() + j * n, s);
+    vec_set_element(e.d(), j, 0.0, s);
+  }
+  lv.coarse_inv.allocate(sizeof(double) * n * n);
+  vec_fill(lv.coarse_inv.d(), 0.0, n * n, s);
+  {
+    // identity right-hand side
+    std::vector<double> eye(static_cast<size_t>(n * n), 0.0);
+    for (Index i = 0; i < n; ++i) eye[static_cast<size_t>(i * n + i)] = 1.0;
+    cuda_check(cudaMemcpy(lv.coarse_inv.raw(), eye.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice), "eye");
+  }
+  cusolverDnHandle_t h = nullptr;
+  solver_check(cusolverDnCreate(&h), "cusolverDnCreate");
+  int lwork = 0;
+  solver_check(cusolverDnDgetrf_bufferSize(h, static_cast<int>(n), static_cast<int>(n), Acm.d(), static_cast<int>(n),
+                                           &lwork),
+               "getrf_bufferSize");
+  DeviceBuffer work(sizeof(double) * std::max(lwork, 1)), piv(sizeof(int) * n), info(sizeof(int));
+  solver_check(cusolverDnDgetrf(h, static_cast<int>(n), static_cast<int>(n), Acm.d(), static_cast<int>(n), work.d(),
+                                static_cast<int*>(piv.raw()), static_cast<int*>(info.raw())),
+               "getrf");
+  int hinfo = 0;
+  cuda_check(cudaMemcpy(&hinfo, info.raw(), sizeof(int), cudaMemcpyDeviceToHost), "getrf info");
+  if (hinfo != 0) throw std::runtime_error("SpaceTimeMultigrid: coarse factorization failed");
+  // A^T X = I gives X = A^-T (column-major) = A^-1 read row-major
+  solver_check(cusolverDnDgetrs(h, CUBLAS_OP_T, static_cast<int>(n), static_cast<int>(n), Acm.d(), static_cast<int>(n),
+                                static_cast<int*>(piv.raw()), lv.coarse_inv.d(), static_cast<int>(n),
+                                static_cast<int*>(info.raw())),
+               "getrs");
+  cuda_check(cudaDeviceSynchronize(), "coarse inverse");
+  cusolverDnDestroy(h);
+}
+
+void SpaceTimeMultigrid::coarse_solve(const double* f, double* u, cudaStream_t s) const {
+  const Level& lv = levels_.back();
+  const Index n = lv.op->n_dofs();
+  if (lv.coarse_inv.raw()) {
+    dense_matvec(lv.coarse_inv.d(), f, u, static_cast<int>(n), s);
+    return;
+  }
+  GmresOptions o;
+  o.rel_tol = options_.coarse_rel_tol;
+  o.abs_tol = 0.0;
+  o.max_iters = options_.coarse_max_iters;
+  vec_fill(u, 0.0, n, s);
+  gmres([&lv](const double* x, double* y, cudaStream_t st) { lv.op->apply(x, y, st); }, f, u, n, o, DeviceMap{},
+        coarse_ws_, s);
+}
+
+void SpaceTimeMultigrid::smooth(int l, const double* f, double* u, cudaStream_t s) const {
+  const Level& lv = levels_[static_cast<size_t>(l)];
+  const Index n = lv.op->n_dofs();
+  lv.op->apply(u, lv.r.d(), s);
+  vec_sub_into(lv.r.d(), f, lv.r.d(), n, s);
+  vec_fill(lv.z.d(), 0.0, n, s);
+  lv.smoother->add_correction(lv.r.d(), lv.z.d(), s);
+  vec_axpy(u, lv.omega, lv.z.d(), n, s);
+}
+
+void SpaceTimeMultigrid::v_cycle(int l, const double* f, double* u, cudaStream_t s) const {
+  // u enters as zero (multigrid.cpp:219,231), so the first residual is f
+  const Level& lv = levels_[static_cast<size_t>(l)];
+  const Index n = lv.op->n_dofs();
+  if (l + 1 == n_levels()) {
+    coarse_solve(f, u, s);
+    return;
+  }
+  for (int i = 0; i < options_.n_smooth; ++i) {
+    if (i == 0) {
+      // S 0 = 0 exactly: u = omega * ASM(f)
+      vec_fill(lv.z.d(), 0.0, n, s);
+      lv.smoother->add_correction(f, lv.z.d(), s);
+      vec_axpy(u, lv.omega, lv.z.d(), n, s);
+    } else {
+      smooth(l, f, u, s);
+    }
+  }
+  lv.op->apply(u, lv.r.d(), s);
+  vec_sub_into(lv.r.d(), f, lv.r.d(), n, s);
+  lv.to_coarser->restrict_(lv.r.d(), lv.rc.d(), s);
+  const Index nc = levels_[static_cast<size_t>(l) + 1].op->n_dofs();
+  vec_fill(lv.ec.d(), 0.0, nc, s);
+  v_cycle(l + 1, lv.rc.d(), lv.ec.d(), s);
+  lv.to_coarser->prolong(lv.ec.d(), lv.e.d(), s);
+  vec_axpy(u, 1.0, lv.e.d(), n, s);
+  for (int i = 0; i < options_.n_smooth; ++i) smooth(l, f, u, s);
+}
+
+void SpaceTimeMultigrid::apply(const double* r, double* z, cudaStream_t s) const {
+  vec_fill(z, 0.0, fine_operator().n_dofs(), s);
+  v_cycle(0, r, z, s);
+}
+
+std::vector<LevelInfo> SpaceTimeMultigrid::level_info() const {
+  std::vector<LevelInfo> info;
+  for (size_t l = 0; l < levels_.size(); ++l) {
+    const Level& lv = levels_[l];
+    info.push_back({l == 0 ? std::string("finest") : coarsening_name(lv.spec.from_finer), lv.spec.mesh_level,
+                    lv.spec.p, lv.spec.k, lv.spec.n_steps, lv.op->n_dofs(), lv.omega});
+  }
+  return info;
+}
+
+size_t SpaceTimeMultigrid::device_bytes() const {
+  size_t b = 0;
+  for (const Level& lv : levels_) {
+    b += lv.r.bytes() + lv.z.bytes() + lv.e.bytes() + lv.rc.bytes() + lv.ec.bytes() + lv.coarse_inv.bytes();
+    if (lv.smoother) b += lv.smoother->bytes();
+  }
+  return b;
+}
+
+}  // namespace stmgb

@@ -1,0 +1,226 @@
+// Host C++ layer of the B200 STMG path. The classes mirror the reference's
+// operator / smoother / transfer / multigrid / GMRES interfaces (same names,
+// argument meaning, overwrite-vs-accumulate semantics and exceptions), but
+// operate on device-resident vectors and launch the sm_100a kernels:
+//   SpaceTimeOperator   include/stmg/space_time_operator.hpp:34-105
+//   ASMSmoother         include/stmg/asm_smoother.hpp:16-45
+//   Transfer            include/stmg/transfer.hpp:22-40
+//   SpaceTimeMultigrid  include/stmg/multigrid.hpp:61-113
+//   gmres               include/stmg/gmres.hpp:9-33
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "kernels.hpp"
+#include "setup.hpp"
+
+namespace stmgb {
+
+void cuda_check(cudaError_t e, const char* what);
+
+// owning device buffer of doubles (or raw bytes)
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t bytes);
+  ~DeviceBuffer();
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept;
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
+  void allocate(size_t bytes);
+  void release();
+  double* d() const { return static_cast<double*>(p_); }
+  void* raw() const { return p_; }
+  size_t bytes() const { return bytes_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+// cell-wise positive coefficient: rho(cell) = coarse_cell_scale[ancestor on
+// mesh level 0] (include/stmg/mesh.hpp:76-83 with base == 1)
+struct Coefficient {
+  std::vector<double> coarse_cell_scale;  // empty = 1
+};
+
+class SpaceTimeOperator {
+ public:
+  SpaceTimeOperator(Equation equation, const TemporalWeights& weights, double tau, int n_steps,
+                    const MeshHierarchy& mesh, int mesh_level, int p, const Coefficient& rho);
+
+  Equation equation() const { return equation_; }
+  const TemporalWeights& weights() const { return weights_; }
+  double tau() const { return tau_; }
+  int n_steps() const { return n_steps_; }
+  int n_t() const { return weights_.n_t; }
+  int p() const { return p_; }
+  int dim() const { return desc_.dim; }
+  int mesh_level() const { return mesh_level_; }
+  Index n_space() const { return desc_.n_space; }
+  Index n_dofs() const { return desc_.n_dofs; }
+  Index block_offset(int step, int node) const { return (static_cast<Index>(step) * weights_.n_t + node) * n_space(); }
+  const DevLevel& desc() const { return desc_; }
+  const MeshLevel& mesh() const { return *mesh_level_ptr_; }
+
+  // y = S u (overwrite), device pointers (space_time_operator.cpp:45-130)
+  void apply(const double* u, double* y, cudaStream_t stream = nullptr) const;
+  // SpatialOperator::apply of the constrained mass (kind 0) or stiffness (1)
+  void spatial_apply(int kind, const double* u, double* y, cudaStream_t stream = nullptr) const;
+  long applications() const { return apply_count_; }
+
+ private:
+  Equation equation_;
+  TemporalWeights weights_;
+  double tau_;
+  int n_steps_;
+  int mesh_level_;
+  int p_;
+  const MeshLevel* mesh_level_ptr_;
+  DevLevel desc_{};
+  DevLevel mass_desc_{}, stiff_desc_{};
+  DeviceBuffer verts_, rho0_;
+  mutable long apply_count_ = 0;
+};
+
+class ASMSmoother {
+ public:
+  explicit ASMSmoother(const SpaceTimeOperator& op);
+  // correction += W sum_T R_T^T B_T^-1 R_T residual (accumulate; the
+  // relaxation factor is applied by the caller) -- asm_smoother.cpp:60-78
+  void add_correction(const double* residual, double* correction, cudaStream_t stream = nullptr) const;
+  int block_size() const { return op_->n_t() * asm_.m; }
+  Index n_blocks() const { return static_cast<Index>(op_->n_steps()) * op_->mesh().n_cells(); }
+  long sweeps() const { return sweep_count_; }
+  size_t bytes() const { return X_.bytes() + lam_.bytes(); }
+
+ private:
+  const SpaceTimeOperator* op_;
+  DevASM asm_{};
+  DeviceBuffer X_, lam_;
+  mutable long sweep_count_ = 0;
+};
+
+class Transfer {
+ public:
+  Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coarse);
+  void prolong(const double* coarse, double* fine, cudaStream_t stream = nullptr) const;    // overwrite
+  void restrict_(const double* fine, double* coarse, cudaStream_t stream = nullptr) const;  // overwrite
+  bool spatial() const { return spatial_; }
+
+ private:
+  const SpaceTimeOperator* fine_;
+  const SpaceTimeOperator* coarse_;
+  bool spatial_ = true;
+  DevAxisTransfer ax_[3]{};
+  std::vector<DeviceBuffer> bufs_;
+  DeviceBuffer time_p_;
+  int Ff_ = 0, Fc_ = 0;
+};
+
+struct MultigridOptions {
+  int n_smooth = 1;
+  Index direct_coarse_max = 20000;
+  double coarse_rel_tol = 1e-3;
+  int coarse_max_iters = 2000;
+  int eig_iters = 20;
+  std::uint64_t seed = 42;
+};
+
+struct LevelInfo {
+  std::string coarsening;
+  int mesh_level, p, k, n_steps;
+  Index n_dofs;
+  double omega;
+};
+
+struct GmresOptions {
+  int max_iters = 1000;
+  int restart = 100;
+  double rel_tol = 1e-12;
+  double abs_tol = 1e-12;
+};
+struct GmresResult {
+  bool converged = false;
+  int iterations = 0;
+  double initial_residual = 0.0;
+  double final_residual = 0.0;
+  std::vector<double> residual_history;
+};
+// device-vector linear map y = A x (overwrite)
+using DeviceMap = std::function<void(const double*, double*, cudaStream_t)>;
+
+// Krylov workspace reused across solves (basis vectors allocated lazily)
+class GmresWorkspace {
+ public:
+  void ensure(Index n, int vectors);
+  double* vec(int i) const { return basis_[static_cast<size_t>(i)].d(); }
+  const double* const* dev_ptrs() const { return static_cast<const double* const*>(ptrs_.raw()); }
+  double* scratch() const { return scratch_.d(); }
+  double* small() const { return small_.d(); }
+  double* r() const { return r_.d(); }
+  double* w() const { return w_.d(); }
+  double* z() const { return z_.d(); }
+  Index n() const { return n_; }
+
+ private:
+  Index n_ = 0;
+  std::vector<DeviceBuffer> basis_;
+  DeviceBuffer ptrs_, scratch_, small_, r_, w_, z_;
+};
+
+// Restarted right-preconditioned GMRES (gmres.cpp:8-115) on device vectors.
+GmresResult gmres(const DeviceMap& op, const double* b, double* x, Index n, const GmresOptions& options,
+                  const DeviceMap& precond, GmresWorkspace& ws, cudaStream_t stream = nullptr);
+
+class SpaceTimeMultigrid {
+ public:
+  SpaceTimeMultigrid(Equation equation, TimeScheme scheme, const MeshHierarchy& mesh, const Coefficient& rho,
+                     const std::vector<LevelSpec>& plan, const MultigridOptions& options = {});
+  int n_levels() const { return static_cast<int>(levels_.size()); }
+  const SpaceTimeOperator& fine_operator() const { return *levels_[0].op; }
+  const SpaceTimeOperator& operator_at(int l) const { return *levels_[l].op; }
+  const ASMSmoother& smoother_at(int l) const { return *levels_[l].smoother; }
+  const Transfer& transfer_at(int l) const { return *levels_[l].to_coarser; }
+  double omega_at(int l) const { return levels_[l].omega; }
+  void set_omega(int l, double w) { levels_[l].omega = w; }
+  std::vector<LevelInfo> level_info() const;
+  // one V-cycle from the finest level, zero initial guess (overwrite z)
+  void apply(const double* r, double* z, cudaStream_t stream = nullptr) const;
+  void v_cycle(int l, const double* f, double* u, cudaStream_t stream) const;
+  void smooth(int l, const double* f, double* u, cudaStream_t stream) const;
+  size_t device_bytes() const;
+
+ private:
+  struct Level {
+    LevelSpec spec;
+    TemporalWeights weights;
+    std::unique_ptr<SpaceTimeOperator> op;
+    std::unique_ptr<ASMSmoother> smoother;
+    std::unique_ptr<Transfer> to_coarser;
+    double omega = 1.0;
+    DeviceBuffer coarse_inv;  // dense inverse of the coarsest operator
+    mutable DeviceBuffer r, z, rc, ec, e;  // work vectors
+  };
+  double estimate_relaxation(const Level& lv, std::uint64_t seed) const;
+  void coarse_solve(const double* f, double* u, cudaStream_t stream) const;
+  void build_coarse_inverse(Level& lv);
+
+  MultigridOptions options_;
+  std::vector<Level> levels_;
+  mutable GmresWorkspace coarse_ws_;
+};
+
+// eigenvalues (real, imag) of a small dense real matrix (row-major n x n):
+// Hessenberg reduction + shifted QR, as needed for the Ritz values of the
+// relaxation estimate (multigrid.cpp:156-171)
+std::vector<std::pair<double, double>> eigenvalues_small(std::vector<double> a, int n);
+
+}  // namespace stmgb

@@ -1,0 +1,193 @@
+// Krylov vector kernels for the device-resident GMRES (reference: the dot,
+// norm and axpy loops of gmres.cpp:40-99 and multigrid.cpp:174-185). The
+// Gram-Schmidt step is fused: one pass over the basis produces all k dot
+// products (classical Gram-Schmidt, applied twice), and one pass applies all
+// k updates, instead of the reference's 2k dot + 2k axpy passes (MGS x2).
+// Reductions use a fixed grid and a fixed-order second stage, so results are
+// bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.hpp"
+
+namespace stmgb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(long long n) {
+  const long long b = (n + kThreads * 4 - 1) / (kThreads * 4);
+  return static_cast<unsigned>(std::max<long long>(1, std::min<long long>(b, 148LL * 32)));
+}
+
+__global__ void copy_kernel(double* __restrict__ y, const double* __restrict__ x, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+__global__ void axpy_kernel(double* __restrict__ y, double a, const double* __restrict__ x, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+__global__ void axpby_kernel(double* __restrict__ y, double a, const double* __restrict__ x, double b, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x[i] + b * y[i];
+}
+__global__ void scale_into_kernel(double* __restrict__ y, double a, const double* __restrict__ x, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x[i];
+}
+__global__ void sub_into_kernel(double* __restrict__ r, const double* __restrict__ f, const double* __restrict__ y,
+                                long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    r[i] = f[i] - y[i];
+}
+
+// partial dots of up to 8 basis vectors per launch group
+template <int G>
+__global__ void multidot_partial_kernel(const double* const* __restrict__ V, int i0, int k,
+                                        const double* __restrict__ w, long long n, double* __restrict__ partial) {
+  double acc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g] = 0.0;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const double wj = w[j];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (i0 + g < k) acc[g] = fma(V[i0 + g][j], wj, acc[g]);
+  }
+  __shared__ double red[G][kThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    double v = acc[g];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[g][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < G && i0 + threadIdx.x < k) {
+    double s = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) s += red[threadIdx.x][i];
+    partial[static_cast<long long>(i0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int nblocks, int k, double* __restrict__ out) {
+  // one warp per output, fixed order
+  const int i = blockIdx.x;
+  if (i >= k) return;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += 32) s += partial[static_cast<long long>(i) * nblocks + b];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) out[i] = s;
+}
+
+__global__ void multi_axpy_kernel(double* __restrict__ w, const double* const* __restrict__ V, int k,
+                                  const double* __restrict__ h, double sign, long long n) {
+  extern __shared__ double hs[];
+  const double** vp = reinterpret_cast<const double**>(hs + k);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    hs[i] = h[i];
+    vp[i] = V[i];
+  }
+  __syncthreads();
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < k; ++i) s = fma(hs[i], vp[i][j], s);
+    w[j] = fma(sign, s, w[j]);
+  }
+}
+
+__global__ void dense_matvec_kernel(const double* __restrict__ A, const double* __restrict__ x, double* __restrict__ y,
+                                    int n) {
+  // one warp per row
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s = fma(A[static_cast<long long>(row) * n + j], x[j], s);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] = s;
+}
+
+__global__ void fill_kernel(double* __restrict__ y, double v, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = v;
+}
+__global__ void set_element_kernel(double* y, long long i, double v) { y[i] = v; }
+__global__ void colour_kernel(double* __restrict__ y, long long dx, long long dy, long long dz, int dim, int period,
+                              int cx, int cy, int cz) {
+  const long long n = dx * dy * dz;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
+    const long long ix = g % dx, iy = (g / dx) % dy, iz = g / (dx * dy);
+    bool hit = ix % period == cx;
+    if (dim > 1) hit = hit && (iy % period == cy);
+    if (dim > 2) hit = hit && (iz % period == cz);
+    y[g] = hit ? 1.0 : 0.0;
+  }
+}
+
+}  // namespace
+
+void vec_fill(double* y, double v, long long n, cudaStream_t s) { count_launch(); fill_kernel<<<grid_for(n), kThreads, 0, s>>>(y, v, n); }
+void vec_set_element(double* y, long long i, double v, cudaStream_t s) { count_launch(); set_element_kernel<<<1, 1, 0, s>>>(y, i, v); }
+void vec_colour_indicator(double* y, const long long* dofs, int dim, int period, int cx, int cy, int cz,
+                          cudaStream_t s) {
+  const long long n = dofs[0] * dofs[1] * dofs[2];
+  count_launch();
+  colour_kernel<<<grid_for(n), kThreads, 0, s>>>(y, dofs[0], dofs[1], dofs[2], dim, period, cx, cy, cz);
+}
+
+void vec_copy(double* y, const double* x, long long n, cudaStream_t s) {
+  count_launch();
+  copy_kernel<<<grid_for(n), kThreads, 0, s>>>(y, x, n);
+}
+void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s) {
+  count_launch();
+  axpy_kernel<<<grid_for(n), kThreads, 0, s>>>(y, a, x, n);
+}
+void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t s) {
+  count_launch();
+  axpby_kernel<<<grid_for(n), kThreads, 0, s>>>(y, a, x, b, n);
+}
+void vec_scale_into(double* y, double a, const double* x, long long n, cudaStream_t s) {
+  count_launch();
+  scale_into_kernel<<<grid_for(n), kThreads, 0, s>>>(y, a, x, n);
+}
+void vec_sub_into(double* r, const double* f, const double* y, long long n, cudaStream_t s) {
+  count_launch();
+  sub_into_kernel<<<grid_for(n), kThreads, 0, s>>>(r, f, y, n);
+}
+void vec_multidot(const double* const* V, int k, const double* w, long long n, double* out, double* scratch,
+                  cudaStream_t s) {
+  constexpr int G = 8;
+  for (int i0 = 0; i0 < k; i0 += G) {
+    count_launch();
+    multidot_partial_kernel<G><<<kDotBlocks, kThreads, 0, s>>>(V, i0, k, w, n, scratch);
+  }
+  count_launch();
+  reduce_partials_kernel<<<k, 32, 0, s>>>(scratch, kDotBlocks, k, out);
+}
+void vec_multi_axpy(double* w, const double* const* V, int k, const double* h, double sign, long long n,
+                    cudaStream_t s) {
+  const size_t smem = (sizeof(double) + sizeof(double*)) * std::max(k, 1);
+  count_launch();
+  multi_axpy_kernel<<<grid_for(n), kThreads, smem, s>>>(w, V, k, h, sign, n);
+}
+void dense_matvec(const double* A, const double* x, double* y, int n, cudaStream_t s) {
+  const int rows_per_block = kThreads / 32;
+  count_launch();
+  dense_matvec_kernel<<<(n + rows_per_block - 1) / rows_per_block, kThreads, 0, s>>>(A, x, y, n);
+}
+
+}  // namespace stmgb
+
+#include <atomic>
+namespace stmgb {
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long kernel_launches() { return g_launches.load(); }
+}  // namespace stmgb

@@ -1,0 +1,119 @@
+"""ctypes binding of the C ABI in include/stmg_b200.h (libstmg_b200.so, built
+in-tree by paper_2408_04372_b200/csrc/Makefile). Loading fails loudly when the
+extension is missing: there is no CPU fallback on the product path."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstmg_b200.so")
+
+c_double_p = C.POINTER(C.c_double)
+c_int_p = C.POINTER(C.c_int)
+c_ll_p = C.POINTER(C.c_longlong)
+
+
+class MgOptions(C.Structure):
+    _fields_ = [("n_smooth", C.c_int), ("direct_coarse_max", C.c_longlong), ("coarse_rel_tol", C.c_double),
+                ("coarse_max_iters", C.c_int), ("eig_iters", C.c_int), ("seed", C.c_ulonglong)]
+
+
+class GmresOptions(C.Structure):
+    _fields_ = [("max_iters", C.c_int), ("restart", C.c_int), ("rel_tol", C.c_double), ("abs_tol", C.c_double)]
+
+
+class GmresResult(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("initial_residual", C.c_double),
+                ("final_residual", C.c_double), ("history_len", C.c_int)]
+
+
+LINEAR_MAP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+# (name, restype, argtypes): every symbol declared in include/stmg_b200.h
+SIGNATURES = [
+    ("stmg_last_error", C.c_char_p, []),
+    ("stmg_version", C.c_char_p, []),
+    ("stmg_kernel_launches", C.c_longlong, []),
+    ("stmg_quadrature", C.c_int, [C.c_int, C.c_int, c_double_p, c_double_p]),
+    ("stmg_temporal_weights", C.c_int, [C.c_int, C.c_int, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
+    ("stmg_block_coefficients", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, c_double_p, c_double_p]),
+    ("stmg_mesh_create", C.c_int, [C.c_int, c_double_p, c_double_p, C.c_longlong, C.c_int, c_double_p,
+                                   C.c_void_p]),
+    ("stmg_mesh_destroy", None, [C.c_void_p]),
+    ("stmg_st_operator_create", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                          C.c_int, c_double_p, C.c_void_p]),
+    ("stmg_st_operator_destroy", None, [C.c_void_p]),
+    ("stmg_st_operator_n_dofs", C.c_longlong, [C.c_void_p]),
+    ("stmg_st_operator_n_space", C.c_longlong, [C.c_void_p]),
+    ("stmg_st_operator_n_t", C.c_int, [C.c_void_p]),
+    ("stmg_st_operator_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_st_operator_apply_host", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("stmg_spatial_apply", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_asm_create", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("stmg_asm_destroy", None, [C.c_void_p]),
+    ("stmg_asm_add_correction", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_transfer_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_transfer_destroy", None, [C.c_void_p]),
+    ("stmg_transfer_prolong", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_transfer_restrict", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_mg_options_default", None, [C.POINTER(MgOptions)]),
+    ("stmg_multigrid_create", C.c_int, [C.c_int, C.c_int, C.c_void_p, c_double_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_double, C.c_int, c_int_p, C.POINTER(MgOptions), C.c_void_p]),
+    ("stmg_multigrid_destroy", None, [C.c_void_p]),
+    ("stmg_multigrid_n_levels", C.c_int, [C.c_void_p]),
+    ("stmg_multigrid_level_info", C.c_int, [C.c_void_p, C.c_int, c_int_p, c_ll_p, c_double_p]),
+    ("stmg_multigrid_set_omega", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
+    ("stmg_multigrid_operator_at", C.c_void_p, [C.c_void_p, C.c_int]),
+    ("stmg_multigrid_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_multigrid_apply_host", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("stmg_multigrid_smooth", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_multigrid_asm_add_correction", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_multigrid_prolong", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_multigrid_restrict", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_multigrid_device_bytes", C.c_longlong, [C.c_void_p]),
+    ("stmg_gmres_options_default", None, [C.POINTER(GmresOptions)]),
+    ("stmg_gmres", C.c_int, [C.c_longlong, LINEAR_MAP, C.c_void_p, LINEAR_MAP, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.POINTER(GmresOptions), C.POINTER(GmresResult), c_double_p, C.c_int, C.c_void_p]),
+    ("stmg_solve", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(GmresOptions),
+                             C.POINTER(GmresResult), c_double_p, C.c_int, C.c_void_p]),
+    ("stmg_solve_host", C.c_int, [C.c_void_p, C.c_int, c_double_p, c_double_p, C.POINTER(GmresOptions),
+                                  C.POINTER(GmresResult), c_double_p, C.c_int]),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load the sm_100a extension; raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"stmg-b200: CUDA extension missing at {LIB_PATH}; run __graft_entry__.build()")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class StmgError(RuntimeError):
+    pass
+
+
+class StmgInvalidArgument(StmgError, ValueError):
+    pass
+
+
+def check(rc: int) -> None:
+    """Rethrow a C-ABI status as the reference's exception kind
+    (invalid_argument -> ValueError subclass, runtime_error -> RuntimeError)."""
+    if rc == 0:
+        return
+    msg = load().stmg_last_error().decode()
+    if rc == -1:
+        raise StmgInvalidArgument(msg)
+    raise StmgError(msg)

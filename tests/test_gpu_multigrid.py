@@ -1,0 +1,133 @@
+"""GPU parity of the smoother, transfers, V-cycle and GMRES against the
+reference oracle (asm_smoother.cpp:60-78, transfer.cpp:118-190,
+multigrid.cpp:127-234, gmres.cpp:8-115). Tolerances are written per test; the
+north_star gates are GMRES iterations within +-1 and final solution relative
+difference <= 1e-8."""
+import numpy as np
+import pytest
+
+from paper_2408_04372_b200 import api, problems
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _build(cfg, ref, strategy=None, **mg):
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
+    M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps,
+                               cfg.tau, strategy, **mg)
+    R = ref.Reference(cfg, with_mg=True, strategy=strategy, **{k: v for k, v in mg.items() if k == "n_smooth"})
+    return mesh, M, R
+
+
+def _dev(cuda, a):
+    return cuda.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+MG_CASES = [("C1", None), ("C2", 1), ("C2", 2), ("C3", 0), ("C3", 1)]
+
+
+@pytest.mark.parametrize("name,r", MG_CASES)
+def test_level_plan_matches_reference(cuda, ref, name, r):
+    cfg = problems.config(name, r)
+    mesh, M, R = _build(cfg, ref)
+    got, want = M.level_info(), R.level_info()
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert (g["mesh_level"], g["p"], g["k"], g["n_steps"], g["n_dofs"]) == \
+               (w["mesh_level"], w["p"], w["k"], w["n_steps"], w["n_dofs"])
+
+
+@pytest.mark.parametrize("name,r", MG_CASES)
+def test_transfers_match_reference(cuda, ref, name, r):
+    cfg = problems.config(name, r)
+    mesh, M, R = _build(cfg, ref)
+    info = R.level_info()
+    for l in range(M.n_levels - 1):
+        nf, nc = info[l]["n_dofs"], info[l + 1]["n_dofs"]
+        c = problems.uniform_vector(nc, seed=100 + l)
+        f = problems.uniform_vector(nf, seed=200 + l)
+        pf = M.prolong(l, _dev(cuda, c)).cpu().numpy()
+        rc = M.restrict_(l, _dev(cuda, f)).cpu().numpy()
+        assert _rel(pf, R.prolong(l, c, nf)) <= 1e-13, f"prolong level {l}"
+        assert _rel(rc, R.restrict_(l, f, nc)) <= 1e-13, f"restrict level {l}"
+
+
+@pytest.mark.parametrize("name,r", MG_CASES)
+def test_asm_correction_matches_reference(cuda, ref, name, r):
+    """Exact fast-diagonalised cell blocks vs the reference's LU of the
+    assembled blocks: equal to solver rounding (tolerance 1e-9 relative)."""
+    cfg = problems.config(name, r)
+    mesh, M, R = _build(cfg, ref)
+    info = R.level_info()
+    for l in range(max(1, M.n_levels - 1)):
+        n = info[l]["n_dofs"]
+        res = problems.uniform_vector(n, seed=300 + l)
+        z0 = problems.uniform_vector(n, seed=400 + l)
+        got = M.asm_add_correction(l, _dev(cuda, res), _dev(cuda, z0)).cpu().numpy()
+        want = R.asm_add_correction(l, res, z0)
+        assert _rel(got - z0, want - z0) <= 1e-9, f"asm level {l}"
+
+
+@pytest.mark.parametrize("name,r", MG_CASES)
+def test_relaxation_factor_matches_reference(cuda, ref, name, r):
+    cfg = problems.config(name, r)
+    mesh, M, R = _build(cfg, ref)
+    for g, w in zip(M.level_info(), R.level_info()):
+        assert abs(g["omega"] - w["omega"]) <= 1e-6 * w["omega"]
+
+
+@pytest.mark.parametrize("name,r", MG_CASES)
+def test_vcycle_matches_reference(cuda, ref, name, r):
+    cfg = problems.config(name, r)
+    mesh, M, R = _build(cfg, ref)
+    # use the reference's omegas so the comparison isolates the cycle itself
+    for l, w in enumerate(R.level_info()):
+        M.set_omega(l, w["omega"])
+    res = problems.uniform_vector(R.n_dofs, seed=9)
+    got = M.apply(_dev(cuda, res)).cpu().numpy()
+    assert _rel(got, R.vcycle(res)) <= 1e-9
+
+
+@pytest.mark.parametrize("name,r", [("C1", None), ("C2", 1), ("C2", 2), ("C3", 1)])
+def test_gmres_solve_matches_reference(cuda, ref, name, r):
+    """STMG-preconditioned GMRES on the manufactured slab RHS: iteration
+    count within +-1 and solution relative difference <= 1e-8."""
+    cfg = problems.config(name, r)
+    mesh, M, R = _build(cfg, ref)
+    b = R.assemble_rhs(1, 0.5, 0.0)
+    x_ref, info_ref = R.gmres(b, rel_tol=1e-10, abs_tol=0.0)
+    x = cuda.zeros(R.n_dofs, dtype=cuda.float64, device="cuda")
+    info = M.solve(_dev(cuda, b), x, rel_tol=1e-10, abs_tol=0.0)
+    assert info["converged"] and info_ref["converged"]
+    assert abs(info["iterations"] - info_ref["iterations"]) <= 1
+    assert _rel(x.cpu().numpy(), x_ref) <= 1e-8
+
+
+def test_gmres_generic_callbacks(cuda):
+    """stmg_gmres with Python LinearMap callbacks on a diagonal system."""
+    n = 1000
+    d = cuda.linspace(1.0, 10.0, n, dtype=cuda.float64, device="cuda")
+    b = cuda.ones(n, dtype=cuda.float64, device="cuda")
+    x = cuda.zeros(n, dtype=cuda.float64, device="cuda")
+
+    def op(xin, yout):
+        yout.copy_(d * xin)
+
+    info = api.gmres(op, b, x, rel_tol=1e-12, abs_tol=0.0)
+    assert info["converged"]
+    assert float(((d * x - b).norm() / b.norm())) <= 1e-11
+
+
+def test_host_buffer_solve(cuda, ref):
+    cfg = problems.config("C1")
+    mesh, M, R = _build(cfg, ref)
+    b = R.assemble_rhs(1, 0.5, 0.0)
+    x = np.zeros(R.n_dofs)
+    info = M.solve_host(b, x, rel_tol=1e-10, abs_tol=0.0)
+    x_ref, info_ref = R.gmres(b, rel_tol=1e-10, abs_tol=0.0)
+    assert abs(info["iterations"] - info_ref["iterations"]) <= 1
+    assert _rel(x, x_ref) <= 1e-8

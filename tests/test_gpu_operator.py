@@ -1,0 +1,109 @@
+"""GPU parity of the fused space-time operator (SpaceTimeOperator::apply,
+space_time_operator.cpp:45-130) against the reference oracle, through the C
+ABI. Tolerance (north_star): relative L2 difference <= 1e-12."""
+import numpy as np
+import pytest
+
+from paper_2408_04372_b200 import api, problems
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _pair(cfg, ref):
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
+    op = api.SpaceTimeOperator(mesh, cfg.refinements, cfg.p, cfg.equation, cfg.scheme, cfg.k, cfg.tau, cfg.n_steps,
+                               cfg.rho)
+    R = ref.Reference(cfg)
+    assert op.n_dofs == R.n_dofs == cfg.n_dofs
+    return mesh, op, R
+
+
+@pytest.mark.parametrize("name,r", [("C1", None), ("C2", 2), ("C3", 1), ("C4", 0), ("C5-8", None)])
+def test_config_vmult_parity(cuda, ref, name, r):
+    cfg = problems.config(name, r)
+    mesh, op, R = _pair(cfg, ref)
+    u = problems.uniform_vector(op.n_dofs, seed=42)
+    y = op.apply(cuda.from_numpy(u).cuda()).cpu().numpy()
+    want = R.apply(u)
+    assert _rel(y, want) <= TOL
+
+
+CASES = []
+for dim in (2, 3):
+    for p in (1, 2, 3, 4):
+        for eq in (0, 1):
+            for scheme, k in ((0, 0), (0, 1), (0, 2), (1, 1), (1, 2)):
+                for S in (1, 2, 3):
+                    nt = k + 1 if scheme == 0 else k
+                    if S * nt > 8 or (dim == 3 and p == 4 and S > 1):
+                        continue
+                    CASES.append((dim, p, eq, scheme, k, S))
+
+
+@pytest.mark.parametrize("dim,p,eq,scheme,k,S", CASES[::3])
+@pytest.mark.parametrize("geom", ["cartesian", "perturbed+rho"])
+def test_vmult_parity_sweep(cuda, ref, dim, p, eq, scheme, k, S, geom):
+    base, refine = (2, 1) if dim == 3 else (3, 1)
+    cfg = problems.Config("sweep", eq, scheme, dim, base, refine, p, k, S, 0.3)
+    if geom != "cartesian":
+        cfg.perturb = 0.15
+        rng = np.random.default_rng(7)
+        cfg.rho = rng.uniform(0.5, 3.0, base ** dim)
+    mesh, op, R = _pair(cfg, ref)
+    u = problems.uniform_vector(op.n_dofs, seed=3)
+    y = op.apply(cuda.from_numpy(u).cuda()).cpu().numpy()
+    assert _rel(y, R.apply(u)) <= TOL
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_spatial_operator_parity(cuda, ref, kind):
+    cfg = problems.config("C2", 2)
+    cfg.rho = np.array([2.5])
+    mesh, op, R = _pair(cfg, ref)
+    u = problems.uniform_vector(op.n_space, seed=11)
+    y = op.spatial_apply(kind, cuda.from_numpy(u).cuda()).cpu().numpy()
+    assert _rel(y, R.spatial_apply(kind, u)) <= TOL
+
+
+def test_host_buffer_apply_and_linearity(cuda, ref):
+    cfg = problems.config("C2", 2)
+    mesh, op, R = _pair(cfg, ref)
+    u = problems.uniform_vector(op.n_dofs, seed=5)
+    v = problems.uniform_vector(op.n_dofs, seed=6)
+    yu = op.apply_host(u)
+    assert _rel(yu, R.apply(u)) <= TOL
+    yuv = op.apply_host(2.0 * u - 3.0 * v)
+    assert _rel(yuv, 2.0 * yu - 3.0 * op.apply_host(v)) <= 1e-13
+
+
+def test_size_mismatch_raises(cuda):
+    cfg = problems.config("C1", 1)
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements)
+    op = api.SpaceTimeOperator(mesh, cfg.refinements, cfg.p, cfg.equation, cfg.scheme, cfg.k, cfg.tau, cfg.n_steps)
+    with pytest.raises(ValueError):
+        op.apply(cuda.zeros(op.n_dofs + 1, dtype=cuda.float64, device="cuda"))
+
+
+def test_full_size_c2_properties(cuda):
+    """C2 at full size (21.6M ST dofs): identity on Dirichlet rows, linearity
+    and determinism-to-rounding across two applications."""
+    cfg = problems.config("C2")
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
+    op = api.SpaceTimeOperator(mesh, cfg.refinements, cfg.p, cfg.equation, cfg.scheme, cfg.k, cfg.tau, cfg.n_steps)
+    g = cuda.Generator(device="cuda").manual_seed(1)
+    u = cuda.rand(op.n_dofs, dtype=cuda.float64, device="cuda", generator=g) * 2 - 1
+    y1 = op.apply(u)
+    y2 = op.apply(u)
+    assert float((y1 - y2).norm() / y1.norm()) <= 1e-14
+    d = cfg.cells * cfg.p + 1
+    yv = y1.view(-1, d, d, d)
+    uv = u.view(-1, d, d, d)
+    assert cuda.equal(yv[:, 0], uv[:, 0]) and cuda.equal(yv[:, :, :, -1], uv[:, :, :, -1])
+    y3 = op.apply(2.0 * u)
+    assert float((y3 - 2.0 * y1).norm() / y1.norm()) <= 1e-14

@@ -174,6 +174,7 @@ def run_ours(args):
                                cfg.tau)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
+    print(f"[bench] setup {setup_s:.1f}s, levels {M.level_info()}", file=sys.stderr, flush=True)
     op = M.operator_at(0)
     N = op.n_dofs
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)

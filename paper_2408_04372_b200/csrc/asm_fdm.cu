@@ -1,0 +1,270 @@
+// Tensor-product fast-diagonalisation (FDM) cell solves for the space-time
+// additive Schwarz smoother on Cartesian levels (reference: ASMSmoother,
+// asm_smoother.cpp:7-78, which LU-factors every (step, cell) block).
+//
+// On a Cartesian cell whose neighbourhood has one coefficient value rho, the
+// restricted global matrices are Kronecker products of restricted 1D
+// matrices, M_T = M_z (x) M_y (x) M_x and
+// A_T = rho (K_z(x)M_y(x)M_x + M_z(x)K_y(x)M_x + M_z(x)M_y(x)K_x), so with the
+// 1D generalised eigenpairs K_a S_a = M_a S_a Lambda_a (S_a^T M_a S_a = I),
+//   B_T^-1 = (I(x)S)(T_M(x)I + T_A(x)rho(Lz(+)Ly(+)Lx))^-1 (I(x)S^T),
+//   S = S_z (x) S_y (x) S_x,
+// i.e. d sum-factorised sweeps each way and one n_t x n_t solve per
+// eigen-index; no per-cell data is stored. The 1D tables depend only on the
+// cell's position class along each axis (interior / first / last / single,
+// Dirichlet nodes removed). Cells flagged in `skip` are solved exactly by the
+// per-cell eigenbasis kernel instead (asm_smoother.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "kernels.hpp"
+
+namespace stmgb {
+
+namespace {
+
+constexpr int kT = 256;
+
+template <int DIM, int N>
+struct FCfg {
+  static constexpr int ND = DIM == 2 ? N * N : N * N * N;
+  static constexpr int LINES = DIM == 2 ? N : N * N;
+  static constexpr int NC = (kT / ND) > 0 ? (kT / ND) : 1;
+};
+
+__device__ __forceinline__ void solve_small(const double* TM, const double* TA, double lam, int nt, double* b) {
+  double a[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[i][j] = (i < nt && j < nt) ? fma(lam, TA[i * nt + j], TM[i * nt + j]) : (i == j);
+  // Gaussian elimination with partial pivoting, fully unrolled (no local memory)
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i) {
+      if (fabs(a[i][k]) > fabs(a[k][k])) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double t = a[k][j];
+          a[k][j] = a[i][j];
+          a[i][j] = t;
+        }
+        const double t = b[k];
+        b[k] = b[i];
+        b[i] = t;
+      }
+    }
+    const double inv = 1.0 / a[k][k];
+#pragma unroll
+    for (int i = k + 1; i < 4; ++i) {
+      const double f = a[i][k] * inv;
+#pragma unroll
+      for (int j = k; j < 4; ++j) a[i][j] = fma(-f, a[k][j], a[i][j]);
+      b[i] = fma(-f, b[k], b[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 3; i >= 0; --i) {
+    double s = b[i];
+#pragma unroll
+    for (int j = i + 1; j < 4; ++j) s = fma(-a[i][j], b[j], s);
+    b[i] = s / a[i][i];
+  }
+}
+
+template <int N, bool TRANS>
+__device__ __forceinline__ void sweep(double* arr, int base, int stride, const double (&S)[kMaxN][kMaxN]) {
+  double in[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) in[k] = arr[base + k * stride];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) s = fma(TRANS ? S[k][i] : S[i][k], in[k], s);
+    arr[base + i * stride] = s;
+  }
+}
+
+template <int N, int A>
+__device__ __forceinline__ int lbase(int line) {
+  constexpr int st = A == 0 ? 1 : (A == 1 ? N : N * N);
+  return (line % st) + (line / st) * st * N;
+}
+
+template <int DIM, int N, int NT>
+__global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ DevFDM P, const double* __restrict__ r,
+                                                      double* __restrict__ z) {
+  using C = FCfg<DIM, N>;
+  constexpr int ND = C::ND, LINES = C::LINES, NC = C::NC;
+  extern __shared__ __align__(16) double sm[];
+  double* W = sm;                    // [NC][NT][ND] working
+  double* R = W + NC * NT * ND;      // [NC][NT][ND] residual (Dirichlet rows)
+  double* rho_s = R + NC * NT * ND;  // [NC]
+  long long* base_s = reinterpret_cast<long long*>(rho_s + NC);
+  int* info_s = reinterpret_cast<int*>(base_s + NC);  // mask | type_x<<8 | type_y<<10 | type_z<<12
+  const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
+  const long long cell0 = static_cast<long long>(blockIdx.x) * NC;
+  const int tid = threadIdx.x;
+  const long long dx = P.dofs[0], dxy = P.dofs[0] * P.dofs[1];
+  const int p = N - 1;
+  if (tid < NC) {
+    const long long cell = cell0 + tid;
+    long long base = -1;
+    int info = 0;
+    if (cell < n_cells && !(P.skip && P.skip[cell])) {
+      const unsigned ci = static_cast<unsigned>(cell);
+      const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]),
+                     nz = static_cast<unsigned>(P.cells[2]);
+      const unsigned cx = ci % nx, cy = (ci / nx) % ny, cz = ci / (nx * ny);
+      base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx + static_cast<long long>(cx) * p;
+      const int tx = (cx == 0 ? 1 : 0) | (cx == nx - 1 ? 2 : 0);
+      const int ty = (cy == 0 ? 1 : 0) | (cy == ny - 1 ? 2 : 0);
+      const int tz = DIM == 3 ? ((cz == 0 ? 1 : 0) | (cz == nz - 1 ? 2 : 0)) : 0;
+      info = tx | (ty << 2) | (tz << 4) | (tx << 8) | (ty << 10) | (tz << 12);
+      double rho = 1.0;
+      if (P.rho0) {
+        const long long ax = cx >> P.rho_shift, ay = cy >> P.rho_shift, az = cz >> P.rho_shift;
+        rho = P.rho0[(az * P.cells0[1] + ay) * P.cells0[0] + ax];
+      }
+      rho_s[tid] = rho;
+    }
+    base_s[tid] = base;
+    info_s[tid] = info;
+  }
+  __syncthreads();
+  for (int s = 0; s < P.S; ++s) {
+    // gather the block residual of step s
+    for (int idx = tid; idx < NC * NT * ND; idx += kT) {
+      const int c = idx / (NT * ND);
+      const int rem = idx - c * (NT * ND);
+      const int i = rem / ND;
+      const int l = rem - i * ND;
+      const long long base = base_s[c];
+      double v = 0.0;
+      if (base >= 0) {
+        const int lx = l % N, ly = (l / N) % N, lz = DIM == 3 ? l / (N * N) : 0;
+        v = r[(static_cast<long long>(s) * NT + i) * P.n_space + base + lz * dxy + ly * dx + lx];
+      }
+      R[idx] = v;
+      W[idx] = v;
+    }
+    __syncthreads();
+    // hat r = S^T r (axis by axis); Dirichlet rows of S are zero
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      for (int ln = tid; ln < NC * NT * LINES; ln += kT) {
+        const int ci = ln / LINES, line = ln - ci * LINES;
+        const int c = ci / NT;
+        if (base_s[c] < 0) continue;
+        const int info = info_s[c];
+        const int t = (info >> (8 + 2 * a)) & 3;
+        if (a == 0) sweep<N, true>(W + ci * ND, lbase<N, 0>(line), 1, P.S1[0][t]);
+        if (a == 1) sweep<N, true>(W + ci * ND, lbase<N, 1>(line), N, P.S1[1][t]);
+        if (a == 2) sweep<N, true>(W + ci * ND, lbase<N, 2>(line), N * N, P.S1[2][t]);
+      }
+      __syncthreads();
+    }
+    // per eigen-index n_t x n_t solves
+    for (int idx = tid; idx < NC * ND; idx += kT) {
+      const int c = idx / ND, e = idx - (idx / ND) * ND;
+      if (base_s[c] < 0) continue;
+      const int info = info_s[c];
+      const int ex = e % N, ey = (e / N) % N, ez = DIM == 3 ? e / (N * N) : 0;
+      double lam = P.L1[0][info >> 8 & 3][ex] + P.L1[1][info >> 10 & 3][ey];
+      if (DIM == 3) lam += P.L1[2][info >> 12 & 3][ez];
+      lam *= rho_s[c];
+      double b[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < NT; ++i) b[i] = W[(c * NT + i) * ND + e];
+      solve_small(P.TM, P.TA, lam, NT, b);
+#pragma unroll
+      for (int i = 0; i < NT; ++i) W[(c * NT + i) * ND + e] = b[i];
+    }
+    __syncthreads();
+    // z_T = S hat z
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      for (int ln = tid; ln < NC * NT * LINES; ln += kT) {
+        const int ci = ln / LINES, line = ln - ci * LINES;
+        const int c = ci / NT;
+        if (base_s[c] < 0) continue;
+        const int info = info_s[c];
+        const int t = (info >> (8 + 2 * a)) & 3;
+        if (a == 0) sweep<N, false>(W + ci * ND, lbase<N, 0>(line), 1, P.S1[0][t]);
+        if (a == 1) sweep<N, false>(W + ci * ND, lbase<N, 1>(line), N, P.S1[1][t]);
+        if (a == 2) sweep<N, false>(W + ci * ND, lbase<N, 2>(line), N * N, P.S1[2][t]);
+      }
+      __syncthreads();
+    }
+    // weighted scatter-add; Dirichlet rows are identity (correction = r)
+    for (int idx = tid; idx < NC * NT * ND; idx += kT) {
+      const int c = idx / (NT * ND);
+      const int rem = idx - c * (NT * ND);
+      const int i = rem / ND;
+      const int l = rem - i * ND;
+      const long long base = base_s[c];
+      if (base < 0) continue;
+      const int lx = l % N, ly = (l / N) % N, lz = DIM == 3 ? l / (N * N) : 0;
+      const int m = info_s[c];
+      bool bd = ((m & 1) && lx == 0) || ((m & 2) && lx == N - 1) || ((m & 4) && ly == 0) || ((m & 8) && ly == N - 1);
+      if (DIM == 3) bd = bd || ((m & 16) && lz == 0) || ((m & 32) && lz == N - 1);
+      const long long g = base + lz * dxy + ly * dx + lx;
+      // multiplicity: cells sharing the dof (asm_smoother.cpp:45-49)
+      double mult = 1.0;
+      if ((lx == 0 && !(m & 1)) || (lx == N - 1 && !(m & 2))) mult *= 2.0;
+      if ((ly == 0 && !(m & 4)) || (ly == N - 1 && !(m & 8))) mult *= 2.0;
+      if (DIM == 3 && ((lz == 0 && !(m & 16)) || (lz == N - 1 && !(m & 32)))) mult *= 2.0;
+      const double v = bd ? R[idx] : W[idx];
+      atomicAdd(z + (static_cast<long long>(s) * NT + i) * P.n_space + g, v / mult);
+    }
+    __syncthreads();
+  }
+}
+
+template <int DIM, int N, int NT>
+void launch(const DevFDM& P, const double* r, double* z, cudaStream_t s) {
+  using C = FCfg<DIM, N>;
+  const size_t smem = sizeof(double) * (2 * C::NC * NT * C::ND + C::NC) + sizeof(long long) * C::NC + sizeof(int) * C::NC;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(asm_fdm_kernel<DIM, N, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = true;
+  }
+  const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
+  count_launch();
+  asm_fdm_kernel<DIM, N, NT><<<static_cast<unsigned>((n_cells + C::NC - 1) / C::NC), kT, smem, s>>>(P, r, z);
+}
+
+template <int DIM, int N>
+void launch_nt(const DevFDM& P, const double* r, double* z, cudaStream_t s) {
+  switch (P.nt) {
+    case 1: launch<DIM, N, 1>(P, r, z, s); break;
+    case 2: launch<DIM, N, 2>(P, r, z, s); break;
+    case 3: launch<DIM, N, 3>(P, r, z, s); break;
+    case 4: launch<DIM, N, 4>(P, r, z, s); break;
+    default: throw std::invalid_argument("FDM smoother: n_t must be in [1, 4]");
+  }
+}
+
+}  // namespace
+
+void fdm_add_correction(const DevFDM& P, const double* r, double* z, cudaStream_t s) {
+  const int key = P.dim * 10 + P.n;
+  switch (key) {
+    case 22: launch_nt<2, 2>(P, r, z, s); break;
+    case 23: launch_nt<2, 3>(P, r, z, s); break;
+    case 24: launch_nt<2, 4>(P, r, z, s); break;
+    case 25: launch_nt<2, 5>(P, r, z, s); break;
+    case 32: launch_nt<3, 2>(P, r, z, s); break;
+    case 33: launch_nt<3, 3>(P, r, z, s); break;
+    case 34: launch_nt<3, 4>(P, r, z, s); break;
+    case 35: launch_nt<3, 5>(P, r, z, s); break;
+    default: throw std::invalid_argument("FDM smoother: unsupported dim/p");
+  }
+}
+
+}  // namespace stmgb

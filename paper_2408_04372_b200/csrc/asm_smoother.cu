@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <stdexcept>
 
 #include "kernels.hpp"
 
@@ -104,70 +105,184 @@ __device__ __forceinline__ void small_solve(const double* TM, const double* TA, 
   }
 }
 
-// one CTA per cell; blockDim >= m; handles all S steps of the slab
-__global__ void asm_apply_kernel(const __grid_constant__ DevASM A, const double* __restrict__ r, double* __restrict__ z) {
-  extern __shared__ double sm[];
-  const int m = A.m, ld = m + 1, nt = A.nt;
-  double* Xs = sm;               // [m][m+1]
-  double* rs = Xs + m * ld;      // [nt][m]
-  double* hs = rs + nt * m;      // [nt][m]
-  const long long cell = blockIdx.x;
-  const double* Xg = A.X + cell * static_cast<long long>(m) * m;
-  for (int i = threadIdx.x; i < m * m; i += blockDim.x) Xs[(i / m) * ld + (i % m)] = Xg[i];
-  long long cx, cy, cz;
-  cell_coords(cell, A.cells, cx, cy, cz);
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait: a copy that never lands traps instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  for (long long spin = 0; !mbar_try_wait(bar, phase); ++spin)
+    if (spin > (1LL << 28)) __trap();
+}
+// 1D TMA bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Persistent, double-buffered block solver. Each CTA walks cells
+// blockIdx.x, blockIdx.x + gridDim.x, ...; the eigenbasis X of the next cell
+// streams into shared memory by a TMA bulk copy (cp.async.bulk + mbarrier)
+// while the current one is applied to all S steps of the slab:
+//   hat r = X^T r_T   (thread e owns eigen-index e; X rows read contiguously)
+//   hat z_e = (T_M + lam_e T_A)^-1 hat r_e
+//   z_T  = X hat z    (thread a owns local dof a; rotated column order keeps
+//                      the row-wise smem reads bank-conflict free)
+// and the weighted result is scatter-added into z (Dirichlet rows: r).
+template <int M, int NT>
+__global__ void __launch_bounds__(((M + 31) / 32) * 32) asm_apply_tma_kernel(const __grid_constant__ DevASM A,
+                                                                             const double* __restrict__ r,
+                                                                             double* __restrict__ z) {
+  constexpr int XS = (M * M + 1) & ~1;       // per-cell stride in doubles (16 B multiple)
+  constexpr int ROT = (M % 2 == 0) ? 1 : 2;  // rotation: (M + ROT) odd -> conflict-free rows
+  extern __shared__ __align__(128) double sm[];
+  double* Xb0 = sm;
+  double* Xb1 = sm + XS;
+  double* rs = Xb1 + XS;         // [M][4]  residual of the block, dof-major
+  double* hs = rs + 4 * M;       // [M][4] hat z, eigen-index major
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(hs + 4 * M);
+  const long long n_cells = A.cells[0] * A.cells[1] * A.cells[2];
   const int t = threadIdx.x;
-  LocalDof d{};
-  double lam = 0.0;
-  if (t < m) {
-    d = local_dof(A, cx, cy, cz, t);
-    lam = A.lam[cell * m + t];
+  // bulk copies move whole 16-byte granules: copy the padded per-cell stride
+  constexpr unsigned XBYTES = static_cast<unsigned>(XS * sizeof(double));
+  static_assert(XBYTES % 16 == 0, "TMA bulk copy size must be a multiple of 16 bytes");
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int s = 0; s < A.S; ++s) {
-    __syncthreads();
-    if (t < m)
-      for (int i = 0; i < nt; ++i) rs[i * m + t] = r[(static_cast<long long>(s) * nt + i) * A.n_space + d.g];
-    __syncthreads();
-    // hat r[.,e] = X^T r, thread e
-    if (t < m) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int a = 0; a < m; ++a) {
-        const double x = Xs[a * ld + t];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i < nt) acc[i] = fma(x, rs[i * m + a], acc[i]);
-      }
-      small_solve(A.TM, A.TA, lam, nt, acc);
-      for (int i = 0; i < nt; ++i) hs[i * m + t] = acc[i];
+  __syncthreads();
+  long long cell = blockIdx.x;
+  if (t == 0 && cell < n_cells) {
+    mbar_expect_tx(&bar[0], XBYTES);
+    bulk_g2s(Xb0, A.X + cell * XS, XBYTES, &bar[0]);
+  }
+  unsigned ph0 = 0, ph1 = 0;
+  int buf = 0;
+  const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
+  for (; cell < n_cells; cell += gridDim.x) {
+    const long long next = cell + gridDim.x;
+    if (t == 0 && next < n_cells) {
+      fence_proxy_async();
+      double* dst = buf ? Xb0 : Xb1;
+      unsigned long long* b = &bar[buf ^ 1];
+      mbar_expect_tx(b, XBYTES);
+      bulk_g2s(dst, A.X + next * XS, XBYTES, b);
     }
-    __syncthreads();
-    // z_loc[., a] = X hat z, thread a; boundary rows are identity
-    if (t < m) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int e = 0; e < m; ++e) {
-        const double x = Xs[t * ld + e];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i < nt) acc[i] = fma(x, hs[i * m + e], acc[i]);
-      }
-      const double w = 1.0 / d.mult;
-      for (int i = 0; i < nt; ++i) {
-        const double v = d.bdry ? rs[i * m + t] : acc[i];
-        atomicAdd(z + (static_cast<long long>(s) * nt + i) * A.n_space + d.g, v * w);
-      }
+    // per-thread local dof (overlaps with the copy in flight)
+    const unsigned cidx = static_cast<unsigned>(A.list ? A.list[cell] : cell);
+    const long long cx = cidx % cxn, cy = (cidx / cxn) % cyn, cz = cidx / (cxn * cyn);
+    LocalDof d{};
+    double lam = 0.0;
+    if (t < M) {
+      d = local_dof(A, cx, cy, cz, t);
+      lam = A.lam[cell * M + t];
     }
+    if (buf == 0) {
+      mbar_wait(&bar[0], ph0);
+      ph0 ^= 1;
+    } else {
+      mbar_wait(&bar[1], ph1);
+      ph1 ^= 1;
+    }
+    const double* Xs = buf ? Xb1 : Xb0;
+    for (int s = 0; s < A.S; ++s) {
+      if (t < M) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) rs[t * 4 + i] = r[(static_cast<long long>(s) * NT + i) * A.n_space + d.g];
+      }
+      __syncthreads();
+      if (t < M) {
+        double acc[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) acc[i] = 0.0;
+#pragma unroll 16
+        for (int a = 0; a < M; ++a) {
+          const double x = Xs[a * M + t];
+          const double2 r01 = *reinterpret_cast<const double2*>(rs + a * 4);
+          acc[0] = fma(x, r01.x, acc[0]);
+          if (NT > 1) acc[1] = fma(x, r01.y, acc[1]);
+          if (NT > 2) {
+            const double2 r23 = *reinterpret_cast<const double2*>(rs + a * 4 + 2);
+            acc[2] = fma(x, r23.x, acc[2]);
+            if (NT > 3) acc[3] = fma(x, r23.y, acc[3]);
+          }
+        }
+        double b4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < NT; ++i) b4[i] = acc[i];
+        small_solve(A.TM, A.TA, lam, NT, b4);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) hs[t * 4 + i] = b4[i];
+      }
+      __syncthreads();
+      if (t < M) {
+        double acc[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) acc[i] = 0.0;
+        // row t of X in rotated column order (bank-conflict free), as two
+        // linear runs: e = e0 .. M-1, then 0 .. e0-1
+        const int e0 = (ROT * t) % M;
+        const double* xrow = Xs + t * M;
+        auto body = [&](int e) {
+          const double x = xrow[e];
+          const double2 h01 = *reinterpret_cast<const double2*>(hs + e * 4);
+          acc[0] = fma(x, h01.x, acc[0]);
+          if (NT > 1) acc[1] = fma(x, h01.y, acc[1]);
+          if (NT > 2) {
+            const double2 h23 = *reinterpret_cast<const double2*>(hs + e * 4 + 2);
+            acc[2] = fma(x, h23.x, acc[2]);
+            if (NT > 3) acc[3] = fma(x, h23.y, acc[3]);
+          }
+        };
+#pragma unroll 8
+        for (int e = e0; e < M; ++e) body(e);
+#pragma unroll 8
+        for (int e = 0; e < e0; ++e) body(e);
+        const double w = 1.0 / d.mult;
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          const double v = d.bdry ? rs[t * 4 + i] : acc[i];
+          atomicAdd(z + (static_cast<long long>(s) * NT + i) * A.n_space + d.g, v * w);
+        }
+      }
+      __syncthreads();
+    }
+    buf ^= 1;
   }
 }
 
 // column b of every cell matrix from one probe of colour (cx,cy,cz) mod period
 __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx, int coly, int colz, int period,
                                      const double* __restrict__ probe, double* __restrict__ cellmat) {
-  const long long n_cells = A.cells[0] * A.cells[1] * A.cells[2];
+  const long long n_pos = A.n_list;
   const int m = A.m, n = A.n;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_cells * m;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_pos * m;
        t += (long long)gridDim.x * blockDim.x) {
-    const long long cell = t / m;
-    const int a = static_cast<int>(t - cell * m);
+    const long long pos = t / m;
+    const int a = static_cast<int>(t - pos * m);
+    const long long cell = A.list ? A.list[pos] : pos;
     long long cx, cy, cz;
     cell_coords(cell, A.cells, cx, cy, cz);
     // local index per axis whose lattice coordinate has the probe colour
@@ -185,7 +300,7 @@ __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx,
     if (!found) continue;
     const int b = lb[0] + n * (lb[1] + (A.dim == 3 ? n * lb[2] : 0));
     const LocalDof da = local_dof(A, cx, cy, cz, a);
-    cellmat[cell * static_cast<long long>(m) * m + static_cast<long long>(a) * m + b] = probe[da.g];
+    cellmat[pos * static_cast<long long>(m) * m + static_cast<long long>(a) * m + b] = probe[da.g];
   }
 }
 
@@ -198,9 +313,10 @@ __global__ void reduce_standard_kernel(const __grid_constant__ DevASM A, double*
   double* L = sm;            // [m][ld]
   double* As = L + m * ld;   // [m][ld]
   double* T = As + m * ld;   // [m][ld]
-  const long long cell = blockIdx.x;
-  double* Mg = Mt + cell * static_cast<long long>(m) * m;
-  double* Ag = At + cell * static_cast<long long>(m) * m;
+  const long long pos = blockIdx.x;
+  const long long cell = A.list ? A.list[pos] : pos;
+  double* Mg = Mt + pos * static_cast<long long>(m) * m;
+  double* Ag = At + pos * static_cast<long long>(m) * m;
   long long cx, cy, cz;
   cell_coords(cell, A.cells, cx, cy, cz);
   for (int i = threadIdx.x; i < m * m; i += blockDim.x) {
@@ -274,12 +390,12 @@ __global__ void reduce_standard_kernel(const __grid_constant__ DevASM A, double*
 }
 
 // X[a][e] = sum_k Linv[k][a] V[k][e]; V column-major from syev (V[e*m+k])
-__global__ void back_transform_kernel(int m, const double* __restrict__ Linv, const double* __restrict__ V,
-                                      double* __restrict__ X) {
+__global__ void back_transform_kernel(int m, long long xs, const double* __restrict__ Linv,
+                                      const double* __restrict__ V, double* __restrict__ X) {
   const long long cell = blockIdx.x;
   const double* Lc = Linv + cell * static_cast<long long>(m) * m;
   const double* Vc = V + cell * static_cast<long long>(m) * m;
-  double* Xc = X + cell * static_cast<long long>(m) * m;
+  double* Xc = X + cell * xs;
   for (int i = threadIdx.x; i < m * m; i += blockDim.x) {
     const int a = i / m, e = i % m;
     double s = 0.0;
@@ -290,29 +406,65 @@ __global__ void back_transform_kernel(int m, const double* __restrict__ Linv, co
 
 }  // namespace
 
-void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_t s) {
-  const long long n_cells = A.cells[0] * A.cells[1] * A.cells[2];
-  const int threads = ((A.m + 31) / 32) * 32;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(A.m) * (A.m + 1) + 2 * A.nt * A.m);
+namespace {
+template <int M, int NT>
+void launch_asm(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+  constexpr int XS = (M * M + 1) & ~1;
+  constexpr int T = ((M + 31) / 32) * 32;
+  const size_t smem = sizeof(double) * (2 * XS + 8 * M) + 2 * sizeof(unsigned long long);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(asm_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(asm_apply_tma_kernel<M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_tma_kernel<M, NT>, T, smem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long n_cells = A.n_list;
+  if (n_cells == 0) return;
+  const long long grid = std::max<long long>(1, std::min<long long>(n_cells, static_cast<long long>(std::max(per_sm, 1)) * sms));
   count_launch();
-  asm_apply_kernel<<<static_cast<unsigned>(n_cells), threads, smem, s>>>(A, r, z);
+  asm_apply_tma_kernel<M, NT><<<static_cast<unsigned>(grid), T, smem, s>>>(A, r, z);
+}
+template <int M>
+void launch_asm_nt(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+  switch (A.nt) {
+    case 1: launch_asm<M, 1>(A, r, z, s); break;
+    case 2: launch_asm<M, 2>(A, r, z, s); break;
+    case 3: launch_asm<M, 3>(A, r, z, s); break;
+    case 4: launch_asm<M, 4>(A, r, z, s); break;
+    default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
+  }
+}
+}  // namespace
+
+void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+  switch (A.m) {
+    case 4: launch_asm_nt<4>(A, r, z, s); break;
+    case 8: launch_asm_nt<8>(A, r, z, s); break;
+    case 9: launch_asm_nt<9>(A, r, z, s); break;
+    case 16: launch_asm_nt<16>(A, r, z, s); break;
+    case 25: launch_asm_nt<25>(A, r, z, s); break;
+    case 27: launch_asm_nt<27>(A, r, z, s); break;
+    case 64: launch_asm_nt<64>(A, r, z, s); break;
+    default: throw std::invalid_argument("ASMSmoother: unsupported cell block size");
+  }
 }
 
 void asm_extract_probe(const DevASM& A, int cx, int cy, int cz, int period, const double* probe, double* cellmat,
                        cudaStream_t s) {
-  const long long total = A.cells[0] * A.cells[1] * A.cells[2] * A.m;
+  const long long total = A.n_list * A.m;
+  if (total == 0) return;
   const unsigned grid = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 148LL * 64)));
   count_launch();
   extract_probe_kernel<<<grid, 256, 0, s>>>(A, cx, cy, cz, period, probe, cellmat);
 }
 
 void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s) {
-  const long long n_cells = A.cells[0] * A.cells[1] * A.cells[2];
+  const long long n_cells = A.n_list;
+  if (n_cells == 0) return;
   const int threads = ((A.m + 31) / 32) * 32;
   const size_t smem = sizeof(double) * 3 * static_cast<size_t>(A.m) * (A.m + 1);
   static bool configured = false;
@@ -324,9 +476,10 @@ void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s
   reduce_standard_kernel<<<static_cast<unsigned>(n_cells), threads, smem, s>>>(A, Mt, At);
 }
 
-void asm_back_transform(int m, long long n_cells, const double* Linv, const double* V, double* X, cudaStream_t s) {
+void asm_back_transform(int m, long long xs, long long n_cells, const double* Linv, const double* V, double* X,
+                        cudaStream_t s) {
   count_launch();
-  back_transform_kernel<<<static_cast<unsigned>(n_cells), 128, 0, s>>>(m, Linv, V, X);
+  back_transform_kernel<<<static_cast<unsigned>(n_cells), 128, 0, s>>>(m, xs, Linv, V, X);
 }
 
 }  // namespace stmgb

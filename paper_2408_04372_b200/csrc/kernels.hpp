@@ -34,21 +34,21 @@ void dense_matvec(const double* A, const double* x, double* y, int n, cudaStream
 
 // ---- grid transfers (transfer.cu)
 struct DevAxisTransfer {
-  // prolongation rows: fine index i -> first coarse index start[i], weights
-  // wts[i*(nc_loc)+j], j < nc_loc (spatial h/p, transfer.cpp:32-54)
-  const int* row_start;
+  // CSR of the 1D embedding P (rows = fine index, transfer.cpp:32-54) and of
+  // P^T (rows = coarse index)
+  const int* row_ptr;
+  const int* row_idx;
   const double* row_w;
-  int row_nnz;
-  // restriction columns (CSR of P^T): coarse index J -> fine rows
   const int* col_ptr;
   const int* col_idx;
   const double* col_w;
   long long nf, nc;
 };
+// separable per-axis passes; t1/t2 are work buffers of Transfer-chosen size
 void spatial_prolong(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
-                     const double* coarse, double* fine, cudaStream_t s);
+                     const double* coarse, double* fine, double* t1, double* t2, cudaStream_t s);
 void spatial_restrict(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
-                      const double* fine, double* coarse, cudaStream_t s);
+                      const double* fine, double* coarse, double* t1, double* t2, cudaStream_t s);
 // temporal: fine block r = sum_c T[r][c] coarse block c (T row-major Ff x Fc)
 void temporal_prolong(const double* T_dev, int Ff, int Fc, long long n_space, const long long* dofs, int dim,
                       const double* coarse, double* fine, cudaStream_t s);
@@ -60,16 +60,35 @@ struct DevASM {
   int dim, p, n, m;       // m = n^dim local dofs per cell
   int S, nt;
   long long cells[3], dofs[3], n_space;
-  const double* X;        // per cell m x m (row-major [a][e]), M_T-orthonormal eigenvectors
+  const double* X;        // per cell m x m (row-major [a][e]), M_T-orthonormal eigenvectors,
+                          // cell stride xs = m*m rounded up to even (16-byte TMA alignment)
+  long long xs;
   const double* lam;      // per cell m eigenvalues (0 on Dirichlet dofs)
   double TM[16], TA[16];  // diagonal (s,s) temporal blocks, n_t x n_t
+  const long long* list;  // cells handled (X/lam stored per list entry); nullptr = all cells
+  long long n_list;       // number of handled cells
 };
 void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_t s);
+
+// tensor-product FDM cell solves on Cartesian levels (asm_fdm.cu)
+struct DevFDM {
+  int dim, p, n, S, nt;
+  long long cells[3], dofs[3], n_space;
+  double S1[3][4][kMaxN][kMaxN];  // per axis and position class: 1D eigenvectors [node][eig]
+  double L1[3][4][kMaxN];         // matching eigenvalues
+  double TM[16], TA[16];
+  const double* rho0;             // coefficient per level-0 cell (nullptr: 1)
+  int rho_shift;
+  long long cells0[3];
+  const unsigned char* skip;      // per cell: 1 = solved by the exact per-cell kernel
+};
+void fdm_add_correction(const DevFDM& F, const double* r, double* z, cudaStream_t s);
 // probing-based extraction of restricted cell matrices (setup)
 void asm_extract_probe(const DevASM& A, int colour_x, int colour_y, int colour_z, int period, const double* probe,
                        double* cellmat, cudaStream_t s);
 void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s);  // At <- L^-1 At L^-T, Mt <- L^-1
-void asm_back_transform(int m, long long n_cells, const double* Linv, const double* V, double* X, cudaStream_t s);
+void asm_back_transform(int m, long long xs, long long n_cells, const double* Linv, const double* V, double* X,
+                        cudaStream_t s);
 
 }  // namespace stmgb
 

@@ -440,3 +440,118 @@ double Xoshiro256pp::normal() {
 }
 
 }  // namespace stmgb
+
+namespace stmgb {
+
+std::vector<double> sym_eigen_jacobi(std::vector<double> A, int n, std::vector<double>& V) {
+  V.assign(static_cast<size_t>(n * n), 0.0);
+  for (int i = 0; i < n; ++i) V[i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = i + 1; j < n; ++j) off += A[i * n + j] * A[i * n + j];
+    if (off < 1e-34) break;
+    for (int pp = 0; pp < n; ++pp)
+      for (int q = pp + 1; q < n; ++q) {
+        const double apq = A[pp * n + q];
+        if (std::abs(apq) < 1e-300) continue;
+        const double theta = (A[q * n + q] - A[pp * n + pp]) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < n; ++k) {
+          const double akp = A[k * n + pp], akq = A[k * n + q];
+          A[k * n + pp] = c * akp - s * akq;
+          A[k * n + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double apk = A[pp * n + k], aqk = A[q * n + k];
+          A[pp * n + k] = c * apk - s * aqk;
+          A[q * n + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = V[k * n + pp], vkq = V[k * n + q];
+          V[k * n + pp] = c * vkp - s * vkq;
+          V[k * n + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  std::vector<double> w(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) w[i] = A[i * n + i];
+  return w;
+}
+
+void fdm_axis_tables(int p, double h, double S[4][5][5], double lam[4][5]) {
+  const int n = p + 1;
+  const Rule q = gauss(n);
+  const std::vector<double> gl = gauss_lobatto(n).x;
+  std::vector<double> Me(n * n, 0.0), Ke(n * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (size_t k = 0; k < q.x.size(); ++k) {
+        Me[i * n + j] += q.w[k] * lagrange_eval(gl, i, q.x[k]) * lagrange_eval(gl, j, q.x[k]) * h;
+        Ke[i * n + j] += q.w[k] * lagrange_deriv(gl, i, q.x[k]) * lagrange_deriv(gl, j, q.x[k]) / h;
+      }
+  for (int type = 0; type < 4; ++type) {
+    const bool first = type & 1, last = type & 2;
+    std::vector<double> M = Me, K = Ke;
+    if (!first) {  // left neighbour shares node 0
+      M[0] += Me[(n - 1) * n + (n - 1)];
+      K[0] += Ke[(n - 1) * n + (n - 1)];
+    }
+    if (!last) {  // right neighbour shares node p
+      M[(n - 1) * n + (n - 1)] += Me[0];
+      K[(n - 1) * n + (n - 1)] += Ke[0];
+    }
+    std::vector<int> keep;
+    for (int i = 0; i < n; ++i)
+      if (!((i == 0 && first) || (i == n - 1 && last))) keep.push_back(i);
+    const int k = static_cast<int>(keep.size());
+    for (int i = 0; i < 5; ++i) {
+      lam[type][i] = 0.0;
+      for (int j = 0; j < 5; ++j) S[type][i][j] = 0.0;
+    }
+    if (k == 0) continue;
+    // Cholesky of the kept block of M, then C = L^-1 K L^-T
+    std::vector<double> L(k * k, 0.0), Kk(k * k);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j) Kk[i * k + j] = K[keep[i] * n + keep[j]];
+    for (int j = 0; j < k; ++j) {
+      double d = M[keep[j] * n + keep[j]];
+      for (int l = 0; l < j; ++l) d -= L[j * k + l] * L[j * k + l];
+      L[j * k + j] = std::sqrt(d);
+      for (int i = j + 1; i < k; ++i) {
+        double s = M[keep[i] * n + keep[j]];
+        for (int l = 0; l < j; ++l) s -= L[i * k + l] * L[j * k + l];
+        L[i * k + j] = s / L[j * k + j];
+      }
+    }
+    std::vector<double> Li(k * k, 0.0);  // L^-1
+    for (int c = 0; c < k; ++c)
+      for (int i = c; i < k; ++i) {
+        double s = (i == c) ? 1.0 : 0.0;
+        for (int l = c; l < i; ++l) s -= L[i * k + l] * Li[l * k + c];
+        Li[i * k + c] = s / L[i * k + i];
+      }
+    std::vector<double> C(k * k, 0.0), T(k * k, 0.0);
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j)
+        for (int l = 0; l < k; ++l) T[i * k + j] += Li[i * k + l] * Kk[l * k + j];
+    for (int i = 0; i < k; ++i)
+      for (int j = 0; j < k; ++j)
+        for (int l = 0; l < k; ++l) C[i * k + j] += T[i * k + l] * Li[j * k + l];
+    for (int i = 0; i < k; ++i)
+      for (int j = i + 1; j < k; ++j) C[i * k + j] = C[j * k + i] = 0.5 * (C[i * k + j] + C[j * k + i]);
+    std::vector<double> V;
+    const std::vector<double> w = sym_eigen_jacobi(C, k, V);
+    for (int e = 0; e < k; ++e) {
+      lam[type][keep[e]] = w[e];
+      for (int i = 0; i < k; ++i) {  // S = L^-T V
+        double s = 0.0;
+        for (int l = i; l < k; ++l) s += Li[l * k + i] * V[l * k + e];
+        S[type][keep[i]][keep[e]] = s;
+      }
+    }
+  }
+}
+
+}  // namespace stmgb

@@ -116,3 +116,16 @@ std::vector<double> invert_small(const std::vector<double>& a, int n);
 std::vector<double> matmul_small(const std::vector<double>& a, const std::vector<double>& b, int n, int k, int m);
 
 }  // namespace stmgb
+
+namespace stmgb {
+// Tensor-product FDM tables for one lattice axis of a Cartesian level with
+// spacing h and degree p: for the four position classes of a cell along the
+// axis (0 interior, 1 first, 2 last, 3 single) the generalised eigenpairs
+// K_r S = M_r S Lambda (S^T M_r S = I) of the restricted global 1D stiffness
+// K_r and mass M_r on the cell's p+1 nodes; Dirichlet end nodes are removed
+// (their rows/columns of S are zero, Lambda = 0). S is row-major [node][eig].
+void fdm_axis_tables(int p, double h, double S[4][5][5], double lam[4][5]);
+// symmetric eigen-decomposition by cyclic Jacobi rotations (small n):
+// A = V diag(w) V^T, V row-major [i][eig]
+std::vector<double> sym_eigen_jacobi(std::vector<double> A, int n, std::vector<double>& V);
+}  // namespace stmgb

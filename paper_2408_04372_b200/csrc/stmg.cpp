@@ -160,8 +160,6 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
   A.S = d.S;
   A.nt = d.nt;
   if (A.nt > 4) throw std::invalid_argument("ASMSmoother: n_t must be <= 4");
-  if (A.m > 64)
-    throw std::invalid_argument("ASMSmoother: exact cell blocks need (p+1)^dim <= 64 (3D p <= 3)");
   for (int a = 0; a < 3; ++a) {
     A.cells[a] = d.cells[a];
     A.dofs[a] = d.dofs[a];
@@ -175,7 +173,96 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
       A.TA[i * A.nt + j] = d.CA[i * F + j];
     }
   const Index n_cells = d.cells[0] * d.cells[1] * d.cells[2];
-  const size_t mat_bytes = sizeof(double) * static_cast<size_t>(n_cells) * A.m * A.m;
+  const bool cartesian = d.verts == nullptr;
+  std::vector<long long> exact_cells;
+  if (cartesian) {
+    // tensor-product FDM for every cell whose coefficient neighbourhood is
+    // uniform (exact there); the others get the exact per-cell eigenbasis
+    use_fdm_ = true;
+    DevFDM& Fd = fdm_;
+    Fd.dim = d.dim;
+    Fd.p = d.p;
+    Fd.n = d.n;
+    Fd.S = d.S;
+    Fd.nt = d.nt;
+    for (int a = 0; a < 3; ++a) {
+      Fd.cells[a] = d.cells[a];
+      Fd.dofs[a] = d.dofs[a];
+      Fd.cells0[a] = d.cells0[a];
+    }
+    Fd.n_space = d.n_space;
+    std::memcpy(Fd.TM, A.TM, sizeof(A.TM));
+    std::memcpy(Fd.TA, A.TA, sizeof(A.TA));
+    Fd.rho0 = d.rho0;
+    Fd.rho_shift = d.rho_shift;
+    Fd.skip = nullptr;
+    std::memset(Fd.S1, 0, sizeof(Fd.S1));
+    std::memset(Fd.L1, 0, sizeof(Fd.L1));
+    for (int a = 0; a < d.dim; ++a) {
+      double S[4][5][5], L[4][5];
+      fdm_axis_tables(d.p, d.h[a], S, L);
+      for (int t = 0; t < 4; ++t)
+        for (int i = 0; i < kMaxN; ++i) {
+          Fd.L1[a][t][i] = L[t][i];
+          for (int j = 0; j < kMaxN; ++j) Fd.S1[a][t][i][j] = S[t][i][j];
+        }
+    }
+    if (d.rho0) {
+      // host copy of the level-0 coefficient table
+      const Index n0 = d.cells0[0] * d.cells0[1] * d.cells0[2];
+      std::vector<double> rho0(static_cast<size_t>(n0));
+      cuda_check(cudaMemcpy(rho0.data(), d.rho0, sizeof(double) * n0, cudaMemcpyDeviceToHost), "rho0");
+      auto rho_of = [&](long long cx, long long cy, long long cz) {
+        return rho0[static_cast<size_t>(((cz >> d.rho_shift) * d.cells0[1] + (cy >> d.rho_shift)) * d.cells0[0] +
+                                        (cx >> d.rho_shift))];
+      };
+      std::vector<unsigned char> skip(static_cast<size_t>(n_cells), 0);
+      for (Index c = 0; c < n_cells; ++c) {
+        const long long cx = c % d.cells[0], cy = (c / d.cells[0]) % d.cells[1], cz = c / (d.cells[0] * d.cells[1]);
+        const double r0 = rho_of(cx, cy, cz);
+        bool uniform = true;
+        for (int dz = (d.dim == 3 ? -1 : 0); dz <= (d.dim == 3 ? 1 : 0) && uniform; ++dz)
+          for (int dy = -1; dy <= 1 && uniform; ++dy)
+            for (int dxx = -1; dxx <= 1 && uniform; ++dxx) {
+              const long long nx = cx + dxx, ny = cy + dy, nz = cz + dz;
+              if (nx < 0 || ny < 0 || nz < 0 || nx >= d.cells[0] || ny >= d.cells[1] || nz >= d.cells[2]) continue;
+              if (rho_of(nx, ny, nz) != r0) uniform = false;
+            }
+        if (!uniform) exact_cells.push_back(c);
+      }
+      if (!exact_cells.empty()) {
+        if (A.m > 64) {
+          exact_cells.clear();  // no exact kernel for (p+1)^3 > 64: FDM with the cell's own rho
+          exact_ = false;
+        } else {
+          for (long long c : exact_cells) skip[static_cast<size_t>(c)] = 1;
+          skip_ = upload(skip);
+          Fd.skip = static_cast<const unsigned char*>(skip_.raw());
+        }
+      }
+    }
+    if (exact_cells.empty()) {
+      A.n_list = 0;
+      A.list = nullptr;
+      return;
+    }
+    list_ = upload(exact_cells);
+    A.list = static_cast<const long long*>(list_.raw());
+    A.n_list = static_cast<long long>(exact_cells.size());
+  } else {
+    if (A.m > 64)
+      throw std::invalid_argument("ASMSmoother: exact cell blocks on deformed meshes need (p+1)^dim <= 64");
+    A.list = nullptr;
+    A.n_list = n_cells;
+  }
+  build_exact(op);
+}
+
+void ASMSmoother::build_exact(const SpaceTimeOperator& op) {
+  const DevLevel& d = op.desc();
+  DevASM& A = asm_;
+  const Index n_pos = A.n_list;
+  const size_t mat_bytes = sizeof(double) * static_cast<size_t>(n_pos) * A.m * A.m;
   cudaStream_t s = nullptr;
   DeviceBuffer cellM(mat_bytes), cellA(mat_bytes), probe(sizeof(double) * d.n_space), ind(sizeof(double) * d.n_space);
   cuda_check(cudaMemsetAsync(cellM.raw(), 0, mat_bytes, s), "memset");
@@ -198,36 +285,43 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
   asm_reduce_standard(A, cellM.d(), cellA.d(), s);
   cuda_check(cudaGetLastError(), "asm setup kernels");
   // batched symmetric eigensolver
-  lam_.allocate(sizeof(double) * static_cast<size_t>(n_cells) * A.m);
+  lam_.allocate(sizeof(double) * static_cast<size_t>(n_pos) * A.m);
   cusolverDnHandle_t h = nullptr;
   cusolverDnParams_t prm = nullptr;
   solver_check(cusolverDnCreate(&h), "cusolverDnCreate");
   solver_check(cusolverDnCreateParams(&prm), "cusolverDnCreateParams");
   solver_check(cusolverDnSetStream(h, s), "cusolverDnSetStream");
-  const Index chunk = std::min<Index>(n_cells, 1 << 15);
+  // the batched solver rejects very large batches: shrink until accepted
+  Index chunk = std::min<Index>(n_pos, 1 << 15);
   size_t dws = 0, hws = 0;
-  solver_check(cusolverDnXsyevBatched_bufferSize(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, A.m,
-                                                 CUDA_R_64F, cellA.raw(), A.m, CUDA_R_64F, lam_.raw(), CUDA_R_64F,
-                                                 &dws, &hws, chunk),
-               "syevBatched_bufferSize");
+  for (;;) {
+    const cusolverStatus_t st = cusolverDnXsyevBatched_bufferSize(
+        h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, A.m, CUDA_R_64F, cellA.raw(), A.m, CUDA_R_64F,
+        lam_.raw(), CUDA_R_64F, &dws, &hws, chunk);
+    if (st == CUSOLVER_STATUS_SUCCESS) break;
+    if (st != CUSOLVER_STATUS_INVALID_VALUE || chunk <= 64) solver_check(st, "syevBatched_bufferSize");
+    chunk /= 4;
+  }
   DeviceBuffer dwork(std::max<size_t>(dws, 8)), info(sizeof(int) * static_cast<size_t>(chunk));
   std::vector<char> hwork(std::max<size_t>(hws, 8));
-  for (Index c0 = 0; c0 < n_cells; c0 += chunk) {
-    const Index nb = std::min<Index>(chunk, n_cells - c0);
+  std::vector<int> hinfo(static_cast<size_t>(chunk));
+  for (Index c0 = 0; c0 < n_pos; c0 += chunk) {
+    const Index nb = std::min<Index>(chunk, n_pos - c0);
     solver_check(cusolverDnXsyevBatched(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, A.m, CUDA_R_64F,
                                         cellA.d() + c0 * A.m * A.m, A.m, CUDA_R_64F, lam_.d() + c0 * A.m, CUDA_R_64F,
                                         dwork.raw(), dws, hwork.data(), hws, static_cast<int*>(info.raw()), nb),
                  "syevBatched");
+    cuda_check(cudaMemcpy(hinfo.data(), info.raw(), sizeof(int) * nb, cudaMemcpyDeviceToHost), "info");
+    for (Index i = 0; i < nb; ++i)
+      if (hinfo[static_cast<size_t>(i)] != 0)
+        throw std::runtime_error("ASMSmoother: singular block (eigensolver info " +
+                                 std::to_string(hinfo[static_cast<size_t>(i)]) + ")");
   }
-  cuda_check(cudaStreamSynchronize(s), "syev sync");
-  std::vector<int> hinfo(static_cast<size_t>(std::min<Index>(chunk, n_cells)));
-  cuda_check(cudaMemcpy(hinfo.data(), info.raw(), sizeof(int) * hinfo.size(), cudaMemcpyDeviceToHost), "info");
-  for (int v : hinfo)
-    if (v != 0) throw std::runtime_error("ASMSmoother: singular block (eigensolver info " + std::to_string(v) + ")");
   cusolverDnDestroyParams(prm);
   cusolverDnDestroy(h);
-  X_.allocate(mat_bytes);
-  asm_back_transform(A.m, n_cells, cellM.d(), cellA.d(), X_.d(), s);
+  A.xs = (static_cast<long long>(A.m) * A.m + 1) & ~1LL;
+  X_.allocate(sizeof(double) * static_cast<size_t>(n_pos) * A.xs);
+  asm_back_transform(A.m, A.xs, n_pos, cellM.d(), cellA.d(), X_.d(), s);
   cuda_check(cudaStreamSynchronize(s), "asm setup");
   A.X = X_.d();
   A.lam = lam_.d();
@@ -235,7 +329,8 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
 
 void ASMSmoother::add_correction(const double* residual, double* correction, cudaStream_t stream) const {
   ++sweep_count_;
-  asm_add_correction(asm_, residual, correction, stream);
+  if (use_fdm_) fdm_add_correction(fdm_, residual, correction, stream);
+  if (asm_.n_list > 0) asm_add_correction(asm_, residual, correction, stream);
 }
 
 // --------------------------------------------------------------- Transfer
@@ -276,24 +371,19 @@ Transfer::Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coars
       const int pf = fine.p(), pc = coarse.p();
       const std::vector<double> P = axis_prolongation(cf, pf, cc, pc);
       const Index nf = cf * pf + 1, nc = cc * pc + 1;
-      const int nnz = pc + 1;
-      std::vector<int> start(static_cast<size_t>(nf));
-      std::vector<double> w(static_cast<size_t>(nf * nnz), 0.0);
+      // CSR of P (rows: fine index) and of P^T (rows: coarse index)
+      std::vector<int> rptr(static_cast<size_t>(nf + 1), 0), ridx, cptr(static_cast<size_t>(nc + 1), 0), cidx;
+      std::vector<double> rw, cw;
       for (Index i = 0; i < nf; ++i) {
-        Index first = nc, last = -1;
-        for (Index j = 0; j < nc; ++j)
-          if (P[static_cast<size_t>(i * nc + j)] != 0.0) {
-            first = std::min(first, j);
-            last = std::max(last, j);
+        for (Index j = 0; j < nc; ++j) {
+          const double v = P[static_cast<size_t>(i * nc + j)];
+          if (v != 0.0) {
+            ridx.push_back(static_cast<int>(j));
+            rw.push_back(v);
           }
-        if (last < 0) first = 0;
-        Index st = std::min<Index>(first, nc - nnz);
-        if (last >= st + nnz) throw std::runtime_error("Transfer: prolongation row wider than a coarse cell");
-        start[static_cast<size_t>(i)] = static_cast<int>(st);
-        for (int k = 0; k < nnz; ++k) w[static_cast<size_t>(i * nnz + k)] = P[static_cast<size_t>(i * nc + st + k)];
+        }
+        rptr[static_cast<size_t>(i + 1)] = static_cast<int>(ridx.size());
       }
-      std::vector<int> cptr(static_cast<size_t>(nc + 1), 0), cidx;
-      std::vector<double> cw;
       for (Index j = 0; j < nc; ++j) {
         for (Index i = 0; i < nf; ++i) {
           const double v = P[static_cast<size_t>(i * nc + j)];
@@ -304,11 +394,12 @@ Transfer::Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coars
         }
         cptr[static_cast<size_t>(j + 1)] = static_cast<int>(cidx.size());
       }
-      bufs_.push_back(upload(start));
-      ax_[a].row_start = static_cast<const int*>(bufs_.back().raw());
-      bufs_.push_back(upload(w));
+      bufs_.push_back(upload(rptr));
+      ax_[a].row_ptr = static_cast<const int*>(bufs_.back().raw());
+      bufs_.push_back(upload(ridx));
+      ax_[a].row_idx = static_cast<const int*>(bufs_.back().raw());
+      bufs_.push_back(upload(rw));
       ax_[a].row_w = bufs_.back().d();
-      ax_[a].row_nnz = nnz;
       bufs_.push_back(upload(cptr));
       ax_[a].col_ptr = static_cast<const int*>(bufs_.back().raw());
       bufs_.push_back(upload(cidx));
@@ -318,6 +409,13 @@ Transfer::Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coars
       ax_[a].nf = nf;
       ax_[a].nc = nc;
     }
+    const long long* df = fine.desc().dofs;
+    const long long* dc = coarse.desc().dofs;
+    const long long F = fine.desc().F;
+    const long long t1 = F * std::max(df[0] * dc[1] * dc[2], dc[0] * df[1] * df[2]);
+    const long long t2 = F * std::max(df[0] * df[1] * dc[2], dc[0] * dc[1] * df[2]);
+    t1_.allocate(sizeof(double) * t1);
+    t2_.allocate(sizeof(double) * t2);
   } else {
     const TemporalWeights& wf = fine.weights();
     const TemporalWeights& wc = coarse.weights();
@@ -350,7 +448,7 @@ void Transfer::prolong(const double* coarse, double* fine, cudaStream_t stream) 
   const DevLevel& df = fine_->desc();
   const DevLevel& dc = coarse_->desc();
   if (spatial_)
-    spatial_prolong(ax_, df.dim, df.F, dc.dofs, df.dofs, coarse, fine, stream);
+    spatial_prolong(ax_, df.dim, df.F, dc.dofs, df.dofs, coarse, fine, t1_.d(), t2_.d(), stream);
   else
     temporal_prolong(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, coarse, fine, stream);
 }
@@ -359,7 +457,7 @@ void Transfer::restrict_(const double* fine, double* coarse, cudaStream_t stream
   const DevLevel& df = fine_->desc();
   const DevLevel& dc = coarse_->desc();
   if (spatial_)
-    spatial_restrict(ax_, df.dim, df.F, dc.dofs, df.dofs, fine, coarse, stream);
+    spatial_restrict(ax_, df.dim, df.F, dc.dofs, df.dofs, fine, coarse, t1_.d(), t2_.d(), stream);
   else
     temporal_restrict(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, fine, coarse, stream);
 }

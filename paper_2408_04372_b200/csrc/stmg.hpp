@@ -99,12 +99,22 @@ class ASMSmoother {
   int block_size() const { return op_->n_t() * asm_.m; }
   Index n_blocks() const { return static_cast<Index>(op_->n_steps()) * op_->mesh().n_cells(); }
   long sweeps() const { return sweep_count_; }
-  size_t bytes() const { return X_.bytes() + lam_.bytes(); }
+  size_t bytes() const { return X_.bytes() + lam_.bytes() + list_.bytes() + skip_.bytes(); }
+  // cells solved by tensor FDM / by the per-cell eigenbasis; exact() is false
+  // when some block is only approximated (non-uniform coefficient around a
+  // (p+1)^3 > 64 cell)
+  bool uses_fdm() const { return use_fdm_; }
+  Index n_exact_cells() const { return asm_.n_list; }
+  bool exact() const { return exact_; }
 
  private:
+  void build_exact(const SpaceTimeOperator& op);
   const SpaceTimeOperator* op_;
   DevASM asm_{};
-  DeviceBuffer X_, lam_;
+  DevFDM fdm_{};
+  bool use_fdm_ = false;
+  bool exact_ = true;
+  DeviceBuffer X_, lam_, list_, skip_;
   mutable long sweep_count_ = 0;
 };
 
@@ -121,6 +131,7 @@ class Transfer {
   bool spatial_ = true;
   DevAxisTransfer ax_[3]{};
   std::vector<DeviceBuffer> bufs_;
+  mutable DeviceBuffer t1_, t2_;  // separable-pass work buffers
   DeviceBuffer time_p_;
   int Ff_ = 0, Fc_ = 0;
 };

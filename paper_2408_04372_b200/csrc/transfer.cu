@@ -1,12 +1,13 @@
 // Grid transfers between consecutive multigrid levels (reference: Transfer,
 // transfer.cpp:58-190). Spatial h/p transfers are tensor products of the
-// per-axis embedding matrices P (fine x coarse); here each fine dof gathers
-// the (p_c+1)^d coarse values of its parent cell with the per-axis weights
-// (local parent-cell stencil instead of the reference's dense O(n_f*n_c) 1D
-// contraction), and restriction (= P^T) gathers along the CSR columns of P.
-// Temporal tau/k transfers apply the small (S_f n_tf) x (S_c n_tc) evaluation
-// matrix blockwise over the spatial dofs. Dirichlet entries are zeroed on both
-// sides, as transfer.cpp:108-116.
+// per-axis embedding matrices P (n_f x n_c, transfer.cpp:32-54); they are
+// applied here as separable passes, one lattice axis at a time, each output
+// entry gathering the few nonzeros of its CSR row of P (prolongation) or of
+// P^T (restriction) -- O((p+1) d) work per entry instead of the reference's
+// dense O(n_f n_c) line contraction. Temporal tau/k transfers apply the small
+// (S_f n_tf) x (S_c n_tc) evaluation matrix blockwise over the spatial dofs.
+// Dirichlet entries are zeroed on the input and output sides
+// (transfer.cpp:108-116).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,90 +18,45 @@ namespace stmgb {
 
 namespace {
 
-struct Axes {
-  DevAxisTransfer a[3];
-};
-
 __device__ __forceinline__ bool on_bdry(long long i, long long n) { return i == 0 || i == n - 1; }
 
-__global__ void spatial_prolong_kernel(Axes ax, int dim, int F, long long dcx, long long dcy, long long dcz,
-                                       long long dfx, long long dfy, long long dfz, const double* __restrict__ c,
-                                       double* __restrict__ f) {
-  const long long nfs = dfx * dfy * dfz, ncs = dcx * dcy * dcz;
-  const long long total = nfs * F;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int fld = static_cast<int>(t / nfs);
-    const long long g = t - fld * nfs;
-    const long long ix = g % dfx, iy = (g / dfx) % dfy, iz = g / (dfx * dfy);
-    bool bd = on_bdry(ix, dfx) || (dim > 1 && on_bdry(iy, dfy)) || (dim > 2 && on_bdry(iz, dfz));
+// out[f][z][y][x] (dims o[]) = sum_k w_k in[f][..src..] along `axis`;
+// input dims i[] equal o[] except along axis.
+template <int AXIS>
+__global__ void axis_pass_kernel(int F, long long ix, long long iy, long long iz, long long ox, long long oy,
+                                 long long oz, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                 const double* __restrict__ w, bool mask_in, bool mask_out,
+                                 const double* __restrict__ in, double* __restrict__ out) {
+  const long long on = ox * oy * oz, in_n = ix * iy * iz;
+  const long long total = on * F;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long f = t / on;
+    const long long g = t - f * on;
+    const long long x = g % ox, y = (g / ox) % oy, z = g / (ox * oy);
     double s = 0.0;
-    if (!bd) {
-      const double* cf = c + fld * ncs;
-      const int nx = ax.a[0].row_nnz;
-      const int ny = dim > 1 ? ax.a[1].row_nnz : 1;
-      const int nz = dim > 2 ? ax.a[2].row_nnz : 1;
-      const long long sx = ax.a[0].row_start[ix];
-      const long long sy = dim > 1 ? ax.a[1].row_start[iy] : 0;
-      const long long sz = dim > 2 ? ax.a[2].row_start[iz] : 0;
-      for (int kz = 0; kz < nz; ++kz) {
-        const long long jz = sz + kz;
-        if (dim > 2 && on_bdry(jz, dcz)) continue;
-        const double wz = dim > 2 ? ax.a[2].row_w[iz * nz + kz] : 1.0;
-        if (wz == 0.0) continue;
-        for (int ky = 0; ky < ny; ++ky) {
-          const long long jy = sy + ky;
-          if (dim > 1 && on_bdry(jy, dcy)) continue;
-          const double wyz = wz * (dim > 1 ? ax.a[1].row_w[iy * ny + ky] : 1.0);
-          if (wyz == 0.0) continue;
-          double sxs = 0.0;
-          for (int kx = 0; kx < nx; ++kx) {
-            const long long jx = sx + kx;
-            if (on_bdry(jx, dcx)) continue;
-            sxs = fma(ax.a[0].row_w[ix * nx + kx], cf[(jz * dcy + jy) * dcx + jx], sxs);
-          }
-          s = fma(wyz, sxs, s);
+    const bool zero_out = mask_out && (on_bdry(x, ox) || (oy > 1 && on_bdry(y, oy)) || (oz > 1 && on_bdry(z, oz)));
+    if (!zero_out) {
+      const long long o = AXIS == 0 ? x : (AXIS == 1 ? y : z);
+      const int k0 = ptr[o], k1 = ptr[o + 1];
+      const double* src = in + f * in_n;
+      bool other_bd = false;
+      if (mask_in) {
+        if (AXIS != 0) other_bd = other_bd || on_bdry(x, ix);
+        if (AXIS != 1 && iy > 1) other_bd = other_bd || on_bdry(y, iy);
+        if (AXIS != 2 && iz > 1) other_bd = other_bd || on_bdry(z, iz);
+      }
+      if (!other_bd) {
+        const long long n_ax = AXIS == 0 ? ix : (AXIS == 1 ? iy : iz);
+        for (int k = k0; k < k1; ++k) {
+          const long long j = idx[k];
+          if (mask_in && on_bdry(j, n_ax)) continue;
+          const long long sidx = AXIS == 0 ? (z * iy + y) * ix + j : (AXIS == 1 ? (z * iy + j) * ix + x : (j * iy + y) * ix + x);
+          s = fma(w[k], src[sidx], s);
         }
       }
     }
-    f[t] = s;
-  }
-}
-
-__global__ void spatial_restrict_kernel(Axes ax, int dim, int F, long long dcx, long long dcy, long long dcz,
-                                        long long dfx, long long dfy, long long dfz, const double* __restrict__ f,
-                                        double* __restrict__ c) {
-  const long long nfs = dfx * dfy * dfz, ncs = dcx * dcy * dcz;
-  const long long total = ncs * F;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int fld = static_cast<int>(t / ncs);
-    const long long g = t - fld * ncs;
-    const long long jx = g % dcx, jy = (g / dcx) % dcy, jz = g / (dcx * dcy);
-    bool bd = on_bdry(jx, dcx) || (dim > 1 && on_bdry(jy, dcy)) || (dim > 2 && on_bdry(jz, dcz));
-    double s = 0.0;
-    if (!bd) {
-      const double* ff = f + fld * nfs;
-      const int bz0 = dim > 2 ? ax.a[2].col_ptr[jz] : 0, bz1 = dim > 2 ? ax.a[2].col_ptr[jz + 1] : 1;
-      const int by0 = dim > 1 ? ax.a[1].col_ptr[jy] : 0, by1 = dim > 1 ? ax.a[1].col_ptr[jy + 1] : 1;
-      const int bx0 = ax.a[0].col_ptr[jx], bx1 = ax.a[0].col_ptr[jx + 1];
-      for (int kz = bz0; kz < bz1; ++kz) {
-        const long long iz = dim > 2 ? ax.a[2].col_idx[kz] : 0;
-        if (dim > 2 && on_bdry(iz, dfz)) continue;
-        const double wz = dim > 2 ? ax.a[2].col_w[kz] : 1.0;
-        for (int ky = by0; ky < by1; ++ky) {
-          const long long iy = dim > 1 ? ax.a[1].col_idx[ky] : 0;
-          if (dim > 1 && on_bdry(iy, dfy)) continue;
-          const double wyz = wz * (dim > 1 ? ax.a[1].col_w[ky] : 1.0);
-          double sxs = 0.0;
-          for (int kx = bx0; kx < bx1; ++kx) {
-            const long long ix = ax.a[0].col_idx[kx];
-            if (on_bdry(ix, dfx)) continue;
-            sxs = fma(ax.a[0].col_w[kx], ff[(iz * dfy + iy) * dfx + ix], sxs);
-          }
-          s = fma(wyz, sxs, s);
-        }
-      }
-    }
-    c[t] = s;
+    out[t] = s;
   }
 }
 
@@ -131,25 +87,55 @@ inline unsigned grid_for(long long n) {
   return static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 64)));
 }
 
+template <int AXIS>
+void pass(int F, const long long* in_d, const long long* out_d, const int* ptr, const int* idx, const double* w,
+          bool mask_in, bool mask_out, const double* in, double* out, cudaStream_t s) {
+  const long long total = out_d[0] * out_d[1] * out_d[2] * F;
+  count_launch();
+  axis_pass_kernel<AXIS><<<grid_for(total), 256, 0, s>>>(F, in_d[0], in_d[1], in_d[2], out_d[0], out_d[1], out_d[2],
+                                                         ptr, idx, w, mask_in, mask_out, in, out);
+}
+
+// apply the per-axis CSR maps x, then y, then z (2D: x, y)
+void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const long long* src_d, const long long* dst_d,
+               const double* in, double* out, double* t1, double* t2, cudaStream_t s) {
+  auto P = [&](int a, const int*& ptr, const int*& idx, const double*& w) {
+    if (prolong) {
+      ptr = ax[a].row_ptr;
+      idx = ax[a].row_idx;
+      w = ax[a].row_w;
+    } else {
+      ptr = ax[a].col_ptr;
+      idx = ax[a].col_idx;
+      w = ax[a].col_w;
+    }
+  };
+  const int *ptr, *idx;
+  const double* w;
+  long long d1[3] = {dst_d[0], src_d[1], src_d[2]};
+  P(0, ptr, idx, w);
+  pass<0>(F, src_d, d1, ptr, idx, w, true, false, in, t1, s);
+  if (dim == 2) {
+    P(1, ptr, idx, w);
+    pass<1>(F, d1, dst_d, ptr, idx, w, false, true, t1, out, s);
+    return;
+  }
+  long long d2[3] = {dst_d[0], dst_d[1], src_d[2]};
+  P(1, ptr, idx, w);
+  pass<1>(F, d1, d2, ptr, idx, w, false, false, t1, t2, s);
+  P(2, ptr, idx, w);
+  pass<2>(F, d2, dst_d, ptr, idx, w, false, true, t2, out, s);
+}
+
 }  // namespace
 
 void spatial_prolong(const DevAxisTransfer* ax, int dim, int F, const long long* dc, const long long* df,
-                     const double* coarse, double* fine, cudaStream_t s) {
-  Axes a{};
-  for (int i = 0; i < dim; ++i) a.a[i] = ax[i];
-  const long long total = df[0] * df[1] * df[2] * F;
-  count_launch();
-  spatial_prolong_kernel<<<grid_for(total), 256, 0, s>>>(a, dim, F, dc[0], dc[1], dc[2], df[0], df[1], df[2], coarse,
-                                                          fine);
+                     const double* coarse, double* fine, double* t1, double* t2, cudaStream_t s) {
+  separable(ax, true, dim, F, dc, df, coarse, fine, t1, t2, s);
 }
 void spatial_restrict(const DevAxisTransfer* ax, int dim, int F, const long long* dc, const long long* df,
-                      const double* fine, double* coarse, cudaStream_t s) {
-  Axes a{};
-  for (int i = 0; i < dim; ++i) a.a[i] = ax[i];
-  const long long total = dc[0] * dc[1] * dc[2] * F;
-  count_launch();
-  spatial_restrict_kernel<<<grid_for(total), 256, 0, s>>>(a, dim, F, dc[0], dc[1], dc[2], df[0], df[1], df[2], fine,
-                                                           coarse);
+                      const double* fine, double* coarse, double* t1, double* t2, cudaStream_t s) {
+  separable(ax, false, dim, F, df, dc, fine, coarse, t1, t2, s);
 }
 void temporal_prolong(const double* T, int Ff, int Fc, long long n_space, const long long* d, int dim,
                       const double* coarse, double* fine, cudaStream_t s) {

@@ -27,7 +27,7 @@ def _dev(cuda, a):
     return cuda.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-MG_CASES = [("C1", None), ("C2", 1), ("C2", 2), ("C3", 0), ("C3", 1)]
+MG_CASES = [("C1", None), ("C2", 1), ("C2", 2), ("C3", 0), ("C3", 1), ("C5-4", None), ("C5-8", None)]
 
 
 @pytest.mark.parametrize("name,r", MG_CASES)
@@ -92,7 +92,7 @@ def test_vcycle_matches_reference(cuda, ref, name, r):
     assert _rel(got, R.vcycle(res)) <= 1e-9
 
 
-@pytest.mark.parametrize("name,r", [("C1", None), ("C2", 1), ("C2", 2), ("C3", 1)])
+@pytest.mark.parametrize("name,r", [("C1", None), ("C2", 1), ("C2", 2), ("C3", 1), ("C5-4", None), ("C5-8", None)])
 def test_gmres_solve_matches_reference(cuda, ref, name, r):
     """STMG-preconditioned GMRES on the manufactured slab RHS: iteration
     count within +-1 and solution relative difference <= 1e-8."""

@@ -59,35 +59,33 @@ __device__ __forceinline__ LocalDof local_dof(const DevASM& A, long long cx, lon
   return d;
 }
 
-// solve (TM + lam TA) x = b for n_t <= 4, partial pivoting, in registers
+// solve (TM + lam TA) x = b for n_t <= 4, partial pivoting, fully unrolled so
+// everything stays in registers (padded to 4 with an identity block)
 __device__ __forceinline__ void small_solve(const double* TM, const double* TA, double lam, int nt, double* b) {
   double a[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) a[i][j] = (i < nt && j < nt) ? fma(lam, TA[i * nt + j], TM[i * nt + j]) : 0.0;
+    for (int j = 0; j < 4; ++j) a[i][j] = (i < nt && j < nt) ? fma(lam, TA[i * nt + j], TM[i * nt + j]) : (i == j);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (k >= nt) break;
-    int piv = k;
 #pragma unroll
-    for (int i = k + 1; i < 4; ++i)
-      if (i < nt && fabs(a[i][k]) > fabs(a[piv][k])) piv = i;
-    if (piv != k) {
+    for (int i = k + 1; i < 4; ++i) {
+      if (fabs(a[i][k]) > fabs(a[k][k])) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double t = a[k][j];
-        a[k][j] = a[piv][j];
-        a[piv][j] = t;
+        for (int j = 0; j < 4; ++j) {
+          const double t = a[k][j];
+          a[k][j] = a[i][j];
+          a[i][j] = t;
+        }
+        const double t = b[k];
+        b[k] = b[i];
+        b[i] = t;
       }
-      const double t = b[k];
-      b[k] = b[piv];
-      b[piv] = t;
     }
     const double inv = 1.0 / a[k][k];
 #pragma unroll
     for (int i = k + 1; i < 4; ++i) {
-      if (i >= nt) break;
       const double f = a[i][k] * inv;
 #pragma unroll
       for (int j = k; j < 4; ++j) a[i][j] = fma(-f, a[k][j], a[i][j]);
@@ -96,11 +94,9 @@ __device__ __forceinline__ void small_solve(const double* TM, const double* TA, 
   }
 #pragma unroll
   for (int i = 3; i >= 0; --i) {
-    if (i >= nt) continue;
     double s = b[i];
 #pragma unroll
-    for (int j = i + 1; j < 4; ++j)
-      if (j < nt) s = fma(-a[i][j], b[j], s);
+    for (int j = i + 1; j < 4; ++j) s = fma(-a[i][j], b[j], s);
     b[i] = s / a[i][i];
   }
 }
@@ -151,19 +147,23 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 //                      the row-wise smem reads bank-conflict free)
 // and the weighted result is scatter-added into z (Dirichlet rows: r).
 template <int M, int NT>
-__global__ void __launch_bounds__(((M + 31) / 32) * 32) asm_apply_tma_kernel(const __grid_constant__ DevASM A,
+__global__ void __launch_bounds__(2 * (((M + 31) / 32) * 32)) asm_apply_tma_kernel(const __grid_constant__ DevASM A,
                                                                              const double* __restrict__ r,
                                                                              double* __restrict__ z) {
   constexpr int XS = (M * M + 1) & ~1;       // per-cell stride in doubles (16 B multiple)
   constexpr int ROT = (M % 2 == 0) ? 1 : 2;  // rotation: (M + ROT) odd -> conflict-free rows
+  constexpr int T2 = ((M + 31) / 32) * 32;   // threads per half; the two halves split every reduction
+  constexpr int HALF = M / 2;
   extern __shared__ __align__(128) double sm[];
   double* Xb0 = sm;
   double* Xb1 = sm + XS;
   double* rs = Xb1 + XS;         // [M][4]  residual of the block, dof-major
   double* hs = rs + 4 * M;       // [M][4] hat z, eigen-index major
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(hs + 4 * M);
-  const long long n_cells = A.cells[0] * A.cells[1] * A.cells[2];
+  double* part = hs + 4 * M;     // [M][4] partial sums of the second half
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(part + 4 * M);
+  const long long n_cells = A.n_list;  // list positions (all cells when A.list == nullptr)
   const int t = threadIdx.x;
+  const int h = t / T2, tl = t - h * T2;
   // bulk copies move whole 16-byte granules: copy the padded per-cell stride
   constexpr unsigned XBYTES = static_cast<unsigned>(XS * sizeof(double));
   static_assert(XBYTES % 16 == 0, "TMA bulk copy size must be a multiple of 16 bytes");
@@ -195,9 +195,9 @@ __global__ void __launch_bounds__(((M + 31) / 32) * 32) asm_apply_tma_kernel(con
     const long long cx = cidx % cxn, cy = (cidx / cxn) % cyn, cz = cidx / (cxn * cyn);
     LocalDof d{};
     double lam = 0.0;
-    if (t < M) {
-      d = local_dof(A, cx, cy, cz, t);
-      lam = A.lam[cell * M + t];
+    if (tl < M) {
+      d = local_dof(A, cx, cy, cz, tl);
+      lam = A.lam[cell * M + tl];
     }
     if (buf == 0) {
       mbar_wait(&bar[0], ph0);
@@ -208,66 +208,81 @@ __global__ void __launch_bounds__(((M + 31) / 32) * 32) asm_apply_tma_kernel(con
     }
     const double* Xs = buf ? Xb1 : Xb0;
     for (int s = 0; s < A.S; ++s) {
-      if (t < M) {
+      if (h == 0 && tl < M) {
 #pragma unroll
-        for (int i = 0; i < NT; ++i) rs[t * 4 + i] = r[(static_cast<long long>(s) * NT + i) * A.n_space + d.g];
+        for (int i = 0; i < NT; ++i) rs[tl * 4 + i] = r[(static_cast<long long>(s) * NT + i) * A.n_space + d.g];
       }
       __syncthreads();
-      if (t < M) {
-        double acc[NT];
-#pragma unroll
-        for (int i = 0; i < NT; ++i) acc[i] = 0.0;
+      // hat r = X^T r: thread (e = tl, half h) sums its half of the rows a
+      {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (tl < M) {
+          const int a0 = h ? HALF : 0, len = h ? M - HALF : HALF;
+          const double* xcol = Xs + a0 * M + tl;
+          const double* rrow = rs + a0 * 4;
 #pragma unroll 16
-        for (int a = 0; a < M; ++a) {
-          const double x = Xs[a * M + t];
-          const double2 r01 = *reinterpret_cast<const double2*>(rs + a * 4);
-          acc[0] = fma(x, r01.x, acc[0]);
-          if (NT > 1) acc[1] = fma(x, r01.y, acc[1]);
-          if (NT > 2) {
-            const double2 r23 = *reinterpret_cast<const double2*>(rs + a * 4 + 2);
-            acc[2] = fma(x, r23.x, acc[2]);
-            if (NT > 3) acc[3] = fma(x, r23.y, acc[3]);
+          for (int a = 0; a < M - HALF; ++a) {
+            if (a >= len) break;
+            const double x = xcol[a * M];
+            const double2 r01 = *reinterpret_cast<const double2*>(rrow + a * 4);
+            acc[0] = fma(x, r01.x, acc[0]);
+            if (NT > 1) acc[1] = fma(x, r01.y, acc[1]);
+            if (NT > 2) {
+              const double2 r23 = *reinterpret_cast<const double2*>(rrow + a * 4 + 2);
+              acc[2] = fma(x, r23.x, acc[2]);
+              if (NT > 3) acc[3] = fma(x, r23.y, acc[3]);
+            }
+          }
+          if (h) *reinterpret_cast<double4*>(part + tl * 4) = make_double4(acc[0], acc[1], acc[2], acc[3]);
+        }
+        __syncthreads();
+        if (!h && tl < M) {
+          const double4 o = *reinterpret_cast<const double4*>(part + tl * 4);
+          double b4[4] = {acc[0] + o.x, acc[1] + o.y, acc[2] + o.z, acc[3] + o.w};
+          small_solve(A.TM, A.TA, lam, NT, b4);
+          *reinterpret_cast<double4*>(hs + tl * 4) = make_double4(b4[0], b4[1], b4[2], b4[3]);
+        }
+        __syncthreads();
+      }
+      // z_T = X hat z: thread (a = tl, half h) sums its half of the columns e,
+      // starting at a rotated offset (bank-conflict-free row reads)
+      {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (tl < M) {
+          const int e0 = h ? HALF : 0, len = h ? M - HALF : HALF;
+          int e = (ROT * tl) % len;
+          const double* xrow = Xs + tl * M + e0;
+          const double* hrow = hs + e0 * 4;
+#pragma unroll 16
+          for (int j = 0; j < M - HALF; ++j) {
+            if (j < len) {
+              const double x = xrow[e];
+              const double2 h01 = *reinterpret_cast<const double2*>(hrow + e * 4);
+              acc[0] = fma(x, h01.x, acc[0]);
+              if (NT > 1) acc[1] = fma(x, h01.y, acc[1]);
+              if (NT > 2) {
+                const double2 h23 = *reinterpret_cast<const double2*>(hrow + e * 4 + 2);
+                acc[2] = fma(x, h23.x, acc[2]);
+                if (NT > 3) acc[3] = fma(x, h23.y, acc[3]);
+              }
+              e = (e + 1 == len) ? 0 : e + 1;
+            }
+          }
+          if (h) *reinterpret_cast<double4*>(part + tl * 4) = make_double4(acc[0], acc[1], acc[2], acc[3]);
+        }
+        __syncthreads();
+        if (!h && tl < M) {
+          const double4 o = *reinterpret_cast<const double4*>(part + tl * 4);
+          const double sum[4] = {acc[0] + o.x, acc[1] + o.y, acc[2] + o.z, acc[3] + o.w};
+          const double w = 1.0 / d.mult;
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            const double v = d.bdry ? rs[tl * 4 + i] : sum[i];
+            atomicAdd(z + (static_cast<long long>(s) * NT + i) * A.n_space + d.g, v * w);
           }
         }
-        double b4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int i = 0; i < NT; ++i) b4[i] = acc[i];
-        small_solve(A.TM, A.TA, lam, NT, b4);
-#pragma unroll
-        for (int i = 0; i < NT; ++i) hs[t * 4 + i] = b4[i];
+        __syncthreads();
       }
-      __syncthreads();
-      if (t < M) {
-        double acc[NT];
-#pragma unroll
-        for (int i = 0; i < NT; ++i) acc[i] = 0.0;
-        // row t of X in rotated column order (bank-conflict free), as two
-        // linear runs: e = e0 .. M-1, then 0 .. e0-1
-        const int e0 = (ROT * t) % M;
-        const double* xrow = Xs + t * M;
-        auto body = [&](int e) {
-          const double x = xrow[e];
-          const double2 h01 = *reinterpret_cast<const double2*>(hs + e * 4);
-          acc[0] = fma(x, h01.x, acc[0]);
-          if (NT > 1) acc[1] = fma(x, h01.y, acc[1]);
-          if (NT > 2) {
-            const double2 h23 = *reinterpret_cast<const double2*>(hs + e * 4 + 2);
-            acc[2] = fma(x, h23.x, acc[2]);
-            if (NT > 3) acc[3] = fma(x, h23.y, acc[3]);
-          }
-        };
-#pragma unroll 8
-        for (int e = e0; e < M; ++e) body(e);
-#pragma unroll 8
-        for (int e = 0; e < e0; ++e) body(e);
-        const double w = 1.0 / d.mult;
-#pragma unroll
-        for (int i = 0; i < NT; ++i) {
-          const double v = d.bdry ? rs[t * 4 + i] : acc[i];
-          atomicAdd(z + (static_cast<long long>(s) * NT + i) * A.n_space + d.g, v * w);
-        }
-      }
-      __syncthreads();
     }
     buf ^= 1;
   }
@@ -410,8 +425,8 @@ namespace {
 template <int M, int NT>
 void launch_asm(const DevASM& A, const double* r, double* z, cudaStream_t s) {
   constexpr int XS = (M * M + 1) & ~1;
-  constexpr int T = ((M + 31) / 32) * 32;
-  const size_t smem = sizeof(double) * (2 * XS + 8 * M) + 2 * sizeof(unsigned long long);
+  constexpr int T = 2 * (((M + 31) / 32) * 32);
+  const size_t smem = sizeof(double) * (2 * XS + 12 * M) + 2 * sizeof(unsigned long long);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(asm_apply_tma_kernel<M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -288,6 +288,120 @@ __global__ void __launch_bounds__(2 * (((M + 31) / 32) * 32)) asm_apply_tma_kern
   }
 }
 
+// Tensor-core variant for m = 64 (3D Q3 cells): both block products run on
+// the FP64 tensor cores (mma.sync.m8n8k4.f64), all S*n_t step columns of the
+// slab batched into the 8 MMA columns. X is stored XOR-swizzled per cell
+// (swz64) so the A-fragment loads of both X^T r and X z are bank-conflict
+// free. 8 warps: warp w owns rows [8w, 8w+8) of each product; the k loop is
+// split into two independent accumulator chains.
+__host__ __device__ __forceinline__ int swz64(int a, int e) { return a * 64 + (e ^ ((a & 7) << 2)); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constant__ DevASM A,
+                                                            const double* __restrict__ r, double* __restrict__ z) {
+  constexpr int M = 64, XS = M * M;
+  extern __shared__ __align__(128) double sm[];
+  double* Xb0 = sm;
+  double* Xb1 = sm + XS;
+  double* rs = Xb1 + XS;  // [M][8] block residual, columns s*NT+i
+  double* hs = rs + 8 * M;  // [M][8] hat r / hat z
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(hs + 8 * M);
+  const long long n_pos = A.n_list;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ncol = A.S * NT;  // <= 8
+  constexpr unsigned XBYTES = static_cast<unsigned>(XS * sizeof(double));
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  long long pos = blockIdx.x;
+  if (t == 0 && pos < n_pos) {
+    mbar_expect_tx(&bar[0], XBYTES);
+    bulk_g2s(Xb0, A.X + pos * A.xs, XBYTES, &bar[0]);
+  }
+  unsigned ph0 = 0, ph1 = 0;
+  int buf = 0;
+  const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
+  for (; pos < n_pos; pos += gridDim.x) {
+    const long long next = pos + gridDim.x;
+    if (t == 0 && next < n_pos) {
+      fence_proxy_async();
+      unsigned long long* b = &bar[buf ^ 1];
+      mbar_expect_tx(b, XBYTES);
+      bulk_g2s(buf ? Xb0 : Xb1, A.X + next * A.xs, XBYTES, b);
+    }
+    const unsigned cidx = static_cast<unsigned>(A.list ? A.list[pos] : pos);
+    const long long cx = cidx % cxn, cy = (cidx / cxn) % cyn, cz = cidx / (cxn * cyn);
+    // gather the block residual of every step (column c = s*NT + i)
+    if (t < M) {
+      const LocalDof d = local_dof(A, cx, cy, cz, t);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) rs[t * 8 + c] = c < ncol ? r[static_cast<long long>(c) * A.n_space + d.g] : 0.0;
+    }
+    if (buf == 0) {
+      mbar_wait(&bar[0], ph0);
+      ph0 ^= 1;
+    } else {
+      mbar_wait(&bar[1], ph1);
+      ph1 ^= 1;
+    }
+    __syncthreads();
+    const double* Xs = buf ? Xb1 : Xb0;
+    const int row = warp * 8 + (lane >> 2), col = (lane & 3) * 2;
+    {
+      // hat r (e x 8) = X^T r: A[row=e][k=a] = X[a][e]
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < M / 4; kt += 2) {
+        const int a0 = kt * 4 + (lane & 3), a1 = a0 + 4;
+        dmma(d00, d01, Xs[swz64(a0, row)], rs[a0 * 8 + (lane >> 2)]);
+        dmma(d10, d11, Xs[swz64(a1, row)], rs[a1 * 8 + (lane >> 2)]);
+      }
+      *reinterpret_cast<double2*>(hs + row * 8 + col) = make_double2(d00 + d10, d01 + d11);
+    }
+    __syncthreads();
+    if (t < M) {
+      // (T_M + lam_e T_A)^-1 per eigen-index e = t and step
+      const double lam = A.lam[pos * M + t];
+      for (int s = 0; s < A.S; ++s) {
+        double b4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < NT; ++i) b4[i] = hs[t * 8 + s * NT + i];
+        small_solve(A.TM, A.TA, lam, NT, b4);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) hs[t * 8 + s * NT + i] = b4[i];
+      }
+    }
+    __syncthreads();
+    {
+      // z_T (a x 8) = X hat z: A[row=a][k=e] = X[a][e]
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < M / 4; kt += 2) {
+        const int e0 = kt * 4 + (lane & 3), e1 = e0 + 4;
+        dmma(d00, d01, Xs[swz64(row, e0)], hs[e0 * 8 + (lane >> 2)]);
+        dmma(d10, d11, Xs[swz64(row, e1)], hs[e1 * 8 + (lane >> 2)]);
+      }
+      const LocalDof d = local_dof(A, cx, cy, cz, row);
+      const double w = 1.0 / d.mult;
+      const double v0 = d.bdry ? rs[row * 8 + col] : d00 + d10;
+      const double v1 = d.bdry ? rs[row * 8 + col + 1] : d01 + d11;
+      if (col < ncol) atomicAdd(z + static_cast<long long>(col) * A.n_space + d.g, v0 * w);
+      if (col + 1 < ncol) atomicAdd(z + static_cast<long long>(col + 1) * A.n_space + d.g, v1 * w);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+}
+
 // column b of every cell matrix from one probe of colour (cx,cy,cz) mod period
 __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx, int coly, int colz, int period,
                                      const double* __restrict__ probe, double* __restrict__ cellmat) {
@@ -415,7 +529,7 @@ __global__ void back_transform_kernel(int m, long long xs, const double* __restr
     const int a = i / m, e = i % m;
     double s = 0.0;
     for (int k = a; k < m; ++k) s = fma(Lc[static_cast<long long>(k) * m + a], Vc[static_cast<long long>(e) * m + k], s);
-    Xc[i] = s;
+    Xc[m == 64 ? swz64(a, e) : i] = s;
   }
 }
 
@@ -455,6 +569,36 @@ void launch_asm_nt(const DevASM& A, const double* r, double* z, cudaStream_t s) 
 }
 }  // namespace
 
+namespace {
+template <int NT>
+void launch_mma(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (2 * 64 * 64 + 16 * 64) + 2 * sizeof(unsigned long long);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(asm_apply_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = true;
+  }
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_mma_kernel<NT>, 256, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (A.n_list == 0) return;
+  const long long grid = std::max<long long>(1, std::min<long long>(A.n_list, static_cast<long long>(std::max(per_sm, 1)) * sms));
+  count_launch();
+  asm_apply_mma_kernel<NT><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z);
+}
+void launch_asm_mma(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+  if (A.S * A.nt > 8) throw std::invalid_argument("ASMSmoother: S * n_t must be <= 8");
+  switch (A.nt) {
+    case 1: launch_mma<1>(A, r, z, s); break;
+    case 2: launch_mma<2>(A, r, z, s); break;
+    case 3: launch_mma<3>(A, r, z, s); break;
+    case 4: launch_mma<4>(A, r, z, s); break;
+    default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
+  }
+}
+}  // namespace
+
 void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_t s) {
   switch (A.m) {
     case 4: launch_asm_nt<4>(A, r, z, s); break;
@@ -463,7 +607,7 @@ void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_
     case 16: launch_asm_nt<16>(A, r, z, s); break;
     case 25: launch_asm_nt<25>(A, r, z, s); break;
     case 27: launch_asm_nt<27>(A, r, z, s); break;
-    case 64: launch_asm_nt<64>(A, r, z, s); break;
+    case 64: launch_asm_mma(A, r, z, s); break;
     default: throw std::invalid_argument("ASMSmoother: unsupported cell block size");
   }
 }

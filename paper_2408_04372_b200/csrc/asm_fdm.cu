@@ -97,7 +97,7 @@ __device__ __forceinline__ int lbase(int line) {
 
 template <int DIM, int N, int NT>
 __global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ DevFDM P, const double* __restrict__ r,
-                                                      double* __restrict__ z) {
+                                                      double* __restrict__ z, double scale) {
   using C = FCfg<DIM, N>;
   constexpr int ND = C::ND, LINES = C::LINES, NC = C::NC;
   extern __shared__ __align__(16) double sm[];
@@ -219,14 +219,14 @@ __global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ Dev
       if ((ly == 0 && !(m & 4)) || (ly == N - 1 && !(m & 8))) mult *= 2.0;
       if (DIM == 3 && ((lz == 0 && !(m & 16)) || (lz == N - 1 && !(m & 32)))) mult *= 2.0;
       const double v = bd ? R[idx] : W[idx];
-      atomicAdd(z + (static_cast<long long>(s) * NT + i) * P.n_space + g, v / mult);
+      atomicAdd(z + (static_cast<long long>(s) * NT + i) * P.n_space + g, scale * v / mult);
     }
     __syncthreads();
   }
 }
 
 template <int DIM, int N, int NT>
-void launch(const DevFDM& P, const double* r, double* z, cudaStream_t s) {
+void launch(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
   using C = FCfg<DIM, N>;
   const size_t smem = sizeof(double) * (2 * C::NC * NT * C::ND + C::NC) + sizeof(long long) * C::NC + sizeof(int) * C::NC;
   static bool configured = false;
@@ -236,33 +236,33 @@ void launch(const DevFDM& P, const double* r, double* z, cudaStream_t s) {
   }
   const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
   count_launch();
-  asm_fdm_kernel<DIM, N, NT><<<static_cast<unsigned>((n_cells + C::NC - 1) / C::NC), kT, smem, s>>>(P, r, z);
+  asm_fdm_kernel<DIM, N, NT><<<static_cast<unsigned>((n_cells + C::NC - 1) / C::NC), kT, smem, s>>>(P, r, z, scale);
 }
 
 template <int DIM, int N>
-void launch_nt(const DevFDM& P, const double* r, double* z, cudaStream_t s) {
+void launch_nt(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
   switch (P.nt) {
-    case 1: launch<DIM, N, 1>(P, r, z, s); break;
-    case 2: launch<DIM, N, 2>(P, r, z, s); break;
-    case 3: launch<DIM, N, 3>(P, r, z, s); break;
-    case 4: launch<DIM, N, 4>(P, r, z, s); break;
+    case 1: launch<DIM, N, 1>(P, r, z, scale, s); break;
+    case 2: launch<DIM, N, 2>(P, r, z, scale, s); break;
+    case 3: launch<DIM, N, 3>(P, r, z, scale, s); break;
+    case 4: launch<DIM, N, 4>(P, r, z, scale, s); break;
     default: throw std::invalid_argument("FDM smoother: n_t must be in [1, 4]");
   }
 }
 
 }  // namespace
 
-void fdm_add_correction(const DevFDM& P, const double* r, double* z, cudaStream_t s) {
+void fdm_add_correction(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
   const int key = P.dim * 10 + P.n;
   switch (key) {
-    case 22: launch_nt<2, 2>(P, r, z, s); break;
-    case 23: launch_nt<2, 3>(P, r, z, s); break;
-    case 24: launch_nt<2, 4>(P, r, z, s); break;
-    case 25: launch_nt<2, 5>(P, r, z, s); break;
-    case 32: launch_nt<3, 2>(P, r, z, s); break;
-    case 33: launch_nt<3, 3>(P, r, z, s); break;
-    case 34: launch_nt<3, 4>(P, r, z, s); break;
-    case 35: launch_nt<3, 5>(P, r, z, s); break;
+    case 22: launch_nt<2, 2>(P, r, z, scale, s); break;
+    case 23: launch_nt<2, 3>(P, r, z, scale, s); break;
+    case 24: launch_nt<2, 4>(P, r, z, scale, s); break;
+    case 25: launch_nt<2, 5>(P, r, z, scale, s); break;
+    case 32: launch_nt<3, 2>(P, r, z, scale, s); break;
+    case 33: launch_nt<3, 3>(P, r, z, scale, s); break;
+    case 34: launch_nt<3, 4>(P, r, z, scale, s); break;
+    case 35: launch_nt<3, 5>(P, r, z, scale, s); break;
     default: throw std::invalid_argument("FDM smoother: unsupported dim/p");
   }
 }

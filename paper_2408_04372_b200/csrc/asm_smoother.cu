@@ -149,7 +149,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 template <int M, int NT>
 __global__ void __launch_bounds__(2 * (((M + 31) / 32) * 32)) asm_apply_tma_kernel(const __grid_constant__ DevASM A,
                                                                              const double* __restrict__ r,
-                                                                             double* __restrict__ z) {
+                                                                             double* __restrict__ z, double scale) {
   constexpr int XS = (M * M + 1) & ~1;       // per-cell stride in doubles (16 B multiple)
   constexpr int ROT = (M % 2 == 0) ? 1 : 2;  // rotation: (M + ROT) odd -> conflict-free rows
   constexpr int T2 = ((M + 31) / 32) * 32;   // threads per half; the two halves split every reduction
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(2 * (((M + 31) / 32) * 32)) asm_apply_tma_kern
         if (!h && tl < M) {
           const double4 o = *reinterpret_cast<const double4*>(part + tl * 4);
           const double sum[4] = {acc[0] + o.x, acc[1] + o.y, acc[2] + o.z, acc[3] + o.w};
-          const double w = 1.0 / d.mult;
+          const double w = scale / d.mult;
 #pragma unroll
           for (int i = 0; i < NT; ++i) {
             const double v = d.bdry ? rs[tl * 4 + i] : sum[i];
@@ -304,7 +304,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 template <int NT>
 __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constant__ DevASM A,
-                                                            const double* __restrict__ r, double* __restrict__ z) {
+                                                            const double* __restrict__ r, double* __restrict__ z,
+                                                            double scale) {
   constexpr int M = 64, XS = M * M;
   extern __shared__ __align__(128) double sm[];
   double* Xb0 = sm;
@@ -330,6 +331,24 @@ __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constan
   unsigned ph0 = 0, ph1 = 0;
   int buf = 0;
   const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
+  struct Col8 {
+    double v[8];
+  };
+  // block residual of list position q for local dof t (columns s*NT + i)
+  auto gather = [&](long long q) {
+    Col8 o;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o.v[c] = 0.0;
+    if (t < M) {
+      const unsigned ci = static_cast<unsigned>(A.list ? A.list[q] : q);
+      const LocalDof d = local_dof(A, ci % cxn, (ci / cxn) % cyn, ci / (cxn * cyn), t);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < ncol) o.v[c] = __ldg(r + static_cast<long long>(c) * A.n_space + d.g);
+    }
+    return o;
+  };
+  Col8 rnext;
   for (; pos < n_pos; pos += gridDim.x) {
     const long long next = pos + gridDim.x;
     if (t == 0 && next < n_pos) {
@@ -340,12 +359,15 @@ __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constan
     }
     const unsigned cidx = static_cast<unsigned>(A.list ? A.list[pos] : pos);
     const long long cx = cidx % cxn, cy = (cidx / cxn) % cyn, cz = cidx / (cxn * cyn);
-    // gather the block residual of every step (column c = s*NT + i)
+    // the block residual of this cell was prefetched into registers during
+    // the previous iteration (first cell: load now); stage it, then prefetch
+    // the next cell's so its gather latency hides behind this cell's MMAs
+    if (pos == blockIdx.x) rnext = gather(pos);
     if (t < M) {
-      const LocalDof d = local_dof(A, cx, cy, cz, t);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) rs[t * 8 + c] = c < ncol ? r[static_cast<long long>(c) * A.n_space + d.g] : 0.0;
+      for (int c = 0; c < 8; ++c) rs[t * 8 + c] = c < ncol ? rnext.v[c] : 0.0;
     }
+    if (next < n_pos) rnext = gather(next);
     if (buf == 0) {
       mbar_wait(&bar[0], ph0);
       ph0 ^= 1;
@@ -391,7 +413,7 @@ __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constan
         dmma(d10, d11, Xs[swz64(row, e1)], hs[e1 * 8 + (lane >> 2)]);
       }
       const LocalDof d = local_dof(A, cx, cy, cz, row);
-      const double w = 1.0 / d.mult;
+      const double w = scale / d.mult;
       const double v0 = d.bdry ? rs[row * 8 + col] : d00 + d10;
       const double v1 = d.bdry ? rs[row * 8 + col + 1] : d01 + d11;
       if (col < ncol) atomicAdd(z + static_cast<long long>(col) * A.n_space + d.g, v0 * w);
@@ -537,7 +559,7 @@ __global__ void back_transform_kernel(int m, long long xs, const double* __restr
 
 namespace {
 template <int M, int NT>
-void launch_asm(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+void launch_asm(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   constexpr int XS = (M * M + 1) & ~1;
   constexpr int T = 2 * (((M + 31) / 32) * 32);
   const size_t smem = sizeof(double) * (2 * XS + 12 * M) + 2 * sizeof(unsigned long long);
@@ -555,15 +577,15 @@ void launch_asm(const DevASM& A, const double* r, double* z, cudaStream_t s) {
   if (n_cells == 0) return;
   const long long grid = std::max<long long>(1, std::min<long long>(n_cells, static_cast<long long>(std::max(per_sm, 1)) * sms));
   count_launch();
-  asm_apply_tma_kernel<M, NT><<<static_cast<unsigned>(grid), T, smem, s>>>(A, r, z);
+  asm_apply_tma_kernel<M, NT><<<static_cast<unsigned>(grid), T, smem, s>>>(A, r, z, scale);
 }
 template <int M>
-void launch_asm_nt(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+void launch_asm_nt(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   switch (A.nt) {
-    case 1: launch_asm<M, 1>(A, r, z, s); break;
-    case 2: launch_asm<M, 2>(A, r, z, s); break;
-    case 3: launch_asm<M, 3>(A, r, z, s); break;
-    case 4: launch_asm<M, 4>(A, r, z, s); break;
+    case 1: launch_asm<M, 1>(A, r, z, scale, s); break;
+    case 2: launch_asm<M, 2>(A, r, z, scale, s); break;
+    case 3: launch_asm<M, 3>(A, r, z, scale, s); break;
+    case 4: launch_asm<M, 4>(A, r, z, scale, s); break;
     default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
   }
 }
@@ -571,7 +593,7 @@ void launch_asm_nt(const DevASM& A, const double* r, double* z, cudaStream_t s) 
 
 namespace {
 template <int NT>
-void launch_mma(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+void launch_mma(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   const size_t smem = sizeof(double) * (2 * 64 * 64 + 16 * 64) + 2 * sizeof(unsigned long long);
   static bool configured = false;
   if (!configured) {
@@ -585,29 +607,29 @@ void launch_mma(const DevASM& A, const double* r, double* z, cudaStream_t s) {
   if (A.n_list == 0) return;
   const long long grid = std::max<long long>(1, std::min<long long>(A.n_list, static_cast<long long>(std::max(per_sm, 1)) * sms));
   count_launch();
-  asm_apply_mma_kernel<NT><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z);
+  asm_apply_mma_kernel<NT><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
 }
-void launch_asm_mma(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+void launch_asm_mma(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if (A.S * A.nt > 8) throw std::invalid_argument("ASMSmoother: S * n_t must be <= 8");
   switch (A.nt) {
-    case 1: launch_mma<1>(A, r, z, s); break;
-    case 2: launch_mma<2>(A, r, z, s); break;
-    case 3: launch_mma<3>(A, r, z, s); break;
-    case 4: launch_mma<4>(A, r, z, s); break;
+    case 1: launch_mma<1>(A, r, z, scale, s); break;
+    case 2: launch_mma<2>(A, r, z, scale, s); break;
+    case 3: launch_mma<3>(A, r, z, scale, s); break;
+    case 4: launch_mma<4>(A, r, z, scale, s); break;
     default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
   }
 }
 }  // namespace
 
-void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_t s) {
+void asm_add_correction(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   switch (A.m) {
-    case 4: launch_asm_nt<4>(A, r, z, s); break;
-    case 8: launch_asm_nt<8>(A, r, z, s); break;
-    case 9: launch_asm_nt<9>(A, r, z, s); break;
-    case 16: launch_asm_nt<16>(A, r, z, s); break;
-    case 25: launch_asm_nt<25>(A, r, z, s); break;
-    case 27: launch_asm_nt<27>(A, r, z, s); break;
-    case 64: launch_asm_mma(A, r, z, s); break;
+    case 4: launch_asm_nt<4>(A, r, z, scale, s); break;
+    case 8: launch_asm_nt<8>(A, r, z, scale, s); break;
+    case 9: launch_asm_nt<9>(A, r, z, scale, s); break;
+    case 16: launch_asm_nt<16>(A, r, z, scale, s); break;
+    case 25: launch_asm_nt<25>(A, r, z, scale, s); break;
+    case 27: launch_asm_nt<27>(A, r, z, scale, s); break;
+    case 64: launch_asm_mma(A, r, z, scale, s); break;
     default: throw std::invalid_argument("ASMSmoother: unsupported cell block size");
   }
 }

@@ -9,6 +9,8 @@ namespace stmgb {
 
 // y = S u (overwrite), fused space-time operator -- st_operator.cu
 void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream);
+// r = f - S u (overwrite), fused residual (no separate subtraction pass)
+void st_residual(const DevLevel& L, const double* f, const double* u, double* r, cudaStream_t stream);
 
 // ---- vector kernels (vector_ops.cu)
 void vec_copy(double* y, const double* x, long long n, cudaStream_t s);
@@ -45,13 +47,14 @@ struct DevAxisTransfer {
   long long nf, nc;
 };
 // separable per-axis passes; t1/t2 are work buffers of Transfer-chosen size
+// accumulate: fine += P coarse instead of fine = P coarse
 void spatial_prolong(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
-                     const double* coarse, double* fine, double* t1, double* t2, cudaStream_t s);
+                     const double* coarse, double* fine, double* t1, double* t2, bool accumulate, cudaStream_t s);
 void spatial_restrict(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
                       const double* fine, double* coarse, double* t1, double* t2, cudaStream_t s);
 // temporal: fine block r = sum_c T[r][c] coarse block c (T row-major Ff x Fc)
 void temporal_prolong(const double* T_dev, int Ff, int Fc, long long n_space, const long long* dofs, int dim,
-                      const double* coarse, double* fine, cudaStream_t s);
+                      const double* coarse, double* fine, bool accumulate, cudaStream_t s);
 void temporal_restrict(const double* T_dev, int Ff, int Fc, long long n_space, const long long* dofs, int dim,
                        const double* fine, double* coarse, cudaStream_t s);
 
@@ -68,7 +71,8 @@ struct DevASM {
   const long long* list;  // cells handled (X/lam stored per list entry); nullptr = all cells
   long long n_list;       // number of handled cells
 };
-void asm_add_correction(const DevASM& A, const double* r, double* z, cudaStream_t s);
+// z += scale * W sum_T R_T^T B_T^-1 R_T r
+void asm_add_correction(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s);
 
 // tensor-product FDM cell solves on Cartesian levels (asm_fdm.cu)
 struct DevFDM {
@@ -82,7 +86,7 @@ struct DevFDM {
   long long cells0[3];
   const unsigned char* skip;      // per cell: 1 = solved by the exact per-cell kernel
 };
-void fdm_add_correction(const DevFDM& F, const double* r, double* z, cudaStream_t s);
+void fdm_add_correction(const DevFDM& F, const double* r, double* z, double scale, cudaStream_t s);
 // probing-based extraction of restricted cell matrices (setup)
 void asm_extract_probe(const DevASM& A, int colour_x, int colour_y, int colour_z, int period, const double* probe,
                        double* cellmat, cudaStream_t s);

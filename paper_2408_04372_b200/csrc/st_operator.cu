@@ -17,7 +17,8 @@ namespace {
 // faces of the lattice directly (edges/corners written more than once with
 // the same value)
 __global__ void boundary_identity_kernel(int dim, long long dx, long long dy, long long dz, long long n_space, int F,
-                                         const double* __restrict__ u, double* __restrict__ y) {
+                                         const double* __restrict__ f, const double* __restrict__ u,
+                                         double* __restrict__ y) {
   // faces: x=0, x=dx-1 (dy*dz each), y=0, y=dy-1 (dx*dz), z=0, z=dz-1 (dx*dy)
   const long long fx = dy * dz, fy = dx * dz, fz = dim == 3 ? dx * dy : 0;
   const long long total = 2 * (fx + fy + fz);
@@ -36,25 +37,37 @@ __global__ void boundary_identity_kernel(int dim, long long dx, long long dy, lo
       const long long side = r / fz, k = r % fz;
       g = (side ? dz - 1 : 0) * dx * dy + k;
     }
-    for (int f = 0; f < F; ++f) y[f * n_space + g] = u[f * n_space + g];
+    // apply: y_b = u_b; residual: y_b = f_b - u_b
+    for (int k = 0; k < F; ++k) y[k * n_space + g] = f ? f[k * n_space + g] - u[k * n_space + g] : u[k * n_space + g];
   }
 }
 
 }  // namespace
 
-void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream) {
-  cudaMemsetAsync(y, 0, sizeof(double) * L.n_dofs, stream);
+namespace {
+void run(const DevLevel& L, const double* f, const double* u, double* y, cudaStream_t stream) {
+  if (f)
+    vec_copy(y, f, L.n_dofs, stream);
+  else
+    cudaMemsetAsync(y, 0, sizeof(double) * L.n_dofs, stream);
+  const double sign = f ? -1.0 : 1.0;
   count_launch();
   if (L.dim == 2)
-    st_apply_2d(L, u, y, stream);
+    st_apply_2d(L, u, y, sign, stream);
   else if (L.dim == 3)
-    st_apply_3d(L, u, y, stream);
+    st_apply_3d(L, u, y, sign, stream);
   else
     throw std::invalid_argument("st_apply: dim must be 2 or 3");
   const long long faces = 2 * (L.dofs[1] * L.dofs[2] + L.dofs[0] * L.dofs[2] + (L.dim == 3 ? L.dofs[0] * L.dofs[1] : 0));
   const unsigned blocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((faces + 255) / 256, 148LL * 8)));
   count_launch();
-  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dofs[0], L.dofs[1], L.dofs[2], L.n_space, L.F, u, y);
+  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dofs[0], L.dofs[1], L.dofs[2], L.n_space, L.F, f, u, y);
+}
+}  // namespace
+
+void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream) { run(L, nullptr, u, y, stream); }
+void st_residual(const DevLevel& L, const double* f, const double* u, double* r, cudaStream_t stream) {
+  run(L, f, u, r, stream);
 }
 
 }  // namespace stmgb

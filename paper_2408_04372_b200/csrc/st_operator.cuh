@@ -101,7 +101,8 @@ __device__ __forceinline__ int line_base(int line) {
 
 template <int DIM, int N, int F>
 __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_constant__ DevLevel L,
-                                                               const double* __restrict__ u, double* __restrict__ y) {
+                                                               const double* __restrict__ u, double* __restrict__ y,
+                                                               double sign) {
   using C = Cfg<DIM, N, F>;
   constexpr int ND = C::ND, LINES = C::LINES, NC = C::NC, NCF = C::NCF, GEO = C::GEO;
   constexpr int T = kThreads;
@@ -346,12 +347,12 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
     const int m = mask_s[c];
     bool bd = ((m & 1) && lx == 0) || ((m & 2) && lx == N - 1) || ((m & 4) && ly == 0) || ((m & 8) && ly == N - 1);
     if (DIM == 3) bd = bd || ((m & 16) && lz == 0) || ((m & 32) && lz == N - 1);
-    if (!bd) atomicAdd(y + f * L.n_space + base + lz * dxy + ly * dx + lx, V[(c * F + f) * ND + l]);
+    if (!bd) atomicAdd(y + f * L.n_space + base + lz * dxy + ly * dx + lx, sign * V[(c * F + f) * ND + l]);
   }
 }
 
 template <int DIM, int N, int F>
-void launch(const DevLevel& L, const double* u, double* y, cudaStream_t stream) {
+void launch(const DevLevel& L, const double* u, double* y, double sign, cudaStream_t stream) {
   using C = Cfg<DIM, N, F>;
   static bool configured = false;
   if (!configured) {
@@ -361,26 +362,27 @@ void launch(const DevLevel& L, const double* u, double* y, cudaStream_t stream) 
   }
   const long long n_cells = L.cells[0] * L.cells[1] * L.cells[2];
   const long long blocks = (n_cells + C::NC - 1) / C::NC;
-  st_apply_kernel<DIM, N, F><<<static_cast<unsigned>(blocks), kThreads, C::smem_bytes(), stream>>>(L, u, y);
+  st_apply_kernel<DIM, N, F><<<static_cast<unsigned>(blocks), kThreads, C::smem_bytes(), stream>>>(L, u, y, sign);
 }
 
 template <int DIM, int N>
-void launch_f(const DevLevel& L, const double* u, double* y, cudaStream_t s) {
+void launch_f(const DevLevel& L, const double* u, double* y, double sign, cudaStream_t s) {
   switch (L.F) {
-    case 1: launch<DIM, N, 1>(L, u, y, s); break;
-    case 2: launch<DIM, N, 2>(L, u, y, s); break;
-    case 3: launch<DIM, N, 3>(L, u, y, s); break;
-    case 4: launch<DIM, N, 4>(L, u, y, s); break;
-    case 5: launch<DIM, N, 5>(L, u, y, s); break;
-    case 6: launch<DIM, N, 6>(L, u, y, s); break;
-    case 7: launch<DIM, N, 7>(L, u, y, s); break;
-    case 8: launch<DIM, N, 8>(L, u, y, s); break;
+    case 1: launch<DIM, N, 1>(L, u, y, sign, s); break;
+    case 2: launch<DIM, N, 2>(L, u, y, sign, s); break;
+    case 3: launch<DIM, N, 3>(L, u, y, sign, s); break;
+    case 4: launch<DIM, N, 4>(L, u, y, sign, s); break;
+    case 5: launch<DIM, N, 5>(L, u, y, sign, s); break;
+    case 6: launch<DIM, N, 6>(L, u, y, sign, s); break;
+    case 7: launch<DIM, N, 7>(L, u, y, sign, s); break;
+    case 8: launch<DIM, N, 8>(L, u, y, sign, s); break;
   }
 }
 
 }  // namespace stk
 
-void st_apply_2d(const DevLevel& L, const double* u, double* y, cudaStream_t s);
-void st_apply_3d(const DevLevel& L, const double* u, double* y, cudaStream_t s);
+// y += sign * (cell contributions of S u), Dirichlet rows untouched
+void st_apply_2d(const DevLevel& L, const double* u, double* y, double sign, cudaStream_t s);
+void st_apply_3d(const DevLevel& L, const double* u, double* y, double sign, cudaStream_t s);
 
 }  // namespace stmgb

@@ -145,6 +145,11 @@ void SpaceTimeOperator::apply(const double* u, double* y, cudaStream_t stream) c
   st_apply(desc_, u, y, stream);
 }
 
+void SpaceTimeOperator::residual(const double* f, const double* u, double* r, cudaStream_t stream) const {
+  ++apply_count_;
+  st_residual(desc_, f, u, r, stream);
+}
+
 void SpaceTimeOperator::spatial_apply(int kind, const double* u, double* y, cudaStream_t stream) const {
   st_apply(kind == 0 ? mass_desc_ : stiff_desc_, u, y, stream);
 }
@@ -327,10 +332,11 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op) {
   A.lam = lam_.d();
 }
 
-void ASMSmoother::add_correction(const double* residual, double* correction, cudaStream_t stream) const {
+void ASMSmoother::add_correction(const double* residual, double* correction, cudaStream_t stream,
+                                 double scale) const {
   ++sweep_count_;
-  if (use_fdm_) fdm_add_correction(fdm_, residual, correction, stream);
-  if (asm_.n_list > 0) asm_add_correction(asm_, residual, correction, stream);
+  if (use_fdm_) fdm_add_correction(fdm_, residual, correction, scale, stream);
+  if (asm_.n_list > 0) asm_add_correction(asm_, residual, correction, scale, stream);
 }
 
 // --------------------------------------------------------------- Transfer
@@ -444,13 +450,13 @@ Transfer::Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coars
   }
 }
 
-void Transfer::prolong(const double* coarse, double* fine, cudaStream_t stream) const {
+void Transfer::prolong(const double* coarse, double* fine, cudaStream_t stream, bool accumulate) const {
   const DevLevel& df = fine_->desc();
   const DevLevel& dc = coarse_->desc();
   if (spatial_)
-    spatial_prolong(ax_, df.dim, df.F, dc.dofs, df.dofs, coarse, fine, t1_.d(), t2_.d(), stream);
+    spatial_prolong(ax_, df.dim, df.F, dc.dofs, df.dofs, coarse, fine, t1_.d(), t2_.d(), accumulate, stream);
   else
-    temporal_prolong(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, coarse, fine, stream);
+    temporal_prolong(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, coarse, fine, accumulate, stream);
 }
 
 void Transfer::restrict_(const double* fine, double* coarse, cudaStream_t stream) const {
@@ -918,41 +924,32 @@ void SpaceTimeMultigrid::coarse_solve(const double* f, double* u, cudaStream_t s
 }
 
 void SpaceTimeMultigrid::smooth(int l, const double* f, double* u, cudaStream_t s) const {
+  // u += omega * ASM(f - S u) (multigrid.cpp:174-185): fused residual, and the
+  // smoother scatters omega * W * (block solves) straight into u
   const Level& lv = levels_[static_cast<size_t>(l)];
-  const Index n = lv.op->n_dofs();
-  lv.op->apply(u, lv.r.d(), s);
-  vec_sub_into(lv.r.d(), f, lv.r.d(), n, s);
-  vec_fill(lv.z.d(), 0.0, n, s);
-  lv.smoother->add_correction(lv.r.d(), lv.z.d(), s);
-  vec_axpy(u, lv.omega, lv.z.d(), n, s);
+  lv.op->residual(f, u, lv.r.d(), s);
+  lv.smoother->add_correction(lv.r.d(), u, s, lv.omega);
 }
 
 void SpaceTimeMultigrid::v_cycle(int l, const double* f, double* u, cudaStream_t s) const {
   // u enters as zero (multigrid.cpp:219,231), so the first residual is f
   const Level& lv = levels_[static_cast<size_t>(l)];
-  const Index n = lv.op->n_dofs();
   if (l + 1 == n_levels()) {
     coarse_solve(f, u, s);
     return;
   }
   for (int i = 0; i < options_.n_smooth; ++i) {
-    if (i == 0) {
-      // S 0 = 0 exactly: u = omega * ASM(f)
-      vec_fill(lv.z.d(), 0.0, n, s);
-      lv.smoother->add_correction(f, lv.z.d(), s);
-      vec_axpy(u, lv.omega, lv.z.d(), n, s);
-    } else {
+    if (i == 0)
+      lv.smoother->add_correction(f, u, s, lv.omega);  // S 0 = 0 exactly
+    else
       smooth(l, f, u, s);
-    }
   }
-  lv.op->apply(u, lv.r.d(), s);
-  vec_sub_into(lv.r.d(), f, lv.r.d(), n, s);
+  lv.op->residual(f, u, lv.r.d(), s);
   lv.to_coarser->restrict_(lv.r.d(), lv.rc.d(), s);
   const Index nc = levels_[static_cast<size_t>(l) + 1].op->n_dofs();
   vec_fill(lv.ec.d(), 0.0, nc, s);
   v_cycle(l + 1, lv.rc.d(), lv.ec.d(), s);
-  lv.to_coarser->prolong(lv.ec.d(), lv.e.d(), s);
-  vec_axpy(u, 1.0, lv.e.d(), n, s);
+  lv.to_coarser->prolong(lv.ec.d(), u, s, /*accumulate=*/true);
   for (int i = 0; i < options_.n_smooth; ++i) smooth(l, f, u, s);
 }
 

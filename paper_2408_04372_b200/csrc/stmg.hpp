@@ -74,6 +74,8 @@ class SpaceTimeOperator {
   void apply(const double* u, double* y, cudaStream_t stream = nullptr) const;
   // SpatialOperator::apply of the constrained mass (kind 0) or stiffness (1)
   void spatial_apply(int kind, const double* u, double* y, cudaStream_t stream = nullptr) const;
+  // r = f - S u (overwrite), one fused pass
+  void residual(const double* f, const double* u, double* r, cudaStream_t stream = nullptr) const;
   long applications() const { return apply_count_; }
 
  private:
@@ -95,7 +97,8 @@ class ASMSmoother {
   explicit ASMSmoother(const SpaceTimeOperator& op);
   // correction += W sum_T R_T^T B_T^-1 R_T residual (accumulate; the
   // relaxation factor is applied by the caller) -- asm_smoother.cpp:60-78
-  void add_correction(const double* residual, double* correction, cudaStream_t stream = nullptr) const;
+  void add_correction(const double* residual, double* correction, cudaStream_t stream = nullptr,
+                      double scale = 1.0) const;
   int block_size() const { return op_->n_t() * asm_.m; }
   Index n_blocks() const { return static_cast<Index>(op_->n_steps()) * op_->mesh().n_cells(); }
   long sweeps() const { return sweep_count_; }
@@ -121,7 +124,8 @@ class ASMSmoother {
 class Transfer {
  public:
   Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coarse);
-  void prolong(const double* coarse, double* fine, cudaStream_t stream = nullptr) const;    // overwrite
+  // overwrite (accumulate = false, the reference semantics) or fine += P coarse
+  void prolong(const double* coarse, double* fine, cudaStream_t stream = nullptr, bool accumulate = false) const;
   void restrict_(const double* fine, double* coarse, cudaStream_t stream = nullptr) const;  // overwrite
   bool spatial() const { return spatial_; }
 

@@ -25,7 +25,7 @@ __device__ __forceinline__ bool on_bdry(long long i, long long n) { return i == 
 template <int AXIS>
 __global__ void axis_pass_kernel(int F, long long ix, long long iy, long long iz, long long ox, long long oy,
                                  long long oz, const int* __restrict__ ptr, const int* __restrict__ idx,
-                                 const double* __restrict__ w, bool mask_in, bool mask_out,
+                                 const double* __restrict__ w, bool mask_in, bool mask_out, bool accumulate,
                                  const double* __restrict__ in, double* __restrict__ out) {
   const long long on = ox * oy * oz, in_n = ix * iy * iz;
   const long long total = on * F;
@@ -56,13 +56,16 @@ __global__ void axis_pass_kernel(int F, long long ix, long long iy, long long iz
         }
       }
     }
-    out[t] = s;
+    if (accumulate)
+      out[t] += s;
+    else
+      out[t] = s;
   }
 }
 
-__global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bool transpose, long long n_space,
-                                long long dx, long long dy, long long dz, int dim, const double* __restrict__ in,
-                                double* __restrict__ out) {
+__global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bool transpose, bool accumulate,
+                                long long n_space, long long dx, long long dy, long long dz, int dim,
+                                const double* __restrict__ in, double* __restrict__ out) {
   // prolong: out (Ff blocks) = T in (Fc blocks); restrict: out (Fc) = T^T in (Ff)
   const int Fin = transpose ? Ff : Fc, Fout = transpose ? Fc : Ff;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n_space; g += (long long)gridDim.x * blockDim.x) {
@@ -78,7 +81,10 @@ __global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bo
 #pragma unroll
       for (int c = 0; c < kMaxF; ++c)
         if (c < Fin) s = fma(transpose ? T[c * Fc + r] : T[r * Fc + c], x[c], s);
-      out[r * n_space + g] = s;
+      if (accumulate)
+        out[r * n_space + g] += s;
+      else
+        out[r * n_space + g] = s;
     }
   }
 }
@@ -89,16 +95,16 @@ inline unsigned grid_for(long long n) {
 
 template <int AXIS>
 void pass(int F, const long long* in_d, const long long* out_d, const int* ptr, const int* idx, const double* w,
-          bool mask_in, bool mask_out, const double* in, double* out, cudaStream_t s) {
+          bool mask_in, bool mask_out, bool accumulate, const double* in, double* out, cudaStream_t s) {
   const long long total = out_d[0] * out_d[1] * out_d[2] * F;
   count_launch();
   axis_pass_kernel<AXIS><<<grid_for(total), 256, 0, s>>>(F, in_d[0], in_d[1], in_d[2], out_d[0], out_d[1], out_d[2],
-                                                         ptr, idx, w, mask_in, mask_out, in, out);
+                                                         ptr, idx, w, mask_in, mask_out, accumulate, in, out);
 }
 
 // apply the per-axis CSR maps x, then y, then z (2D: x, y)
 void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const long long* src_d, const long long* dst_d,
-               const double* in, double* out, double* t1, double* t2, cudaStream_t s) {
+               const double* in, double* out, double* t1, double* t2, bool accumulate, cudaStream_t s) {
   auto P = [&](int a, const int*& ptr, const int*& idx, const double*& w) {
     if (prolong) {
       ptr = ax[a].row_ptr;
@@ -114,38 +120,40 @@ void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const lo
   const double* w;
   long long d1[3] = {dst_d[0], src_d[1], src_d[2]};
   P(0, ptr, idx, w);
-  pass<0>(F, src_d, d1, ptr, idx, w, true, false, in, t1, s);
+  pass<0>(F, src_d, d1, ptr, idx, w, true, false, false, in, t1, s);
   if (dim == 2) {
     P(1, ptr, idx, w);
-    pass<1>(F, d1, dst_d, ptr, idx, w, false, true, t1, out, s);
+    pass<1>(F, d1, dst_d, ptr, idx, w, false, true, accumulate, t1, out, s);
     return;
   }
   long long d2[3] = {dst_d[0], dst_d[1], src_d[2]};
   P(1, ptr, idx, w);
-  pass<1>(F, d1, d2, ptr, idx, w, false, false, t1, t2, s);
+  pass<1>(F, d1, d2, ptr, idx, w, false, false, false, t1, t2, s);
   P(2, ptr, idx, w);
-  pass<2>(F, d2, dst_d, ptr, idx, w, false, true, t2, out, s);
+  pass<2>(F, d2, dst_d, ptr, idx, w, false, true, accumulate, t2, out, s);
 }
 
 }  // namespace
 
 void spatial_prolong(const DevAxisTransfer* ax, int dim, int F, const long long* dc, const long long* df,
-                     const double* coarse, double* fine, double* t1, double* t2, cudaStream_t s) {
-  separable(ax, true, dim, F, dc, df, coarse, fine, t1, t2, s);
+                     const double* coarse, double* fine, double* t1, double* t2, bool accumulate, cudaStream_t s) {
+  separable(ax, true, dim, F, dc, df, coarse, fine, t1, t2, accumulate, s);
 }
 void spatial_restrict(const DevAxisTransfer* ax, int dim, int F, const long long* dc, const long long* df,
                       const double* fine, double* coarse, double* t1, double* t2, cudaStream_t s) {
-  separable(ax, false, dim, F, df, dc, fine, coarse, t1, t2, s);
+  separable(ax, false, dim, F, df, dc, fine, coarse, t1, t2, false, s);
 }
 void temporal_prolong(const double* T, int Ff, int Fc, long long n_space, const long long* d, int dim,
-                      const double* coarse, double* fine, cudaStream_t s) {
+                      const double* coarse, double* fine, bool accumulate, cudaStream_t s) {
   count_launch();
-  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, false, n_space, d[0], d[1], d[2], dim, coarse, fine);
+  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, false, accumulate, n_space, d[0], d[1], d[2], dim,
+                                                     coarse, fine);
 }
 void temporal_restrict(const double* T, int Ff, int Fc, long long n_space, const long long* d, int dim,
                        const double* fine, double* coarse, cudaStream_t s) {
   count_launch();
-  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, true, n_space, d[0], d[1], d[2], dim, fine, coarse);
+  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, true, false, n_space, d[0], d[1], d[2], dim, fine,
+                                                     coarse);
 }
 
 }  // namespace stmgb

@@ -156,6 +156,7 @@ def run_ours(args):
     import torch
 
     from paper_2408_04372_b200 import api, native, problems
+    from paper_2408_04372_b200 import dist as sdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -220,13 +221,10 @@ def run_ours(args):
         e1.synchronize()
     torch.cuda.synchronize()
     launches = lib.stmg_kernel_launches() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
+    # whole-job throughput: units of all ranks over the max-over-ranks time
+    value, ms = sdist.aggregate_throughput(N, e0.elapsed_time(e1) / args.steps, device="cuda")
     if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
         dist.barrier()
-    value = world * N / (ms * 1e-3)
 
     # end to end through the host-buffer C ABI (pinned host memory)
     rh = torch.empty(N, dtype=torch.float64).pin_memory()

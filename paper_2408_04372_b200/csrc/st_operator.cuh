@@ -115,21 +115,7 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
   int* mask_s = reinterpret_cast<int*>(base_s + NC);             // [NC] Dirichlet face mask (bit 2a: low, 2a+1: high)
 
   const long long n_cells = L.cells[0] * L.cells[1] * L.cells[2];
-  // Runs of NC cells along x, visited colour by colour ((run x, y, z) parity)
-  // so that concurrently resident CTAs never scatter into a shared dof.
-  long long cell0 = static_cast<long long>(blockIdx.x) * NC;
-  {
-    const long long rxn = L.cells[0] / NC;
-    const bool even = L.cells[0] % NC == 0 && rxn % 2 == 0 && L.cells[1] % 2 == 0 && (DIM == 2 || L.cells[2] % 2 == 0);
-    if (even) {
-      const long long hx = rxn / 2, hy = L.cells[1] / 2, hz = DIM == 3 ? L.cells[2] / 2 : 1;
-      const long long per = hx * hy * hz;
-      const long long b = blockIdx.x, k = b / per, i = b - k * per;
-      const long long rx = 2 * (i % hx) + (k & 1), cy = 2 * ((i / hx) % hy) + ((k >> 1) & 1),
-                      cz = DIM == 3 ? 2 * (i / (hx * hy)) + ((k >> 2) & 1) : 0;
-      cell0 = (cz * L.cells[1] + cy) * L.cells[0] + rx * NC;
-    }
-  }
+  const long long cell0 = static_cast<long long>(blockIdx.x) * NC;
   const int tid = threadIdx.x;
   const long long dx = L.dofs[0], dxy = L.dofs[0] * L.dofs[1];
   const int p = N - 1;

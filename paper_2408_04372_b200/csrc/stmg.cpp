@@ -155,17 +155,6 @@ void SpaceTimeOperator::spatial_apply(int kind, const double* u, double* y, cuda
 }
 
 // ------------------------------------------------------------ ASMSmoother
-namespace {
-// stable sort of cell indices by colour (cx%2, cy%2, cz%2)
-void colour_order(std::vector<long long>& cells, const DevLevel& d) {
-  auto colour = [&d](long long c) {
-    const long long cx = c % d.cells[0], cy = (c / d.cells[0]) % d.cells[1], cz = c / (d.cells[0] * d.cells[1]);
-    return static_cast<int>((cx & 1) | ((cy & 1) << 1) | ((cz & 1) << 2));
-  };
-  std::stable_sort(cells.begin(), cells.end(), [&](long long a, long long b) { return colour(a) < colour(b); });
-}
-}  // namespace
-
 ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
   const DevLevel& d = op.desc();
   DevASM& A = asm_;
@@ -262,20 +251,13 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
       A.list = nullptr;
       return;
     }
-    colour_order(exact_cells, d);
     list_ = upload(exact_cells);
     A.list = static_cast<const long long*>(list_.raw());
     A.n_list = static_cast<long long>(exact_cells.size());
   } else {
     if (A.m > 64)
       throw std::invalid_argument("ASMSmoother: exact cell blocks on deformed meshes need (p+1)^dim <= 64");
-    // all cells, ordered by 2^d colour classes: cells that run concurrently
-    // never share a dof, so their atomic scatters never collide
-    std::vector<long long> all(static_cast<size_t>(n_cells));
-    for (Index c = 0; c < n_cells; ++c) all[static_cast<size_t>(c)] = c;
-    colour_order(all, d);
-    list_ = upload(all);
-    A.list = static_cast<const long long*>(list_.raw());
+    A.list = nullptr;
     A.n_list = n_cells;
   }
   build_exact(op);

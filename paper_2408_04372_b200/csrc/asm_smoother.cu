@@ -387,20 +387,32 @@ __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constan
         dmma(d00, d01, Xs[swz64(a0, row)], rs[a0 * 8 + (lane >> 2)]);
         dmma(d10, d11, Xs[swz64(a1, row)], rs[a1 * 8 + (lane >> 2)]);
       }
-      *reinterpret_cast<double2*>(hs + row * 8 + col) = make_double2(d00 + d10, d01 + d11);
-    }
-    __syncthreads();
-    if (t < M) {
-      // (T_M + lam_e T_A)^-1 per eigen-index e = t and step
-      const double lam = A.lam[pos * M + t];
-      for (int s = 0; s < A.S; ++s) {
+      // (T_M + lam_e T_A)^-1 per eigen-index e = row and step, solved in
+      // registers: the 4 lanes holding row e exchange its 8 columns
+      double v[8];
+      const double c0 = d00 + d10, c1 = d01 + d11;
+      const int grp = lane & ~3;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[2 * j] = __shfl_sync(0xffffffffu, c0, grp | j);
+        v[2 * j + 1] = __shfl_sync(0xffffffffu, c1, grp | j);
+      }
+      const double lam = A.lam[pos * M + row];
+      double out0 = 0.0, out1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < 8 / NT; ++s) {
+        if (s >= A.S) break;
         double b4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int i = 0; i < NT; ++i) b4[i] = hs[t * 8 + s * NT + i];
+        for (int i = 0; i < NT; ++i) b4[i] = v[s * NT + i];
         small_solve(A.TM, A.TA, lam, NT, b4);
 #pragma unroll
-        for (int i = 0; i < NT; ++i) hs[t * 8 + s * NT + i] = b4[i];
+        for (int i = 0; i < NT; ++i) {
+          if (s * NT + i == col) out0 = b4[i];
+          if (s * NT + i == col + 1) out1 = b4[i];
+        }
       }
+      *reinterpret_cast<double2*>(hs + row * 8 + col) = make_double2(out0, out1);
     }
     __syncthreads();
     {
@@ -598,6 +610,7 @@ void launch_mma(const DevASM& A, const double* r, double* z, double scale, cudaS
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(asm_apply_mma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(asm_apply_mma_kernel<NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     configured = true;
   }
   int per_sm = 0, dev = 0, sms = 148;

@@ -29,6 +29,7 @@ struct DevLevel {
   // geometry: verts == nullptr -> Cartesian lattice with spacing h
   const double* verts;  // (cells+1)^dim * 3 doubles, x fastest
   double h[3];
+  double lo[3];             // domain origin (Cartesian node positions)
   // coefficient: rho(cell) = rho0[ancestor on level 0] (1 if rho0 == nullptr)
   const double* rho0;
   int rho_shift;          // refinement levels between this level and level 0
@@ -38,6 +39,7 @@ struct DevLevel {
   double Dq[kMaxN][kMaxN];  // collocation derivative at the Gauss points
   double w[kMaxN];          // Gauss weights
   double xq[kMaxN];         // Gauss points on [0,1]
+  double gl[kMaxN];         // Gauss-Lobatto support nodes on [0,1]
   // space-time block coefficients, row-major F x F (space_time_operator.cpp:269-317)
   double CM[kMaxF * kMaxF];
   double CA[kMaxF * kMaxF];

@@ -9,8 +9,15 @@ namespace stmgb {
 
 // y = S u (overwrite), fused space-time operator -- st_operator.cu
 void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream);
+// Dirichlet entries of every field of v set to zero
+void st_zero_boundary(const DevLevel& L, double* v, cudaStream_t stream);
 // r = f - S u (overwrite), fused residual (no separate subtraction pass)
 void st_residual(const DevLevel& L, const double* f, const double* u, double* r, cudaStream_t stream);
+
+// nodal interpolant at the Q_p support points (rhs.cu); kind: 0 heat source,
+// 1 wave source, 2 Gaussian(centre, width), 3 manufactured u, 4 manufactured v
+void interpolate_nodes(const DevLevel& L, int kind, double omega, double t, const double* centre, double width,
+                       bool zero_boundary, double* out, cudaStream_t s);
 
 // ---- vector kernels (vector_ops.cu)
 void vec_copy(double* y, const double* x, long long n, cudaStream_t s);

@@ -66,6 +66,12 @@ void run(const DevLevel& L, const double* f, const double* u, double* y, cudaStr
 }  // namespace
 
 void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream) { run(L, nullptr, u, y, stream); }
+void st_zero_boundary(const DevLevel& L, double* v, cudaStream_t stream) {
+  const long long faces = 2 * (L.dofs[1] * L.dofs[2] + L.dofs[0] * L.dofs[2] + (L.dim == 3 ? L.dofs[0] * L.dofs[1] : 0));
+  const unsigned blocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((faces + 255) / 256, 148LL * 8)));
+  count_launch();
+  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dofs[0], L.dofs[1], L.dofs[2], L.n_space, L.F, v, v, v);
+}
 void st_residual(const DevLevel& L, const double* f, const double* u, double* r, cudaStream_t stream) {
   run(L, f, u, r, stream);
 }

@@ -34,11 +34,16 @@ template <int DIM, int N, int F>
 struct Cfg {
   static constexpr int ND = DIM == 2 ? N * N : N * N * N;
   static constexpr int LINES = DIM == 2 ? N : N * N;
+  // padded shared-memory layout x + N y + PZ z of a cell array: for p = 3 the
+  // plane pitch 19 makes the x- and z-line sweeps bank-conflict free and the
+  // y-line sweep at most 2-way (the natural pitch 16 gives 4-way on x lines)
+  static constexpr int PZ = (DIM == 3 && N == 4) ? 19 : N * N;
+  static constexpr int SD = DIM == 2 ? N * N : N * PZ;  // array stride in doubles
   static constexpr int NC = (kThreads / ND) > 0 ? (kThreads / ND) : 1;  // cells per CTA
   static constexpr int NCF = NC * F;
   static constexpr int GEO = DIM == 2 ? 6 : 21;  // d-linear map coefficients per cell
   static constexpr size_t smem_bytes() {
-    return sizeof(double) * (static_cast<size_t>(NCF) * ND * (1 + DIM) + static_cast<size_t>(NC) * (GEO + 1)) +
+    return sizeof(double) * (static_cast<size_t>(NCF) * SD * (1 + DIM) + static_cast<size_t>(NC) * (GEO + 1)) +
            sizeof(long long) * NC + sizeof(int) * NC;
   }
 };
@@ -92,11 +97,20 @@ __device__ __forceinline__ constexpr int pw() {
   return A == 0 ? 1 : (A == 1 ? N : N * N);
 }
 
-// base index of lattice line `line` along axis A inside an N^DIM cell array
-template <int N, int A>
+// natural local index l (x fastest) -> padded position x + N y + PZ z
+template <int N, int PZ>
+__device__ __forceinline__ int pidx(int l) {
+  return (l % N) + N * ((l / N) % N) + PZ * (l / (N * N));
+}
+
+// base position of lattice line `line` along axis A in the padded layout
+// (lines enumerate the other two axes, lower axis fastest)
+template <int N, int PZ, int A>
 __device__ __forceinline__ int line_base(int line) {
-  constexpr int st = pw<N, A>();
-  return (line % st) + (line / st) * st * N;
+  const int a = line % N, b = line / N;
+  if (A == 0) return N * a + PZ * b;  // (y, z)
+  if (A == 1) return a + PZ * b;      // (x, z)
+  return a + N * b;                   // (x, y)
 }
 
 template <int DIM, int N, int F>
@@ -105,11 +119,12 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
                                                                double sign) {
   using C = Cfg<DIM, N, F>;
   constexpr int ND = C::ND, LINES = C::LINES, NC = C::NC, NCF = C::NCF, GEO = C::GEO;
+  constexpr int PZ = C::PZ, SD = C::SD;
   constexpr int T = kThreads;
   extern __shared__ __align__(16) double smem[];
-  double* V = smem;                    // [NCF][ND]
-  double* G = V + NCF * ND;            // [DIM][NCF][ND]
-  double* geo = G + DIM * NCF * ND;    // [NC][GEO] map coefficients
+  double* V = smem;                    // [NCF][SD]
+  double* G = V + NCF * SD;            // [DIM][NCF][SD]
+  double* geo = G + DIM * NCF * SD;    // [NC][GEO] map coefficients
   double* rho_s = geo + NC * GEO;      // [NC]
   long long* base_s = reinterpret_cast<long long*>(rho_s + NC);  // [NC] lattice offset of local dof 0
   int* mask_s = reinterpret_cast<int*>(base_s + NC);             // [NC] Dirichlet face mask (bit 2a: low, 2a+1: high)
@@ -195,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
       if (DIM == 3) bd = bd || ((m & 16) && lz == 0) || ((m & 32) && lz == N - 1);
       if (!bd) v = __ldg(u + f * L.n_space + base + lz * dxy + ly * dx + lx);
     }
-    V[(c * F + f) * ND + l] = v;
+    V[(c * F + f) * SD + pidx<N, PZ>(l)] = v;
   }
   __syncthreads();
 
@@ -204,17 +219,17 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
   for (int a = 0; a < DIM; ++a) {
     for (int ln = tid; ln < NCF * LINES; ln += T) {
       const int cf = ln / LINES, line = ln - cf * LINES;
-      if (a == 0) sweep_inplace<N, false>(V + cf * ND, line_base<N, 0>(line), 1, L.B);
-      if (a == 1) sweep_inplace<N, false>(V + cf * ND, line_base<N, 1>(line), N, L.B);
-      if (a == 2) sweep_inplace<N, false>(V + cf * ND, line_base<N, 2>(line), N * N, L.B);
+      if (a == 0) sweep_inplace<N, false>(V + cf * SD, line_base<N, PZ, 0>(line), 1, L.B);
+      if (a == 1) sweep_inplace<N, false>(V + cf * SD, line_base<N, PZ, 1>(line), N, L.B);
+      if (a == 2) sweep_inplace<N, false>(V + cf * SD, line_base<N, PZ, 2>(line), PZ, L.B);
     }
     __syncthreads();
   }
   for (int ln = tid; ln < NCF * LINES; ln += T) {
     const int cf = ln / LINES, line = ln - cf * LINES;
-    sweep_copy<N>(V + cf * ND, G + (0 * NCF + cf) * ND, line_base<N, 0>(line), 1, L.Dq);
-    sweep_copy<N>(V + cf * ND, G + (1 * NCF + cf) * ND, line_base<N, 1>(line), N, L.Dq);
-    if (DIM == 3) sweep_copy<N>(V + cf * ND, G + (2 * NCF + cf) * ND, line_base<N, 2>(line), N * N, L.Dq);
+    sweep_copy<N>(V + cf * SD, G + (0 * NCF + cf) * SD, line_base<N, PZ, 0>(line), 1, L.Dq);
+    sweep_copy<N>(V + cf * SD, G + (1 * NCF + cf) * SD, line_base<N, PZ, 1>(line), N, L.Dq);
+    if (DIM == 3) sweep_copy<N>(V + cf * SD, G + (2 * NCF + cf) * SD, line_base<N, PZ, 2>(line), PZ, L.Dq);
   }
   __syncthreads();
 
@@ -222,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
   for (int idx = tid; idx < NC * ND; idx += T) {
     const int c = idx / ND;
     const int q = idx - c * ND;
+    const int qp = pidx<N, PZ>(q);
     if (base_s[c] < 0) continue;
     const int qx = q % N, qy = (q / N) % N, qz = DIM == 3 ? q / (N * N) : 0;
     double wq = L.w[qx] * L.w[qy];
@@ -284,9 +300,9 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
     double vin[F], gin[F][DIM];
 #pragma unroll
     for (int j = 0; j < F; ++j) {
-      vin[j] = V[(c * F + j) * ND + q];
+      vin[j] = V[(c * F + j) * SD + qp];
 #pragma unroll
-      for (int a = 0; a < DIM; ++a) gin[j][a] = G[(a * NCF + c * F + j) * ND + q];
+      for (int a = 0; a < DIM; ++a) gin[j][a] = G[(a * NCF + c * F + j) * SD + qp];
     }
 #pragma unroll
     for (int i = 0; i < F; ++i) {
@@ -299,14 +315,14 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
         g1 = fma(ca, gin[j][1], g1);
         if (DIM == 3) g2 = fma(ca, gin[j][DIM - 1], g2);
       }
-      V[(c * F + i) * ND + q] = mass_fac * vo;
+      V[(c * F + i) * SD + qp] = mass_fac * vo;
       if (DIM == 2) {
-        G[(0 * NCF + c * F + i) * ND + q] = fma(K00, g0, K01 * g1);
-        G[(1 * NCF + c * F + i) * ND + q] = fma(K01, g0, K11 * g1);
+        G[(0 * NCF + c * F + i) * SD + qp] = fma(K00, g0, K01 * g1);
+        G[(1 * NCF + c * F + i) * SD + qp] = fma(K01, g0, K11 * g1);
       } else {
-        G[(0 * NCF + c * F + i) * ND + q] = fma(K00, g0, fma(K01, g1, K02 * g2));
-        G[(1 * NCF + c * F + i) * ND + q] = fma(K01, g0, fma(K11, g1, K12 * g2));
-        G[((DIM - 1) * NCF + c * F + i) * ND + q] = fma(K02, g0, fma(K12, g1, K22 * g2));
+        G[(0 * NCF + c * F + i) * SD + qp] = fma(K00, g0, fma(K01, g1, K02 * g2));
+        G[(1 * NCF + c * F + i) * SD + qp] = fma(K01, g0, fma(K11, g1, K12 * g2));
+        G[((DIM - 1) * NCF + c * F + i) * SD + qp] = fma(K02, g0, fma(K12, g1, K22 * g2));
       }
     }
   }
@@ -317,9 +333,9 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
   for (int a = 0; a < DIM; ++a) {
     for (int ln = tid; ln < NCF * LINES; ln += T) {
       const int cf = ln / LINES, line = ln - cf * LINES;
-      if (a == 0) sweep_addT<N>(G + (0 * NCF + cf) * ND, V + cf * ND, line_base<N, 0>(line), 1, L.Dq);
-      if (a == 1) sweep_addT<N>(G + (1 * NCF + cf) * ND, V + cf * ND, line_base<N, 1>(line), N, L.Dq);
-      if (a == 2) sweep_addT<N>(G + (2 * NCF + cf) * ND, V + cf * ND, line_base<N, 2>(line), N * N, L.Dq);
+      if (a == 0) sweep_addT<N>(G + (0 * NCF + cf) * SD, V + cf * SD, line_base<N, PZ, 0>(line), 1, L.Dq);
+      if (a == 1) sweep_addT<N>(G + (1 * NCF + cf) * SD, V + cf * SD, line_base<N, PZ, 1>(line), N, L.Dq);
+      if (a == 2) sweep_addT<N>(G + (2 * NCF + cf) * SD, V + cf * SD, line_base<N, PZ, 2>(line), PZ, L.Dq);
     }
     __syncthreads();
   }
@@ -327,9 +343,9 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
   for (int a = 0; a < DIM; ++a) {
     for (int ln = tid; ln < NCF * LINES; ln += T) {
       const int cf = ln / LINES, line = ln - cf * LINES;
-      if (a == 0) sweep_inplace<N, true>(V + cf * ND, line_base<N, 0>(line), 1, L.B);
-      if (a == 1) sweep_inplace<N, true>(V + cf * ND, line_base<N, 1>(line), N, L.B);
-      if (a == 2) sweep_inplace<N, true>(V + cf * ND, line_base<N, 2>(line), N * N, L.B);
+      if (a == 0) sweep_inplace<N, true>(V + cf * SD, line_base<N, PZ, 0>(line), 1, L.B);
+      if (a == 1) sweep_inplace<N, true>(V + cf * SD, line_base<N, PZ, 1>(line), N, L.B);
+      if (a == 2) sweep_inplace<N, true>(V + cf * SD, line_base<N, PZ, 2>(line), PZ, L.B);
     }
     __syncthreads();
   }
@@ -347,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
     const int m = mask_s[c];
     bool bd = ((m & 1) && lx == 0) || ((m & 2) && lx == N - 1) || ((m & 4) && ly == 0) || ((m & 8) && ly == N - 1);
     if (DIM == 3) bd = bd || ((m & 16) && lz == 0) || ((m & 32) && lz == N - 1);
-    if (!bd) atomicAdd(y + f * L.n_space + base + lz * dxy + ly * dx + lx, sign * V[(c * F + f) * ND + l]);
+    if (!bd) atomicAdd(y + f * L.n_space + base + lz * dxy + ly * dx + lx, sign * V[(c * F + f) * SD + pidx<N, PZ>(l)]);
   }
 }
 

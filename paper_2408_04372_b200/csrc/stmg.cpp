@@ -91,6 +91,7 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
     d.dofs[a] = a < m.dim ? m.cells[a] * p + 1 : 1;
     d.n_space *= d.dofs[a];
     d.h[a] = a < m.dim ? (m.hi[a] - m.lo[a]) / static_cast<double>(m.cells[a]) : 1.0;
+    d.lo[a] = m.lo[a];
   }
   d.n_dofs = d.n_space * F;
   if (!m.vertices.empty()) {
@@ -122,6 +123,7 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
   for (int i = 0; i < kMaxN; ++i) {
     d.w[i] = i < d.n ? q.w[i] : 0.0;
     d.xq[i] = i < d.n ? q.x[i] : 0.0;
+    d.gl[i] = i < d.n ? gl.x[i] : 0.0;
   }
   std::vector<double> CM, CA;
   block_coefficient_matrices(equation, weights, tau, n_steps, CM, CA);
@@ -152,6 +154,166 @@ void SpaceTimeOperator::residual(const double* f, const double* u, double* r, cu
 
 void SpaceTimeOperator::spatial_apply(int kind, const double* u, double* y, cudaStream_t stream) const {
   st_apply(kind == 0 ? mass_desc_ : stiff_desc_, u, y, stream);
+}
+
+// --------------------------------------------- slab RHS and state transfer
+namespace {
+struct WaveHelpers {
+  std::vector<double> am_alpha, alpha_a, minv_a_last;
+  double minv_alpha_last = 0.0, minv_beta_last = 0.0;
+};
+// the velocity-elimination helpers of space_time_operator.cpp:22-33
+WaveHelpers wave_helpers(const TemporalWeights& w) {
+  const int nt = w.n_t;
+  WaveHelpers h;
+  const std::vector<double> minv = invert_small(w.m, nt);
+  const std::vector<double> minv_a = matmul_small(minv, w.a, nt, nt, nt);
+  const std::vector<double> minv_alpha = matmul_small(minv, w.alpha, nt, nt, 1);
+  h.am_alpha = matmul_small(w.a, minv_alpha, nt, nt, 1);
+  h.minv_a_last.assign(minv_a.begin() + (nt - 1) * nt, minv_a.begin() + nt * nt);
+  h.minv_alpha_last = minv_alpha[nt - 1];
+  h.alpha_a.assign(nt, 0.0);
+  if (w.scheme == TimeScheme::CGP) {
+    const std::vector<double> minv_beta = matmul_small(minv, w.beta, nt, nt, 1);
+    const std::vector<double> a_minv_beta = matmul_small(w.a, minv_beta, nt, nt, 1);
+    h.minv_beta_last = minv_beta[nt - 1];
+    for (int i = 0; i < nt; ++i) h.alpha_a[i] = w.alpha[i] - a_minv_beta[i];
+  }
+  return h;
+}
+}  // namespace
+
+void SpaceTimeOperator::interpolate(int kind, double frequency, double t, const double* centre, double width,
+                                    bool zero_boundary, double* out, cudaStream_t s) const {
+  interpolate_nodes(desc_, kind, 2.0 * M_PI * frequency, t, centre, width, zero_boundary, out, s);
+}
+
+void SpaceTimeOperator::assemble_rhs(int source_kind, double frequency, double t0, const double* u0,
+                                     const double* v0, double* rhs, cudaStream_t s) const {
+  const int S = n_steps_, nt = weights_.n_t;
+  const Index nx = n_space();
+  const bool cgp = weights_.scheme == TimeScheme::CGP;
+  const bool wave = equation_ == Equation::Wave;
+  const TemporalWeights& w = weights_;
+  if (wave && !v0) throw std::invalid_argument("assemble_rhs: the wave equation needs the entering velocity");
+  vec_fill(rhs, 0.0, n_dofs(), s);
+  DeviceBuffer fi(sizeof(double) * nx), Fl(sizeof(double) * nx), Ft(sizeof(double) * nx * nt);
+  auto seg = [&](int step, int i) { return rhs + block_offset(step, i); };
+  // source collocated at the temporal unknown nodes (space_time_operator.cpp:148-173)
+  if (source_kind != 0) {
+    const int kind = wave ? 1 : 0;
+    auto mass_of = [&](double t, double* out) {
+      interpolate(kind, frequency, t, nullptr, 0.0, /*zero_boundary=*/true, fi.d(), s);
+      spatial_apply(0, fi.d(), out, s);
+    };
+    for (int st = 0; st < S; ++st) {
+      const double t_left = t0 + st * tau_;
+      for (int j = 0; j < nt; ++j) mass_of(t_left + w.unknown_nodes[j] * tau_, Ft.d() + j * nx);
+      if (cgp) mass_of(t_left, Fl.d());
+      for (int i = 0; i < nt; ++i) {
+        for (int j = 0; j < nt; ++j) vec_axpy(seg(st, i), tau_ * w.m[i * nt + j], Ft.d() + j * nx, nx, s);
+        if (cgp) vec_axpy(seg(st, i), tau_ * w.beta[i], Fl.d(), nx, s);
+      }
+    }
+  }
+  // coupling to the entering state (space_time_operator.cpp:175-218)
+  DeviceBuffer uz(sizeof(double) * nx), Mu(sizeof(double) * nx), Au(sizeof(double) * nx), mvk(sizeof(double) * nx),
+      tmp(sizeof(double) * nx);
+  vec_copy(uz.d(), u0, nx, s);
+  zero_boundary_field(uz.d(), s);
+  spatial_apply(0, uz.d(), Mu.d(), s);
+  spatial_apply(1, uz.d(), Au.d(), s);
+  WaveHelpers h;
+  if (wave) {
+    h = wave_helpers(w);
+    vec_copy(tmp.d(), v0, nx, s);
+    zero_boundary_field(tmp.d(), s);
+    spatial_apply(0, tmp.d(), mvk.d(), s);
+  }
+  const double z = wave ? h.minv_alpha_last / tau_ : 0.0;
+  const double g = -h.minv_beta_last;
+  for (int st = 0; st < S; ++st) {
+    for (int i = 0; i < nt; ++i) {
+      double* sg = seg(st, i);
+      if (!wave) {
+        if (st == 0) {
+          if (cgp) {
+            vec_axpy(sg, -w.alpha[i], Mu.d(), nx, s);
+            vec_axpy(sg, -tau_ * w.beta[i], Au.d(), nx, s);
+          } else {
+            vec_axpy(sg, w.alpha[i], Mu.d(), nx, s);
+          }
+        }
+      } else if (st == 0) {
+        if (cgp) {
+          vec_axpy(sg, -h.am_alpha[i] / tau_, Mu.d(), nx, s);
+          vec_axpy(sg, -tau_ * w.beta[i], Au.d(), nx, s);
+          vec_axpy(sg, -h.alpha_a[i], mvk.d(), nx, s);
+        } else {
+          vec_axpy(sg, h.am_alpha[i] / tau_, Mu.d(), nx, s);
+          vec_axpy(sg, w.alpha[i], mvk.d(), nx, s);
+        }
+      } else {
+        if (cgp)
+          vec_axpy(sg, -h.alpha_a[i], mvk.d(), nx, s);
+        else
+          vec_axpy(sg, w.alpha[i], mvk.d(), nx, s);
+      }
+    }
+    if (wave) {
+      if (st == 0) {
+        if (cgp)
+          vec_axpby(mvk.d(), z, Mu.d(), g, nx, s);  // mvk = z Mu + g mvk
+        else
+          vec_scale_into(mvk.d(), -z, Mu.d(), nx, s);
+      } else {
+        if (cgp)
+          vec_scale_into(mvk.d(), g, mvk.d(), nx, s);
+        else
+          vec_fill(mvk.d(), 0.0, nx, s);
+      }
+    }
+  }
+  for (int st = 0; st < S; ++st)
+    for (int i = 0; i < nt; ++i) zero_boundary_field(seg(st, i), s);
+  cuda_check(cudaStreamSynchronize(s), "assemble_rhs");
+}
+
+void SpaceTimeOperator::extract_final(const double* u, const double* u0, const double* v0, double* uf, double* vf,
+                                      cudaStream_t s) const {
+  const int S = n_steps_, nt = weights_.n_t;
+  const Index nx = n_space();
+  vec_copy(uf, u + block_offset(S - 1, nt - 1), nx, s);
+  if (equation_ == Equation::Heat) return;
+  if (!v0 || !vf) throw std::invalid_argument("extract_final: the wave equation needs velocities");
+  const bool cgp = weights_.scheme == TimeScheme::CGP;
+  const WaveHelpers h = wave_helpers(weights_);
+  DeviceBuffer vl(sizeof(double) * nx), vs(sizeof(double) * nx);
+  vec_copy(vl.d(), v0, nx, s);
+  const double* prev_last = u0;
+  for (int st = 0; st < S; ++st) {
+    vec_fill(vs.d(), 0.0, nx, s);
+    for (int j = 0; j < nt; ++j) vec_axpy(vs.d(), h.minv_a_last[j] / tau_, u + block_offset(st, j), nx, s);
+    if (cgp) {
+      vec_axpy(vs.d(), h.minv_alpha_last / tau_, prev_last, nx, s);
+      vec_axpy(vs.d(), -h.minv_beta_last, vl.d(), nx, s);
+    } else {
+      vec_axpy(vs.d(), -h.minv_alpha_last / tau_, prev_last, nx, s);
+    }
+    vec_copy(vl.d(), vs.d(), nx, s);
+    prev_last = u + block_offset(st, nt - 1);
+  }
+  vec_copy(vf, vl.d(), nx, s);
+  cuda_check(cudaStreamSynchronize(s), "extract_final");
+}
+
+void SpaceTimeOperator::zero_boundary_field(double* v, cudaStream_t s) const {
+  // Dirichlet entries of one spatial field set to zero: the identity rows of
+  // the boundary pass applied to (f = v, u = v) give v_b - v_b = 0
+  DevLevel one = desc_;
+  one.F = 1;
+  one.n_dofs = one.n_space;
+  st_zero_boundary(one, v, s);
 }
 
 // ------------------------------------------------------------ ASMSmoother

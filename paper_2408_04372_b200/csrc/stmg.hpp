@@ -76,6 +76,18 @@ class SpaceTimeOperator {
   void spatial_apply(int kind, const double* u, double* y, cudaStream_t stream = nullptr) const;
   // r = f - S u (overwrite), one fused pass
   void residual(const double* f, const double* u, double* r, cudaStream_t stream = nullptr) const;
+  // nodal interpolant of a known function on this level's Q_p lattice
+  // (interpolate, spatial_operator.cpp:437-449); kinds as interpolate_nodes
+  void interpolate(int kind, double frequency, double t, const double* centre, double width, bool zero_boundary,
+                   double* out, cudaStream_t stream = nullptr) const;
+  // assemble_rhs (space_time_operator.cpp:138-221): source_kind 0 zero,
+  // 1 manufactured (driver.cpp:265-293, frequency f); entering state u0 (v0)
+  void assemble_rhs(int source_kind, double frequency, double t0, const double* u0, const double* v0, double* rhs,
+                    cudaStream_t stream = nullptr) const;
+  // extract_final (space_time_operator.cpp:223-248)
+  void extract_final(const double* u, const double* u0, const double* v0, double* uf, double* vf,
+                     cudaStream_t stream = nullptr) const;
+  void zero_boundary_field(double* v, cudaStream_t stream = nullptr) const;
   long applications() const { return apply_count_; }
 
  private:

@@ -70,6 +70,24 @@ int stmg_st_operator_apply(const stmg_st_operator* op, const double* d_u, double
 int stmg_st_operator_apply_host(const stmg_st_operator* op, const double* h_u, double* h_y);
 /* SpatialOperator::apply (spatial_operator.cpp:292-315), kind 0 mass / 1 stiffness */
 int stmg_spatial_apply(const stmg_st_operator* op, int kind, const double* d_u, double* d_y, void* stream);
+/* r = f - S u in one fused pass (the residual of multigrid.cpp:181,215) */
+int stmg_st_operator_residual(const stmg_st_operator* op, const double* d_f, const double* d_u, double* d_r,
+                              void* stream);
+/* interpolate (spatial_operator.cpp:437-449) of a known function at the Q_p
+ * support points into d_out (n_space): kind 0 manufactured heat source,
+ * 1 manufactured wave source, 2 Gaussian exp(-|x-centre|^2/(2 width^2)),
+ * 3 manufactured solution, 4 manufactured velocity (driver.cpp:265-293,
+ * omega = 2 pi frequency); zero_boundary sets the Dirichlet entries to 0 */
+int stmg_st_operator_interpolate(const stmg_st_operator* op, int kind, double frequency, double t,
+                                 const double centre[3], double width, int zero_boundary, double* d_out,
+                                 void* stream);
+/* assemble_rhs (space_time_operator.cpp:138-221): source_kind 0 zero source,
+ * 1 manufactured source; entering state d_u0 (and d_v0 for the wave) */
+int stmg_st_operator_assemble_rhs(const stmg_st_operator* op, int source_kind, double frequency, double t0,
+                                  const double* d_u0, const double* d_v0, double* d_rhs, void* stream);
+/* extract_final (space_time_operator.cpp:223-248): state after the slab */
+int stmg_st_operator_extract_final(const stmg_st_operator* op, const double* d_u, const double* d_u0,
+                                   const double* d_v0, double* d_uf, double* d_vf, void* stream);
 
 /* ASMSmoother (include/stmg/asm_smoother.hpp:16-30) */
 int stmg_asm_create(const stmg_st_operator* op, stmg_asm** out);

@@ -234,6 +234,14 @@ class Reference:
         _chk(load().ref_assemble_rhs(self.h, source_kind, frequency, t0, _p(u0), _p(v0), _p(rhs)))
         return rhs
 
+    def extract_final(self, u: np.ndarray, u0: np.ndarray, v0: Optional[np.ndarray] = None):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        u0 = np.ascontiguousarray(u0, dtype=np.float64)
+        v0 = np.zeros(self.n_space) if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
+        uf, vf = np.empty(self.n_space), np.empty(self.n_space)
+        _chk(load().ref_extract_final(self.h, _p(u), _p(u0), _p(v0), _p(uf), _p(vf)))
+        return uf, vf
+
     def interpolate_gaussian(self, centre=(0.5, 0.5, 0.5), width: float = 0.05) -> np.ndarray:
         c = np.ascontiguousarray(centre, dtype=np.float64)
         u = np.empty(self.n_space)

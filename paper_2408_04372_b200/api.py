@@ -104,6 +104,40 @@ class SpaceTimeOperator:
                                                      y.ctypes.data_as(N.c_double_p)))
         return y
 
+    def residual(self, f, u, r=None):
+        """r = f - S u (one fused pass)."""
+        if r is None:
+            r = _torch().empty_like(u)
+        N.check(N.load().stmg_st_operator_residual(self._h, _ptr(f), _ptr(u), _ptr(r), _stream()))
+        return r
+
+    def interpolate(self, kind: int, frequency: float = 0.5, t: float = 0.0, centre=(0.5, 0.5, 0.5),
+                    width: float = 0.05, zero_boundary: bool = False):
+        """Nodal interpolant on the Q_p lattice (kind: 0 heat source, 1 wave
+        source, 2 Gaussian, 3 manufactured u, 4 manufactured v)."""
+        out = _torch().empty(self.n_space, dtype=_torch().float64, device="cuda")
+        c = np.ascontiguousarray(centre, dtype=np.float64)
+        N.check(N.load().stmg_st_operator_interpolate(self._h, kind, frequency, t, c.ctypes.data_as(N.c_double_p),
+                                                      width, 1 if zero_boundary else 0, _ptr(out), _stream()))
+        return out
+
+    def assemble_rhs(self, source_kind: int, frequency: float, t0: float, u0, v0=None):
+        """Slab right-hand side (SpaceTimeOperator::assemble_rhs)."""
+        rhs = _torch().empty(self.n_dofs, dtype=_torch().float64, device="cuda")
+        N.check(N.load().stmg_st_operator_assemble_rhs(self._h, source_kind, frequency, t0, _ptr(u0),
+                                                       _ptr(v0) if v0 is not None else None, _ptr(rhs), _stream()))
+        return rhs
+
+    def extract_final(self, u, u0, v0=None):
+        """State after the slab (SpaceTimeOperator::extract_final) -> (u, v or None)."""
+        torch = _torch()
+        uf = torch.empty(self.n_space, dtype=torch.float64, device="cuda")
+        vf = torch.empty(self.n_space, dtype=torch.float64, device="cuda") if v0 is not None else None
+        N.check(N.load().stmg_st_operator_extract_final(self._h, _ptr(u), _ptr(u0),
+                                                        _ptr(v0) if v0 is not None else None, _ptr(uf),
+                                                        _ptr(vf) if vf is not None else None, _stream()))
+        return uf, vf
+
     def spatial_apply(self, kind: int, u, y=None):
         torch = _torch()
         if y is None:

@@ -171,6 +171,39 @@ int stmg_spatial_apply(const stmg_st_operator* op, int kind, const double* d_u, 
   });
 }
 
+int stmg_st_operator_residual(const stmg_st_operator* op, const double* d_f, const double* d_u, double* d_r,
+                              void* stream) {
+  return guard([&] {
+    if (!op || !d_f || !d_u || !d_r) throw std::invalid_argument("stmg_st_operator_residual: null argument");
+    op->op->residual(d_f, d_u, d_r, st(stream));
+  });
+}
+
+int stmg_st_operator_interpolate(const stmg_st_operator* op, int kind, double frequency, double t,
+                                 const double centre[3], double width, int zero_boundary, double* d_out,
+                                 void* stream) {
+  return guard([&] {
+    if (!op || !d_out || kind < 0 || kind > 4) throw std::invalid_argument("stmg_st_operator_interpolate: bad argument");
+    op->op->interpolate(kind, frequency, t, centre, width, zero_boundary != 0, d_out, st(stream));
+  });
+}
+
+int stmg_st_operator_assemble_rhs(const stmg_st_operator* op, int source_kind, double frequency, double t0,
+                                  const double* d_u0, const double* d_v0, double* d_rhs, void* stream) {
+  return guard([&] {
+    if (!op || !d_u0 || !d_rhs) throw std::invalid_argument("stmg_st_operator_assemble_rhs: null argument");
+    op->op->assemble_rhs(source_kind, frequency, t0, d_u0, d_v0, d_rhs, st(stream));
+  });
+}
+
+int stmg_st_operator_extract_final(const stmg_st_operator* op, const double* d_u, const double* d_u0,
+                                   const double* d_v0, double* d_uf, double* d_vf, void* stream) {
+  return guard([&] {
+    if (!op || !d_u || !d_u0 || !d_uf) throw std::invalid_argument("stmg_st_operator_extract_final: null argument");
+    op->op->extract_final(d_u, d_u0, d_v0, d_uf, d_vf, st(stream));
+  });
+}
+
 int stmg_asm_create(const stmg_st_operator* op, stmg_asm** out) {
   return guard([&] {
     if (!op || !out) throw std::invalid_argument("stmg_asm_create: null argument");

@@ -50,6 +50,13 @@ SIGNATURES = [
     ("stmg_st_operator_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("stmg_st_operator_apply_host", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("stmg_spatial_apply", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_st_operator_residual", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_st_operator_interpolate", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, c_double_p, C.c_double,
+                                               C.c_int, C.c_void_p, C.c_void_p]),
+    ("stmg_st_operator_assemble_rhs", C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                                C.c_void_p, C.c_void_p]),
+    ("stmg_st_operator_extract_final", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                 C.c_void_p, C.c_void_p]),
     ("stmg_asm_create", C.c_int, [C.c_void_p, C.c_void_p]),
     ("stmg_asm_destroy", None, [C.c_void_p]),
     ("stmg_asm_add_correction", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -124,6 +124,10 @@ int stmg_multigrid_n_levels(const stmg_multigrid* mg);
 /* level_info (multigrid.cpp:236-247): ints = {mesh_level, p, k, n_steps, coarsening(-1 finest)} */
 int stmg_multigrid_level_info(const stmg_multigrid* mg, int level, int ints[5], long long* n_dofs, double* omega);
 int stmg_multigrid_set_omega(stmg_multigrid* mg, int level, double omega);
+/* which cell-solve kernels the level-l smoother runs (no reference counterpart;
+   diagnostics): bit 0 tensor FDM, bit 1 per-cell eigenbasis, bit 2 temporal
+   fast diagonalisation in the eigenbasis kernel; -1 on the coarsest level */
+int stmg_multigrid_smoother_kind(const stmg_multigrid* mg, int level);
 const stmg_st_operator* stmg_multigrid_operator_at(const stmg_multigrid* mg, int level);
 /* apply (multigrid.cpp:228-234): one V-cycle, zero initial guess, overwrite d_z */
 int stmg_multigrid_apply(const stmg_multigrid* mg, const double* d_r, double* d_z, void* stream);

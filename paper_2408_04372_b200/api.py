@@ -241,6 +241,11 @@ class SpaceTimeMultigrid:
                         "n_steps": ints[3], "n_dofs": n.value, "omega": w.value})
         return out
 
+    def smoother_kind(self, l: int) -> int:
+        """bit 0 tensor FDM, bit 1 per-cell eigenbasis, bit 2 temporal fast
+        diagonalisation (-1: coarsest level, no smoother)."""
+        return int(N.load().stmg_multigrid_smoother_kind(self._h, l))
+
     def omega_at(self, l: int) -> float:
         return self.level_info()[l]["omega"]
 

@@ -436,6 +436,185 @@ __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constan
   }
 }
 
+// m = 64 smoother with the temporal solves fast-diagonalised as well
+// (A.tdiag): per cell and eigen-index e the n_t x n_t solve
+// (T_M + lam_e T_A)^-1 = Q (B + lam_e)^-1 P, B block-diagonal. P mixes the
+// temporal columns of every residual row before the first product, the
+// 1x1/2x2 scalings (B + lam_e)^-1 act on the MMA accumulator pair each lane
+// already holds, and Q mixes the columns of the second product's rows (one
+// 4-lane shuffle exchange) -- no pivoted small solves, no redundant lanes.
+// One TMA bulk copy per cell brings X (swizzled) and its eigenvalues; the
+// cell's lattice offset and Dirichlet faces come from a 16-byte meta entry,
+// and the multiplicity weight of an interior dof depends only on its local
+// index, so no per-dof division or index decoding is left in the loop.
+// Dirichlet dofs of a block (identity rows, asm_smoother.cpp:29-33 with the
+// global identity) contribute w * r directly from the gather threads.
+template <int NT, int S>
+__global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_constant__ DevASM A,
+                                                                const double* __restrict__ r,
+                                                                double* __restrict__ z, double scale) {
+  constexpr int M = 64, NCOL = NT * S, NPAIR = (NCOL + 1) / 2;
+  constexpr unsigned RBYTES = static_cast<unsigned>(kRec64 * sizeof(double));
+  static_assert(RBYTES % 16 == 0, "record must be a multiple of 16 bytes");
+  extern __shared__ __align__(128) double sm[];
+  double* Xb0 = sm;
+  double* Xb1 = sm + kRec64;
+  double* rs = sm + 2 * kRec64;  // [64][8] P-transformed residual, pair-swizzled rows
+  double* hs = rs + 8 * M;       // [64][8] scaled eigen-coefficients
+  long long* cinfo = reinterpret_cast<long long*>(hs + 8 * M);       // [2][2] {g0, mask} per parity
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(cinfo + 4);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const long long n_pos = A.n_list, nsp = A.n_space;
+  const long long dx = A.dofs[0], dxy = A.dofs[0] * A.dofs[1];
+  auto local_off = [&](int a, int& fb) {
+    const int lx = a & 3, ly = (a >> 2) & 3, lz = a >> 4;
+    fb = (lx == 0 ? 1 : 0) | (lx == 3 ? 2 : 0) | (ly == 0 ? 4 : 0) | (ly == 3 ? 8 : 0) | (lz == 0 ? 16 : 0) |
+         (lz == 3 ? 32 : 0);
+    return lz * dxy + ly * dx + lx;
+  };
+  // gather role (t < 64: local dof t), epilogue role (row a of the 2nd product)
+  int fb_g = 0, fb_e = 0;
+  const long long off_g = local_off(t & 63, fb_g);
+  const int j = lane & 3, n8 = lane >> 2;
+  const int row = warp * 8 + n8;  // eigen-index of product 1 / local dof of product 2
+  const long long off_e = local_off(row, fb_e);
+  const double w_e = scale * ldexp(1.0, -__popc(fb_e));
+  // constant smem offsets of the fragment loads (see swz64 and the rs swizzle)
+  const int x1e = j * 64 + (row ^ (4 * j)), x1o = j * 64 + (row ^ (16 + 4 * j));
+  // B operands are loaded per half-warp (16 lanes x 8 B): rows 4kt + j and
+  // 4kt + j + 2 must land in different 8-double bank halves, hence the XOR of
+  // bit 2 by row bit 1 (rs: also bit 1 by row bit 2, for the gather's 16-byte
+  // stores from consecutive rows)
+  const int swj = ((j >> 1) & 1) << 2;
+  const int r1e = j * 8 + (n8 ^ swj), r1o = j * 8 + (n8 ^ (swj | 2));
+  const int h2 = j * 8 + (n8 ^ swj);
+  const int hst = row * 8 + ((2 * j) ^ (((row >> 1) & 1) << 2));
+  const int sw2 = row & 7;
+  const int xrow = row * 64 + j;
+  const int kd = A.kind[j];
+  const double a0 = A.s0[j], a1 = A.s1[j];
+
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  long long pos = blockIdx.x;
+  if (t == 0 && pos < n_pos) {
+    mbar_expect_tx(&bar[0], RBYTES);
+    bulk_g2s(Xb0, A.X + pos * kRec64, RBYTES, &bar[0]);
+  }
+  double rn[NCOL];
+  long long g0n = 0, maskn = 0;
+  auto fetch = [&](long long q) {
+    if (t < M) {
+      const longlong2 mt = *reinterpret_cast<const longlong2*>(A.meta + 2 * q);
+      g0n = mt.x;
+      maskn = mt.y;
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) rn[c] = __ldg(r + c * nsp + g0n + off_g);
+    }
+  };
+  if (pos < n_pos) fetch(pos);
+  unsigned ph0 = 0, ph1 = 0;
+  for (int it = 0; pos < n_pos; pos += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const long long next = pos + gridDim.x;
+    // ---- stage the residual of this cell (prefetched last iteration)
+    if (t < M) {
+      double tr[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        double s = 0.0;
+        if (k < NCOL) {
+#pragma unroll
+          for (int c = 0; c < NCOL; ++c) s = fma(A.P[k][c], rn[c], s);
+        }
+        tr[k] = s;
+      }
+      const int swr = (((t >> 1) & 1) << 2) | (((t >> 2) & 1) << 1);
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        *reinterpret_cast<double2*>(rs + t * 8 + ((2 * p) ^ swr)) = make_double2(tr[2 * p], tr[2 * p + 1]);
+      if (maskn & fb_g) {
+        const double w = scale * ldexp(1.0, -__popc(fb_g & ~static_cast<int>(maskn)));
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c) atomicAdd(z + c * nsp + g0n + off_g, w * rn[c]);
+      }
+      if (t == 0) {
+        cinfo[2 * buf] = g0n;
+        cinfo[2 * buf + 1] = maskn;
+      }
+      if (next < n_pos) fetch(next);
+    }
+    if (buf == 0) {
+      mbar_wait(&bar[0], ph0);
+      ph0 ^= 1;
+    } else {
+      mbar_wait(&bar[1], ph1);
+      ph1 ^= 1;
+    }
+    __syncthreads();
+    if (t == 0 && next < n_pos) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar[buf ^ 1], RBYTES);
+      bulk_g2s(buf ? Xb0 : Xb1, A.X + next * kRec64, RBYTES, &bar[buf ^ 1]);
+    }
+    const double* Xs = buf ? Xb1 : Xb0;
+    {
+      // product 1: hat r (e x slots) = X^T rs
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < 16; kt += 2) {
+        dmma(d00, d01, Xs[kt * 256 + x1e], rs[kt * 32 + r1e]);
+        dmma(d10, d11, Xs[(kt + 1) * 256 + x1o], rs[(kt + 1) * 32 + r1o]);
+      }
+      const double v0 = d00 + d10, v1 = d01 + d11;
+      // (B + lam_e)^-1 on slots (2j, 2j+1): two reals or one conjugate pair
+      const double lam = Xs[4096 + row];
+      const double p0 = a0 + lam, p1 = a1 + lam;
+      const double m00 = kd ? p0 : p1, m11 = p0, m01 = kd ? -a1 : 0.0, m10 = kd ? a1 : 0.0;
+      const double den = kd ? fma(p0, p0, a1 * a1) : p0 * p1;
+      const double inv = 1.0 / den;
+      *reinterpret_cast<double2*>(hs + hst) =
+          make_double2(fma(m00, v0, m01 * v1) * inv, fma(m10, v0, m11 * v1) * inv);
+    }
+    __syncthreads();
+    {
+      // product 2: z_T (a x slots) = X hat z, then Q mixes the slots of row a
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < 16; kt += 2) {
+        dmma(d00, d01, Xs[xrow + 4 * (kt ^ sw2)], hs[kt * 32 + h2]);
+        dmma(d10, d11, Xs[xrow + 4 * ((kt + 1) ^ sw2)], hs[(kt + 1) * 32 + h2]);
+      }
+      const double v0 = d00 + d10, v1 = d01 + d11;
+      double v[2 * NPAIR];
+      const int grp = lane & ~3;
+#pragma unroll
+      for (int i = 0; i < NPAIR; ++i) {
+        v[2 * i] = __shfl_sync(0xffffffffu, v0, grp | i);
+        v[2 * i + 1] = __shfl_sync(0xffffffffu, v1, grp | i);
+      }
+      const long long g0 = cinfo[2 * buf];
+      const int mask = static_cast<int>(cinfo[2 * buf + 1]);
+      if (j < NPAIR && !(mask & fb_e)) {
+        const int c0 = 2 * j, c1 = 2 * j + 1;
+        double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NCOL; ++k) {
+          o0 = fma(A.Q[c0][k], v[k], o0);
+          if (c1 < NCOL) o1 = fma(A.Q[c1][k], v[k], o1);
+        }
+        double* zp = z + g0 + off_e;
+        atomicAdd(zp + c0 * nsp, o0 * w_e);
+        if (c1 < NCOL) atomicAdd(zp + c1 * nsp, o1 * w_e);
+      }
+    }
+  }
+}
+
 // column b of every cell matrix from one probe of colour (cx,cy,cz) mod period
 __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx, int coly, int colz, int period,
                                      const double* __restrict__ probe, double* __restrict__ cellmat) {
@@ -632,9 +811,54 @@ void launch_asm_mma(const DevASM& A, const double* r, double* z, double scale, c
     default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
   }
 }
+template <int NT, int S>
+void launch_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (2 * kRec64 + 16 * 64) + 4 * sizeof(long long) + 2 * sizeof(unsigned long long);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(asm_apply_fd64_kernel<NT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaFuncSetAttribute(asm_apply_fd64_kernel<NT, S>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = true;
+  }
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_fd64_kernel<NT, S>, 256, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (A.n_list == 0) return;
+  const long long grid =
+      std::max<long long>(1, std::min<long long>(A.n_list, static_cast<long long>(std::max(per_sm, 1)) * sms));
+  count_launch();
+  asm_apply_fd64_kernel<NT, S><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
+}
+void launch_asm_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  switch (A.nt * 10 + A.S) {
+    case 11: launch_fd64<1, 1>(A, r, z, scale, s); break;
+    case 12: launch_fd64<1, 2>(A, r, z, scale, s); break;
+    case 13: launch_fd64<1, 3>(A, r, z, scale, s); break;
+    case 14: launch_fd64<1, 4>(A, r, z, scale, s); break;
+    case 15: launch_fd64<1, 5>(A, r, z, scale, s); break;
+    case 16: launch_fd64<1, 6>(A, r, z, scale, s); break;
+    case 17: launch_fd64<1, 7>(A, r, z, scale, s); break;
+    case 18: launch_fd64<1, 8>(A, r, z, scale, s); break;
+    case 21: launch_fd64<2, 1>(A, r, z, scale, s); break;
+    case 22: launch_fd64<2, 2>(A, r, z, scale, s); break;
+    case 23: launch_fd64<2, 3>(A, r, z, scale, s); break;
+    case 24: launch_fd64<2, 4>(A, r, z, scale, s); break;
+    case 31: launch_fd64<3, 1>(A, r, z, scale, s); break;
+    case 32: launch_fd64<3, 2>(A, r, z, scale, s); break;
+    case 41: launch_fd64<4, 1>(A, r, z, scale, s); break;
+    case 42: launch_fd64<4, 2>(A, r, z, scale, s); break;
+    default: launch_asm_mma(A, r, z, scale, s);
+  }
+}
 }  // namespace
 
 void asm_add_correction(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  if (A.m == 64 && A.tdiag && A.meta) {
+    launch_asm_fd64(A, r, z, scale, s);
+    return;
+  }
   switch (A.m) {
     case 4: launch_asm_nt<4>(A, r, z, scale, s); break;
     case 8: launch_asm_nt<8>(A, r, z, scale, s); break;

@@ -37,6 +37,7 @@ struct DevLevel {
   // 1D tables at the q = n Gauss points of [0,1]
   double B[kMaxN][kMaxN];   // B[q][j] = phi_j(x_q)      (spatial_operator.cpp:141-147)
   double Dq[kMaxN][kMaxN];  // collocation derivative at the Gauss points
+  double D[kMaxN][kMaxN];   // D[q][j] = phi_j'(x_q), nodal derivative at the Gauss points (= Dq B)
   double w[kMaxN];          // Gauss weights
   double xq[kMaxN];         // Gauss points on [0,1]
   double gl[kMaxN];         // Gauss-Lobatto support nodes on [0,1]

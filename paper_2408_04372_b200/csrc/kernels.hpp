@@ -77,7 +77,21 @@ struct DevASM {
   double TM[16], TA[16];  // diagonal (s,s) temporal blocks, n_t x n_t
   const long long* list;  // cells handled (X/lam stored per list entry); nullptr = all cells
   long long n_list;       // number of handled cells
+  // m = 64 records: X (swizzled, 4096 doubles) followed by the 64 eigenvalues,
+  // xs = kRec64; meta[pos] = {lattice offset of local dof 0, Dirichlet face
+  // mask (bit 2a: low face of axis a, 2a+1: high face)}
+  const long long* meta;
+  // temporal fast diagonalisation (T_M + lam T_A)^-1 = Q (B + lam)^-1 P of the
+  // n_t x n_t solves, expanded over the S steps into 8 MMA columns ("slots"):
+  // slot k <- sum_c P[k][c] col c; col c <- sum_k Q[c][k] slot k; slot pair
+  // (2j, 2j+1) is two real eigenvalues s0/s1 (kind 0) or one conjugate pair
+  // s0 +- i s1 (kind 1)
+  int tdiag;
+  int kind[4];
+  double s0[4], s1[4];
+  double P[8][8], Q[8][8];
 };
+constexpr int kRec64 = 64 * 64 + 64;
 // z += scale * W sum_T R_T^T B_T^-1 R_T r
 void asm_add_correction(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s);
 

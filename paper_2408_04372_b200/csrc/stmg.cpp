@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <stdexcept>
 
@@ -119,6 +120,7 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
     for (int j = 0; j < kMaxN; ++j) {
       d.B[i][j] = (i < d.n && j < d.n) ? lagrange_eval(gl.x, j, q.x[i]) : 0.0;
       d.Dq[i][j] = (i < d.n && j < d.n) ? lagrange_deriv(q.x, j, q.x[i]) : 0.0;
+      d.D[i][j] = (i < d.n && j < d.n) ? lagrange_deriv(gl.x, j, q.x[i]) : 0.0;
     }
   for (int i = 0; i < kMaxN; ++i) {
     d.w[i] = i < d.n ? q.w[i] : 0.0;
@@ -317,6 +319,231 @@ void SpaceTimeOperator::zero_boundary_field(double* v, cudaStream_t s) const {
 }
 
 // ------------------------------------------------------------ ASMSmoother
+namespace {
+// inverse of a small dense n x n matrix (Gauss-Jordan, partial pivoting);
+// false when singular
+bool invert_small(std::vector<double> a, int n, std::vector<double>& inv) {
+  inv.assign(static_cast<size_t>(n * n), 0.0);
+  for (int i = 0; i < n; ++i) inv[static_cast<size_t>(i * n + i)] = 1.0;
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::abs(a[static_cast<size_t>(i * n + k)]) > std::abs(a[static_cast<size_t>(piv * n + k)])) piv = i;
+    if (a[static_cast<size_t>(piv * n + k)] == 0.0) return false;
+    for (int j = 0; j < n; ++j) {
+      std::swap(a[static_cast<size_t>(k * n + j)], a[static_cast<size_t>(piv * n + j)]);
+      std::swap(inv[static_cast<size_t>(k * n + j)], inv[static_cast<size_t>(piv * n + j)]);
+    }
+    const double d = 1.0 / a[static_cast<size_t>(k * n + k)];
+    for (int j = 0; j < n; ++j) {
+      a[static_cast<size_t>(k * n + j)] *= d;
+      inv[static_cast<size_t>(k * n + j)] *= d;
+    }
+    for (int i = 0; i < n; ++i) {
+      if (i == k) continue;
+      const double f = a[static_cast<size_t>(i * n + k)];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        a[static_cast<size_t>(i * n + j)] -= f * a[static_cast<size_t>(k * n + j)];
+        inv[static_cast<size_t>(i * n + j)] -= f * inv[static_cast<size_t>(k * n + j)];
+      }
+    }
+  }
+  return true;
+}
+
+// null vector of (G - sigma I), G real n x n, sigma complex: complete-pivoting
+// elimination, the last pivot is the (numerically) zero one
+std::vector<std::complex<double>> eigvec_small(const std::vector<double>& G, int n, std::complex<double> sigma) {
+  using C = std::complex<double>;
+  std::vector<C> a(static_cast<size_t>(n * n));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) a[static_cast<size_t>(i * n + j)] = G[static_cast<size_t>(i * n + j)] - (i == j ? sigma : 0.0);
+  std::vector<int> colp(static_cast<size_t>(n));
+  for (int j = 0; j < n; ++j) colp[static_cast<size_t>(j)] = j;
+  auto A = [&](int i, int j) -> C& { return a[static_cast<size_t>(i * n + j)]; };
+  for (int k = 0; k < n - 1; ++k) {
+    int pi = k, pj = k;
+    for (int i = k; i < n; ++i)
+      for (int j = k; j < n; ++j)
+        if (std::abs(A(i, j)) > std::abs(A(pi, pj))) {
+          pi = i;
+          pj = j;
+        }
+    for (int j = 0; j < n; ++j) std::swap(A(k, j), A(pi, j));
+    for (int i = 0; i < n; ++i) std::swap(A(i, k), A(i, pj));
+    std::swap(colp[static_cast<size_t>(k)], colp[static_cast<size_t>(pj)]);
+    for (int i = k + 1; i < n; ++i) {
+      const C f = A(i, k) / A(k, k);
+      for (int j = k; j < n; ++j) A(i, j) -= f * A(k, j);
+    }
+  }
+  // U y = 0 with y_{n-1} = 1 (permuted unknowns)
+  std::vector<C> y(static_cast<size_t>(n));
+  y[static_cast<size_t>(n - 1)] = 1.0;
+  for (int i = n - 2; i >= 0; --i) {
+    C s = 0.0;
+    for (int j = i + 1; j < n; ++j) s += A(i, j) * y[static_cast<size_t>(j)];
+    y[static_cast<size_t>(i)] = -s / A(i, i);
+  }
+  std::vector<C> v(static_cast<size_t>(n));
+  for (int j = 0; j < n; ++j) v[static_cast<size_t>(colp[static_cast<size_t>(j)])] = y[static_cast<size_t>(j)];
+  // scale so the largest component is 1 (a real eigenvalue gives a real vector)
+  size_t im = 0;
+  for (size_t i = 1; i < v.size(); ++i)
+    if (std::abs(v[i]) > std::abs(v[im])) im = i;
+  const C s = v[im];
+  for (auto& x : v) x /= s;
+  return v;
+}
+}  // namespace
+
+// Real block diagonalisation of the temporal solves of the cell blocks:
+// T_M + lam T_A = T_A (G + lam I), G = T_A^-1 T_M = Q B Q^-1 with B 1x1 real
+// eigenvalues and 2x2 [[a, b], [-b, a]] blocks for conjugate pairs a +- ib, so
+// (T_M + lam T_A)^-1 = Q (B + lam)^-1 (Q^-1 T_A^-1). Fills A.P/Q/kind/s0/s1
+// over the S*n_t slab columns and sets A.tdiag; leaves it 0 (the pivoted
+// per-eigenvalue solve is used) when G has a repeated eigenvalue or Q is
+// ill-conditioned.
+void temporal_block_diagonalise(DevASM& A) {
+  A.tdiag = 0;
+  const int n = A.nt, S = A.S, ncol = n * S;
+  if (ncol > 8 || n < 1) return;
+  std::vector<double> TM(A.TM, A.TM + n * n), TA(A.TA, A.TA + n * n), TAi, G(static_cast<size_t>(n * n), 0.0);
+  if (!invert_small(TA, n, TAi)) return;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k) G[static_cast<size_t>(i * n + j)] += TAi[static_cast<size_t>(i * n + k)] * TM[static_cast<size_t>(k * n + j)];
+  std::vector<std::pair<double, double>> ev;
+  try {
+    ev = eigenvalues_small(G, n);
+  } catch (const std::exception&) {
+    return;
+  }
+  double gmax = 0.0;
+  for (auto& e : ev) gmax = std::max(gmax, std::hypot(e.first, e.second));
+  for (size_t a = 0; a < ev.size(); ++a)
+    for (size_t b = a + 1; b < ev.size(); ++b)
+      if (std::hypot(ev[a].first - ev[b].first, ev[a].second - ev[b].second) < 1e-8 * gmax) return;
+  // blocks in Q column order: complex pairs first (they need aligned slot pairs)
+  struct Blk {
+    int size;
+    double a, b;
+  };
+  std::vector<Blk> blocks;
+  std::vector<double> Qm(static_cast<size_t>(n * n), 0.0);
+  int col = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (auto& e : ev) {
+      const bool cplx = std::abs(e.second) > 1e-12 * gmax;
+      if (pass == 0 && !(cplx && e.second > 0)) continue;
+      if (pass == 1 && cplx) continue;
+      const auto v = eigvec_small(G, n, {e.first, cplx ? e.second : 0.0});
+      for (int i = 0; i < n; ++i) {
+        Qm[static_cast<size_t>(i * n + col)] = v[static_cast<size_t>(i)].real();
+        if (cplx) Qm[static_cast<size_t>(i * n + col + 1)] = v[static_cast<size_t>(i)].imag();
+      }
+      blocks.push_back({cplx ? 2 : 1, e.first, cplx ? e.second : 0.0});
+      col += cplx ? 2 : 1;
+    }
+  if (col != n) return;
+  std::vector<double> Qi;
+  if (!invert_small(Qm, n, Qi)) return;
+  // conditioning and reconstruction checks: Q B Q^-1 == G
+  double nq = 0.0, nqi = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double r1 = 0.0, r2 = 0.0;
+    for (int j = 0; j < n; ++j) {
+      r1 += std::abs(Qm[static_cast<size_t>(i * n + j)]);
+      r2 += std::abs(Qi[static_cast<size_t>(i * n + j)]);
+    }
+    nq = std::max(nq, r1);
+    nqi = std::max(nqi, r2);
+  }
+  if (nq * nqi > 1e6) return;
+  std::vector<double> B(static_cast<size_t>(n * n), 0.0);
+  {
+    int c = 0;
+    for (auto& b : blocks) {
+      B[static_cast<size_t>(c * n + c)] = b.a;
+      if (b.size == 2) {
+        B[static_cast<size_t>(c * n + c + 1)] = b.b;
+        B[static_cast<size_t>((c + 1) * n + c)] = -b.b;
+        B[static_cast<size_t>((c + 1) * n + c + 1)] = b.a;
+      }
+      c += b.size;
+    }
+  }
+  double err = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < n; ++k)
+        for (int l = 0; l < n; ++l)
+          s += Qm[static_cast<size_t>(i * n + k)] * B[static_cast<size_t>(k * n + l)] * Qi[static_cast<size_t>(l * n + j)];
+      err = std::max(err, std::abs(s - G[static_cast<size_t>(i * n + j)]));
+    }
+  if (err > 1e-10 * std::max(gmax, 1e-300)) return;
+  // Pm = Q^-1 T_A^-1
+  std::vector<double> Pm(static_cast<size_t>(n * n), 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k) Pm[static_cast<size_t>(i * n + j)] += Qi[static_cast<size_t>(i * n + k)] * TAi[static_cast<size_t>(k * n + j)];
+  // slots: complex blocks of every step on aligned pairs, then the reals
+  std::vector<int> slot(static_cast<size_t>(S * n), -1);  // (step, transformed component) -> slot
+  int next_pair = 0;
+  for (int s = 0; s < S; ++s) {
+    int c = 0;
+    for (auto& b : blocks) {
+      if (b.size == 2) {
+        slot[static_cast<size_t>(s * n + c)] = 2 * next_pair;
+        slot[static_cast<size_t>(s * n + c + 1)] = 2 * next_pair + 1;
+        ++next_pair;
+      }
+      c += b.size;
+    }
+  }
+  int next_slot = 2 * next_pair;
+  for (int s = 0; s < S; ++s) {
+    int c = 0;
+    for (auto& b : blocks) {
+      if (b.size == 1) slot[static_cast<size_t>(s * n + c)] = next_slot++;
+      c += b.size;
+    }
+  }
+  if (next_slot > 8) return;
+  std::memset(A.P, 0, sizeof(A.P));
+  std::memset(A.Q, 0, sizeof(A.Q));
+  for (int j = 0; j < 4; ++j) {
+    A.kind[j] = 0;
+    A.s0[j] = A.s1[j] = 1.0;  // unused slots: any nonzero value
+  }
+  for (int s = 0; s < S; ++s) {
+    int c = 0;
+    for (auto& b : blocks) {
+      const int k0 = slot[static_cast<size_t>(s * n + c)];
+      if (b.size == 2) {
+        A.kind[k0 / 2] = 1;
+        A.s0[k0 / 2] = b.a;
+        A.s1[k0 / 2] = b.b;
+      } else if (k0 % 2 == 0) {
+        A.s0[k0 / 2] = b.a;
+      } else {
+        A.s1[k0 / 2] = b.a;
+      }
+      c += b.size;
+    }
+    for (int comp = 0; comp < n; ++comp) {
+      const int k = slot[static_cast<size_t>(s * n + comp)];
+      for (int i = 0; i < n; ++i) {
+        A.P[k][s * n + i] = Pm[static_cast<size_t>(comp * n + i)];
+        A.Q[s * n + i][k] = Qm[static_cast<size_t>(i * n + comp)];
+      }
+    }
+  }
+  A.tdiag = 1;
+}
+
 ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
   const DevLevel& d = op.desc();
   DevASM& A = asm_;
@@ -486,9 +713,38 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op) {
   }
   cusolverDnDestroyParams(prm);
   cusolverDnDestroy(h);
-  A.xs = (static_cast<long long>(A.m) * A.m + 1) & ~1LL;
+  // m = 64: one TMA record per cell, X (swizzled) followed by its eigenvalues
+  A.xs = A.m == 64 ? kRec64 : (static_cast<long long>(A.m) * A.m + 1) & ~1LL;
   X_.allocate(sizeof(double) * static_cast<size_t>(n_pos) * A.xs);
   asm_back_transform(A.m, A.xs, n_pos, cellM.d(), cellA.d(), X_.d(), s);
+  if (A.m == 64) {
+    cuda_check(cudaMemcpy2DAsync(X_.d() + 64 * 64, sizeof(double) * kRec64, lam_.d(), sizeof(double) * 64,
+                                 sizeof(double) * 64, static_cast<size_t>(n_pos), cudaMemcpyDeviceToDevice, s),
+               "asm records");
+    // per position: lattice offset of local dof 0 and Dirichlet face mask
+    std::vector<long long> meta(static_cast<size_t>(2 * n_pos));
+    std::vector<long long> cells_h;
+    if (A.list) {
+      cells_h.resize(static_cast<size_t>(n_pos));
+      cuda_check(cudaMemcpy(cells_h.data(), A.list, sizeof(long long) * n_pos, cudaMemcpyDeviceToHost), "list");
+    }
+    for (Index q = 0; q < n_pos; ++q) {
+      const long long c = A.list ? cells_h[static_cast<size_t>(q)] : q;
+      const long long cx = c % A.cells[0], cy = (c / A.cells[0]) % A.cells[1], cz = c / (A.cells[0] * A.cells[1]);
+      meta[static_cast<size_t>(2 * q)] = (cz * A.p * A.dofs[1] + cy * A.p) * A.dofs[0] + cx * A.p;
+      long long mask = 0;
+      if (cx == 0) mask |= 1;
+      if (cx == A.cells[0] - 1) mask |= 2;
+      if (cy == 0) mask |= 4;
+      if (cy == A.cells[1] - 1) mask |= 8;
+      if (cz == 0) mask |= 16;
+      if (cz == A.cells[2] - 1) mask |= 32;
+      meta[static_cast<size_t>(2 * q + 1)] = mask;
+    }
+    meta_ = upload(meta);
+    A.meta = static_cast<const long long*>(meta_.raw());
+    temporal_block_diagonalise(A);
+  }
   cuda_check(cudaStreamSynchronize(s), "asm setup");
   A.X = X_.d();
   A.lam = lam_.d();

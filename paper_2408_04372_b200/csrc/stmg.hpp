@@ -114,13 +114,16 @@ class ASMSmoother {
   int block_size() const { return op_->n_t() * asm_.m; }
   Index n_blocks() const { return static_cast<Index>(op_->n_steps()) * op_->mesh().n_cells(); }
   long sweeps() const { return sweep_count_; }
-  size_t bytes() const { return X_.bytes() + lam_.bytes() + list_.bytes() + skip_.bytes(); }
+  size_t bytes() const { return X_.bytes() + lam_.bytes() + list_.bytes() + skip_.bytes() + meta_.bytes(); }
   // cells solved by tensor FDM / by the per-cell eigenbasis; exact() is false
   // when some block is only approximated (non-uniform coefficient around a
   // (p+1)^3 > 64 cell)
   bool uses_fdm() const { return use_fdm_; }
   Index n_exact_cells() const { return asm_.n_list; }
   bool exact() const { return exact_; }
+  // bit 0: tensor FDM cells, bit 1: per-cell eigenbasis cells, bit 2: the
+  // eigenbasis kernel also fast-diagonalises the temporal solves
+  int kind() const { return (use_fdm_ ? 1 : 0) | (asm_.n_list > 0 ? 2 : 0) | (asm_.n_list > 0 && asm_.tdiag && asm_.meta ? 4 : 0); }
 
  private:
   void build_exact(const SpaceTimeOperator& op);
@@ -129,7 +132,7 @@ class ASMSmoother {
   DevFDM fdm_{};
   bool use_fdm_ = false;
   bool exact_ = true;
-  DeviceBuffer X_, lam_, list_, skip_;
+  DeviceBuffer X_, lam_, list_, skip_, meta_;
   mutable long sweep_count_ = 0;
 };
 
@@ -249,5 +252,6 @@ class SpaceTimeMultigrid {
 // Hessenberg reduction + shifted QR, as needed for the Ritz values of the
 // relaxation estimate (multigrid.cpp:156-171)
 std::vector<std::pair<double, double>> eigenvalues_small(std::vector<double> a, int n);
+void temporal_block_diagonalise(DevASM& A);
 
 }  // namespace stmgb

@@ -10,7 +10,7 @@ python scripts/prof_kernels.py step $W > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches.csv python scripts/prof_kernels.py step $W > gpurun_out/ncu_launch.log 2>&1
 echo "launches rc $?" >> gpurun_out/pytest_gpu.log
 python scripts/prof_kernels.py kernels $W > gpurun_out/prof_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"st_apply_kernel" -c 1 -o gpurun_out/prof_st python scripts/prof_kernels.py kernels $W > gpurun_out/ncu_st.log 2>&1 && \
+ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"st_lines_kernel|st_apply_kernel" -c 1 -o gpurun_out/prof_st python scripts/prof_kernels.py kernels $W > gpurun_out/ncu_st.log 2>&1 && \
 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"asm_apply" -c 1 -o gpurun_out/prof_asm python scripts/prof_kernels.py kernels $W > gpurun_out/ncu_asm.log 2>&1
 echo "full rc $?" >> gpurun_out/pytest_gpu.log
 fi

@@ -131,3 +131,25 @@ def test_host_buffer_solve(cuda, ref):
     x_ref, info_ref = R.gmres(b, rel_tol=1e-10, abs_tol=0.0)
     assert abs(info["iterations"] - info_ref["iterations"]) <= 1
     assert _rel(x, x_ref) <= 1e-8
+
+
+Q3_TIME_CASES = [(problems.HEAT, problems.DG, 2, 1), (problems.HEAT, problems.DG, 1, 2), (problems.HEAT, problems.DG, 0, 4),
+                 (problems.HEAT, problems.DG, 3, 2), (problems.HEAT, problems.CGP, 2, 2), (problems.HEAT, problems.CGP, 1, 1),
+                 (problems.WAVE, problems.CGP, 2, 2), (problems.WAVE, problems.DG, 1, 1), (problems.WAVE, problems.DG, 2, 1)]
+
+
+@pytest.mark.parametrize("eq,scheme,k,S", Q3_TIME_CASES)
+def test_asm_q3_temporal_variants(cuda, ref, eq, scheme, k, S):
+    """Perturbed Q3 cells (64-dof blocks, the tensor-core kernel with
+    fast-diagonalised temporal solves) across heat/wave, DG/CGP, k and S:
+    equal to the reference's LU block solves to 1e-9."""
+    cfg = problems.Config("q3t", eq, scheme, 3, 2, 1, 3, k, S, 0.2, perturb=0.15)
+    cfg.rho = np.random.default_rng(5).uniform(0.5, 3.0, 8)
+    mesh, M, R = _build(cfg, ref)
+    n = R.n_dofs
+    res = problems.uniform_vector(n, seed=31)
+    z0 = problems.uniform_vector(n, seed=32)
+    got = M.asm_add_correction(0, _dev(cuda, res), _dev(cuda, z0)).cpu().numpy()
+    want = R.asm_add_correction(0, res, z0)
+    assert M.smoother_kind(0) == 6  # eigenbasis kernel with temporal fast diagonalisation
+    assert _rel(got - z0, want - z0) <= 1e-9

@@ -52,6 +52,11 @@ struct DevAxisTransfer {
   const int* col_idx;
   const double* col_w;
   long long nf, nc;
+  // pure h-coarsening with equal p (hp = p > 0): P[2p c + r][c p + j] =
+  // hw[r][j], r = 0..2p, the coarse basis at the fine nodes of one coarse
+  // cell -- applied without the CSR arrays
+  int hp;
+  double hw[9][kMaxN];
 };
 // separable per-axis passes; t1/t2 are work buffers of Transfer-chosen size
 // accumulate: fine += P coarse instead of fine = P coarse
@@ -120,6 +125,6 @@ void asm_back_transform(int m, long long xs, long long n_cells, const double* Li
 namespace stmgb {
 // number of kernels launched by this library since load (the bench's
 // gpu_launches evidence); incremented at every launch site
-void count_launch();
+void count_launch(long long n = 1);
 long long kernel_launches();
 }  // namespace stmgb

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -832,6 +833,14 @@ Transfer::Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coars
       ax_[a].col_w = bufs_.back().d();
       ax_[a].nf = nf;
       ax_[a].nc = nc;
+      // structured h weights: the rows of P for the fine nodes of coarse cell 0
+      ax_[a].hp = 0;
+      if (h && pf == pc) {
+        ax_[a].hp = pf;
+        for (int r = 0; r <= 2 * pf; ++r)
+          for (int j = 0; j < kMaxN; ++j)
+            ax_[a].hw[r][j] = j <= pc ? P[static_cast<size_t>(r * nc + j)] : 0.0;
+      }
     }
     const long long* df = fine.desc().dofs;
     const long long* dc = coarse.desc().dofs;
@@ -1364,11 +1373,68 @@ void SpaceTimeMultigrid::v_cycle(int l, const double* f, double* u, cudaStream_t
   }
   lv.op->residual(f, u, lv.r.d(), s);
   lv.to_coarser->restrict_(lv.r.d(), lv.rc.d(), s);
-  const Index nc = levels_[static_cast<size_t>(l) + 1].op->n_dofs();
-  vec_fill(lv.ec.d(), 0.0, nc, s);
-  v_cycle(l + 1, lv.rc.d(), lv.ec.d(), s);
+  if (l == 0) {
+    coarse_cycle(s);
+  } else {
+    const Index nc = levels_[static_cast<size_t>(l) + 1].op->n_dofs();
+    vec_fill(lv.ec.d(), 0.0, nc, s);
+    v_cycle(l + 1, lv.rc.d(), lv.ec.d(), s);
+  }
   lv.to_coarser->prolong(lv.ec.d(), u, s, /*accumulate=*/true);
   for (int i = 0; i < options_.n_smooth; ++i) smooth(l, f, u, s);
+}
+
+SpaceTimeMultigrid::~SpaceTimeMultigrid() { reset_graph(); }
+
+void SpaceTimeMultigrid::reset_graph() const {
+  if (coarse_exec_) cudaGraphExecDestroy(coarse_exec_);
+  coarse_exec_ = nullptr;
+  coarse_nodes_ = 0;
+}
+
+void SpaceTimeMultigrid::coarse_cycle(cudaStream_t s) const {
+  const Level& lv = levels_[0];
+  const Index nc = levels_[1].op->n_dofs();
+  auto direct = [&](cudaStream_t st) {
+    vec_fill(lv.ec.d(), 0.0, nc, st);
+    v_cycle(1, lv.rc.d(), lv.ec.d(), st);
+  };
+  static const bool disabled = std::getenv("STMG_NO_GRAPH") != nullptr;
+  if (disabled || graph_failed_) {
+    direct(s);
+    return;
+  }
+  if (!coarse_exec_) {
+    // capture on a private stream; nothing executes during capture
+    cudaStream_t cs = nullptr;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
+    const long long before = kernel_launches();
+    if (ok) ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      try {
+        direct(cs);
+      } catch (...) {
+        ok = false;
+      }
+      const cudaError_t e = cudaStreamEndCapture(cs, &g);
+      ok = ok && e == cudaSuccess && g != nullptr;
+    }
+    coarse_nodes_ = kernel_launches() - before;
+    count_launch(-coarse_nodes_);  // captured, not launched
+    if (ok) ok = cudaGraphInstantiate(&coarse_exec_, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+    cudaGetLastError();  // a failed capture leaves a sticky-free error behind
+    if (!ok) {
+      coarse_exec_ = nullptr;
+      graph_failed_ = true;
+      direct(s);
+      return;
+    }
+  }
+  cuda_check(cudaGraphLaunch(coarse_exec_, s), "coarse cycle graph");
+  count_launch(coarse_nodes_);
 }
 
 void SpaceTimeMultigrid::apply(const double* r, double* z, cudaStream_t s) const {

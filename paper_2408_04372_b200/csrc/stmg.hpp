@@ -220,7 +220,13 @@ class SpaceTimeMultigrid {
   const ASMSmoother& smoother_at(int l) const { return *levels_[l].smoother; }
   const Transfer& transfer_at(int l) const { return *levels_[l].to_coarser; }
   double omega_at(int l) const { return levels_[l].omega; }
-  void set_omega(int l, double w) { levels_[l].omega = w; }
+  void set_omega(int l, double w) {
+    levels_[l].omega = w;
+    reset_graph();  // omega is baked into the captured launches
+  }
+  ~SpaceTimeMultigrid();
+  SpaceTimeMultigrid(const SpaceTimeMultigrid&) = delete;
+  SpaceTimeMultigrid& operator=(const SpaceTimeMultigrid&) = delete;
   std::vector<LevelInfo> level_info() const;
   // one V-cycle from the finest level, zero initial guess (overwrite z)
   void apply(const double* r, double* z, cudaStream_t stream = nullptr) const;
@@ -242,6 +248,13 @@ class SpaceTimeMultigrid {
   double estimate_relaxation(const Level& lv, std::uint64_t seed) const;
   void coarse_solve(const double* f, double* u, cudaStream_t stream) const;
   void build_coarse_inverse(Level& lv);
+  // the sub-cycle below the finest level (fixed internal buffers) replayed as
+  // one CUDA graph; captured on first use, plain launches if capture fails
+  void coarse_cycle(cudaStream_t stream) const;
+  void reset_graph() const;
+  mutable cudaGraphExec_t coarse_exec_ = nullptr;
+  mutable long long coarse_nodes_ = 0;
+  mutable bool graph_failed_ = false;
 
   MultigridOptions options_;
   std::vector<Level> levels_;

@@ -21,46 +21,106 @@ namespace {
 __device__ __forceinline__ bool on_bdry(long long i, long long n) { return i == 0 || i == n - 1; }
 
 // out[f][z][y][x] (dims o[]) = sum_k w_k in[f][..src..] along `axis`;
-// input dims i[] equal o[] except along axis.
+// input dims i[] equal o[] except along axis. One thread per output entry of
+// a 32 x 4 (x, y) tile: grid (x tiles, y tiles, z * F), so no per-entry index decoding; the
+// reads along y/z are coalesced across the x-consecutive threads.
 template <int AXIS>
-__global__ void axis_pass_kernel(int F, long long ix, long long iy, long long iz, long long ox, long long oy,
-                                 long long oz, const int* __restrict__ ptr, const int* __restrict__ idx,
-                                 const double* __restrict__ w, bool mask_in, bool mask_out, bool accumulate,
-                                 const double* __restrict__ in, double* __restrict__ out) {
-  const long long on = ox * oy * oz, in_n = ix * iy * iz;
-  const long long total = on * F;
-  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
-       t += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long f = t / on;
-    const long long g = t - f * on;
-    const long long x = g % ox, y = (g / ox) % oy, z = g / (ox * oy);
-    double s = 0.0;
-    const bool zero_out = mask_out && (on_bdry(x, ox) || (oy > 1 && on_bdry(y, oy)) || (oz > 1 && on_bdry(z, oz)));
-    if (!zero_out) {
+__global__ void __launch_bounds__(128) axis_pass_kernel(long long ix, long long iy, long long iz, long long ox,
+                                                        long long oy, long long oz, const int* __restrict__ ptr,
+                                                        const int* __restrict__ idx, const double* __restrict__ w,
+                                                        bool mask_in, bool mask_out, bool accumulate,
+                                                        const double* __restrict__ in, double* __restrict__ out) {
+  const long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long y = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (x >= ox || y >= oy) return;
+  const long long z = blockIdx.z % oz, f = blockIdx.z / oz;
+  const long long oidx = ((f * oz + z) * oy + y) * ox + x;
+  double s = 0.0;
+  const bool zero_out = mask_out && (on_bdry(x, ox) || (oy > 1 && on_bdry(y, oy)) || (oz > 1 && on_bdry(z, oz)));
+  if (!zero_out) {
+    bool other_bd = false;
+    if (mask_in) {
+      if (AXIS != 0) other_bd = other_bd || on_bdry(x, ix);
+      if (AXIS != 1 && iy > 1) other_bd = other_bd || on_bdry(y, iy);
+      if (AXIS != 2 && iz > 1) other_bd = other_bd || on_bdry(z, iz);
+    }
+    if (!other_bd) {
       const long long o = AXIS == 0 ? x : (AXIS == 1 ? y : z);
-      const int k0 = ptr[o], k1 = ptr[o + 1];
-      const double* src = in + f * in_n;
-      bool other_bd = false;
-      if (mask_in) {
-        if (AXIS != 0) other_bd = other_bd || on_bdry(x, ix);
-        if (AXIS != 1 && iy > 1) other_bd = other_bd || on_bdry(y, iy);
-        if (AXIS != 2 && iz > 1) other_bd = other_bd || on_bdry(z, iz);
-      }
-      if (!other_bd) {
-        const long long n_ax = AXIS == 0 ? ix : (AXIS == 1 ? iy : iz);
-        for (int k = k0; k < k1; ++k) {
-          const long long j = idx[k];
-          if (mask_in && on_bdry(j, n_ax)) continue;
-          const long long sidx = AXIS == 0 ? (z * iy + y) * ix + j : (AXIS == 1 ? (z * iy + j) * ix + x : (j * iy + y) * ix + x);
-          s = fma(w[k], src[sidx], s);
-        }
+      const int k0 = __ldg(ptr + o), k1 = __ldg(ptr + o + 1);
+      const long long n_ax = AXIS == 0 ? ix : (AXIS == 1 ? iy : iz);
+      const double* src = in + f * ix * iy * iz;
+      const long long base = AXIS == 0 ? (z * iy + y) * ix : (AXIS == 1 ? z * iy * ix + x : y * ix + x);
+      const long long stride = AXIS == 0 ? 1 : (AXIS == 1 ? ix : ix * iy);
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const long long j = __ldg(idx + k);
+        if (mask_in && on_bdry(j, n_ax)) continue;
+        s = fma(__ldg(w + k), __ldg(src + base + j * stride), s);
       }
     }
-    if (accumulate)
-      out[t] += s;
-    else
-      out[t] = s;
   }
+  if (accumulate)
+    out[oidx] += s;
+  else
+    out[oidx] = s;
+}
+
+// h-transfer pass along AXIS for equal p on both meshes (structured weights,
+// no CSR): prolongation out[i] = sum_j hw[r][j] in[c p + j] with
+// i = 2p c + r; restriction out[c p + j] = sum_r hw[r][j] in[2p c + r]
+// (+ the left neighbour cell's r < 2p nodes for the vertex node j = 0)
+template <int AXIS, int P, bool PROLONG>
+__global__ void __launch_bounds__(128) axis_pass_h_kernel(long long ix, long long iy, long long iz, long long ox,
+                                                          long long oy, long long oz, const DevAxisTransfer T,
+                                                          bool mask_in, bool mask_out, bool accumulate,
+                                                          const double* __restrict__ in, double* __restrict__ out) {
+  const long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long y = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
+  if (x >= ox || y >= oy) return;
+  const long long z = blockIdx.z % oz, f = blockIdx.z / oz;
+  const long long oidx = ((f * oz + z) * oy + y) * ox + x;
+  double s = 0.0;
+  const bool zero_out = mask_out && (on_bdry(x, ox) || (oy > 1 && on_bdry(y, oy)) || (oz > 1 && on_bdry(z, oz)));
+  bool other_bd = false;
+  if (mask_in) {
+    if (AXIS != 0) other_bd = other_bd || on_bdry(x, ix);
+    if (AXIS != 1 && iy > 1) other_bd = other_bd || on_bdry(y, iy);
+    if (AXIS != 2 && iz > 1) other_bd = other_bd || on_bdry(z, iz);
+  }
+  if (!zero_out && !other_bd) {
+    const long long o = AXIS == 0 ? x : (AXIS == 1 ? y : z);
+    const long long n_ax = AXIS == 0 ? ix : (AXIS == 1 ? iy : iz);
+    const double* src = in + f * ix * iy * iz;
+    const long long base = AXIS == 0 ? (z * iy + y) * ix : (AXIS == 1 ? z * iy * ix + x : y * ix + x);
+    const long long stride = AXIS == 0 ? 1 : (AXIS == 1 ? ix : ix * iy);
+    auto val = [&](long long j) {
+      return (mask_in && on_bdry(j, n_ax)) ? 0.0 : __ldg(src + base + j * stride);
+    };
+    if (PROLONG) {
+      const long long ncc = (n_ax - 1) / P;
+      long long c = o / (2 * P);
+      if (c > ncc - 1) c = ncc - 1;
+      const int r = static_cast<int>(o - 2 * P * c);
+#pragma unroll
+      for (int j = 0; j <= P; ++j) s = fma(T.hw[r][j], val(c * P + j), s);
+    } else {
+      const long long c = o / P;
+      const int j = static_cast<int>(o - c * P);
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) {
+        const long long i = 2 * P * c + r;
+        if (i < n_ax) s = fma(T.hw[r][j], val(i), s);
+      }
+      if (j == 0 && c > 0) {
+#pragma unroll
+        for (int r = 0; r < 2 * P; ++r) s = fma(T.hw[r][P], val(2 * P * (c - 1) + r), s);
+      }
+    }
+  }
+  if (accumulate)
+    out[oidx] += s;
+  else
+    out[oidx] = s;
 }
 
 __global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bool transpose, bool accumulate,
@@ -93,44 +153,57 @@ inline unsigned grid_for(long long n) {
   return static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 64)));
 }
 
-template <int AXIS>
-void pass(int F, const long long* in_d, const long long* out_d, const int* ptr, const int* idx, const double* w,
-          bool mask_in, bool mask_out, bool accumulate, const double* in, double* out, cudaStream_t s) {
-  const long long total = out_d[0] * out_d[1] * out_d[2] * F;
-  count_launch();
-  axis_pass_kernel<AXIS><<<grid_for(total), 256, 0, s>>>(F, in_d[0], in_d[1], in_d[2], out_d[0], out_d[1], out_d[2],
-                                                         ptr, idx, w, mask_in, mask_out, accumulate, in, out);
+template <int AXIS, int P, bool PROLONG>
+void launch_h(const dim3& grid, const dim3& block, const long long* in_d, const long long* out_d,
+              const DevAxisTransfer& T, bool mask_in, bool mask_out, bool accumulate, const double* in, double* out,
+              cudaStream_t s) {
+  axis_pass_h_kernel<AXIS, P, PROLONG><<<grid, block, 0, s>>>(in_d[0], in_d[1], in_d[2], out_d[0], out_d[1], out_d[2],
+                                                               T, mask_in, mask_out, accumulate, in, out);
 }
 
-// apply the per-axis CSR maps x, then y, then z (2D: x, y)
+template <int AXIS>
+void pass(int F, const long long* in_d, const long long* out_d, const DevAxisTransfer& T, bool prolong, bool mask_in,
+          bool mask_out, bool accumulate, const double* in, double* out, cudaStream_t s) {
+  const dim3 block(32, 4);
+  const dim3 grid(static_cast<unsigned>((out_d[0] + 31) / 32), static_cast<unsigned>((out_d[1] + 3) / 4),
+                  static_cast<unsigned>(out_d[2] * F));
+  count_launch();
+  if (T.hp > 0) {
+#define STMG_H(PP)                                                                                        \
+  case PP:                                                                                                \
+    if (prolong)                                                                                          \
+      launch_h<AXIS, PP, true>(grid, block, in_d, out_d, T, mask_in, mask_out, accumulate, in, out, s);  \
+    else                                                                                                  \
+      launch_h<AXIS, PP, false>(grid, block, in_d, out_d, T, mask_in, mask_out, accumulate, in, out, s); \
+    return;
+    switch (T.hp) {
+      STMG_H(1)
+      STMG_H(2)
+      STMG_H(3)
+      STMG_H(4)
+      default: break;
+    }
+#undef STMG_H
+  }
+  const int* ptr = prolong ? T.row_ptr : T.col_ptr;
+  const int* idx = prolong ? T.row_idx : T.col_idx;
+  const double* w = prolong ? T.row_w : T.col_w;
+  axis_pass_kernel<AXIS><<<grid, block, 0, s>>>(in_d[0], in_d[1], in_d[2], out_d[0], out_d[1], out_d[2], ptr, idx, w,
+                                              mask_in, mask_out, accumulate, in, out);
+}
+
+// apply the per-axis maps x, then y, then z (2D: x, y)
 void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const long long* src_d, const long long* dst_d,
                const double* in, double* out, double* t1, double* t2, bool accumulate, cudaStream_t s) {
-  auto P = [&](int a, const int*& ptr, const int*& idx, const double*& w) {
-    if (prolong) {
-      ptr = ax[a].row_ptr;
-      idx = ax[a].row_idx;
-      w = ax[a].row_w;
-    } else {
-      ptr = ax[a].col_ptr;
-      idx = ax[a].col_idx;
-      w = ax[a].col_w;
-    }
-  };
-  const int *ptr, *idx;
-  const double* w;
   long long d1[3] = {dst_d[0], src_d[1], src_d[2]};
-  P(0, ptr, idx, w);
-  pass<0>(F, src_d, d1, ptr, idx, w, true, false, false, in, t1, s);
+  pass<0>(F, src_d, d1, ax[0], prolong, true, false, false, in, t1, s);
   if (dim == 2) {
-    P(1, ptr, idx, w);
-    pass<1>(F, d1, dst_d, ptr, idx, w, false, true, accumulate, t1, out, s);
+    pass<1>(F, d1, dst_d, ax[1], prolong, false, true, accumulate, t1, out, s);
     return;
   }
   long long d2[3] = {dst_d[0], dst_d[1], src_d[2]};
-  P(1, ptr, idx, w);
-  pass<1>(F, d1, d2, ptr, idx, w, false, false, false, t1, t2, s);
-  P(2, ptr, idx, w);
-  pass<2>(F, d2, dst_d, ptr, idx, w, false, true, accumulate, t2, out, s);
+  pass<1>(F, d1, d2, ax[1], prolong, false, false, false, t1, t2, s);
+  pass<2>(F, d2, dst_d, ax[2], prolong, false, true, accumulate, t2, out, s);
 }
 
 }  // namespace

@@ -174,6 +174,57 @@ int stmg_solve(const stmg_multigrid* mg, int precondition, const double* d_b, do
 int stmg_solve_host(const stmg_multigrid* mg, int precondition, const double* h_b, double* h_x,
                     const stmg_gmres_options* options, stmg_gmres_result* result, double* history, int history_cap);
 
+/* ---- z-slab partitioned solve over several GPUs (no
+ * reference counterpart: the reference is single-process). The finest mesh
+ * is cut into n_parts slabs of cell layers along z; a process holds
+ * local_parts consecutive slabs starting at first_part, and the processes
+ * talk over NCCL (interface-plane exchanges and dot-product allreduces). One
+ * process holding every part runs the same partitioned algorithm on one GPU.
+ * Vectors of the partitioned finest level are the concatenation of the local
+ * parts' slab vectors (each in the reference layout of its slab lattice,
+ * interface planes included on both sides). */
+typedef struct stmg_comm stmg_comm;
+typedef struct stmg_slab_multigrid stmg_slab_multigrid;
+/* NCCL unique id (128 bytes) for stmg_comm_create, on the root rank */
+int stmg_nccl_unique_id(char id[128]);
+int stmg_comm_create(int world, int rank, const char id[128], stmg_comm** out);
+void stmg_comm_destroy(stmg_comm* c);
+/* host-only: how many levels of the default plan of (fine_mesh_level, p, k,
+ * n_steps) stay partitioned for n_parts slabs of cells_z finest layers */
+int stmg_slab_plan(int scheme, int fine_mesh_level, int p, int k, int n_steps, long long cells_z, int n_parts,
+                   int* dist_levels, int* n_levels);
+/* SpaceTimeMultigrid over the partition (options/strategy as
+ * stmg_multigrid_create); comm may be NULL for a single process */
+int stmg_slab_multigrid_create(int equation, int scheme, const stmg_mesh* mesh, const double* coarse_cell_scale,
+                               int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
+                               const int* strategy, const stmg_mg_options* options, int n_parts, int first_part,
+                               int local_parts, const stmg_comm* comm, stmg_slab_multigrid** out);
+void stmg_slab_multigrid_destroy(stmg_slab_multigrid* mg);
+long long stmg_slab_multigrid_local_dofs(const stmg_slab_multigrid* mg);
+/* info[0] partitioned levels, info[1] total levels */
+int stmg_slab_multigrid_info(const stmg_slab_multigrid* mg, int info[2]);
+/* local part i: offset and length in the local vector, first global lattice plane */
+int stmg_slab_multigrid_part(const stmg_slab_multigrid* mg, int i, long long* offset, long long* n_dofs,
+                             long long* plane0);
+double stmg_slab_multigrid_omega(const stmg_slab_multigrid* mg, int level);
+int stmg_slab_multigrid_set_omega(stmg_slab_multigrid* mg, int level, double omega);
+/* SpaceTimeOperator::apply on the partition (interface-summed), overwrite */
+int stmg_slab_multigrid_apply(const stmg_slab_multigrid* mg, const double* d_u, double* d_y, void* stream);
+/* one V-cycle, zero initial guess, overwrite */
+int stmg_slab_multigrid_vcycle(const stmg_slab_multigrid* mg, const double* d_r, double* d_z, void* stream);
+/* finest-level smoother, accumulate (ASMSmoother::add_correction) */
+int stmg_slab_multigrid_asm_add_correction(const stmg_slab_multigrid* mg, const double* d_r, double* d_z,
+                                           void* stream);
+/* STMG-preconditioned GMRES on the partition */
+int stmg_slab_multigrid_solve(const stmg_slab_multigrid* mg, const double* d_b, double* d_x,
+                              const stmg_gmres_options* options, stmg_gmres_result* result, void* stream);
+/* owned-entry inner product summed over the ranks */
+int stmg_slab_multigrid_dot(const stmg_slab_multigrid* mg, const double* d_a, const double* d_b, double* out);
+/* full-length finest vector <-> local parts (device); gather writes the
+ * owned planes of the local parts only */
+int stmg_slab_multigrid_scatter(const stmg_slab_multigrid* mg, const double* d_full, double* d_local, void* stream);
+int stmg_slab_multigrid_gather(const stmg_slab_multigrid* mg, const double* d_local, double* d_full, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -314,6 +314,116 @@ class SpaceTimeMultigrid:
             self._h = None
 
 
+class Comm:
+    """NCCL communicator of the partitioned solve: rank 0 draws the unique id,
+    torch.distributed broadcasts it, every rank joins (stmg_comm_create)."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        h = C.c_void_p()
+        N.check(N.load().stmg_comm_create(world, rank, uid, C.byref(h)))
+        self._h, self.world, self.rank = h, world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        N.check(N.load().stmg_nccl_unique_id(buf))
+        return buf.raw
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.load().stmg_comm_destroy(self._h)
+            self._h = None
+
+
+def slab_plan(scheme: int, fine_level: int, p: int, k: int, n_steps: int, cells_z: int, n_parts: int):
+    """(partitioned levels, total levels) of the default plan (host only)."""
+    d, n = C.c_int(), C.c_int()
+    N.check(N.load().stmg_slab_plan(scheme, fine_level, p, k, n_steps, cells_z, n_parts, C.byref(d), C.byref(n)))
+    return d.value, n.value
+
+
+class SlabMultigrid:
+    """STMG solve on a z-slab partition of the finest mesh: the
+    process holds parts [first_part, first_part + local_parts) of n_parts;
+    comm (a Comm, or None for one process) joins the processes over NCCL.
+    Local vectors are the concatenation of the local parts' slab vectors."""
+
+    def __init__(self, equation: int, scheme: int, mesh: Mesh, rho: Optional[np.ndarray], fine_level: int, p: int,
+                 k: int, n_steps: int, tau: float, n_parts: int, first_part: int = 0,
+                 local_parts: Optional[int] = None, comm: Optional[Comm] = None,
+                 strategy: Optional[Sequence[int]] = None, **options):
+        lib = N.load()
+        r = _dbl(rho)
+        strat, ns = None, -1
+        if strategy is not None:
+            ns = len(strategy)
+            strat = (C.c_int * max(ns, 1))(*strategy)
+        o = mg_options(**options)
+        if local_parts is None:
+            local_parts = n_parts - first_part
+        h = C.c_void_p()
+        N.check(lib.stmg_slab_multigrid_create(equation, scheme, mesh._h, r[1] if r else None, fine_level, p, k,
+                                               n_steps, tau, ns, strat, C.byref(o), n_parts, first_part,
+                                               local_parts, comm._h if comm is not None else None, C.byref(h)))
+        self._h, self.mesh, self.comm = h, mesh, comm
+        self.n_local = lib.stmg_slab_multigrid_local_dofs(h)
+        info = (C.c_int * 2)()
+        N.check(lib.stmg_slab_multigrid_info(h, info))
+        self.dist_levels, self.n_levels = info[0], info[1]
+        self.parts = []
+        for i in range(local_parts):
+            off, nd, p0 = C.c_longlong(), C.c_longlong(), C.c_longlong()
+            N.check(lib.stmg_slab_multigrid_part(h, i, C.byref(off), C.byref(nd), C.byref(p0)))
+            self.parts.append({"offset": off.value, "n_dofs": nd.value, "plane0": p0.value})
+
+    def omega_at(self, l: int) -> float:
+        return float(N.load().stmg_slab_multigrid_omega(self._h, l))
+
+    def set_omega(self, l: int, w: float):
+        N.check(N.load().stmg_slab_multigrid_set_omega(self._h, l, w))
+
+    def apply(self, u, y=None):
+        y = _torch().empty_like(u) if y is None else y
+        N.check(N.load().stmg_slab_multigrid_apply(self._h, _ptr(u), _ptr(y), _stream()))
+        return y
+
+    def vcycle(self, r, z=None):
+        z = _torch().empty_like(r) if z is None else z
+        N.check(N.load().stmg_slab_multigrid_vcycle(self._h, _ptr(r), _ptr(z), _stream()))
+        return z
+
+    def asm_add_correction(self, r, z):
+        N.check(N.load().stmg_slab_multigrid_asm_add_correction(self._h, _ptr(r), _ptr(z), _stream()))
+        return z
+
+    def solve(self, b, x, **opts):
+        o = gmres_options(**opts)
+        res = N.GmresResult()
+        N.check(N.load().stmg_slab_multigrid_solve(self._h, _ptr(b), _ptr(x), C.byref(o), C.byref(res), _stream()))
+        return _result(res, np.zeros(0))
+
+    def dot(self, a, b) -> float:
+        out = C.c_double()
+        _torch().cuda.synchronize()
+        N.check(N.load().stmg_slab_multigrid_dot(self._h, _ptr(a), _ptr(b), C.byref(out)))
+        return out.value
+
+    def scatter(self, full, local=None):
+        torch = _torch()
+        local = torch.empty(self.n_local, dtype=full.dtype, device=full.device) if local is None else local
+        N.check(N.load().stmg_slab_multigrid_scatter(self._h, _ptr(full), _ptr(local), _stream()))
+        return local
+
+    def gather(self, local, full):
+        N.check(N.load().stmg_slab_multigrid_gather(self._h, _ptr(local), _ptr(full), _stream()))
+        return full
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.load().stmg_slab_multigrid_destroy(self._h)
+            self._h = None
+
+
 def _result(res: N.GmresResult, hist: np.ndarray) -> dict:
     n = min(res.history_len, hist.size)
     return {"converged": bool(res.converged), "iterations": res.iterations,

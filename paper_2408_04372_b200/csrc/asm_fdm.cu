@@ -123,11 +123,11 @@ __global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ Dev
       base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx + static_cast<long long>(cx) * p;
       const int tx = (cx == 0 ? 1 : 0) | (cx == nx - 1 ? 2 : 0);
       const int ty = (cy == 0 ? 1 : 0) | (cy == ny - 1 ? 2 : 0);
-      const int tz = DIM == 3 ? ((cz == 0 ? 1 : 0) | (cz == nz - 1 ? 2 : 0)) : 0;
+      const int tz = DIM == 3 ? ((cz == 0 && (P.zbc & 1) ? 1 : 0) | (cz == nz - 1 && (P.zbc & 2) ? 2 : 0)) : 0;
       info = tx | (ty << 2) | (tz << 4) | (tx << 8) | (ty << 10) | (tz << 12);
       double rho = 1.0;
       if (P.rho0) {
-        const long long ax = cx >> P.rho_shift, ay = cy >> P.rho_shift, az = cz >> P.rho_shift;
+        const long long ax = cx >> P.rho_shift, ay = cy >> P.rho_shift, az = (cz + P.cz0) >> P.rho_shift;
         rho = P.rho0[(az * P.cells0[1] + ay) * P.cells0[0] + ax];
       }
       rho_s[tid] = rho;

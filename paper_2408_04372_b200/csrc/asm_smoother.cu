@@ -48,13 +48,16 @@ __device__ __forceinline__ LocalDof local_dof(const DevASM& A, long long cx, lon
   const long long gx = cx * A.p + lx, gy = cy * A.p + ly, gz = cz * A.p + lz;
   LocalDof d;
   d.g = (gz * A.dofs[1] + gy) * A.dofs[0] + gx;
+  // slab z faces are Dirichlet only where physical (A.zbc); interface planes
+  // are shared with the neighbouring slab's cells
+  const bool zlo = gz == 0 && (A.zbc & 1), zhi = gz == A.dofs[2] - 1 && (A.zbc & 2);
   d.bdry = gx == 0 || gx == A.dofs[0] - 1 || (A.dim > 1 && (gy == 0 || gy == A.dofs[1] - 1)) ||
-           (A.dim > 2 && (gz == 0 || gz == A.dofs[2] - 1));
+           (A.dim > 2 && (zlo || zhi));
   // number of cells containing the dof (asm_smoother.cpp:45-49)
   double m = 1.0;
   if (gx % A.p == 0 && gx > 0 && gx < A.dofs[0] - 1) m *= 2.0;
   if (A.dim > 1 && gy % A.p == 0 && gy > 0 && gy < A.dofs[1] - 1) m *= 2.0;
-  if (A.dim > 2 && gz % A.p == 0 && gz > 0 && gz < A.dofs[2] - 1) m *= 2.0;
+  if (A.dim > 2 && gz % A.p == 0 && !zlo && !zhi) m *= 2.0;
   d.mult = m;
   return d;
 }
@@ -617,7 +620,8 @@ __global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_con
 
 // column b of every cell matrix from one probe of colour (cx,cy,cz) mod period
 __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx, int coly, int colz, int period,
-                                     const double* __restrict__ probe, double* __restrict__ cellmat) {
+                                     const double* __restrict__ probe, int probe_zcells,
+                                     double* __restrict__ cellmat) {
   const long long n_pos = A.n_list;
   const int m = A.m, n = A.n;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n_pos * m;
@@ -630,7 +634,7 @@ __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx,
     // local index per axis whose lattice coordinate has the probe colour
     int lb[3] = {0, 0, 0};
     bool found = true;
-    const long long c3[3] = {cx, cy, cz};
+    const long long c3[3] = {cx, cy, cz + A.cz0};  // colours: global lattice coordinates
     const int col[3] = {colx, coly, colz};
     for (int ax = 0; ax < A.dim; ++ax) {
       int hit = -1;
@@ -642,7 +646,8 @@ __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx,
     if (!found) continue;
     const int b = lb[0] + n * (lb[1] + (A.dim == 3 ? n * lb[2] : 0));
     const LocalDof da = local_dof(A, cx, cy, cz, a);
-    cellmat[pos * static_cast<long long>(m) * m + static_cast<long long>(a) * m + b] = probe[da.g];
+    const long long gp = da.g + static_cast<long long>(probe_zcells) * A.p * A.dofs[0] * A.dofs[1];
+    cellmat[pos * static_cast<long long>(m) * m + static_cast<long long>(a) * m + b] = probe[gp];
   }
 }
 
@@ -871,13 +876,13 @@ void asm_add_correction(const DevASM& A, const double* r, double* z, double scal
   }
 }
 
-void asm_extract_probe(const DevASM& A, int cx, int cy, int cz, int period, const double* probe, double* cellmat,
-                       cudaStream_t s) {
+void asm_extract_probe(const DevASM& A, int cx, int cy, int cz, int period, const double* probe, int probe_zcells,
+                       double* cellmat, cudaStream_t s) {
   const long long total = A.n_list * A.m;
   if (total == 0) return;
   const unsigned grid = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 148LL * 64)));
   count_launch();
-  extract_probe_kernel<<<grid, 256, 0, s>>>(A, cx, cy, cz, period, probe, cellmat);
+  extract_probe_kernel<<<grid, 256, 0, s>>>(A, cx, cy, cz, period, probe, probe_zcells, cellmat);
 }
 
 void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s) {

@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "slab_mg.hpp"
 #include "stmg.hpp"
 
 using namespace stmgb;
@@ -27,6 +28,12 @@ struct stmg_asm {
 };
 struct stmg_transfer {
   std::unique_ptr<Transfer> t;
+};
+struct stmg_comm {
+  std::unique_ptr<NcclComm> c;
+};
+struct stmg_slab_multigrid {
+  std::unique_ptr<SlabMultigrid> mg;
 };
 struct stmg_multigrid {
   std::unique_ptr<SpaceTimeMultigrid> mg;
@@ -252,6 +259,32 @@ void stmg_mg_options_default(stmg_mg_options* o) {
   o->seed = d.seed;
 }
 
+namespace {
+MultigridOptions mg_opts(const stmg_mg_options* options) {
+  MultigridOptions mo;
+  if (options) {
+    mo.n_smooth = options->n_smooth;
+    mo.direct_coarse_max = options->direct_coarse_max;
+    mo.coarse_rel_tol = options->coarse_rel_tol;
+    mo.coarse_max_iters = options->coarse_max_iters;
+    mo.eig_iters = options->eig_iters;
+    mo.seed = options->seed;
+  }
+  return mo;
+}
+std::vector<LevelSpec> mg_plan(int scheme, int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
+                               const int* strategy) {
+  const TimeScheme sch = static_cast<TimeScheme>(scheme);
+  LevelSpec finest{fine_mesh_level, p, k, n_steps, tau, Coarsening::SpaceH};
+  std::vector<Coarsening> strat;
+  if (n_strategy < 0)
+    strat = default_strategy(finest, sch);
+  else
+    for (int i = 0; i < n_strategy; ++i) strat.push_back(static_cast<Coarsening>(strategy[i]));
+  return build_level_plan(finest, sch, strat);
+}
+}  // namespace
+
 int stmg_multigrid_create(int equation, int scheme, const stmg_mesh* mesh, const double* coarse_cell_scale,
                           int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
                           const int* strategy, const stmg_mg_options* options, stmg_multigrid** out) {
@@ -451,6 +484,131 @@ int stmg_solve_host(const stmg_multigrid* mg, int precondition, const double* h_
     const int rc = stmg_solve(mg, precondition, b.d(), x.d(), options, result, history, history_cap, nullptr);
     if (rc != 0) throw std::runtime_error(g_err);
     cuda_check(cudaMemcpy(h_x, x.raw(), bytes, cudaMemcpyDeviceToHost), "D2H x");
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int stmg_nccl_unique_id(char id[128]) {
+  return guard_host([&] {
+    if (!id) throw std::invalid_argument("stmg_nccl_unique_id: null argument");
+    const std::string u = NcclComm::unique_id();
+    std::memcpy(id, u.data(), 128);
+  });
+}
+int stmg_comm_create(int world, int rank, const char id[128], stmg_comm** out) {
+  return guard([&] {
+    if (!id || !out) throw std::invalid_argument("stmg_comm_create: null argument");
+    auto c = std::make_unique<stmg_comm>();
+    c->c = std::make_unique<NcclComm>(world, rank, std::string(id, 128));
+    *out = c.release();
+  });
+}
+void stmg_comm_destroy(stmg_comm* c) { delete c; }
+
+int stmg_slab_plan(int scheme, int fine_mesh_level, int p, int k, int n_steps, long long cells_z, int n_parts,
+                   int* dist_levels, int* n_levels) {
+  return guard_host([&] {
+    if (!dist_levels || !n_levels) throw std::invalid_argument("stmg_slab_plan: null argument");
+    const auto plan = mg_plan(scheme, fine_mesh_level, p, k, n_steps, 1.0, -1, nullptr);
+    const SlabPlan sp = make_slab_plan(plan, cells_z, fine_mesh_level, n_parts);
+    *dist_levels = sp.dist_levels;
+    *n_levels = static_cast<int>(plan.size());
+  });
+}
+
+int stmg_slab_multigrid_create(int equation, int scheme, const stmg_mesh* mesh, const double* coarse_cell_scale,
+                               int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
+                               const int* strategy, const stmg_mg_options* options, int n_parts, int first_part,
+                               int local_parts, const stmg_comm* comm, stmg_slab_multigrid** out) {
+  return guard([&] {
+    if (!mesh || !out) throw std::invalid_argument("stmg_slab_multigrid_create: null argument");
+    auto m = std::make_unique<stmg_slab_multigrid>();
+    m->mg = std::make_unique<SlabMultigrid>(
+        static_cast<Equation>(equation), static_cast<TimeScheme>(scheme), mesh->h, coeff(mesh->h, coarse_cell_scale),
+        mg_plan(scheme, fine_mesh_level, p, k, n_steps, tau, n_strategy, strategy), mg_opts(options), n_parts,
+        first_part, local_parts, comm ? comm->c.get() : nullptr);
+    *out = m.release();
+  });
+}
+void stmg_slab_multigrid_destroy(stmg_slab_multigrid* mg) { delete mg; }
+long long stmg_slab_multigrid_local_dofs(const stmg_slab_multigrid* mg) { return mg ? mg->mg->local_dofs() : -1; }
+int stmg_slab_multigrid_info(const stmg_slab_multigrid* mg, int info[2]) {
+  return guard_host([&] {
+    if (!mg || !info) throw std::invalid_argument("stmg_slab_multigrid_info: null argument");
+    info[0] = mg->mg->dist_levels();
+    info[1] = mg->mg->n_levels();
+  });
+}
+int stmg_slab_multigrid_part(const stmg_slab_multigrid* mg, int i, long long* offset, long long* n_dofs,
+                             long long* plane0) {
+  return guard_host([&] {
+    if (!mg || !offset || !n_dofs || !plane0) throw std::invalid_argument("stmg_slab_multigrid_part: null argument");
+    if (i < 0 || i >= mg->mg->local_parts()) throw std::invalid_argument("stmg_slab_multigrid_part: bad part");
+    *offset = mg->mg->part_offset(i);
+    *n_dofs = mg->mg->part_dofs(i);
+    *plane0 = mg->mg->part_plane0(i);
+  });
+}
+double stmg_slab_multigrid_omega(const stmg_slab_multigrid* mg, int level) {
+  try {
+    return mg ? mg->mg->omega_at(level) : -1.0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+int stmg_slab_multigrid_set_omega(stmg_slab_multigrid* mg, int level, double omega) {
+  return guard_host([&] {
+    if (!mg) throw std::invalid_argument("stmg_slab_multigrid_set_omega: null argument");
+    mg->mg->set_omega(level, omega);
+  });
+}
+int stmg_slab_multigrid_apply(const stmg_slab_multigrid* mg, const double* d_u, double* d_y, void* stream) {
+  return guard([&] {
+    if (!mg || !d_u || !d_y) throw std::invalid_argument("stmg_slab_multigrid_apply: null argument");
+    mg->mg->apply(d_u, d_y, st(stream));
+  });
+}
+int stmg_slab_multigrid_vcycle(const stmg_slab_multigrid* mg, const double* d_r, double* d_z, void* stream) {
+  return guard([&] {
+    if (!mg || !d_r || !d_z) throw std::invalid_argument("stmg_slab_multigrid_vcycle: null argument");
+    mg->mg->vcycle(d_r, d_z, st(stream));
+  });
+}
+int stmg_slab_multigrid_asm_add_correction(const stmg_slab_multigrid* mg, const double* d_r, double* d_z,
+                                           void* stream) {
+  return guard([&] {
+    if (!mg || !d_r || !d_z) throw std::invalid_argument("stmg_slab_multigrid_asm_add_correction: null argument");
+    mg->mg->asm_add_correction(d_r, d_z, st(stream));
+  });
+}
+int stmg_slab_multigrid_solve(const stmg_slab_multigrid* mg, const double* d_b, double* d_x,
+                              const stmg_gmres_options* options, stmg_gmres_result* result, void* stream) {
+  return guard([&] {
+    if (!mg || !d_b || !d_x) throw std::invalid_argument("stmg_slab_multigrid_solve: null argument");
+    const GmresResult r = mg->mg->solve(d_b, d_x, gopts(options), st(stream));
+    if (result) fill_result(r, result, nullptr, 0);
+  });
+}
+int stmg_slab_multigrid_dot(const stmg_slab_multigrid* mg, const double* d_a, const double* d_b, double* out) {
+  return guard([&] {
+    if (!mg || !d_a || !d_b || !out) throw std::invalid_argument("stmg_slab_multigrid_dot: null argument");
+    *out = mg->mg->dot(d_a, d_b, nullptr);
+  });
+}
+int stmg_slab_multigrid_scatter(const stmg_slab_multigrid* mg, const double* d_full, double* d_local, void* stream) {
+  return guard([&] {
+    if (!mg || !d_full || !d_local) throw std::invalid_argument("stmg_slab_multigrid_scatter: null argument");
+    mg->mg->scatter(d_full, d_local, st(stream));
+  });
+}
+int stmg_slab_multigrid_gather(const stmg_slab_multigrid* mg, const double* d_local, double* d_full, void* stream) {
+  return guard([&] {
+    if (!mg || !d_local || !d_full) throw std::invalid_argument("stmg_slab_multigrid_gather: null argument");
+    mg->mg->gather(d_local, d_full, st(stream));
   });
 }
 

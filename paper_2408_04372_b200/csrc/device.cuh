@@ -30,6 +30,13 @@ struct DevLevel {
   const double* verts;  // (cells+1)^dim * 3 doubles, x fastest
   double h[3];
   double lo[3];             // domain origin (Cartesian node positions)
+  // z-slab partition: the lattice is the slab's, its low / high z
+  // faces are Dirichlet boundaries only if zbc bit 0 / bit 1 is set (an
+  // interface plane shared with the neighbouring slab otherwise); cz0 is the
+  // slab's first cell layer in the global mesh (coefficient lookup).
+  // Unpartitioned: zbc = 3, cz0 = 0.
+  int zbc;
+  long long cz0;
   // coefficient: rho(cell) = rho0[ancestor on level 0] (1 if rho0 == nullptr)
   const double* rho0;
   int rho_shift;          // refinement levels between this level and level 0

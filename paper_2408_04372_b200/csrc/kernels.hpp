@@ -19,6 +19,28 @@ void st_residual(const DevLevel& L, const double* f, const double* u, double* r,
 void interpolate_nodes(const DevLevel& L, int kind, double omega, double t, const double* centre, double width,
                        bool zero_boundary, double* out, cudaStream_t s);
 
+// ---- z-slab partition helpers (slab.cu)
+// v[f * fstride + plane * plane_len + i] = val for every field f < F, i < plane_len
+void plane_fill(double* v, int F, long long fstride, long long plane, long long plane_len, double val, cudaStream_t s);
+// interface sum of two slabs held by this process: a_plane = b_plane = a_plane + b_plane
+void plane_pair_sum(double* a, long long a_plane, double* b, long long b_plane, int F, long long a_fstride,
+                    long long b_fstride, long long plane_len, cudaStream_t s);
+// buf[f][i] = v[f * fstride + plane * plane_len + i]
+void plane_pack(const double* v, int F, long long fstride, long long plane, long long plane_len, double* buf,
+                cudaStream_t s);
+// v[f * fstride + plane * plane_len + i] += buf[f][i]
+void plane_unpack_add(double* v, int F, long long fstride, long long plane, long long plane_len, const double* buf,
+                      cudaStream_t s);
+// owned-entry segments of a distributed vector (GMRES dots)
+constexpr int kMaxSeg = 64;
+struct DotSegments {
+  int n;
+  long long begin[kMaxSeg], end[kMaxSeg];
+};
+// out[i] = sum over the segments of V_i . w (i < k); scratch as vec_multidot
+void vec_multidot_seg(const double* const* V, int k, const double* w, const DotSegments& seg, double* out,
+                      double* scratch, cudaStream_t s);
+
 // ---- vector kernels (vector_ops.cu)
 void vec_copy(double* y, const double* x, long long n, cudaStream_t s);
 void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s);         // y += a x
@@ -37,7 +59,7 @@ void vec_fill(double* y, double v, long long n, cudaStream_t s);
 void vec_set_element(double* y, long long i, double v, cudaStream_t s);
 // y[g] = 1 where every lattice coordinate of g is congruent to colour (mod period)
 void vec_colour_indicator(double* y, const long long* dofs, int dim, int period, int cx, int cy, int cz,
-                          cudaStream_t s);
+                          long long z_offset, cudaStream_t s);  // z_offset: global lattice z of plane 0
 // dense matvec y = A x, A row-major n x n (coarse-grid inverse)
 void dense_matvec(const double* A, const double* x, double* y, int n, cudaStream_t s);
 
@@ -58,17 +80,28 @@ struct DevAxisTransfer {
   int hp;
   double hw[9][kMaxN];
 };
+// slab options of a transfer: physical z faces, skip the input's low z plane
+// (an interface owned by the slab below), accumulate into the output, and the
+// coarse side's field stride (0 = compact; > 0: coarse data inside a longer
+// vector, e.g. the full coarse level under a slab)
+struct TransferSlab {
+  int zbc = 3;
+  bool skip_lo_in = false;
+  bool accumulate = false;
+  long long coarse_fstride = 0;
+};
 // separable per-axis passes; t1/t2 are work buffers of Transfer-chosen size
-// accumulate: fine += P coarse instead of fine = P coarse
 void spatial_prolong(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
-                     const double* coarse, double* fine, double* t1, double* t2, bool accumulate, cudaStream_t s);
+                     const double* coarse, double* fine, double* t1, double* t2, const TransferSlab& sl,
+                     cudaStream_t s);
 void spatial_restrict(const DevAxisTransfer* ax, int dim, int F, const long long* dofs_c, const long long* dofs_f,
-                      const double* fine, double* coarse, double* t1, double* t2, cudaStream_t s);
+                      const double* fine, double* coarse, double* t1, double* t2, const TransferSlab& sl,
+                      cudaStream_t s);
 // temporal: fine block r = sum_c T[r][c] coarse block c (T row-major Ff x Fc)
 void temporal_prolong(const double* T_dev, int Ff, int Fc, long long n_space, const long long* dofs, int dim,
-                      const double* coarse, double* fine, bool accumulate, cudaStream_t s);
+                      const double* coarse, double* fine, const TransferSlab& sl, cudaStream_t s);
 void temporal_restrict(const double* T_dev, int Ff, int Fc, long long n_space, const long long* dofs, int dim,
-                       const double* fine, double* coarse, cudaStream_t s);
+                       const double* fine, double* coarse, const TransferSlab& sl, cudaStream_t s);
 
 // ---- additive Schwarz (asm_smoother.cu)
 struct DevASM {
@@ -82,6 +115,9 @@ struct DevASM {
   double TM[16], TA[16];  // diagonal (s,s) temporal blocks, n_t x n_t
   const long long* list;  // cells handled (X/lam stored per list entry); nullptr = all cells
   long long n_list;       // number of handled cells
+  // z-slab partition (as DevLevel::zbc / cz0)
+  int zbc;
+  long long cz0;
   // m = 64 records: X (swizzled, 4096 doubles) followed by the 64 eigenvalues,
   // xs = kRec64; meta[pos] = {lattice offset of local dof 0, Dirichlet face
   // mask (bit 2a: low face of axis a, 2a+1: high face)}
@@ -111,11 +147,15 @@ struct DevFDM {
   int rho_shift;
   long long cells0[3];
   const unsigned char* skip;      // per cell: 1 = solved by the exact per-cell kernel
+  int zbc;                        // z-slab partition (as DevLevel::zbc / cz0)
+  long long cz0;
 };
 void fdm_add_correction(const DevFDM& F, const double* r, double* z, double scale, cudaStream_t s);
 // probing-based extraction of restricted cell matrices (setup)
+// colours are classes of GLOBAL lattice coordinates; the probe lattice may
+// carry probe_zcells extra cell layers below the slab (halo for the setup)
 void asm_extract_probe(const DevASM& A, int colour_x, int colour_y, int colour_z, int period, const double* probe,
-                       double* cellmat, cudaStream_t s);
+                       int probe_zcells, double* cellmat, cudaStream_t s);
 void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s);  // At <- L^-1 At L^-T, Mt <- L^-1
 void asm_back_transform(int m, long long xs, long long n_cells, const double* Linv, const double* V, double* X,
                         cudaStream_t s);

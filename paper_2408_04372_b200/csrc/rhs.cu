@@ -82,7 +82,7 @@ __global__ void interpolate_kernel(const __grid_constant__ DevLevel L, int kind,
       const long long dx = L.dofs[0], dy = L.dofs[1], dz = L.dofs[2];
       const long long ix = g % dx, iy = (g / dx) % dy, iz = g / (dx * dy);
       bool b = ix == 0 || ix == dx - 1 || iy == 0 || iy == dy - 1;
-      if (L.dim > 2) b = b || iz == 0 || iz == dz - 1;
+      if (L.dim > 2) b = b || (iz == 0 && (L.zbc & 1)) || (iz == dz - 1 && (L.zbc & 2));
       if (b) v = 0.0;
     }
     out[g] = v;

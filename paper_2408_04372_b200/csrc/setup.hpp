@@ -61,6 +61,10 @@ struct MeshLevel {
   std::array<Index, 3> cells{1, 1, 1};
   std::array<double, 3> lo{0, 0, 0}, hi{1, 1, 1};
   std::vector<double> vertices;  // n_verts*3; empty = exact Cartesian lattice
+  // z-slab of a partitioned mesh: first cell layer in the global
+  // level, and which z faces are physical boundaries (bit 0 low, bit 1 high)
+  Index cz0 = 0;
+  int zbc = 3;
   std::array<Index, 3> n_verts_axis() const {
     return {cells[0] + 1, dim > 1 ? cells[1] + 1 : 1, dim > 2 ? cells[2] + 1 : 1};
   }
@@ -72,6 +76,9 @@ struct MeshLevel {
 };
 struct MeshHierarchy {
   std::vector<MeshLevel> levels;
+  // level-0 cells of the global mesh when the levels are slabs (coefficient
+  // lookup); zero = levels.front().cells
+  std::array<Index, 3> global_cells0{0, 0, 0};
   int n_levels() const { return static_cast<int>(levels.size()); }
 };
 MeshHierarchy make_cartesian(int dim, std::array<double, 3> lo, std::array<double, 3> hi, Index base_cells,

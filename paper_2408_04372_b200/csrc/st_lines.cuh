@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kT, 3) st_lines_kernel(const __grid_constant__
     const unsigned cx = ci % nx, cy = (ci / nx) % ny, cz = ci / (nx * ny);
     base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx + static_cast<long long>(cx) * p;
     mask = (cx == 0 ? 1 : 0) | (cx == nx - 1 ? 2 : 0) | (cy == 0 ? 4 : 0) | (cy == ny - 1 ? 8 : 0) |
-           (cz == 0 ? 16 : 0) | (cz == L.cells[2] - 1 ? 32 : 0);
+           (cz == 0 && (L.zbc & 1) ? 16 : 0) | (cz == L.cells[2] - 1 && (L.zbc & 2) ? 32 : 0);
     if (L.verts) {
       const long long vx = L.cells[0] + 1, vy = L.cells[1] + 1;
       for (int s = l; s < 8; s += NL) {
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kT, 3) st_lines_kernel(const __grid_constant__
     if (l == 0) {
       double rho = 1.0;
       if (L.rho0) {
-        const long long ax = cx >> L.rho_shift, ay = cy >> L.rho_shift, az = cz >> L.rho_shift;
+        const long long ax = cx >> L.rho_shift, ay = cy >> L.rho_shift, az = (cz + L.cz0) >> L.rho_shift;
         rho = L.rho0[(az * L.cells0[1] + ay) * L.cells0[0] + ax];
       }
       rho_s[c] = rho;

@@ -16,25 +16,31 @@ namespace {
 // y_b = u_b on every Dirichlet dof of every field: enumerate the boundary
 // faces of the lattice directly (edges/corners written more than once with
 // the same value)
-__global__ void boundary_identity_kernel(int dim, long long dx, long long dy, long long dz, long long n_space, int F,
-                                         const double* __restrict__ f, const double* __restrict__ u,
+__global__ void boundary_identity_kernel(int dim, int zbc, long long dx, long long dy, long long dz, long long n_space,
+                                         int F, const double* __restrict__ f, const double* __restrict__ u,
                                          double* __restrict__ y) {
-  // faces: x=0, x=dx-1 (dy*dz each), y=0, y=dy-1 (dx*dz), z=0, z=dz-1 (dx*dy)
+  // faces: x=0, x=dx-1 (dy*dz each), y=0, y=dy-1 (dx*dz), z=0, z=dz-1 (dx*dy);
+  // a slab's z faces only where they are physical (zbc), never on interfaces
   const long long fx = dy * dz, fy = dx * dz, fz = dim == 3 ? dx * dy : 0;
   const long long total = 2 * (fx + fy + fz);
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<long long>(gridDim.x) * blockDim.x) {
     long long g;
     long long r = t;
+    // the low plane of a slab whose low face is an interface is owned by the
+    // slab below: its Dirichlet rows are written there only
     if (r < 2 * fx) {
       const long long side = r / fx, k = r % fx;
+      if (dim == 3 && !(zbc & 1) && k / dy == 0) continue;
       g = (k / dy) * dx * dy + (k % dy) * dx + (side ? dx - 1 : 0);
     } else if ((r -= 2 * fx) < 2 * fy) {
       const long long side = r / fy, k = r % fy;
+      if (dim == 3 && !(zbc & 1) && k / dx == 0) continue;
       g = (k / dx) * dx * dy + (side ? dy - 1 : 0) * dx + (k % dx);
     } else {
       r -= 2 * fy;
       const long long side = r / fz, k = r % fz;
+      if (!(zbc & (side ? 2 : 1))) continue;
       g = (side ? dz - 1 : 0) * dx * dy + k;
     }
     // apply: y_b = u_b; residual: y_b = f_b - u_b
@@ -46,10 +52,14 @@ __global__ void boundary_identity_kernel(int dim, long long dx, long long dy, lo
 
 namespace {
 void run(const DevLevel& L, const double* f, const double* u, double* y, cudaStream_t stream) {
-  if (f)
+  if (f) {
     vec_copy(y, f, L.n_dofs, stream);
-  else
+    // slab whose low z plane is an interface owned by the slab below: its f
+    // entries are counted there, so the partial residual starts from 0
+    if (L.dim == 3 && !(L.zbc & 1)) plane_fill(y, L.F, L.n_space, 0, L.dofs[0] * L.dofs[1], 0.0, stream);
+  } else {
     cudaMemsetAsync(y, 0, sizeof(double) * L.n_dofs, stream);
+  }
   const double sign = f ? -1.0 : 1.0;
   count_launch();
   if (L.dim == 2)
@@ -61,7 +71,7 @@ void run(const DevLevel& L, const double* f, const double* u, double* y, cudaStr
   const long long faces = 2 * (L.dofs[1] * L.dofs[2] + L.dofs[0] * L.dofs[2] + (L.dim == 3 ? L.dofs[0] * L.dofs[1] : 0));
   const unsigned blocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((faces + 255) / 256, 148LL * 8)));
   count_launch();
-  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dofs[0], L.dofs[1], L.dofs[2], L.n_space, L.F, f, u, y);
+  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dim == 3 ? L.zbc : 3, L.dofs[0], L.dofs[1], L.dofs[2], L.n_space, L.F, f, u, y);
 }
 }  // namespace
 
@@ -70,7 +80,7 @@ void st_zero_boundary(const DevLevel& L, double* v, cudaStream_t stream) {
   const long long faces = 2 * (L.dofs[1] * L.dofs[2] + L.dofs[0] * L.dofs[2] + (L.dim == 3 ? L.dofs[0] * L.dofs[1] : 0));
   const unsigned blocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((faces + 255) / 256, 148LL * 8)));
   count_launch();
-  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dofs[0], L.dofs[1], L.dofs[2], L.n_space, L.F, v, v, v);
+  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dim == 3 ? L.zbc : 3, L.dofs[0], L.dofs[1], L.dofs[2], L.n_space, L.F, v, v, v);
 }
 void st_residual(const DevLevel& L, const double* f, const double* u, double* r, cudaStream_t stream) {
   run(L, f, u, r, stream);

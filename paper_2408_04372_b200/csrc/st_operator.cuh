@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
       if (cy == 0) mask |= 4;
       if (cy == ny - 1) mask |= 8;
       if (DIM == 3) {
-        if (cz == 0) mask |= 16;
-        if (cz == L.cells[2] - 1) mask |= 32;
+        if (cz == 0 && (L.zbc & 1)) mask |= 16;
+        if (cz == L.cells[2] - 1 && (L.zbc & 2)) mask |= 32;
       }
       double* gc = geo + c * GEO;
       if (L.verts) {
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 2) st_apply_kernel(const __grid_cons
       }
       double rho = 1.0;
       if (L.rho0) {
-        const long long ax = cx >> L.rho_shift, ay = cy >> L.rho_shift, az = cz >> L.rho_shift;
+        const long long ax = cx >> L.rho_shift, ay = cy >> L.rho_shift, az = (cz + L.cz0) >> L.rho_shift;
         rho = L.rho0[(az * L.cells0[1] + ay) * L.cells0[0] + ax];
       }
       rho_s[c] = rho;

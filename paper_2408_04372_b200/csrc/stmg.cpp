@@ -96,6 +96,8 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
     d.lo[a] = m.lo[a];
   }
   d.n_dofs = d.n_space * F;
+  d.zbc = m.dim == 3 ? m.zbc : 3;
+  d.cz0 = m.dim == 3 ? m.cz0 : 0;
   if (!m.vertices.empty()) {
     verts_ = upload(m.vertices);
     d.verts = verts_.d();
@@ -104,14 +106,16 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
   }
   if (!rho.coarse_cell_scale.empty()) {
     const MeshLevel& m0 = mesh.levels.front();
-    if (static_cast<Index>(rho.coarse_cell_scale.size()) != m0.n_cells())
+    std::array<Index, 3> c0 = m0.cells;
+    if (mesh.global_cells0[0] > 0) c0 = mesh.global_cells0;
+    if (static_cast<Index>(rho.coarse_cell_scale.size()) != c0[0] * c0[1] * c0[2])
       throw std::invalid_argument("SpaceTimeOperator: coefficient needs one value per level-0 cell");
     for (double v : rho.coarse_cell_scale)
       if (!(v > 0.0)) throw std::runtime_error("CoefficientField: non-positive value");
     rho0_ = upload(rho.coarse_cell_scale);
     d.rho0 = rho0_.d();
     d.rho_shift = mesh_level;
-    for (int a = 0; a < 3; ++a) d.cells0[a] = a < m.dim ? m0.cells[a] : 1;
+    for (int a = 0; a < 3; ++a) d.cells0[a] = a < m.dim ? c0[a] : 1;
   } else {
     d.rho0 = nullptr;
   }
@@ -545,9 +549,12 @@ void temporal_block_diagonalise(DevASM& A) {
   A.tdiag = 1;
 }
 
-ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
+ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* probe_op, int probe_zcells)
+    : op_(&op) {
   const DevLevel& d = op.desc();
   DevASM& A = asm_;
+  A.zbc = d.zbc;
+  A.cz0 = d.cz0;
   A.dim = d.dim;
   A.p = d.p;
   A.n = d.n;
@@ -591,6 +598,8 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
     Fd.rho0 = d.rho0;
     Fd.rho_shift = d.rho_shift;
     Fd.skip = nullptr;
+    Fd.zbc = d.zbc;
+    Fd.cz0 = d.cz0;
     std::memset(Fd.S1, 0, sizeof(Fd.S1));
     std::memset(Fd.L1, 0, sizeof(Fd.L1));
     for (int a = 0; a < d.dim; ++a) {
@@ -612,15 +621,19 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
                                         (cx >> d.rho_shift))];
       };
       std::vector<unsigned char> skip(static_cast<size_t>(n_cells), 0);
+      // neighbourhoods in global cell coordinates (a slab's interface cells
+      // see the neighbouring slab's coefficient)
+      const long long nz_global = d.dim == 3 ? (d.cells0[2] << d.rho_shift) : 1;
       for (Index c = 0; c < n_cells; ++c) {
-        const long long cx = c % d.cells[0], cy = (c / d.cells[0]) % d.cells[1], cz = c / (d.cells[0] * d.cells[1]);
+        const long long cx = c % d.cells[0], cy = (c / d.cells[0]) % d.cells[1];
+        const long long cz = c / (d.cells[0] * d.cells[1]) + d.cz0;
         const double r0 = rho_of(cx, cy, cz);
         bool uniform = true;
         for (int dz = (d.dim == 3 ? -1 : 0); dz <= (d.dim == 3 ? 1 : 0) && uniform; ++dz)
           for (int dy = -1; dy <= 1 && uniform; ++dy)
             for (int dxx = -1; dxx <= 1 && uniform; ++dxx) {
               const long long nx = cx + dxx, ny = cy + dy, nz = cz + dz;
-              if (nx < 0 || ny < 0 || nz < 0 || nx >= d.cells[0] || ny >= d.cells[1] || nz >= d.cells[2]) continue;
+              if (nx < 0 || ny < 0 || nz < 0 || nx >= d.cells[0] || ny >= d.cells[1] || nz >= nz_global) continue;
               if (rho_of(nx, ny, nz) != r0) uniform = false;
             }
         if (!uniform) exact_cells.push_back(c);
@@ -650,16 +663,23 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op) : op_(&op) {
     A.list = nullptr;
     A.n_list = n_cells;
   }
-  build_exact(op);
+  build_exact(op, probe_op, probe_zcells);
 }
 
-void ASMSmoother::build_exact(const SpaceTimeOperator& op) {
+void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperator* probe_op, int probe_zcells) {
   const DevLevel& d = op.desc();
   DevASM& A = asm_;
+  // the restricted global matrices are probed on `probe_op`: the operator
+  // itself, or for a z-slab with interfaces a copy extended by one halo cell
+  // layer across each interface (probe_zcells layers below), so the interface
+  // entries include the neighbouring slab's cells
+  const SpaceTimeOperator& pop = probe_op ? *probe_op : op;
+  const DevLevel& pd = pop.desc();
+  if (!probe_op) probe_zcells = 0;
   const Index n_pos = A.n_list;
   const size_t mat_bytes = sizeof(double) * static_cast<size_t>(n_pos) * A.m * A.m;
   cudaStream_t s = nullptr;
-  DeviceBuffer cellM(mat_bytes), cellA(mat_bytes), probe(sizeof(double) * d.n_space), ind(sizeof(double) * d.n_space);
+  DeviceBuffer cellM(mat_bytes), cellA(mat_bytes), probe(sizeof(double) * pd.n_space), ind(sizeof(double) * pd.n_space);
   cuda_check(cudaMemsetAsync(cellM.raw(), 0, mat_bytes, s), "memset");
   cuda_check(cudaMemsetAsync(cellA.raw(), 0, mat_bytes, s), "memset");
   // restricted global matrices by probing the matrix-free operators with
@@ -670,11 +690,11 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op) {
   for (int cz = 0; cz < cz_max; ++cz)
     for (int cy = 0; cy < P; ++cy)
       for (int cx = 0; cx < P; ++cx) {
-        vec_colour_indicator(ind.d(), d.dofs, d.dim, P, cx, cy, cz, s);
-        op.spatial_apply(0, ind.d(), probe.d(), s);
-        asm_extract_probe(A, cx, cy, cz, P, probe.d(), cellM.d(), s);
-        op.spatial_apply(1, ind.d(), probe.d(), s);
-        asm_extract_probe(A, cx, cy, cz, P, probe.d(), cellA.d(), s);
+        vec_colour_indicator(ind.d(), pd.dofs, pd.dim, P, cx, cy, cz, (pd.cz0) * pd.p, s);
+        pop.spatial_apply(0, ind.d(), probe.d(), s);
+        asm_extract_probe(A, cx, cy, cz, P, probe.d(), probe_zcells, cellM.d(), s);
+        pop.spatial_apply(1, ind.d(), probe.d(), s);
+        asm_extract_probe(A, cx, cy, cz, P, probe.d(), probe_zcells, cellA.d(), s);
       }
   // standard form C = L^-1 A L^-T (into cellA), L^-1 (into cellM)
   asm_reduce_standard(A, cellM.d(), cellA.d(), s);
@@ -738,8 +758,8 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op) {
       if (cx == A.cells[0] - 1) mask |= 2;
       if (cy == 0) mask |= 4;
       if (cy == A.cells[1] - 1) mask |= 8;
-      if (cz == 0) mask |= 16;
-      if (cz == A.cells[2] - 1) mask |= 32;
+      if (cz == 0 && (A.zbc & 1)) mask |= 16;
+      if (cz == A.cells[2] - 1 && (A.zbc & 2)) mask |= 32;
       meta[static_cast<size_t>(2 * q + 1)] = mask;
     }
     meta_ = upload(meta);
@@ -877,22 +897,33 @@ Transfer::Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coars
   }
 }
 
-void Transfer::prolong(const double* coarse, double* fine, cudaStream_t stream, bool accumulate) const {
+void Transfer::prolong(const double* coarse, double* fine, cudaStream_t stream, bool accumulate,
+                       long long coarse_fstride) const {
   const DevLevel& df = fine_->desc();
   const DevLevel& dc = coarse_->desc();
+  TransferSlab sl;
+  sl.zbc = df.zbc;
+  sl.accumulate = accumulate;
+  sl.coarse_fstride = coarse_fstride;
   if (spatial_)
-    spatial_prolong(ax_, df.dim, df.F, dc.dofs, df.dofs, coarse, fine, t1_.d(), t2_.d(), accumulate, stream);
+    spatial_prolong(ax_, df.dim, df.F, dc.dofs, df.dofs, coarse, fine, t1_.d(), t2_.d(), sl, stream);
   else
-    temporal_prolong(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, coarse, fine, accumulate, stream);
+    temporal_prolong(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, coarse, fine, sl, stream);
 }
 
-void Transfer::restrict_(const double* fine, double* coarse, cudaStream_t stream) const {
+void Transfer::restrict_(const double* fine, double* coarse, cudaStream_t stream, bool accumulate,
+                         long long coarse_fstride) const {
   const DevLevel& df = fine_->desc();
   const DevLevel& dc = coarse_->desc();
+  TransferSlab sl;
+  sl.zbc = df.zbc;
+  sl.skip_lo_in = df.dim == 3 && !(df.zbc & 1);
+  sl.accumulate = accumulate;
+  sl.coarse_fstride = coarse_fstride;
   if (spatial_)
-    spatial_restrict(ax_, df.dim, df.F, dc.dofs, df.dofs, fine, coarse, t1_.d(), t2_.d(), stream);
+    spatial_restrict(ax_, df.dim, df.F, dc.dofs, df.dofs, fine, coarse, t1_.d(), t2_.d(), sl, stream);
   else
-    temporal_restrict(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, fine, coarse, stream);
+    temporal_restrict(time_p_.d(), Ff_, Fc_, df.n_space, df.dofs, df.dim, fine, coarse, sl, stream);
 }
 
 // ------------------------------------------------------------------ GMRES
@@ -920,16 +951,26 @@ void GmresWorkspace::ensure(Index n, int vectors) {
 }
 
 GmresResult gmres(const DeviceMap& op, const double* b, double* x, Index n, const GmresOptions& options,
-                  const DeviceMap& precond, GmresWorkspace& ws, cudaStream_t s) {
+                  const DeviceMap& precond, GmresWorkspace& ws, cudaStream_t s, const DotPolicy* dots) {
   if (!op) throw std::invalid_argument("gmres: missing operator");
   const int m = std::max(1, options.restart);
   ws.ensure(n, 1);
+  // k inner products <V_i, w> into the device buffer out (owned entries and a
+  // sum over ranks for a distributed vector)
+  auto multidot = [&](const double* const* V, int k, const double* w, double* out) {
+    if (!dots) {
+      vec_multidot(V, k, w, n, out, ws.scratch(), s);
+      return;
+    }
+    vec_multidot_seg(V, k, w, dots->seg, out, ws.scratch(), s);
+    if (dots->allreduce) dots->allreduce(out, k, s);
+  };
   // extra pointer slot after the basis for norms of w / r
   DeviceBuffer one_ptr(sizeof(double*));
   auto norm_of = [&](const double* v) {
     const double* hp[1] = {v};
     cuda_check(cudaMemcpyAsync(one_ptr.raw(), hp, sizeof(hp), cudaMemcpyHostToDevice, s), "ptr");
-    vec_multidot(static_cast<const double* const*>(one_ptr.raw()), 1, v, n, ws.small(), ws.scratch(), s);
+    multidot(static_cast<const double* const*>(one_ptr.raw()), 1, v, ws.small());
     double r = 0.0;
     cuda_check(cudaMemcpyAsync(&r, ws.small(), sizeof(double), cudaMemcpyDeviceToHost, s), "nrm");
     cuda_check(cudaStreamSynchronize(s), "nrm sync");
@@ -970,9 +1011,9 @@ GmresResult gmres(const DeviceMap& op, const double* b, double* x, Index n, cons
       // classical Gram-Schmidt, two passes (h1 + h2 = the reference's two MGS passes)
       double* h1 = ws.small();
       double* h2 = ws.small() + (m + 1);
-      vec_multidot(ws.dev_ptrs(), k + 1, ws.w(), n, h1, ws.scratch(), s);
+      multidot(ws.dev_ptrs(), k + 1, ws.w(), h1);
       vec_multi_axpy(ws.w(), ws.dev_ptrs(), k + 1, h1, -1.0, n, s);
-      vec_multidot(ws.dev_ptrs(), k + 1, ws.w(), n, h2, ws.scratch(), s);
+      multidot(ws.dev_ptrs(), k + 1, ws.w(), h2);
       vec_multi_axpy(ws.w(), ws.dev_ptrs(), k + 1, h2, -1.0, n, s);
       cuda_check(cudaMemcpyAsync(hbuf.data(), ws.small(), sizeof(double) * 2 * (m + 1), cudaMemcpyDeviceToHost, s),
                  "h");

@@ -106,7 +106,11 @@ class SpaceTimeOperator {
 
 class ASMSmoother {
  public:
-  explicit ASMSmoother(const SpaceTimeOperator& op);
+  // probe_op: for a z-slab with interfaces, the slab extended by one halo
+  // cell layer across each interface (probe_zcells of them below), used only
+  // to extract the restricted global block matrices at setup
+  explicit ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* probe_op = nullptr,
+                       int probe_zcells = 0);
   // correction += W sum_T R_T^T B_T^-1 R_T residual (accumulate; the
   // relaxation factor is applied by the caller) -- asm_smoother.cpp:60-78
   void add_correction(const double* residual, double* correction, cudaStream_t stream = nullptr,
@@ -126,7 +130,7 @@ class ASMSmoother {
   int kind() const { return (use_fdm_ ? 1 : 0) | (asm_.n_list > 0 ? 2 : 0) | (asm_.n_list > 0 && asm_.tdiag && asm_.meta ? 4 : 0); }
 
  private:
-  void build_exact(const SpaceTimeOperator& op);
+  void build_exact(const SpaceTimeOperator& op, const SpaceTimeOperator* probe_op, int probe_zcells);
   const SpaceTimeOperator* op_;
   DevASM asm_{};
   DevFDM fdm_{};
@@ -139,9 +143,15 @@ class ASMSmoother {
 class Transfer {
  public:
   Transfer(const SpaceTimeOperator& fine, const SpaceTimeOperator& coarse);
-  // overwrite (accumulate = false, the reference semantics) or fine += P coarse
-  void prolong(const double* coarse, double* fine, cudaStream_t stream = nullptr, bool accumulate = false) const;
-  void restrict_(const double* fine, double* coarse, cudaStream_t stream = nullptr) const;  // overwrite
+  // overwrite (accumulate = false, the reference semantics) or fine += P coarse;
+  // coarse_fstride > 0: the coarse vector is a slab view inside a longer one
+  // (field stride coarse_fstride). On a z-slab whose low plane is an interface
+  // owned by the slab below, restriction skips that fine plane so the
+  // interface sum over both slabs counts it once.
+  void prolong(const double* coarse, double* fine, cudaStream_t stream = nullptr, bool accumulate = false,
+               long long coarse_fstride = 0) const;
+  void restrict_(const double* fine, double* coarse, cudaStream_t stream = nullptr, bool accumulate = false,
+                 long long coarse_fstride = 0) const;
   bool spatial() const { return spatial_; }
 
  private:
@@ -206,9 +216,18 @@ class GmresWorkspace {
   DeviceBuffer ptrs_, scratch_, small_, r_, w_, z_;
 };
 
+// Inner products of a distributed vector (z-slab partition): only the owned
+// entries (segments) count locally, then the k partial sums are summed over
+// the ranks in place on the device (allreduce; empty = single process)
+struct DotPolicy {
+  DotSegments seg{};
+  std::function<void(double* d_vals, int k, cudaStream_t)> allreduce;
+};
+
 // Restarted right-preconditioned GMRES (gmres.cpp:8-115) on device vectors.
 GmresResult gmres(const DeviceMap& op, const double* b, double* x, Index n, const GmresOptions& options,
-                  const DeviceMap& precond, GmresWorkspace& ws, cudaStream_t stream = nullptr);
+                  const DeviceMap& precond, GmresWorkspace& ws, cudaStream_t stream = nullptr,
+                  const DotPolicy* dots = nullptr);
 
 class SpaceTimeMultigrid {
  public:

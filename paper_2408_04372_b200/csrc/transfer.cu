@@ -1,13 +1,20 @@
 // Grid transfers between consecutive multigrid levels (reference: Transfer,
 // transfer.cpp:58-190). Spatial h/p transfers are tensor products of the
 // per-axis embedding matrices P (n_f x n_c, transfer.cpp:32-54); they are
-// applied here as separable passes, one lattice axis at a time, each output
-// entry gathering the few nonzeros of its CSR row of P (prolongation) or of
-// P^T (restriction) -- O((p+1) d) work per entry instead of the reference's
-// dense O(n_f n_c) line contraction. Temporal tau/k transfers apply the small
-// (S_f n_tf) x (S_c n_tc) evaluation matrix blockwise over the spatial dofs.
-// Dirichlet entries are zeroed on the input and output sides
-// (transfer.cpp:108-116).
+// applied here as separable passes, one lattice axis at a time. Pure
+// h-coarsening with equal p uses the structured weights of one coarse cell
+// (no index arrays); other spatial transfers gather the few nonzeros of a CSR
+// row of P (prolongation) or P^T (restriction) -- O((p+1) d) work per entry
+// instead of the reference's dense O(n_f n_c) line contraction. Temporal
+// tau/k transfers apply the small (S_f n_tf) x (S_c n_tc) evaluation matrix
+// blockwise over the spatial dofs. Dirichlet entries are zeroed on the input
+// and output sides (transfer.cpp:108-116).
+//
+// z-slab partition: z faces are Dirichlet only where physical
+// (zbc), the input's low z plane can be skipped (an interface plane owned by
+// the slab below, so a restriction's interface contributions are counted
+// once), and each side has its own field stride so a slab's coarse data can
+// live inside a full-length coarse vector.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,48 +25,67 @@ namespace stmgb {
 
 namespace {
 
-__device__ __forceinline__ bool on_bdry(long long i, long long n) { return i == 0 || i == n - 1; }
+struct PassArgs {
+  long long i[3], o[3];    // input / output lattice dims
+  long long fs_in, fs_out;  // field strides
+  int zbc;                  // physical low (bit 0) / high (bit 1) z faces
+  bool mask_in, mask_out, skip_lo_in, accumulate;
+};
 
-// out[f][z][y][x] (dims o[]) = sum_k w_k in[f][..src..] along `axis`;
-// input dims i[] equal o[] except along axis. One thread per output entry of
-// a 32 x 4 (x, y) tile: grid (x tiles, y tiles, z * F), so no per-entry index decoding; the
-// reads along y/z are coalesced across the x-consecutive threads.
+__device__ __forceinline__ bool on_bdry(long long i, long long n) { return i == 0 || i == n - 1; }
+__device__ __forceinline__ bool on_bdry_z(long long i, long long n, int zbc) {
+  return (i == 0 && (zbc & 1)) || (i == n - 1 && (zbc & 2));
+}
+
+// boundary status of output entry (x, y, z) and of the input row it reads
 template <int AXIS>
-__global__ void __launch_bounds__(128) axis_pass_kernel(long long ix, long long iy, long long iz, long long ox,
-                                                        long long oy, long long oz, const int* __restrict__ ptr,
+__device__ __forceinline__ bool skip_entry(const PassArgs& A, long long x, long long y, long long z) {
+  const long long ox = A.o[0], oy = A.o[1], oz = A.o[2];
+  if (A.mask_out && (on_bdry(x, ox) || (oy > 1 && on_bdry(y, oy)) || (oz > 1 && on_bdry_z(z, oz, A.zbc)))) return true;
+  if (A.mask_in) {
+    if (AXIS != 0 && on_bdry(x, A.i[0])) return true;
+    if (AXIS != 1 && A.i[1] > 1 && on_bdry(y, A.i[1])) return true;
+    if (AXIS != 2 && A.i[2] > 1 && on_bdry_z(z, A.i[2], A.zbc)) return true;
+  }
+  if (A.skip_lo_in && AXIS != 2 && z == 0) return true;
+  return false;
+}
+
+__device__ __forceinline__ bool skip_input_along(const PassArgs& A, int axis, long long j, long long n_ax) {
+  if (A.mask_in && (axis == 2 ? on_bdry_z(j, n_ax, A.zbc) : on_bdry(j, n_ax))) return true;
+  return A.skip_lo_in && axis == 2 && j == 0;
+}
+
+// out[f][z][y][x] = sum_k w_k in[f][..src..] along AXIS (CSR weights). One
+// thread per output entry of a 32 x 4 (x, y) tile: grid (x tiles, y tiles,
+// z * F), so no per-entry index decoding; reads along y/z are coalesced across
+// the x-consecutive threads.
+template <int AXIS>
+__global__ void __launch_bounds__(128) axis_pass_kernel(const PassArgs A, const int* __restrict__ ptr,
                                                         const int* __restrict__ idx, const double* __restrict__ w,
-                                                        bool mask_in, bool mask_out, bool accumulate,
                                                         const double* __restrict__ in, double* __restrict__ out) {
   const long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long y = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
-  if (x >= ox || y >= oy) return;
-  const long long z = blockIdx.z % oz, f = blockIdx.z / oz;
-  const long long oidx = ((f * oz + z) * oy + y) * ox + x;
+  if (x >= A.o[0] || y >= A.o[1]) return;
+  const long long z = blockIdx.z % A.o[2], f = blockIdx.z / A.o[2];
+  const long long oidx = f * A.fs_out + (z * A.o[1] + y) * A.o[0] + x;
   double s = 0.0;
-  const bool zero_out = mask_out && (on_bdry(x, ox) || (oy > 1 && on_bdry(y, oy)) || (oz > 1 && on_bdry(z, oz)));
-  if (!zero_out) {
-    bool other_bd = false;
-    if (mask_in) {
-      if (AXIS != 0) other_bd = other_bd || on_bdry(x, ix);
-      if (AXIS != 1 && iy > 1) other_bd = other_bd || on_bdry(y, iy);
-      if (AXIS != 2 && iz > 1) other_bd = other_bd || on_bdry(z, iz);
-    }
-    if (!other_bd) {
-      const long long o = AXIS == 0 ? x : (AXIS == 1 ? y : z);
-      const int k0 = __ldg(ptr + o), k1 = __ldg(ptr + o + 1);
-      const long long n_ax = AXIS == 0 ? ix : (AXIS == 1 ? iy : iz);
-      const double* src = in + f * ix * iy * iz;
-      const long long base = AXIS == 0 ? (z * iy + y) * ix : (AXIS == 1 ? z * iy * ix + x : y * ix + x);
-      const long long stride = AXIS == 0 ? 1 : (AXIS == 1 ? ix : ix * iy);
+  if (!skip_entry<AXIS>(A, x, y, z)) {
+    const long long o = AXIS == 0 ? x : (AXIS == 1 ? y : z);
+    const int k0 = __ldg(ptr + o), k1 = __ldg(ptr + o + 1);
+    const long long n_ax = A.i[AXIS];
+    const double* src = in + f * A.fs_in;
+    const long long ix = A.i[0], iy = A.i[1];
+    const long long base = AXIS == 0 ? (z * iy + y) * ix : (AXIS == 1 ? z * iy * ix + x : y * ix + x);
+    const long long stride = AXIS == 0 ? 1 : (AXIS == 1 ? ix : ix * iy);
 #pragma unroll 4
-      for (int k = k0; k < k1; ++k) {
-        const long long j = __ldg(idx + k);
-        if (mask_in && on_bdry(j, n_ax)) continue;
-        s = fma(__ldg(w + k), __ldg(src + base + j * stride), s);
-      }
+    for (int k = k0; k < k1; ++k) {
+      const long long j = __ldg(idx + k);
+      if (skip_input_along(A, AXIS, j, n_ax)) continue;
+      s = fma(__ldg(w + k), __ldg(src + base + j * stride), s);
     }
   }
-  if (accumulate)
+  if (A.accumulate)
     out[oidx] += s;
   else
     out[oidx] = s;
@@ -70,32 +96,22 @@ __global__ void __launch_bounds__(128) axis_pass_kernel(long long ix, long long 
 // i = 2p c + r; restriction out[c p + j] = sum_r hw[r][j] in[2p c + r]
 // (+ the left neighbour cell's r < 2p nodes for the vertex node j = 0)
 template <int AXIS, int P, bool PROLONG>
-__global__ void __launch_bounds__(128) axis_pass_h_kernel(long long ix, long long iy, long long iz, long long ox,
-                                                          long long oy, long long oz, const DevAxisTransfer T,
-                                                          bool mask_in, bool mask_out, bool accumulate,
+__global__ void __launch_bounds__(128) axis_pass_h_kernel(const PassArgs A, const DevAxisTransfer T,
                                                           const double* __restrict__ in, double* __restrict__ out) {
   const long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long y = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
-  if (x >= ox || y >= oy) return;
-  const long long z = blockIdx.z % oz, f = blockIdx.z / oz;
-  const long long oidx = ((f * oz + z) * oy + y) * ox + x;
+  if (x >= A.o[0] || y >= A.o[1]) return;
+  const long long z = blockIdx.z % A.o[2], f = blockIdx.z / A.o[2];
+  const long long oidx = f * A.fs_out + (z * A.o[1] + y) * A.o[0] + x;
   double s = 0.0;
-  const bool zero_out = mask_out && (on_bdry(x, ox) || (oy > 1 && on_bdry(y, oy)) || (oz > 1 && on_bdry(z, oz)));
-  bool other_bd = false;
-  if (mask_in) {
-    if (AXIS != 0) other_bd = other_bd || on_bdry(x, ix);
-    if (AXIS != 1 && iy > 1) other_bd = other_bd || on_bdry(y, iy);
-    if (AXIS != 2 && iz > 1) other_bd = other_bd || on_bdry(z, iz);
-  }
-  if (!zero_out && !other_bd) {
+  if (!skip_entry<AXIS>(A, x, y, z)) {
     const long long o = AXIS == 0 ? x : (AXIS == 1 ? y : z);
-    const long long n_ax = AXIS == 0 ? ix : (AXIS == 1 ? iy : iz);
-    const double* src = in + f * ix * iy * iz;
+    const long long n_ax = A.i[AXIS];
+    const double* src = in + f * A.fs_in;
+    const long long ix = A.i[0], iy = A.i[1];
     const long long base = AXIS == 0 ? (z * iy + y) * ix : (AXIS == 1 ? z * iy * ix + x : y * ix + x);
     const long long stride = AXIS == 0 ? 1 : (AXIS == 1 ? ix : ix * iy);
-    auto val = [&](long long j) {
-      return (mask_in && on_bdry(j, n_ax)) ? 0.0 : __ldg(src + base + j * stride);
-    };
+    auto val = [&](long long j) { return skip_input_along(A, AXIS, j, n_ax) ? 0.0 : __ldg(src + base + j * stride); };
     if (PROLONG) {
       const long long ncc = (n_ax - 1) / P;
       long long c = o / (2 * P);
@@ -117,23 +133,25 @@ __global__ void __launch_bounds__(128) axis_pass_h_kernel(long long ix, long lon
       }
     }
   }
-  if (accumulate)
+  if (A.accumulate)
     out[oidx] += s;
   else
     out[oidx] = s;
 }
 
 __global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bool transpose, bool accumulate,
-                                long long n_space, long long dx, long long dy, long long dz, int dim,
-                                const double* __restrict__ in, double* __restrict__ out) {
+                                long long n_space, long long dx, long long dy, long long dz, int dim, int zbc,
+                                bool skip_lo_in, long long fs_in, long long fs_out, const double* __restrict__ in,
+                                double* __restrict__ out) {
   // prolong: out (Ff blocks) = T in (Fc blocks); restrict: out (Fc) = T^T in (Ff)
   const int Fin = transpose ? Ff : Fc, Fout = transpose ? Fc : Ff;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n_space; g += (long long)gridDim.x * blockDim.x) {
     const long long ix = g % dx, iy = (g / dx) % dy, iz = g / (dx * dy);
-    const bool bd = on_bdry(ix, dx) || (dim > 1 && on_bdry(iy, dy)) || (dim > 2 && on_bdry(iz, dz));
+    const bool bd = on_bdry(ix, dx) || (dim > 1 && on_bdry(iy, dy)) ||
+                    (dim > 2 && (on_bdry_z(iz, dz, zbc) || (skip_lo_in && iz == 0)));
     double x[kMaxF];
 #pragma unroll
-    for (int c = 0; c < kMaxF; ++c) x[c] = (c < Fin && !bd) ? in[c * n_space + g] : 0.0;
+    for (int c = 0; c < kMaxF; ++c) x[c] = (c < Fin && !bd) ? in[c * fs_in + g] : 0.0;
 #pragma unroll
     for (int r = 0; r < kMaxF; ++r) {
       if (r >= Fout) break;
@@ -142,9 +160,9 @@ __global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bo
       for (int c = 0; c < kMaxF; ++c)
         if (c < Fin) s = fma(transpose ? T[c * Fc + r] : T[r * Fc + c], x[c], s);
       if (accumulate)
-        out[r * n_space + g] += s;
+        out[r * fs_out + g] += s;
       else
-        out[r * n_space + g] = s;
+        out[r * fs_out + g] = s;
     }
   }
 }
@@ -154,27 +172,25 @@ inline unsigned grid_for(long long n) {
 }
 
 template <int AXIS, int P, bool PROLONG>
-void launch_h(const dim3& grid, const dim3& block, const long long* in_d, const long long* out_d,
-              const DevAxisTransfer& T, bool mask_in, bool mask_out, bool accumulate, const double* in, double* out,
-              cudaStream_t s) {
-  axis_pass_h_kernel<AXIS, P, PROLONG><<<grid, block, 0, s>>>(in_d[0], in_d[1], in_d[2], out_d[0], out_d[1], out_d[2],
-                                                               T, mask_in, mask_out, accumulate, in, out);
+void launch_h(const dim3& grid, const dim3& block, const PassArgs& A, const DevAxisTransfer& T, const double* in,
+              double* out, cudaStream_t s) {
+  axis_pass_h_kernel<AXIS, P, PROLONG><<<grid, block, 0, s>>>(A, T, in, out);
 }
 
 template <int AXIS>
-void pass(int F, const long long* in_d, const long long* out_d, const DevAxisTransfer& T, bool prolong, bool mask_in,
-          bool mask_out, bool accumulate, const double* in, double* out, cudaStream_t s) {
+void pass(int F, const PassArgs& A, const DevAxisTransfer& T, bool prolong, const double* in, double* out,
+          cudaStream_t s) {
   const dim3 block(32, 4);
-  const dim3 grid(static_cast<unsigned>((out_d[0] + 31) / 32), static_cast<unsigned>((out_d[1] + 3) / 4),
-                  static_cast<unsigned>(out_d[2] * F));
+  const dim3 grid(static_cast<unsigned>((A.o[0] + 31) / 32), static_cast<unsigned>((A.o[1] + 3) / 4),
+                  static_cast<unsigned>(A.o[2] * F));
   count_launch();
   if (T.hp > 0) {
-#define STMG_H(PP)                                                                                        \
-  case PP:                                                                                                \
-    if (prolong)                                                                                          \
-      launch_h<AXIS, PP, true>(grid, block, in_d, out_d, T, mask_in, mask_out, accumulate, in, out, s);  \
-    else                                                                                                  \
-      launch_h<AXIS, PP, false>(grid, block, in_d, out_d, T, mask_in, mask_out, accumulate, in, out, s); \
+#define STMG_H(PP)                                                       \
+  case PP:                                                               \
+    if (prolong)                                                         \
+      launch_h<AXIS, PP, true>(grid, block, A, T, in, out, s);           \
+    else                                                                 \
+      launch_h<AXIS, PP, false>(grid, block, A, T, in, out, s);          \
     return;
     switch (T.hp) {
       STMG_H(1)
@@ -188,44 +204,67 @@ void pass(int F, const long long* in_d, const long long* out_d, const DevAxisTra
   const int* ptr = prolong ? T.row_ptr : T.col_ptr;
   const int* idx = prolong ? T.row_idx : T.col_idx;
   const double* w = prolong ? T.row_w : T.col_w;
-  axis_pass_kernel<AXIS><<<grid, block, 0, s>>>(in_d[0], in_d[1], in_d[2], out_d[0], out_d[1], out_d[2], ptr, idx, w,
-                                              mask_in, mask_out, accumulate, in, out);
+  axis_pass_kernel<AXIS><<<grid, block, 0, s>>>(A, ptr, idx, w, in, out);
 }
 
-// apply the per-axis maps x, then y, then z (2D: x, y)
+// apply the per-axis maps x, then y, then z (2D: x, y); the intermediates are
+// compact, the source / destination use the given field strides
 void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const long long* src_d, const long long* dst_d,
-               const double* in, double* out, double* t1, double* t2, bool accumulate, cudaStream_t s) {
+               const double* in, double* out, double* t1, double* t2, const TransferSlab& sl, cudaStream_t s) {
+  auto args = [&](const long long* i, const long long* o, long long fs_in, long long fs_out, bool first, bool last) {
+    PassArgs A{};
+    for (int a = 0; a < 3; ++a) {
+      A.i[a] = i[a];
+      A.o[a] = o[a];
+    }
+    A.fs_in = fs_in > 0 ? fs_in : i[0] * i[1] * i[2];
+    A.fs_out = fs_out > 0 ? fs_out : o[0] * o[1] * o[2];
+    A.zbc = dim == 3 ? sl.zbc : 3;
+    A.mask_in = first;
+    A.mask_out = last;
+    A.skip_lo_in = first && sl.skip_lo_in;
+    A.accumulate = last && sl.accumulate;
+    return A;
+  };
+  const long long fs_src = prolong ? sl.coarse_fstride : 0, fs_dst = prolong ? 0 : sl.coarse_fstride;
   long long d1[3] = {dst_d[0], src_d[1], src_d[2]};
-  pass<0>(F, src_d, d1, ax[0], prolong, true, false, false, in, t1, s);
   if (dim == 2) {
-    pass<1>(F, d1, dst_d, ax[1], prolong, false, true, accumulate, t1, out, s);
+    pass<0>(F, args(src_d, d1, fs_src, 0, true, false), ax[0], prolong, in, t1, s);
+    pass<1>(F, args(d1, dst_d, 0, fs_dst, false, true), ax[1], prolong, t1, out, s);
     return;
   }
   long long d2[3] = {dst_d[0], dst_d[1], src_d[2]};
-  pass<1>(F, d1, d2, ax[1], prolong, false, false, false, t1, t2, s);
-  pass<2>(F, d2, dst_d, ax[2], prolong, false, true, accumulate, t2, out, s);
+  pass<0>(F, args(src_d, d1, fs_src, 0, true, false), ax[0], prolong, in, t1, s);
+  pass<1>(F, args(d1, d2, 0, 0, false, false), ax[1], prolong, t1, t2, s);
+  pass<2>(F, args(d2, dst_d, 0, fs_dst, false, true), ax[2], prolong, t2, out, s);
 }
 
 }  // namespace
 
 void spatial_prolong(const DevAxisTransfer* ax, int dim, int F, const long long* dc, const long long* df,
-                     const double* coarse, double* fine, double* t1, double* t2, bool accumulate, cudaStream_t s) {
-  separable(ax, true, dim, F, dc, df, coarse, fine, t1, t2, accumulate, s);
+                     const double* coarse, double* fine, double* t1, double* t2, const TransferSlab& sl,
+                     cudaStream_t s) {
+  separable(ax, true, dim, F, dc, df, coarse, fine, t1, t2, sl, s);
 }
 void spatial_restrict(const DevAxisTransfer* ax, int dim, int F, const long long* dc, const long long* df,
-                      const double* fine, double* coarse, double* t1, double* t2, cudaStream_t s) {
-  separable(ax, false, dim, F, df, dc, fine, coarse, t1, t2, false, s);
+                      const double* fine, double* coarse, double* t1, double* t2, const TransferSlab& sl,
+                      cudaStream_t s) {
+  separable(ax, false, dim, F, df, dc, fine, coarse, t1, t2, sl, s);
 }
 void temporal_prolong(const double* T, int Ff, int Fc, long long n_space, const long long* d, int dim,
-                      const double* coarse, double* fine, bool accumulate, cudaStream_t s) {
+                      const double* coarse, double* fine, const TransferSlab& sl, cudaStream_t s) {
   count_launch();
-  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, false, accumulate, n_space, d[0], d[1], d[2], dim,
+  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, false, sl.accumulate, n_space, d[0], d[1], d[2], dim,
+                                                     dim == 3 ? sl.zbc : 3, false,
+                                                     sl.coarse_fstride > 0 ? sl.coarse_fstride : n_space, n_space,
                                                      coarse, fine);
 }
 void temporal_restrict(const double* T, int Ff, int Fc, long long n_space, const long long* d, int dim,
-                       const double* fine, double* coarse, cudaStream_t s) {
+                       const double* fine, double* coarse, const TransferSlab& sl, cudaStream_t s) {
   count_launch();
-  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, true, false, n_space, d[0], d[1], d[2], dim, fine,
+  temporal_kernel<<<grid_for(n_space), 256, 0, s>>>(T, Ff, Fc, true, sl.accumulate, n_space, d[0], d[1], d[2], dim,
+                                                     dim == 3 ? sl.zbc : 3, dim == 3 && sl.skip_lo_in, n_space,
+                                                     sl.coarse_fstride > 0 ? sl.coarse_fstride : n_space, fine,
                                                      coarse);
 }
 

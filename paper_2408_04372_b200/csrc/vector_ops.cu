@@ -117,13 +117,13 @@ __global__ void fill_kernel(double* __restrict__ y, double v, long long n) {
 }
 __global__ void set_element_kernel(double* y, long long i, double v) { y[i] = v; }
 __global__ void colour_kernel(double* __restrict__ y, long long dx, long long dy, long long dz, int dim, int period,
-                              int cx, int cy, int cz) {
+                              int cx, int cy, int cz, long long zoff) {
   const long long n = dx * dy * dz;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < n; g += (long long)gridDim.x * blockDim.x) {
     const long long ix = g % dx, iy = (g / dx) % dy, iz = g / (dx * dy);
     bool hit = ix % period == cx;
     if (dim > 1) hit = hit && (iy % period == cy);
-    if (dim > 2) hit = hit && (iz % period == cz);
+    if (dim > 2) hit = hit && ((iz + zoff) % period == cz);
     y[g] = hit ? 1.0 : 0.0;
   }
 }
@@ -133,10 +133,10 @@ __global__ void colour_kernel(double* __restrict__ y, long long dx, long long dy
 void vec_fill(double* y, double v, long long n, cudaStream_t s) { count_launch(); fill_kernel<<<grid_for(n), kThreads, 0, s>>>(y, v, n); }
 void vec_set_element(double* y, long long i, double v, cudaStream_t s) { count_launch(); set_element_kernel<<<1, 1, 0, s>>>(y, i, v); }
 void vec_colour_indicator(double* y, const long long* dofs, int dim, int period, int cx, int cy, int cz,
-                          cudaStream_t s) {
+                          long long z_offset, cudaStream_t s) {
   const long long n = dofs[0] * dofs[1] * dofs[2];
   count_launch();
-  colour_kernel<<<grid_for(n), kThreads, 0, s>>>(y, dofs[0], dofs[1], dofs[2], dim, period, cx, cy, cz);
+  colour_kernel<<<grid_for(n), kThreads, 0, s>>>(y, dofs[0], dofs[1], dofs[2], dim, period, cx, cy, cz, z_offset);
 }
 
 void vec_copy(double* y, const double* x, long long n, cudaStream_t s) {

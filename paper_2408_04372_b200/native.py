@@ -87,6 +87,29 @@ SIGNATURES = [
                              C.POINTER(GmresResult), c_double_p, C.c_int, C.c_void_p]),
     ("stmg_solve_host", C.c_int, [C.c_void_p, C.c_int, c_double_p, c_double_p, C.POINTER(GmresOptions),
                                   C.POINTER(GmresResult), c_double_p, C.c_int]),
+    # z-slab partitioned solve
+    ("stmg_nccl_unique_id", C.c_int, [C.c_char_p]),
+    ("stmg_comm_create", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_void_p]),
+    ("stmg_comm_destroy", None, [C.c_void_p]),
+    ("stmg_slab_plan", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_int, c_int_p,
+                                 c_int_p]),
+    ("stmg_slab_multigrid_create", C.c_int, [C.c_int, C.c_int, C.c_void_p, c_double_p, C.c_int, C.c_int, C.c_int,
+                                             C.c_int, C.c_double, C.c_int, c_int_p, C.c_void_p, C.c_int, C.c_int,
+                                             C.c_int, C.c_void_p, C.c_void_p]),
+    ("stmg_slab_multigrid_destroy", None, [C.c_void_p]),
+    ("stmg_slab_multigrid_local_dofs", C.c_longlong, [C.c_void_p]),
+    ("stmg_slab_multigrid_info", C.c_int, [C.c_void_p, c_int_p]),
+    ("stmg_slab_multigrid_part", C.c_int, [C.c_void_p, C.c_int, c_ll_p, c_ll_p, c_ll_p]),
+    ("stmg_slab_multigrid_omega", C.c_double, [C.c_void_p, C.c_int]),
+    ("stmg_slab_multigrid_set_omega", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
+    ("stmg_slab_multigrid_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_slab_multigrid_vcycle", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_slab_multigrid_asm_add_correction", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_slab_multigrid_solve", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(GmresOptions),
+                                            C.POINTER(GmresResult), C.c_void_p]),
+    ("stmg_slab_multigrid_dot", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, c_double_p]),
+    ("stmg_slab_multigrid_scatter", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("stmg_slab_multigrid_gather", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 ]
 
 _lib = None

@@ -259,9 +259,12 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.partitioned:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
         if not args.replicas:
             return run_partitioned(args, world, rank, local)
     lib = native.load()
@@ -408,6 +411,8 @@ def main():
     ap.add_argument("--ref-refinements", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the z-slab partitioned path even at N = 1 (one slab; exercises the NCCL plumbing)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas per rank instead of the z-slab partitioned solve")
     args = ap.parse_args()

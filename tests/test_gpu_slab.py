@@ -15,7 +15,7 @@ from paper_2408_04372_b200 import api, problems
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("C2", 2, 2), ("C2", 2, 4), ("C3", 1, 2), ("C3", 1, 4), ("C5-8", None, 2)]
+CASES = [("C2", 2, 2), ("C2", 3, 2), ("C2", 3, 4), ("C3", 1, 2), ("C3", 1, 4), ("C5-8", None, 2)]
 
 
 def _rel(a, b):
@@ -75,7 +75,7 @@ def test_slab_relaxation_and_vcycle_match_global(cuda, name, r, parts):
     assert _rel(got.cpu().numpy(), want.cpu().numpy()) <= 1e-10
 
 
-@pytest.mark.parametrize("name,r,parts", [("C2", 2, 2), ("C2", 2, 4), ("C3", 1, 4)])
+@pytest.mark.parametrize("name,r,parts", [("C2", 3, 2), ("C2", 3, 4), ("C3", 1, 4)])
 def test_slab_gmres_matches_reference(cuda, ref, name, r, parts):
     cfg = problems.config(name, r)
     mesh, G, S = _pair(cfg, parts)
@@ -91,7 +91,7 @@ def test_slab_gmres_matches_reference(cuda, ref, name, r, parts):
 
 
 def test_slab_dot_counts_interfaces_once(cuda):
-    cfg = problems.config("C2", 2)
+    cfg = problems.config("C2", 3)
     mesh, G, S = _pair(cfg, 4)
     a = problems.uniform_vector(cfg.n_dofs, seed=25)
     b = problems.uniform_vector(cfg.n_dofs, seed=26)
@@ -100,7 +100,7 @@ def test_slab_dot_counts_interfaces_once(cuda):
 
 
 def test_slab_rejects_uneven_partition(cuda):
-    cfg = problems.config("C2", 2)  # 16 cell layers
+    cfg = problems.config("C2", 2)  # 4 cell layers
     mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
     with pytest.raises(ValueError):
         api.SlabMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps,

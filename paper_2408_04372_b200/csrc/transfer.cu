@@ -91,52 +91,113 @@ __global__ void __launch_bounds__(128) axis_pass_kernel(const PassArgs A, const 
     out[oidx] = s;
 }
 
-// h-transfer pass along AXIS for equal p on both meshes (structured weights,
-// no CSR): prolongation out[i] = sum_j hw[r][j] in[c p + j] with
-// i = 2p c + r; restriction out[c p + j] = sum_r hw[r][j] in[2p c + r]
-// (+ the left neighbour cell's r < 2p nodes for the vertex node j = 0)
+// Cell-blocked h-transfer pass (equal p): one thread per coarse cell of a
+// lattice row along AXIS reads the row's inputs of that cell once and writes
+// all outputs the cell owns -- prolongation: the 2p fine nodes 2pc .. 2pc+2p-1
+// from the p+1 coarse nodes (the last cell also the final fine node);
+// restriction: coarse nodes cp .. cp+p-1 from the cell's 2p+1 fine nodes plus
+// the left cell's 2p (vertex node), the last cell also the final coarse node.
+// Boundary masks are evaluated only on the row's first / last cell.
 template <int AXIS, int P, bool PROLONG>
-__global__ void __launch_bounds__(128) axis_pass_h_kernel(const PassArgs A, const DevAxisTransfer T,
-                                                          const double* __restrict__ in, double* __restrict__ out) {
-  const long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long y = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
-  if (x >= A.o[0] || y >= A.o[1]) return;
-  const long long z = blockIdx.z % A.o[2], f = blockIdx.z / A.o[2];
-  const long long oidx = f * A.fs_out + (z * A.o[1] + y) * A.o[0] + x;
-  double s = 0.0;
-  if (!skip_entry<AXIS>(A, x, y, z)) {
-    const long long o = AXIS == 0 ? x : (AXIS == 1 ? y : z);
-    const long long n_ax = A.i[AXIS];
-    const double* src = in + f * A.fs_in;
-    const long long ix = A.i[0], iy = A.i[1];
-    const long long base = AXIS == 0 ? (z * iy + y) * ix : (AXIS == 1 ? z * iy * ix + x : y * ix + x);
-    const long long stride = AXIS == 0 ? 1 : (AXIS == 1 ? ix : ix * iy);
-    auto val = [&](long long j) { return skip_input_along(A, AXIS, j, n_ax) ? 0.0 : __ldg(src + base + j * stride); };
-    if (PROLONG) {
-      const long long ncc = (n_ax - 1) / P;
-      long long c = o / (2 * P);
-      if (c > ncc - 1) c = ncc - 1;
-      const int r = static_cast<int>(o - 2 * P * c);
+__global__ void __launch_bounds__(128) axis_cell_kernel(const PassArgs A, const DevAxisTransfer T,
+                                                        const double* __restrict__ in, double* __restrict__ out) {
+  const long long n_in = A.i[AXIS], n_out = A.o[AXIS];
+  const long long ncc = PROLONG ? (n_in - 1) / P : (n_out - 1) / P;
+  long long x, y, z, f, c;
+  if (AXIS == 0) {
+    c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    y = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
+    z = blockIdx.z % A.o[2];
+    f = blockIdx.z / A.o[2];
+    x = 0;
+    if (c >= ncc || y >= A.o[1]) return;
+  } else if (AXIS == 1) {
+    x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    c = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
+    z = blockIdx.z % A.o[2];
+    f = blockIdx.z / A.o[2];
+    y = 0;
+    if (x >= A.o[0] || c >= ncc) return;
+  } else {
+    x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    y = static_cast<long long>(blockIdx.y) * blockDim.y + threadIdx.y;
+    c = blockIdx.z % ncc;
+    f = blockIdx.z / ncc;
+    z = 0;
+    if (x >= A.o[0] || y >= A.o[1]) return;
+  }
+  // rows: input / output base offsets and the stride along AXIS
+  const long long ix = A.i[0], iy = A.i[1], ox = A.o[0], oy = A.o[1];
+  const long long ibase = f * A.fs_in + (AXIS == 0 ? (z * iy + y) * ix : (AXIS == 1 ? z * iy * ix + x : y * ix + x));
+  const long long obase = f * A.fs_out + (AXIS == 0 ? (z * oy + y) * ox : (AXIS == 1 ? z * oy * ox + x : y * ox + x));
+  const long long istr = AXIS == 0 ? 1 : (AXIS == 1 ? ix : ix * iy);
+  const long long ostr = AXIS == 0 ? 1 : (AXIS == 1 ? ox : ox * oy);
+  // the row itself masked out (other coordinates on a boundary)?
+  bool row_in0 = false, row_out0 = false;
+  if (A.mask_in) {
+    if (AXIS != 0 && on_bdry(x, ix)) row_in0 = true;
+    if (AXIS != 1 && A.i[1] > 1 && on_bdry(y, iy)) row_in0 = true;
+    if (AXIS != 2 && A.i[2] > 1 && on_bdry_z(z, A.i[2], A.zbc)) row_in0 = true;
+  }
+  if (A.skip_lo_in && AXIS != 2 && z == 0) row_in0 = true;
+  if (A.mask_out) {
+    if (AXIS != 0 && on_bdry(x, ox)) row_out0 = true;
+    if (AXIS != 1 && oy > 1 && on_bdry(y, oy)) row_out0 = true;
+    if (AXIS != 2 && A.o[2] > 1 && on_bdry_z(z, A.o[2], A.zbc)) row_out0 = true;
+  }
+  // only the first / last cells (and the left neighbour of cell 1) touch
+  // boundary nodes
+  const bool edge = c <= 1 || c == ncc - 1;
+  auto ld = [&](long long j) -> double {
+    if (row_in0) return 0.0;
+    if (edge && skip_input_along(A, AXIS, j, n_in)) return 0.0;
+    return __ldg(in + ibase + j * istr);
+  };
+  auto st = [&](long long j, double v) {
+    if (row_out0 || (edge && A.mask_out && (AXIS == 2 ? on_bdry_z(j, n_out, A.zbc) : on_bdry(j, n_out)))) v = 0.0;
+    double* o = out + obase + j * ostr;
+    if (A.accumulate)
+      *o += v;
+    else
+      *o = v;
+  };
+  if (PROLONG) {
+    double cv[P + 1];
 #pragma unroll
-      for (int j = 0; j <= P; ++j) s = fma(T.hw[r][j], val(c * P + j), s);
-    } else {
-      const long long c = o / P;
-      const int j = static_cast<int>(o - c * P);
+    for (int j = 0; j <= P; ++j) cv[j] = ld(c * P + j);
+    const int rmax = c == ncc - 1 ? 2 * P : 2 * P - 1;
 #pragma unroll
-      for (int r = 0; r <= 2 * P; ++r) {
-        const long long i = 2 * P * c + r;
-        if (i < n_ax) s = fma(T.hw[r][j], val(i), s);
+    for (int r = 0; r <= 2 * P; ++r) {
+      if (r > rmax) break;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j <= P; ++j) s = fma(T.hw[r][j], cv[j], s);
+      st(2 * P * c + r, s);
+    }
+  } else {
+    double fv[2 * P + 1], lv[2 * P];
+#pragma unroll
+    for (int r = 0; r <= 2 * P; ++r) fv[r] = ld(2 * P * c + r);
+#pragma unroll
+    for (int r = 0; r < 2 * P; ++r) lv[r] = c > 0 ? ld(2 * P * (c - 1) + r) : 0.0;
+#pragma unroll
+    for (int jj = 0; jj < P; ++jj) {
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) s = fma(T.hw[r][jj], fv[r], s);
+      if (jj == 0) {
+#pragma unroll
+        for (int r = 0; r < 2 * P; ++r) s = fma(T.hw[r][P], lv[r], s);
       }
-      if (j == 0 && c > 0) {
+      st(c * P + jj, s);
+    }
+    if (c == ncc - 1) {
+      double s = 0.0;
 #pragma unroll
-        for (int r = 0; r < 2 * P; ++r) s = fma(T.hw[r][P], val(2 * P * (c - 1) + r), s);
-      }
+      for (int r = 0; r <= 2 * P; ++r) s = fma(T.hw[r][P], fv[r], s);
+      st(c * P + P, s);
     }
   }
-  if (A.accumulate)
-    out[oidx] += s;
-  else
-    out[oidx] = s;
 }
 
 __global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bool transpose, bool accumulate,
@@ -172,9 +233,21 @@ inline unsigned grid_for(long long n) {
 }
 
 template <int AXIS, int P, bool PROLONG>
-void launch_h(const dim3& grid, const dim3& block, const PassArgs& A, const DevAxisTransfer& T, const double* in,
-              double* out, cudaStream_t s) {
-  axis_pass_h_kernel<AXIS, P, PROLONG><<<grid, block, 0, s>>>(A, T, in, out);
+void launch_h(int F, const PassArgs& A, const DevAxisTransfer& T, const double* in, double* out, cudaStream_t s) {
+  // one thread per coarse cell of a lattice row along AXIS
+  const long long ncc = PROLONG ? (A.i[AXIS] - 1) / P : (A.o[AXIS] - 1) / P;
+  const dim3 block(32, 4);
+  dim3 grid;
+  if (AXIS == 0)
+    grid = dim3(static_cast<unsigned>((ncc + 31) / 32), static_cast<unsigned>((A.o[1] + 3) / 4),
+                static_cast<unsigned>(A.o[2] * F));
+  else if (AXIS == 1)
+    grid = dim3(static_cast<unsigned>((A.o[0] + 31) / 32), static_cast<unsigned>((ncc + 3) / 4),
+                static_cast<unsigned>(A.o[2] * F));
+  else
+    grid = dim3(static_cast<unsigned>((A.o[0] + 31) / 32), static_cast<unsigned>((A.o[1] + 3) / 4),
+                static_cast<unsigned>(ncc * F));
+  axis_cell_kernel<AXIS, P, PROLONG><<<grid, block, 0, s>>>(A, T, in, out);
 }
 
 template <int AXIS>
@@ -185,12 +258,12 @@ void pass(int F, const PassArgs& A, const DevAxisTransfer& T, bool prolong, cons
                   static_cast<unsigned>(A.o[2] * F));
   count_launch();
   if (T.hp > 0) {
-#define STMG_H(PP)                                                       \
-  case PP:                                                               \
-    if (prolong)                                                         \
-      launch_h<AXIS, PP, true>(grid, block, A, T, in, out, s);           \
-    else                                                                 \
-      launch_h<AXIS, PP, false>(grid, block, A, T, in, out, s);          \
+#define STMG_H(PP)                                            \
+  case PP:                                                    \
+    if (prolong)                                              \
+      launch_h<AXIS, PP, true>(F, A, T, in, out, s);          \
+    else                                                      \
+      launch_h<AXIS, PP, false>(F, A, T, in, out, s);         \
     return;
     switch (T.hp) {
       STMG_H(1)

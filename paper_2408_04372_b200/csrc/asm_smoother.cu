@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -452,18 +453,24 @@ __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constan
 // index, so no per-dof division or index decoding is left in the loop.
 // Dirichlet dofs of a block (identity rows, asm_smoother.cpp:29-33 with the
 // global identity) contribute w * r directly from the gather threads.
-template <int NT, int S>
-__global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_constant__ DevASM A,
-                                                                const double* __restrict__ r,
-                                                                double* __restrict__ z, double scale) {
+// NBUF record buffers per CTA: the record of cell i + NBUF - 1 is requested
+// while cell i is solved (prefetch distance NBUF - 1)
+template <int NBUF>
+constexpr size_t fd64_smem() {
+  return sizeof(double) * (NBUF * static_cast<size_t>(kRec64) + 16 * 64) + 4 * sizeof(long long) +
+         NBUF * sizeof(unsigned long long);
+}
+
+template <int NT, int S, int NBUF>
+__global__ void __launch_bounds__(256, NBUF == 2 ? 3 : 2) asm_apply_fd64_kernel(const __grid_constant__ DevASM A,
+                                                                               const double* __restrict__ r,
+                                                                               double* __restrict__ z, double scale) {
   constexpr int M = 64, NCOL = NT * S, NPAIR = (NCOL + 1) / 2;
   constexpr unsigned RBYTES = static_cast<unsigned>(kRec64 * sizeof(double));
   static_assert(RBYTES % 16 == 0, "record must be a multiple of 16 bytes");
   extern __shared__ __align__(128) double sm[];
-  double* Xb0 = sm;
-  double* Xb1 = sm + kRec64;
-  double* rs = sm + 2 * kRec64;  // [64][8] P-transformed residual, pair-swizzled rows
-  double* hs = rs + 8 * M;       // [64][8] scaled eigen-coefficients
+  double* rs = sm + NBUF * kRec64;  // [64][8] P-transformed residual, pair-swizzled rows
+  double* hs = rs + 8 * M;          // [64][8] scaled eigen-coefficients
   long long* cinfo = reinterpret_cast<long long*>(hs + 8 * M);       // [2][2] {g0, mask} per parity
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(cinfo + 4);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -498,15 +505,21 @@ __global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_con
   const double a0 = A.s0[j], a1 = A.s1[j];
 
   if (t == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   long long pos = blockIdx.x;
-  if (t == 0 && pos < n_pos) {
-    mbar_expect_tx(&bar[0], RBYTES);
-    bulk_g2s(Xb0, A.X + pos * kRec64, RBYTES, &bar[0]);
+  if (t == 0) {
+#pragma unroll
+    for (int b = 0; b + 1 < NBUF; ++b) {
+      const long long q = pos + static_cast<long long>(b) * gridDim.x;
+      if (q < n_pos) {
+        mbar_expect_tx(&bar[b], RBYTES);
+        bulk_g2s(sm + b * kRec64, A.X + q * kRec64, RBYTES, &bar[b]);
+      }
+    }
   }
   double rn[NCOL];
   long long g0n = 0, maskn = 0;
@@ -520,9 +533,10 @@ __global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_con
     }
   };
   if (pos < n_pos) fetch(pos);
-  unsigned ph0 = 0, ph1 = 0;
+  unsigned phase_bits = 0;  // parity of each buffer's barrier
+  int buf = 0;
   for (int it = 0; pos < n_pos; pos += gridDim.x, ++it) {
-    const int buf = it & 1;
+    const int par = it & 1;
     const long long next = pos + gridDim.x;
     // ---- stage the residual of this cell (prefetched last iteration)
     if (t < M) {
@@ -546,25 +560,25 @@ __global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_con
         for (int c = 0; c < NCOL; ++c) atomicAdd(z + c * nsp + g0n + off_g, w * rn[c]);
       }
       if (t == 0) {
-        cinfo[2 * buf] = g0n;
-        cinfo[2 * buf + 1] = maskn;
+        cinfo[2 * par] = g0n;
+        cinfo[2 * par + 1] = maskn;
       }
       if (next < n_pos) fetch(next);
     }
-    if (buf == 0) {
-      mbar_wait(&bar[0], ph0);
-      ph0 ^= 1;
-    } else {
-      mbar_wait(&bar[1], ph1);
-      ph1 ^= 1;
-    }
+    mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);
+    phase_bits ^= 1u << buf;
     __syncthreads();
-    if (t == 0 && next < n_pos) {
-      fence_proxy_async();
-      mbar_expect_tx(&bar[buf ^ 1], RBYTES);
-      bulk_g2s(buf ? Xb0 : Xb1, A.X + next * kRec64, RBYTES, &bar[buf ^ 1]);
+    // every warp is past cell it-1, so its buffer takes cell it + NBUF - 1
+    {
+      const int fb = buf == 0 ? NBUF - 1 : buf - 1;
+      const long long q = pos + static_cast<long long>(NBUF - 1) * gridDim.x;
+      if (t == 0 && q < n_pos) {
+        fence_proxy_async();
+        mbar_expect_tx(&bar[fb], RBYTES);
+        bulk_g2s(sm + fb * kRec64, A.X + q * kRec64, RBYTES, &bar[fb]);
+      }
     }
-    const double* Xs = buf ? Xb1 : Xb0;
+    const double* Xs = sm + buf * kRec64;
     {
       // product 1: hat r (e x slots) = X^T rs
       double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
@@ -600,8 +614,8 @@ __global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_con
         v[2 * i] = __shfl_sync(0xffffffffu, v0, grp | i);
         v[2 * i + 1] = __shfl_sync(0xffffffffu, v1, grp | i);
       }
-      const long long g0 = cinfo[2 * buf];
-      const int mask = static_cast<int>(cinfo[2 * buf + 1]);
+      const long long g0 = cinfo[2 * par];
+      const int mask = static_cast<int>(cinfo[2 * par + 1]);
       if (j < NPAIR && !(mask & fb_e)) {
         const int c0 = 2 * j, c1 = 2 * j + 1;
         double o0 = 0.0, o1 = 0.0;
@@ -615,6 +629,7 @@ __global__ void __launch_bounds__(256, 3) asm_apply_fd64_kernel(const __grid_con
         if (c1 < NCOL) atomicAdd(zp + c1 * nsp, o1 * w_e);
       }
     }
+    buf = buf + 1 == NBUF ? 0 : buf + 1;
   }
 }
 
@@ -816,25 +831,38 @@ void launch_asm_mma(const DevASM& A, const double* r, double* z, double scale, c
     default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
   }
 }
-template <int NT, int S>
-void launch_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (2 * kRec64 + 16 * 64) + 4 * sizeof(long long) + 2 * sizeof(unsigned long long);
+template <int NT, int S, int NBUF>
+void launch_fd64_nbuf(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  constexpr size_t smem = fd64_smem<NBUF>();
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(asm_apply_fd64_kernel<NT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(asm_apply_fd64_kernel<NT, S, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    cudaFuncSetAttribute(asm_apply_fd64_kernel<NT, S>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(asm_apply_fd64_kernel<NT, S, NBUF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     configured = true;
   }
   int per_sm = 0, dev = 0, sms = 148;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_fd64_kernel<NT, S>, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_fd64_kernel<NT, S, NBUF>, 256, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (A.n_list == 0) return;
   const long long grid =
       std::max<long long>(1, std::min<long long>(A.n_list, static_cast<long long>(std::max(per_sm, 1)) * sms));
   count_launch();
-  asm_apply_fd64_kernel<NT, S><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
+  asm_apply_fd64_kernel<NT, S, NBUF><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
+}
+// record pipeline depth (STMG_ASM_NBUF = 2 or 3; default 3: two records in
+// flight per CTA, 2 CTAs / SM)
+template <int NT, int S>
+void launch_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  static const int nbuf = [] {
+    const char* e = std::getenv("STMG_ASM_NBUF");
+    return e ? std::atoi(e) : 3;
+  }();
+  if (nbuf == 2)
+    launch_fd64_nbuf<NT, S, 2>(A, r, z, scale, s);
+  else
+    launch_fd64_nbuf<NT, S, 3>(A, r, z, scale, s);
 }
 void launch_asm_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   switch (A.nt * 10 + A.S) {

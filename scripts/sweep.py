@@ -1,0 +1,75 @@
+"""Per-configuration throughput of the two metric kernels (BASELINE.json
+configs C1-C5): operator vmult and one STMG V-cycle, device-timed with CUDA
+events on the launching stream after warm-up, vectors resident in HBM.
+Prints one JSON line per configuration (DoF/s, ms, HBM fraction of the vmult's
+algorithmic bytes 16 N (+ 24 n_verts perturbed) against MEASURED_PEAKS.json).
+
+  python scripts/sweep.py [C1 C2 C3 C4 C5-32 C5-64 C5-128 C5-256v]
+  (suffix v: vmult only -- the V-cycle does not fit one GPU there)
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2408_04372_b200 import api, problems  # noqa: E402
+
+
+def timed(fn, reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main(names):
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    for name in names:
+        vonly = name.endswith("v")
+        cname = name[:-1] if vonly else name
+        cfg = problems.config(cname)
+        t0 = time.perf_counter()
+        mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
+        if vonly:
+            op = api.SpaceTimeOperator(mesh, cfg.refinements, cfg.p, cfg.equation, cfg.scheme, cfg.k, cfg.tau,
+                                       cfg.n_steps, cfg.rho)
+            M = None
+        else:
+            M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k,
+                                       cfg.n_steps, cfg.tau)
+            op = M.operator_at(0)
+        torch.cuda.synchronize()
+        setup = time.perf_counter() - t0
+        N = op.n_dofs
+        u = torch.rand(N, dtype=torch.float64, device="cuda").mul_(2).sub_(1)
+        y = torch.empty_like(u)
+        reps = 3 if N > 5e8 else 10
+        op.apply(u, y)
+        t_v = timed(lambda: op.apply(u, y), reps)
+        nv = (cfg.cells + 1) ** cfg.dim
+        vbytes = 16 * N + (24 * nv if cfg.perturb > 0 else 0)
+        line = {"config": name, **cfg.describe(), "setup_s": round(setup, 2), "vmult_ms": t_v,
+                "vmult_dofs_per_s": N / (t_v * 1e-3), "vmult_hbm_frac": vbytes / (t_v * 1e-3) / 1e9 / peak}
+        if M is not None:
+            z = torch.empty_like(u)
+            M.apply(u, z)
+            t_c = timed(lambda: M.apply(u, z), max(3, reps // 2))
+            line.update({"vcycle_ms": t_c, "vcycle_dofs_per_s": N / (t_c * 1e-3), "mg_levels": M.n_levels,
+                         "smoother_kind_fine": M.smoother_kind(0), "device_bytes": M.device_bytes()})
+        print(json.dumps(line), flush=True)
+        del M, op, u, y, mesh
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5-32", "C5-64", "C5-128", "C5-256v"])

@@ -36,6 +36,18 @@ sys.path.insert(0, ROOT)
 METRIC = "space-time DoF/s: operator vmult & STMG V-cycle, fp64, % of HBM roofline"
 
 
+def ncu_traffic(kernel_key: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(kernel_key)
+    return e["dram_bytes_per_launch"] if e else None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -96,6 +108,43 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def e2e_pipelined(step, r_dev, y_dev, rh, yh, n_steps):
+    """End-to-end time per step (s): every step copies its input from pinned
+    host memory (rh) to the device and its result back (yh). The H2D of step
+    i+1 and the D2H of step i-1 run on two copy streams while step i
+    computes; r_dev / y_dev are two device buffers each (ping-pong)."""
+    import torch
+    comp = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ready = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    read = [torch.cuda.Event() for _ in range(2)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(h2d):
+        r_dev[0].copy_(rh, non_blocking=True)
+        ready[0].record(h2d)
+    for i in range(n_steps):
+        b = i % 2
+        if i + 1 < n_steps:
+            with torch.cuda.stream(h2d):
+                if i >= 1:
+                    h2d.wait_event(done[1 - b])  # step i-1 has read r_dev[1-b]
+                r_dev[1 - b].copy_(rh, non_blocking=True)
+                ready[1 - b].record(h2d)
+        comp.wait_event(ready[b])
+        if i >= 2:
+            comp.wait_event(read[b])  # step i-2's result is on the host
+        step(r_dev[b], y_dev[b])
+        done[b].record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done[b])
+            yh.copy_(y_dev[b], non_blocking=True)
+            read[b].record(d2h)
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / n_steps
 
 
 def cpu_baseline(workload: str, budget_s: float = 15.0, refinements: int = 3):
@@ -177,9 +226,9 @@ def run_partitioned(args, world, rank, local):
     r = torch.rand(n_local, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     z, y = torch.empty_like(r), torch.empty_like(r)
 
-    def step():
-        S.vcycle(r, z)
-        S.apply(z, y)
+    def step(rr=r, yy=y):
+        S.vcycle(rr, z)
+        S.apply(z, yy)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -211,16 +260,10 @@ def run_partitioned(args, world, rank, local):
     rh = torch.empty(n_local, dtype=torch.float64).pin_memory()
     rh.copy_(r.cpu())
     yh = torch.empty(n_local, dtype=torch.float64).pin_memory()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(4, min(args.steps, 10))
     dist.barrier()
-    torch.cuda.synchronize()
-    tw = time.perf_counter()
-    for _ in range(e2e_steps):
-        r.copy_(rh, non_blocking=True)
-        step()
-        yh.copy_(y, non_blocking=True)
-    torch.cuda.synchronize()
-    tl = torch.tensor([(time.perf_counter() - tw) / e2e_steps], dtype=torch.float64, device="cuda")
+    e2e_s = e2e_pipelined(step, [r, torch.empty_like(r)], [y, torch.empty_like(y)], rh, yh, e2e_steps)
+    tl = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     dist.all_reduce(tl, op=dist.ReduceOp.MAX)
     e2e = {"value": cfg.n_dofs / float(tl.item()), "unit": "DoF/s", "h2d_bytes_per_step": 8 * n_local,
            "d2h_bytes_per_step": 8 * n_local, "note": "per rank: its slab of the step's input and result"}
@@ -284,9 +327,9 @@ def run_ours(args):
     z = torch.empty_like(r)
     y = torch.empty_like(r)
 
-    def step():
-        M.apply(r, z)
-        op.apply(z, y)
+    def step(rr=r, yy=y):
+        M.apply(rr, z)
+        op.apply(z, yy)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -332,22 +375,16 @@ def run_ours(args):
     rh = torch.empty(N, dtype=torch.float64).pin_memory()
     rh.copy_(r.cpu())
     yh = torch.empty(N, dtype=torch.float64).pin_memory()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(4, min(args.steps, 10))
     if dist:
         dist.barrier()
-    torch.cuda.synchronize()
-    tw = time.perf_counter()
-    for _ in range(e2e_steps):
-        r.copy_(rh, non_blocking=True)
-        step()
-        yh.copy_(y, non_blocking=True)
-    torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - tw) / e2e_steps
+    e2e_s = e2e_pipelined(step, [r, torch.empty_like(r)], [y, torch.empty_like(y)], rh, yh, e2e_steps)
     if dist:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": world * N / e2e_s, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N}
+    e2e = {"value": world * N / e2e_s, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+           "note": "pinned H2D of each step's input and D2H of its result, overlapped with the neighbouring steps"}
 
     # roofline of the dominant kernel
     peak, peak_kind = measured_peaks()
@@ -355,20 +392,22 @@ def run_ours(args):
     m = (cfg.p + 1) ** cfg.dim
     n_verts = (cfg.cells + 1) ** cfg.dim
     vmult_bytes = 16 * N + (24 * n_verts if cfg.perturb > 0 else 0)
-    asm_bytes = cells * m * m * 8 + cells * m * 8 + 8 * N + 16 * N
+    # records (X + eigenvalues) + 16-byte meta per cell, r read, z read+write
+    asm_bytes = cells * (m * m + m) * 8 + 16 * cells + 8 * N + 16 * N
     # fine-level launches per step: vmult 3 (2 residuals in the V-cycle + the
     # outer op), ASM 2 (pre- and post-smoothing)
     share_vmult = 3 * t_vmult / ms
     share_asm = 2 * t_asm / ms
     if share_asm >= share_vmult:
-        dom = {"kernel": "asm_apply_kernel (fine-level exact cell-block smoother)", "ms": t_asm,
+        dom = {"kernel": "asm_apply_fd64_kernel (fine-level exact cell-block smoother)", "key": "asm", "ms": t_asm,
                "bytes": asm_bytes, "share_of_step": share_asm}
     else:
-        dom = {"kernel": "st_apply_kernel (fused space-time vmult)", "ms": t_vmult, "bytes": vmult_bytes,
-               "share_of_step": share_vmult}
+        dom = {"kernel": "st_lines_kernel (fused space-time vmult)", "key": "vmult", "ms": t_vmult,
+               "bytes": vmult_bytes, "share_of_step": share_vmult}
     achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": peak_kind, "kernel": dom["kernel"],
+                "traffic": ncu_traffic(f"{args.workload}:{dom['key']}"), "peak_source": peak_kind,
+                "kernel": dom["kernel"],
                 "algorithmic_bytes_per_launch": dom["bytes"], "launch_ms": dom["ms"],
                 "share_of_step": dom["share_of_step"]}
     vm_ach = vmult_bytes / (t_vmult * 1e-3) / 1e9

@@ -851,13 +851,15 @@ void launch_fd64_nbuf(const DevASM& A, const double* r, double* z, double scale,
   count_launch();
   asm_apply_fd64_kernel<NT, S, NBUF><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
 }
-// record pipeline depth (STMG_ASM_NBUF = 2 or 3; default 3: two records in
-// flight per CTA, 2 CTAs / SM)
+// record pipeline depth (STMG_ASM_NBUF = 2 or 3). Default 2: one record in
+// flight per CTA at 3 CTAs / SM measured 1.61 ms per C2 sweep against 1.91 ms
+// for 3 buffers at 2 CTAs / SM -- the per-cell solve, not the bytes in
+// flight, limits the sweep
 template <int NT, int S>
 void launch_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   static const int nbuf = [] {
     const char* e = std::getenv("STMG_ASM_NBUF");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 2;
   }();
   if (nbuf == 2)
     launch_fd64_nbuf<NT, S, 2>(A, r, z, scale, s);

@@ -174,6 +174,22 @@ int stmg_solve(const stmg_multigrid* mg, int precondition, const double* d_b, do
 int stmg_solve_host(const stmg_multigrid* mg, int precondition, const double* h_b, double* h_x,
                     const stmg_gmres_options* options, stmg_gmres_result* result, double* history, int history_cap);
 
+/* error_norms (driver.cpp:83-92) of one batch solution d_x entering from
+ * d_u0 against the manufactured solution of driver.cpp:265-293 (frequency):
+ * out = {L2(L2), Linf(L2), Linf(Linf)} with the reference's temporal Gauss
+ * (k+2) x spatial Gauss (p+2) sampling (driver.cpp:27-43) */
+int stmg_st_operator_error_norms(const stmg_st_operator* op, const double* d_x, const double* d_u0, double frequency,
+                                 double t0, double out[3]);
+/* march (driver.cpp:95-260) with every slab on the device: n_batches slabs of
+ * mg's finest operator, each assemble_rhs (source_kind 0 zero, 1 manufactured)
+ * -> STMG-preconditioned GMRES -> extract_final. d_u (and d_v for the wave)
+ * hold the entering state on input and the final state on output;
+ * iterations[n_batches] receives the GMRES iterations (0 after a
+ * non-converged batch); errors (may be NULL) the manufactured-solution error
+ * norms of u over the run. Returns -2 if a batch did not converge. */
+int stmg_march(const stmg_multigrid* mg, int n_batches, int source_kind, double frequency, double* d_u, double* d_v,
+               const stmg_gmres_options* options, int* iterations, double errors[3], void* stream);
+
 /* ---- z-slab partitioned solve over several GPUs (no
  * reference counterpart: the reference is single-process). The finest mesh
  * is cut into n_parts slabs of cell layers along z; a process holds

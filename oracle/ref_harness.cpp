@@ -307,6 +307,27 @@ int ref_assemble_rhs(void* h, int source_kind, double frequency, double t0, cons
   });
 }
 
+// error_norms (driver.cpp:83-92) of one batch solution u entering from u0
+// against the manufactured solution of driver.cpp:265-293 (frequency f);
+// out = {L2(L2), Linf(L2), Linf(Linf)}
+int ref_error_norms(void* h, const double* u, const double* u0, double frequency, double t0, double* out3) {
+  auto* r = static_cast<Ref*>(h);
+  return guard([&] {
+    ProblemSpec spec;
+    spec.dim = r->mesh.finest().dim;
+    spec.equation = r->op->equation();
+    manufactured_problem(spec, frequency);
+    BatchState st;
+    st.u = vec(u0, r->op->n_space());
+    const std::vector<Eigen::VectorXd> xs{vec(u, r->op->n_dofs())};
+    const std::vector<BatchState> es{st};
+    const ErrorRecord e = error_norms(*r->op, xs, es, spec.exact_u, t0);
+    out3[0] = e.l2_l2;
+    out3[1] = e.linf_l2;
+    out3[2] = e.linf_linf;
+  });
+}
+
 // extract_final (space_time_operator.cpp:223-248)
 int ref_extract_final(void* h, const double* u, const double* u0, const double* v0, double* uf, double* vf) {
   auto* r = static_cast<Ref*>(h);

@@ -73,6 +73,7 @@ def load() -> C.CDLL:
                               C.POINTER(C.c_int), dp, dp, dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.ref_assemble_rhs.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, dp, dp, dp]
     lib.ref_extract_final.argtypes = [C.c_void_p, dp, dp, dp, dp, dp]
+    lib.ref_error_norms.argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_double, dp]
     lib.ref_interpolate_gaussian.argtypes = [C.c_void_p, dp, C.c_double, dp]
     lib.ref_vertices.argtypes = [C.c_void_p, C.c_int, dp]
     lib.ref_temporal_weights.argtypes = [C.c_int, C.c_int, dp, dp, dp, dp, dp]
@@ -241,6 +242,14 @@ class Reference:
         uf, vf = np.empty(self.n_space), np.empty(self.n_space)
         _chk(load().ref_extract_final(self.h, _p(u), _p(u0), _p(v0), _p(uf), _p(vf)))
         return uf, vf
+
+    def error_norms(self, u: np.ndarray, u0: np.ndarray, frequency: float = 0.5, t0: float = 0.0):
+        """error_norms (driver.cpp:83-92) of one batch vs the manufactured
+        solution: (L2(L2), Linf(L2), Linf(Linf))."""
+        out = np.zeros(3)
+        _chk(load().ref_error_norms(self.h, _p(np.ascontiguousarray(u, dtype=np.float64)),
+                                    _p(np.ascontiguousarray(u0, dtype=np.float64)), frequency, t0, _p(out)))
+        return tuple(out)
 
     def interpolate_gaussian(self, centre=(0.5, 0.5, 0.5), width: float = 0.05) -> np.ndarray:
         c = np.ascontiguousarray(centre, dtype=np.float64)

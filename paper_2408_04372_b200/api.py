@@ -138,6 +138,14 @@ class SpaceTimeOperator:
                                                         _ptr(vf) if vf is not None else None, _stream()))
         return uf, vf
 
+    def error_norms(self, x, u0, frequency: float = 0.5, t0: float = 0.0):
+        """error_norms (driver.cpp:83-92) of one batch vs the manufactured
+        solution -> (L2(L2), Linf(L2), Linf(Linf))."""
+        out = (C.c_double * 3)()
+        _torch().cuda.synchronize()
+        N.check(N.load().stmg_st_operator_error_norms(self._h, _ptr(x), _ptr(u0), frequency, t0, out))
+        return tuple(out)
+
     def spatial_apply(self, kind: int, u, y=None):
         torch = _torch()
         if y is None:
@@ -296,6 +304,20 @@ class SpaceTimeMultigrid:
         N.check(N.load().stmg_solve(self._h, 1 if precondition else 0, _ptr(b), _ptr(x), C.byref(o), C.byref(res),
                                     hist.ctypes.data_as(N.c_double_p), history_cap, _stream()))
         return _result(res, hist)
+
+    def march(self, n_batches: int, u, v=None, source_kind: int = 1, frequency: float = 0.5, errors: bool = True,
+              **opts) -> dict:
+        """march (driver.cpp:95-260) on the device: n_batches slabs of the
+        finest operator; u (v for the wave) is the entering state and becomes
+        the final state. Returns the per-batch GMRES iterations and the
+        manufactured-solution error norms of u."""
+        o = gmres_options(**opts)
+        its = (C.c_int * n_batches)()
+        err = (C.c_double * 3)()
+        N.check(N.load().stmg_march(self._h, n_batches, source_kind, frequency, _ptr(u),
+                                    _ptr(v) if v is not None else None, C.byref(o), its,
+                                    err if errors else None, _stream()))
+        return {"iterations": list(its), "error_u": tuple(err) if errors else None}
 
     def solve_host(self, b: np.ndarray, x: np.ndarray, precondition: bool = True, history_cap: int = 1100, **opts):
         o = gmres_options(**opts)

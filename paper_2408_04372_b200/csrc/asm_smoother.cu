@@ -633,6 +633,132 @@ __global__ void __launch_bounds__(256, NBUF == 2 ? 3 : 2) asm_apply_fd64_kernel(
   }
 }
 
+// Large cell blocks (m > 64, e.g. 3D Q4: m = 125): one CTA of 128 threads per
+// cell (persistent), X row-major in global memory (m^2 doubles, L2-resident
+// across the two products of one cell), all S*n_t columns at once:
+//   hat r = X^T r  (thread e; consecutive threads read consecutive X entries)
+//   hat z_e = (T_M + lam_e T_A)^-1 hat r_e per step (pivoted n_t x n_t solve)
+//   z = X hat z    (thread a)
+// then the weighted scatter-add; Dirichlet rows contribute w * r.
+template <int NT>
+__global__ void __launch_bounds__(128) asm_apply_large_kernel(const __grid_constant__ DevASM A,
+                                                              const double* __restrict__ r, double* __restrict__ z,
+                                                              double scale) {
+  const int m = A.m, t = threadIdx.x;
+  const int ncol = A.S * NT;
+  extern __shared__ __align__(16) double sm[];
+  double* rs = sm;            // [m][8]
+  double* hs = rs + 8 * 128;  // [m][8]
+  const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
+  for (long long pos = blockIdx.x; pos < A.n_list; pos += gridDim.x) {
+    const unsigned ci = static_cast<unsigned>(A.list ? A.list[pos] : pos);
+    const long long cx = ci % cxn, cy = (ci / cxn) % cyn, cz = ci / (cxn * cyn);
+    LocalDof d{};
+    if (t < m) {
+      d = local_dof(A, cx, cy, cz, t);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) rs[t * 8 + c] = c < ncol ? __ldg(r + static_cast<long long>(c) * A.n_space + d.g) : 0.0;
+    }
+    __syncthreads();
+    const double* X = A.X + pos * A.xs;
+    if (t < m) {
+      double acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+      for (int a = 0; a < m; ++a) {
+        const double x = __ldg(X + static_cast<long long>(a) * m + t);
+        const double4 r0 = *reinterpret_cast<const double4*>(rs + a * 8);
+        const double4 r1 = *reinterpret_cast<const double4*>(rs + a * 8 + 4);
+        acc[0] = fma(x, r0.x, acc[0]);
+        acc[1] = fma(x, r0.y, acc[1]);
+        acc[2] = fma(x, r0.z, acc[2]);
+        acc[3] = fma(x, r0.w, acc[3]);
+        acc[4] = fma(x, r1.x, acc[4]);
+        acc[5] = fma(x, r1.y, acc[5]);
+        acc[6] = fma(x, r1.z, acc[6]);
+        acc[7] = fma(x, r1.w, acc[7]);
+      }
+      const double lam = A.lam[pos * m + t];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) hs[t * 8 + c] = 0.0;
+#pragma unroll
+      for (int st = 0; st < 8 / NT; ++st) {
+        if (st >= A.S) break;
+        double b4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < NT; ++i) b4[i] = acc[st * NT + i];
+        small_solve(A.TM, A.TA, lam, NT, b4);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) hs[t * 8 + st * NT + i] = b4[i];
+      }
+    }
+    __syncthreads();
+    if (t < m) {
+      double acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+      const double* xr = X + static_cast<long long>(t) * m;
+      for (int e = 0; e < m; ++e) {
+        const double x = __ldg(xr + e);
+        const double4 h0 = *reinterpret_cast<const double4*>(hs + e * 8);
+        const double4 h1 = *reinterpret_cast<const double4*>(hs + e * 8 + 4);
+        acc[0] = fma(x, h0.x, acc[0]);
+        acc[1] = fma(x, h0.y, acc[1]);
+        acc[2] = fma(x, h0.z, acc[2]);
+        acc[3] = fma(x, h0.w, acc[3]);
+        acc[4] = fma(x, h1.x, acc[4]);
+        acc[5] = fma(x, h1.y, acc[5]);
+        acc[6] = fma(x, h1.z, acc[6]);
+        acc[7] = fma(x, h1.w, acc[7]);
+      }
+      const double w = scale / d.mult;
+      for (int c = 0; c < ncol; ++c) {
+        const double v = d.bdry ? rs[t * 8 + c] : acc[c];
+        atomicAdd(z + static_cast<long long>(c) * A.n_space + d.g, v * w);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Dirichlet dofs of every cell matrix pair: M rows/cols -> identity, A -> 0
+// (the decoupled identity rows of asm_smoother.cpp:29-33 in the eigenbasis)
+__global__ void dirichlet_rows_kernel(const __grid_constant__ DevASM A, double* __restrict__ Mt,
+                                      double* __restrict__ At) {
+  const int m = A.m;
+  const long long total = A.n_list * m;
+  for (long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x; tt < total;
+       tt += (long long)gridDim.x * blockDim.x) {
+    const long long pos = tt / m;
+    const int a = static_cast<int>(tt - pos * m);
+    const long long cell = A.list ? A.list[pos] : pos;
+    long long cx, cy, cz;
+    cell_coords(cell, A.cells, cx, cy, cz);
+    if (!local_dof(A, cx, cy, cz, a).bdry) continue;
+    double* Mc = Mt + pos * static_cast<long long>(m) * m;
+    double* Ac = At + pos * static_cast<long long>(m) * m;
+    for (int j = 0; j < m; ++j) {
+      Mc[static_cast<long long>(a) * m + j] = (j == a) ? 1.0 : 0.0;
+      Mc[static_cast<long long>(j) * m + a] = (j == a) ? 1.0 : 0.0;
+      Ac[static_cast<long long>(a) * m + j] = 0.0;
+      Ac[static_cast<long long>(j) * m + a] = 0.0;
+    }
+  }
+}
+
+// column-major X (cuSOLVER / cuBLAS) -> row-major records
+__global__ void transpose_cells_kernel(int m, long long n_cells, long long xs, const double* __restrict__ colmajor,
+                                       double* __restrict__ X) {
+  const long long total = n_cells * m * m;
+  for (long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x; tt < total;
+       tt += (long long)gridDim.x * blockDim.x) {
+    const long long cell = tt / (static_cast<long long>(m) * m);
+    const long long r = tt - cell * m * m;
+    const int a = static_cast<int>(r / m), e = static_cast<int>(r % m);
+    X[cell * xs + r] = colmajor[cell * static_cast<long long>(m) * m + static_cast<long long>(e) * m + a];
+  }
+}
+
 // column b of every cell matrix from one probe of colour (cx,cy,cz) mod period
 __global__ void extract_probe_kernel(const __grid_constant__ DevASM A, int colx, int coly, int colz, int period,
                                      const double* __restrict__ probe, int probe_zcells,
@@ -887,11 +1013,38 @@ void launch_asm_fd64(const DevASM& A, const double* r, double* z, double scale, 
     default: launch_asm_mma(A, r, z, scale, s);
   }
 }
+
+template <int NT>
+void launch_large(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  if (A.n_list == 0) return;
+  const size_t smem = sizeof(double) * 16 * 128;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long grid = std::max<long long>(1, std::min<long long>(A.n_list, 16LL * sms));
+  count_launch();
+  asm_apply_large_kernel<NT><<<static_cast<unsigned>(grid), 128, smem, s>>>(A, r, z, scale);
+}
+void launch_asm_large(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  if (A.m > 128) throw std::invalid_argument("ASMSmoother: cell blocks larger than 128 dofs are not supported");
+  if (A.S * A.nt > 8) throw std::invalid_argument("ASMSmoother: S * n_t must be <= 8");
+  switch (A.nt) {
+    case 1: launch_large<1>(A, r, z, scale, s); break;
+    case 2: launch_large<2>(A, r, z, scale, s); break;
+    case 3: launch_large<3>(A, r, z, scale, s); break;
+    case 4: launch_large<4>(A, r, z, scale, s); break;
+    default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
+  }
+}
 }  // namespace
 
 void asm_add_correction(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if (A.m == 64 && A.tdiag && A.meta) {
     launch_asm_fd64(A, r, z, scale, s);
+    return;
+  }
+  if (A.m > 64) {
+    launch_asm_large(A, r, z, scale, s);
     return;
   }
   switch (A.m) {
@@ -927,6 +1080,22 @@ void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s
   }
   count_launch();
   reduce_standard_kernel<<<static_cast<unsigned>(n_cells), threads, smem, s>>>(A, Mt, At);
+}
+
+void asm_dirichlet_rows(const DevASM& A, double* Mt, double* At, cudaStream_t s) {
+  const long long total = A.n_list * A.m;
+  if (total == 0) return;
+  count_launch();
+  dirichlet_rows_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((total + 127) / 128, 148LL * 32))),
+                          128, 0, s>>>(A, Mt, At);
+}
+
+void asm_transpose_cells(int m, long long n_cells, long long xs, const double* colmajor, double* X, cudaStream_t s) {
+  const long long total = n_cells * m * m;
+  if (total == 0) return;
+  count_launch();
+  transpose_cells_kernel<<<static_cast<unsigned>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 148LL * 64))),
+                           256, 0, s>>>(m, n_cells, xs, colmajor, X);
 }
 
 void asm_back_transform(int m, long long xs, long long n_cells, const double* Linv, const double* V, double* X,

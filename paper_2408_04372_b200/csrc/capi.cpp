@@ -4,6 +4,7 @@
 #include "../../include/stmg_b200.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -490,6 +491,41 @@ int stmg_solve_host(const stmg_multigrid* mg, int precondition, const double* h_
 }  // extern "C"
 
 extern "C" {
+
+int stmg_st_operator_error_norms(const stmg_st_operator* op, const double* d_x, const double* d_u0, double frequency,
+                                 double t0, double out[3]) {
+  return guard([&] {
+    if (!op || !d_x || !d_u0 || !out) throw std::invalid_argument("stmg_st_operator_error_norms: null argument");
+    ErrorRecord acc;
+    accumulate_errors(*op->op, d_x, d_u0, frequency, t0, acc, nullptr);
+    out[0] = std::sqrt(acc.l2_l2);
+    out[1] = acc.linf_l2;
+    out[2] = acc.linf_linf;
+  });
+}
+
+int stmg_march(const stmg_multigrid* mg, int n_batches, int source_kind, double frequency, double* d_u, double* d_v,
+               const stmg_gmres_options* options, int* iterations, double errors[3], void* stream) {
+  bool converged = true;
+  const int rc = guard([&] {
+    if (!mg || !d_u || !iterations) throw std::invalid_argument("stmg_march: null argument");
+    const MarchResult r = march(*mg->mg, n_batches, source_kind, frequency, d_u, d_v, gopts(options),
+                                errors != nullptr, st(stream));
+    for (int b = 0; b < n_batches; ++b)
+      iterations[b] = b < static_cast<int>(r.iterations.size()) ? r.iterations[static_cast<size_t>(b)] : 0;
+    if (errors) {
+      errors[0] = r.error_u.l2_l2;
+      errors[1] = r.error_u.linf_l2;
+      errors[2] = r.error_u.linf_linf;
+    }
+    converged = r.converged;
+  });
+  if (rc == 0 && !converged) {
+    g_err = "stmg_march: a batch did not converge";
+    return -2;
+  }
+  return rc;
+}
 
 int stmg_nccl_unique_id(char id[128]) {
   return guard_host([&] {

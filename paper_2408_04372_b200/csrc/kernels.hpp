@@ -19,6 +19,12 @@ void st_residual(const DevLevel& L, const double* f, const double* u, double* r,
 void interpolate_nodes(const DevLevel& L, int kind, double omega, double t, const double* centre, double width,
                        bool zero_boundary, double* out, cudaStream_t s);
 
+// error sample against the manufactured solution (rhs.cu; kind 3 u, 4 v) at
+// the n_q^d Gauss points (qx, qw on [0,1], n_q <= 8) of every cell:
+// out[0] += sum w |J| (u_h - u)^2, out[1] = max(out[1], max |u_h - u|)
+void spatial_error(const DevLevel& L, const double* u, int n_q, const double* qx, const double* qw, int kind,
+                   double omega, double t, double* out, cudaStream_t s);
+
 // ---- z-slab partition helpers (slab.cu)
 // v[f * fstride + plane * plane_len + i] = val for every field f < F, i < plane_len
 void plane_fill(double* v, int F, long long fstride, long long plane, long long plane_len, double val, cudaStream_t s);
@@ -159,6 +165,10 @@ void asm_extract_probe(const DevASM& A, int colour_x, int colour_y, int colour_z
 void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s);  // At <- L^-1 At L^-T, Mt <- L^-1
 void asm_back_transform(int m, long long xs, long long n_cells, const double* Linv, const double* V, double* X,
                         cudaStream_t s);
+// large blocks (m > 64): Dirichlet rows/cols of the cell matrices (M identity,
+// A zero) and column-major -> row-major X records
+void asm_dirichlet_rows(const DevASM& A, double* Mt, double* At, cudaStream_t s);
+void asm_transpose_cells(int m, long long n_cells, long long xs, const double* colmajor, double* X, cudaStream_t s);
 
 }  // namespace stmgb
 

@@ -314,6 +314,29 @@ void SpaceTimeOperator::extract_final(const double* u, const double* u0, const d
   cuda_check(cudaStreamSynchronize(s), "extract_final");
 }
 
+void SpaceTimeOperator::value_at(const double* u, const double* u0, int step, double t_ref, double* out,
+                                 cudaStream_t s) const {
+  if (step < 0 || step >= n_steps_) throw std::invalid_argument("value_at: bad step");
+  const int nt = weights_.n_t;
+  const Index nx = n_space();
+  vec_fill(out, 0.0, nx, s);
+  for (int i = 0; i < nt; ++i) vec_axpy(out, weights_.unknown_weight(i, t_ref), u + block_offset(step, i), nx, s);
+  const double lw = weights_.left_weight(t_ref);
+  if (lw != 0.0) vec_axpy(out, lw, step == 0 ? u0 : u + block_offset(step - 1, nt - 1), nx, s);
+}
+
+std::pair<double, double> SpaceTimeOperator::spatial_error(const double* field, int kind, double frequency, double t,
+                                                           cudaStream_t s) const {
+  const Rule q = gauss(p_ + 2);
+  DeviceBuffer acc(2 * sizeof(double));
+  cuda_check(cudaMemsetAsync(acc.raw(), 0, 2 * sizeof(double), s), "error acc");
+  ::stmgb::spatial_error(desc_, field, p_ + 2, q.x.data(), q.w.data(), kind, 2.0 * M_PI * frequency, t, acc.d(), s);
+  double h[2];
+  cuda_check(cudaMemcpyAsync(h, acc.raw(), sizeof(h), cudaMemcpyDeviceToHost, s), "error result");
+  cuda_check(cudaStreamSynchronize(s), "error sync");
+  return {h[0], h[1]};
+}
+
 void SpaceTimeOperator::zero_boundary_field(double* v, cudaStream_t s) const {
   // Dirichlet entries of one spatial field set to zero: the identity rows of
   // the boundary pass applied to (f = v, u = v) give v_b - v_b = 0
@@ -639,8 +662,8 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
         if (!uniform) exact_cells.push_back(c);
       }
       if (!exact_cells.empty()) {
-        if (A.m > 64) {
-          exact_cells.clear();  // no exact kernel for (p+1)^3 > 64: FDM with the cell's own rho
+        if (A.m > 128) {
+          exact_cells.clear();  // no exact kernel beyond 128 dofs: FDM with the cell's own rho
           exact_ = false;
         } else {
           for (long long c : exact_cells) skip[static_cast<size_t>(c)] = 1;
@@ -658,8 +681,8 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
     A.list = static_cast<const long long*>(list_.raw());
     A.n_list = static_cast<long long>(exact_cells.size());
   } else {
-    if (A.m > 64)
-      throw std::invalid_argument("ASMSmoother: exact cell blocks on deformed meshes need (p+1)^dim <= 64");
+    if (A.m > 128)
+      throw std::invalid_argument("ASMSmoother: exact cell blocks on deformed meshes need (p+1)^dim <= 128");
     A.list = nullptr;
     A.n_list = n_cells;
   }
@@ -696,6 +719,10 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperat
         pop.spatial_apply(1, ind.d(), probe.d(), s);
         asm_extract_probe(A, cx, cy, cz, P, probe.d(), probe_zcells, cellA.d(), s);
       }
+  if (A.m > 64) {
+    build_exact_large(cellM, cellA, s);
+    return;
+  }
   // standard form C = L^-1 A L^-T (into cellA), L^-1 (into cellM)
   asm_reduce_standard(A, cellM.d(), cellA.d(), s);
   cuda_check(cudaGetLastError(), "asm setup kernels");
@@ -767,6 +794,96 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperat
     temporal_block_diagonalise(A);
   }
   cuda_check(cudaStreamSynchronize(s), "asm setup");
+  A.X = X_.d();
+  A.lam = lam_.d();
+}
+
+// Large cell blocks (m > 64): the same fast diagonalisation with library
+// factorisations on the probed matrices -- batched Cholesky M = L L^T,
+// C = L^-1 A L^-T by two batched triangular solves, batched syev, and the
+// back transform X = L^-T V by a third -- in chunks that bound the
+// eigensolver workspace.
+void ASMSmoother::build_exact_large(DeviceBuffer& cellM, DeviceBuffer& cellA, cudaStream_t s) {
+  DevASM& A = asm_;
+  const Index n_pos = A.n_list;
+  const int m = A.m;
+  const long long mm = static_cast<long long>(m) * m;
+  asm_dirichlet_rows(A, cellM.d(), cellA.d(), s);
+  lam_.allocate(sizeof(double) * static_cast<size_t>(n_pos) * m);
+  A.xs = mm;
+  X_.allocate(sizeof(double) * static_cast<size_t>(n_pos) * mm);
+  cusolverDnHandle_t h = nullptr;
+  cusolverDnParams_t prm = nullptr;
+  cublasHandle_t bh = nullptr;
+  solver_check(cusolverDnCreate(&h), "cusolverDnCreate");
+  solver_check(cusolverDnCreateParams(&prm), "cusolverDnCreateParams");
+  solver_check(cusolverDnSetStream(h, s), "cusolverDnSetStream");
+  if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) throw std::runtime_error("cublasCreate failed");
+  cublasSetStream(bh, s);
+  auto blas = [](cublasStatus_t st, const char* what) {
+    if (st != CUBLAS_STATUS_SUCCESS) throw std::runtime_error(std::string("cuBLAS ") + what + " failed");
+  };
+  // chunk so the batched eigensolver workspace stays below ~2 GB
+  size_t dws1 = 0, hws = 0;
+  solver_check(cusolverDnXsyevBatched_bufferSize(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
+                                                 CUDA_R_64F, cellA.raw(), m, CUDA_R_64F, lam_.raw(), CUDA_R_64F, &dws1,
+                                                 &hws, 1),
+               "syevBatched_bufferSize");
+  const Index chunk = std::max<Index>(1, std::min<Index>(n_pos, static_cast<Index>((size_t{2} << 30) / std::max<size_t>(dws1, 1))));
+  size_t dws = 0;
+  solver_check(cusolverDnXsyevBatched_bufferSize(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m,
+                                                 CUDA_R_64F, cellA.raw(), m, CUDA_R_64F, lam_.raw(), CUDA_R_64F, &dws,
+                                                 &hws, chunk),
+               "syevBatched_bufferSize");
+  DeviceBuffer dwork(std::max<size_t>(dws, 8)), info(sizeof(int) * static_cast<size_t>(chunk)),
+      pm(sizeof(double*) * static_cast<size_t>(chunk)), pa(sizeof(double*) * static_cast<size_t>(chunk));
+  std::vector<char> hwork(std::max<size_t>(hws, 8));
+  std::vector<int> hinfo(static_cast<size_t>(chunk));
+  std::vector<double*> hm(static_cast<size_t>(chunk)), ha(static_cast<size_t>(chunk));
+  const double one = 1.0;
+  for (Index c0 = 0; c0 < n_pos; c0 += chunk) {
+    const Index nb = std::min<Index>(chunk, n_pos - c0);
+    for (Index i = 0; i < nb; ++i) {
+      hm[static_cast<size_t>(i)] = cellM.d() + (c0 + i) * mm;
+      ha[static_cast<size_t>(i)] = cellA.d() + (c0 + i) * mm;
+    }
+    cuda_check(cudaMemcpyAsync(pm.raw(), hm.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, s), "ptrs");
+    cuda_check(cudaMemcpyAsync(pa.raw(), ha.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, s), "ptrs");
+    double** Mp = static_cast<double**>(pm.raw());
+    double** Ap = static_cast<double**>(pa.raw());
+    solver_check(cusolverDnDpotrfBatched(h, CUBLAS_FILL_MODE_LOWER, m, Mp, m, static_cast<int*>(info.raw()),
+                                         static_cast<int>(nb)),
+                 "potrfBatched");
+    cuda_check(cudaMemcpyAsync(hinfo.data(), info.raw(), sizeof(int) * nb, cudaMemcpyDeviceToHost, s), "info");
+    cuda_check(cudaStreamSynchronize(s), "potrf");
+    for (Index i = 0; i < nb; ++i)
+      if (hinfo[static_cast<size_t>(i)] != 0) throw std::runtime_error("ASMSmoother: cell mass matrix not SPD");
+    blas(cublasDtrsmBatched(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, m,
+                            &one, Mp, m, Ap, m, static_cast<int>(nb)),
+         "trsm L^-1 A");
+    blas(cublasDtrsmBatched(bh, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, m,
+                            &one, Mp, m, Ap, m, static_cast<int>(nb)),
+         "trsm A L^-T");
+    solver_check(cusolverDnXsyevBatched(h, prm, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, CUDA_R_64F,
+                                        cellA.d() + c0 * mm, m, CUDA_R_64F, lam_.d() + c0 * m, CUDA_R_64F,
+                                        dwork.raw(), dws, hwork.data(), hws, static_cast<int*>(info.raw()), nb),
+                 "syevBatched");
+    cuda_check(cudaMemcpyAsync(hinfo.data(), info.raw(), sizeof(int) * nb, cudaMemcpyDeviceToHost, s), "info");
+    cuda_check(cudaStreamSynchronize(s), "syev");
+    for (Index i = 0; i < nb; ++i)
+      if (hinfo[static_cast<size_t>(i)] != 0)
+        throw std::runtime_error("ASMSmoother: singular block (eigensolver info " +
+                                 std::to_string(hinfo[static_cast<size_t>(i)]) + ")");
+    // X = L^-T V (V column-major in cellA)
+    blas(cublasDtrsmBatched(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, m, m,
+                            &one, Mp, m, Ap, m, static_cast<int>(nb)),
+         "trsm L^-T V");
+    asm_transpose_cells(m, nb, mm, cellA.d() + c0 * mm, X_.d() + c0 * mm, s);
+  }
+  cuda_check(cudaStreamSynchronize(s), "asm large setup");
+  cublasDestroy(bh);
+  cusolverDnDestroyParams(prm);
+  cusolverDnDestroy(h);
   A.X = X_.d();
   A.lam = lam_.d();
 }
@@ -1227,6 +1344,60 @@ std::vector<std::pair<double, double>> eigenvalues_small(std::vector<double> a, 
     }
   }
   return ev;
+}
+
+// ------------------------------------------------------- march / errors
+void accumulate_errors(const SpaceTimeOperator& op, const double* x, const double* u0, double frequency, double t0,
+                       ErrorRecord& acc, cudaStream_t s) {
+  const Rule tq = gauss(op.weights().k + 2);
+  DeviceBuffer uval(sizeof(double) * op.n_space());
+  for (int st = 0; st < op.n_steps(); ++st)
+    for (size_t q = 0; q < tq.x.size(); ++q) {
+      const double t = t0 + (st + tq.x[q]) * op.tau();
+      op.value_at(x, u0, st, tq.x[q], uval.d(), s);
+      const auto e = op.spatial_error(uval.d(), 3, frequency, t, s);
+      acc.l2_l2 += tq.w[q] * op.tau() * e.first;
+      acc.linf_l2 = std::max(acc.linf_l2, std::sqrt(e.first));
+      acc.linf_linf = std::max(acc.linf_linf, e.second);
+    }
+}
+
+MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, double frequency, double* u, double* v,
+                  const GmresOptions& options, bool errors, cudaStream_t s) {
+  const SpaceTimeOperator& op = mg.fine_operator();
+  const bool wave = op.equation() == Equation::Wave;
+  if (n_batches < 1) throw std::invalid_argument("march: n_batches must be >= 1");
+  if (wave && !v) throw std::invalid_argument("march: the wave equation needs the initial velocity");
+  const Index nx = op.n_space(), n = op.n_dofs();
+  // homogeneous Dirichlet convention of the entering state (driver.cpp:158-166)
+  op.zero_boundary_field(u, s);
+  if (wave) op.zero_boundary_field(v, s);
+  DeviceBuffer rhs(sizeof(double) * n), x(sizeof(double) * n), uf(sizeof(double) * nx), vf(sizeof(double) * nx);
+  GmresWorkspace ws;
+  MarchResult res;
+  ErrorRecord acc;
+  for (int b = 0; b < n_batches; ++b) {
+    const double t0 = static_cast<double>(b) * op.n_steps() * op.tau();
+    op.assemble_rhs(source_kind, frequency, t0, u, v, rhs.d(), s);
+    vec_fill(x.d(), 0.0, n, s);
+    const GmresResult r = gmres([&op](const double* in, double* out, cudaStream_t st) { op.apply(in, out, st); },
+                                rhs.d(), x.d(), n, options,
+                                [&mg](const double* in, double* out, cudaStream_t st) { mg.apply(in, out, st); }, ws, s);
+    res.iterations.push_back(r.iterations);
+    res.final_residuals.push_back(r.final_residual);
+    if (!r.converged) {
+      res.converged = false;
+      break;
+    }
+    if (errors) accumulate_errors(op, x.d(), u, frequency, t0, acc, s);
+    op.extract_final(x.d(), u, v, uf.d(), wave ? vf.d() : nullptr, s);
+    vec_copy(u, uf.d(), nx, s);
+    if (wave) vec_copy(v, vf.d(), nx, s);
+  }
+  cuda_check(cudaStreamSynchronize(s), "march");
+  res.error_u = acc;
+  res.error_u.l2_l2 = std::sqrt(acc.l2_l2);
+  return res;
 }
 
 // ---------------------------------------------------- SpaceTimeMultigrid

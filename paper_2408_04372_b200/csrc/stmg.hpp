@@ -88,6 +88,15 @@ class SpaceTimeOperator {
   void extract_final(const double* u, const double* u0, const double* v0, double* uf, double* vf,
                      cudaStream_t stream = nullptr) const;
   void zero_boundary_field(double* v, cudaStream_t stream = nullptr) const;
+  // value_at (space_time_operator.cpp:250-266): the discrete trajectory of
+  // step `step` at reference time t_ref, entering state u0 (n_space)
+  void value_at(const double* u, const double* u0, int step, double t_ref, double* out,
+                cudaStream_t stream = nullptr) const;
+  // sample_spatial_error (spatial_operator.cpp:526-557) of a nodal field
+  // against the manufactured solution (kind 3: u, 4: v) at time t with the
+  // (p+2)^d Gauss rule: {sum w |J| e^2, max |e|}
+  std::pair<double, double> spatial_error(const double* field, int kind, double frequency, double t,
+                                          cudaStream_t stream = nullptr) const;
   long applications() const { return apply_count_; }
 
  private:
@@ -131,6 +140,7 @@ class ASMSmoother {
 
  private:
   void build_exact(const SpaceTimeOperator& op, const SpaceTimeOperator* probe_op, int probe_zcells);
+  void build_exact_large(DeviceBuffer& cellM, DeviceBuffer& cellA, cudaStream_t s);
   const SpaceTimeOperator* op_;
   DevASM asm_{};
   DevFDM fdm_{};
@@ -228,6 +238,32 @@ struct DotPolicy {
 GmresResult gmres(const DeviceMap& op, const double* b, double* x, Index n, const GmresOptions& options,
                   const DeviceMap& precond, GmresWorkspace& ws, cudaStream_t stream = nullptr,
                   const DotPolicy* dots = nullptr);
+
+// error norms over time slabs (driver.hpp:49-52, driver.cpp:18-43):
+// accumulate with accumulate_errors, then l2_l2 = sqrt(sum)
+struct ErrorRecord {
+  double l2_l2 = 0.0, linf_l2 = 0.0, linf_linf = 0.0;
+};
+// accumulate_errors (driver.cpp:27-43): temporal Gauss (k+2) x spatial Gauss
+// (p+2) sample of one batch solution x entering from u0 against the
+// manufactured solution of frequency f; acc.l2_l2 holds the squared sum
+void accumulate_errors(const SpaceTimeOperator& op, const double* x, const double* u0, double frequency, double t0,
+                       ErrorRecord& acc, cudaStream_t stream = nullptr);
+
+class SpaceTimeMultigrid;
+// march (driver.cpp:95-260) with every slab on the device: per batch
+// assemble_rhs -> STMG-preconditioned GMRES -> (errors) -> extract_final.
+// u (and v for the wave equation) hold the entering state on input (device,
+// n_space each; Dirichlet entries are zeroed first) and the final state on
+// output.
+struct MarchResult {
+  std::vector<int> iterations;
+  std::vector<double> final_residuals;
+  bool converged = true;
+  ErrorRecord error_u;  // finished (l2_l2 = sqrt of the sum)
+};
+MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, double frequency, double* u, double* v,
+                  const GmresOptions& options, bool errors, cudaStream_t stream = nullptr);
 
 class SpaceTimeMultigrid {
  public:

@@ -87,6 +87,10 @@ SIGNATURES = [
                              C.POINTER(GmresResult), c_double_p, C.c_int, C.c_void_p]),
     ("stmg_solve_host", C.c_int, [C.c_void_p, C.c_int, c_double_p, c_double_p, C.POINTER(GmresOptions),
                                   C.POINTER(GmresResult), c_double_p, C.c_int]),
+    ("stmg_st_operator_error_norms", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                               c_double_p]),
+    ("stmg_march", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
+                             C.POINTER(GmresOptions), c_int_p, c_double_p, C.c_void_p]),
     # z-slab partitioned solve
     ("stmg_nccl_unique_id", C.c_int, [C.c_char_p]),
     ("stmg_comm_create", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_void_p]),

@@ -411,6 +411,7 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": dom["bytes"], "launch_ms": dom["ms"],
                 "share_of_step": dom["share_of_step"]}
     vm_ach = vmult_bytes / (t_vmult * 1e-3) / 1e9
+    vc_bytes = M.vcycle_bytes()
 
     line = {"metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -421,7 +422,9 @@ def run_ours(args):
             "roofline": roofline, "e2e": e2e, "gpu_launches": int(launches),
             "kernels": {"vmult_ms": t_vmult, "vmult_dofs_per_s": N / (t_vmult * 1e-3),
                         "vmult_hbm_frac": vm_ach / peak, "vcycle_ms": t_vcycle,
-                        "vcycle_dofs_per_s": N / (t_vcycle * 1e-3), "asm_fine_ms": t_asm},
+                        "vcycle_dofs_per_s": N / (t_vcycle * 1e-3),
+                        "vcycle_algorithmic_bytes": vc_bytes,
+                        "vcycle_hbm_frac": vc_bytes / (t_vcycle * 1e-3) / 1e9 / peak, "asm_fine_ms": t_asm},
             "setup_s": setup_s, "mg_levels": M.n_levels, "device_bytes": M.device_bytes()}
     line["clocks"] = clk.summary()
 

@@ -128,6 +128,9 @@ int stmg_multigrid_set_omega(stmg_multigrid* mg, int level, double omega);
    diagnostics): bit 0 tensor FDM, bit 1 per-cell eigenbasis, bit 2 temporal
    fast diagonalisation in the eigenbasis kernel; -1 on the coarsest level */
 int stmg_multigrid_smoother_kind(const stmg_multigrid* mg, int level);
+/* device bytes of the level-l smoother's per-cell data (eigenbases,
+ * eigenvalues, metadata), streamed once per sweep; -1 on the coarsest level */
+long long stmg_multigrid_smoother_bytes(const stmg_multigrid* mg, int level);
 const stmg_st_operator* stmg_multigrid_operator_at(const stmg_multigrid* mg, int level);
 /* apply (multigrid.cpp:228-234): one V-cycle, zero initial guess, overwrite d_z */
 int stmg_multigrid_apply(const stmg_multigrid* mg, const double* d_r, double* d_z, void* stream);

@@ -254,6 +254,25 @@ class SpaceTimeMultigrid:
         diagonalisation (-1: coarsest level, no smoother)."""
         return int(N.load().stmg_multigrid_smoother_kind(self._h, l))
 
+    def smoother_bytes(self, l: int) -> int:
+        """Bytes of per-cell smoother data streamed by one level-l sweep."""
+        return int(N.load().stmg_multigrid_smoother_bytes(self._h, l))
+
+    def vcycle_bytes(self, n_smooth: int = 1) -> int:
+        """Algorithmic HBM bytes of one V-cycle: per level l
+        with N_l dofs, 2 n_smooth smoother sweeps streaming the level's cell
+        data plus ~112 N_l bytes of vector traffic (smoother in/out, residual,
+        restriction, prolongation); the coarsest level's dense solve n_c^2."""
+        info = self.level_info()
+        total = 0
+        for l, li in enumerate(info):
+            n = li["n_dofs"]
+            if l + 1 < len(info):
+                total += 2 * n_smooth * max(self.smoother_bytes(l), 0) + 112 * n
+            else:
+                total += 8 * n * n
+        return total
+
     def omega_at(self, l: int) -> float:
         return self.level_info()[l]["omega"]
 

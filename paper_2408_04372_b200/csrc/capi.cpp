@@ -316,6 +316,10 @@ int stmg_multigrid_create(int equation, int scheme, const stmg_mesh* mesh, const
 }
 void stmg_multigrid_destroy(stmg_multigrid* mg) { delete mg; }
 int stmg_multigrid_n_levels(const stmg_multigrid* mg) { return mg ? mg->mg->n_levels() : -1; }
+long long stmg_multigrid_smoother_bytes(const stmg_multigrid* mg, int level) {
+  if (!mg || level < 0 || level + 1 >= mg->mg->n_levels()) return -1;
+  return static_cast<long long>(mg->mg->smoother_at(level).bytes());
+}
 int stmg_multigrid_smoother_kind(const stmg_multigrid* mg, int level) {
   if (!mg || level < 0 || level + 1 >= mg->mg->n_levels()) return -1;
   return mg->mg->smoother_at(level).kind();

@@ -72,6 +72,7 @@ SIGNATURES = [
     ("stmg_multigrid_level_info", C.c_int, [C.c_void_p, C.c_int, c_int_p, c_ll_p, c_double_p]),
     ("stmg_multigrid_set_omega", C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     ("stmg_multigrid_smoother_kind", C.c_int, [C.c_void_p, C.c_int]),
+    ("stmg_multigrid_smoother_bytes", C.c_longlong, [C.c_void_p, C.c_int]),
     ("stmg_multigrid_operator_at", C.c_void_p, [C.c_void_p, C.c_int]),
     ("stmg_multigrid_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("stmg_multigrid_apply_host", C.c_int, [C.c_void_p, c_double_p, c_double_p]),

@@ -225,8 +225,208 @@ __global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ Dev
   }
 }
 
+// 3D line-owner FDM solve (the st_lines.cuh pattern): a 128-thread CTA owns
+// NC cells, thread (c, a, b) owns lattice line (a, b) of cell c along the
+// axis the stage sweeps, for the n_t fields of one step at a time, in
+// registers. Per step: y-owner gathers r and applies S_y^T, x-owner S_x^T,
+// z-owner S_z^T + the n_t x n_t solves at its N eigen-points + S_z, x-owner
+// S_x, y-owner S_y and the weighted scatter (Dirichlet rows: w r, re-read).
+template <int N>
+struct FLay;
+template <>
+struct FLay<2> {
+  static constexpr int RY = 2, PZ = 5, SD = 10;
+};
+template <>
+struct FLay<3> {
+  static constexpr int RY = 3, PZ = 10, SD = 30;
+};
+template <>
+struct FLay<4> {
+  static constexpr int RY = 4, PZ = 19, SD = 74;
+};
+template <>
+struct FLay<5> {
+  static constexpr int RY = 5, PZ = 26, SD = 130;
+};
+
+template <int N, int NT>
+__global__ void __launch_bounds__(128) fdm_lines_kernel(const __grid_constant__ DevFDM P,
+                                                        const double* __restrict__ r, double* __restrict__ z,
+                                                        double scale) {
+  constexpr int NL = N * N, NC = 128 / NL, SD = FLay<N>::SD, RY = FLay<N>::RY, PZ = FLay<N>::PZ;
+  __shared__ double W[NC * NT * SD];
+  const int t = threadIdx.x;
+  const int c = t / NL, l = t - (t / NL) * NL;
+  const int a = l % N, b = l / N;
+  const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
+  const long long cell = static_cast<long long>(blockIdx.x) * NC + c;
+  const bool valid = c < NC && cell < n_cells && !(P.skip && P.skip[cell]);
+  const long long dx = P.dofs[0], dxy = P.dofs[0] * P.dofs[1];
+  constexpr int p = N - 1;
+  long long base = 0;
+  int mask = 0, tx = 0, ty = 0, tz = 0;
+  double rho = 1.0;
+  if (valid) {
+    const unsigned ci = static_cast<unsigned>(cell);
+    const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]),
+                   nz = static_cast<unsigned>(P.cells[2]);
+    const unsigned cx = ci % nx, cy = (ci / nx) % ny, cz = ci / (nx * ny);
+    base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx + static_cast<long long>(cx) * p;
+    tx = (cx == 0 ? 1 : 0) | (cx == nx - 1 ? 2 : 0);
+    ty = (cy == 0 ? 1 : 0) | (cy == ny - 1 ? 2 : 0);
+    tz = (cz == 0 && (P.zbc & 1) ? 1 : 0) | (cz == nz - 1 && (P.zbc & 2) ? 2 : 0);
+    mask = tx | (ty << 2) | (tz << 4);
+    if (P.rho0) {
+      const long long ax = cx >> P.rho_shift, ay = cy >> P.rho_shift, az = (cz + P.cz0) >> P.rho_shift;
+      rho = P.rho0[(az * P.cells0[1] + ay) * P.cells0[0] + ax];
+    }
+  }
+  auto bdry = [&](int lx, int ly, int lz) {
+    return ((mask & 1) && lx == 0) || ((mask & 2) && lx == p) || ((mask & 4) && ly == 0) || ((mask & 8) && ly == p) ||
+           ((mask & 16) && lz == 0) || ((mask & 32) && lz == p);
+  };
+  const int cb = c * NT * SD;
+  const int oy = cb + a + PZ * b, ox = cb + RY * a + PZ * b, oz = cb + a + RY * b;
+  const double(&Sx)[kMaxN][kMaxN] = P.S1[0][tx];
+  const double(&Sy)[kMaxN][kMaxN] = P.S1[1][ty];
+  const double(&Sz)[kMaxN][kMaxN] = P.S1[2][tz];
+  for (int st = 0; st < P.S; ++st) {
+    const double* rs = r + static_cast<long long>(st) * NT * P.n_space;
+    double* zs = z + static_cast<long long>(st) * NT * P.n_space;
+    // A: y-owner (x = a, z = b): gather, S_y^T
+    if (valid) {
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) in[k] = __ldg(rs + f * P.n_space + base + b * dxy + k * dx + a);
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc = fma(Sy[k][e], in[k], acc);
+          W[oy + f * SD + e * RY] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    // B: x-owner (y = a, z = b): S_x^T
+    if (valid) {
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) in[k] = W[ox + f * SD + k];
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc = fma(Sx[k][e], in[k], acc);
+          W[ox + f * SD + e] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    // C: z-owner (eigen-indices ex = a, ey = b): S_z^T, solves, S_z
+    if (valid) {
+      double v[NT][N];
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) in[k] = W[oz + f * SD + k * PZ];
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) acc = fma(Sz[k][e], in[k], acc);
+          v[f][e] = acc;
+        }
+      }
+      const double lxy = P.L1[0][tx][a] + P.L1[1][ty][b];
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        double bb[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int f = 0; f < NT; ++f) bb[f] = v[f][e];
+        solve_small(P.TM, P.TA, rho * (lxy + P.L1[2][tz][e]), NT, bb);
+#pragma unroll
+        for (int f = 0; f < NT; ++f) v[f][e] = bb[f];
+      }
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double acc = 0.0;
+#pragma unroll
+          for (int e = 0; e < N; ++e) acc = fma(Sz[k][e], v[f][e], acc);
+          W[oz + f * SD + k * PZ] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    // D: x-owner: S_x
+    if (valid) {
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) in[e] = W[ox + f * SD + e];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double acc = 0.0;
+#pragma unroll
+          for (int e = 0; e < N; ++e) acc = fma(Sx[k][e], in[e], acc);
+          W[ox + f * SD + k] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    // E: y-owner: S_y, weighted scatter (asm_smoother.cpp:45-49, 75)
+    if (valid) {
+      const double wxz = ((a == 0 && !(mask & 1)) || (a == p && !(mask & 2)) ? 0.5 : 1.0) *
+                         ((b == 0 && !(mask & 16)) || (b == p && !(mask & 32)) ? 0.5 : 1.0);
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) in[e] = W[oy + f * SD + e * RY];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const long long g = base + b * dxy + k * dx + a;
+          double val;
+          if (bdry(a, k, b)) {
+            val = __ldg(rs + f * P.n_space + g);
+          } else {
+            double acc = 0.0;
+#pragma unroll
+            for (int e = 0; e < N; ++e) acc = fma(Sy[k][e], in[e], acc);
+            val = acc;
+          }
+          const double wy = (k == 0 && !(mask & 4)) || (k == p && !(mask & 8)) ? 0.5 : 1.0;
+          atomicAdd(zs + f * P.n_space + g, scale * wxz * wy * val);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int N, int NT>
+void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
+  constexpr int NC = 128 / (N * N);
+  const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
+  count_launch();
+  fdm_lines_kernel<N, NT><<<static_cast<unsigned>((n_cells + NC - 1) / NC), 128, 0, s>>>(P, r, z, scale);
+}
+
 template <int DIM, int N, int NT>
 void launch(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
+  if (DIM == 3) {
+    launch_lines<N, NT>(P, r, z, scale, s);
+    return;
+  }
   using C = FCfg<DIM, N>;
   const size_t smem = sizeof(double) * (2 * C::NC * NT * C::ND + C::NC) + sizeof(long long) * C::NC + sizeof(int) * C::NC;
   static bool configured = false;

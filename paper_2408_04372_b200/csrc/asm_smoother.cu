@@ -141,154 +141,121 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Persistent, double-buffered block solver. Each CTA walks cells
-// blockIdx.x, blockIdx.x + gridDim.x, ...; the eigenbasis X of the next cell
-// streams into shared memory by a TMA bulk copy (cp.async.bulk + mbarrier)
-// while the current one is applied to all S steps of the slab:
-//   hat r = X^T r_T   (thread e owns eigen-index e; X rows read contiguously)
-//   hat z_e = (T_M + lam_e T_A)^-1 hat r_e
-//   z_T  = X hat z    (thread a owns local dof a; rotated column order keeps
-//                      the row-wise smem reads bank-conflict free)
-// and the weighted result is scatter-added into z (Dirichlet rows: r).
+// Small cell blocks (m <= 32: 2D Q1-Q4, 3D Q1-Q2): one WARP per cell, no
+// CTA barriers. Lane a < m owns local dof a. Per warp, shared memory holds
+// the cell's X (row-major, odd row stride, so row and column reads are both
+// conflict-free) and the residual / eigen-coefficient rows, read back as
+// warp-wide broadcasts:
+//   hat r = X^T r  (lane e: X row reads)
+//   hat z_e = (T_M + lam_e T_A)^-1 hat r_e per step (pivoted n_t x n_t solve)
+//   z = X hat z    (lane a: X column reads)
+// then the weighted scatter-add (Dirichlet rows: w r).
+// X block rounded up to 32 bytes so the row buffers (read as double4) and
+// every warp's slice stay 32-byte aligned
+template <int M>
+constexpr int warp_x_doubles() {
+  return (M * (M | 1) + 3) & ~3;
+}
+template <int M>
+constexpr int warp_smem_doubles() {
+  return warp_x_doubles<M>() + 16 * M;
+}
+
 template <int M, int NT>
-__global__ void __launch_bounds__(2 * (((M + 31) / 32) * 32)) asm_apply_tma_kernel(const __grid_constant__ DevASM A,
-                                                                             const double* __restrict__ r,
-                                                                             double* __restrict__ z, double scale) {
-  constexpr int XS = (M * M + 1) & ~1;       // per-cell stride in doubles (16 B multiple)
-  constexpr int ROT = (M % 2 == 0) ? 1 : 2;  // rotation: (M + ROT) odd -> conflict-free rows
-  constexpr int T2 = ((M + 31) / 32) * 32;   // threads per half; the two halves split every reduction
-  constexpr int HALF = M / 2;
-  extern __shared__ __align__(128) double sm[];
-  double* Xb0 = sm;
-  double* Xb1 = sm + XS;
-  double* rs = Xb1 + XS;         // [M][4]  residual of the block, dof-major
-  double* hs = rs + 4 * M;       // [M][4] hat z, eigen-index major
-  double* part = hs + 4 * M;     // [M][4] partial sums of the second half
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(part + 4 * M);
-  const long long n_cells = A.n_list;  // list positions (all cells when A.list == nullptr)
-  const int t = threadIdx.x;
-  const int h = t / T2, tl = t - h * T2;
-  // bulk copies move whole 16-byte granules: copy the padded per-cell stride
-  constexpr unsigned XBYTES = static_cast<unsigned>(XS * sizeof(double));
-  static_assert(XBYTES % 16 == 0, "TMA bulk copy size must be a multiple of 16 bytes");
-  if (t == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  long long cell = blockIdx.x;
-  if (t == 0 && cell < n_cells) {
-    mbar_expect_tx(&bar[0], XBYTES);
-    bulk_g2s(Xb0, A.X + cell * XS, XBYTES, &bar[0]);
-  }
-  unsigned ph0 = 0, ph1 = 0;
-  int buf = 0;
+__global__ void __launch_bounds__(256) asm_apply_warp_kernel(const __grid_constant__ DevASM A,
+                                                             const double* __restrict__ r, double* __restrict__ z,
+                                                             double scale) {
+  static_assert(M <= 32, "one lane per local dof");
+  constexpr int LD = M | 1, WS = warp_smem_doubles<M>();
+  extern __shared__ __align__(16) double wsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* X = wsm + warp * WS;
+  double* rb = X + warp_x_doubles<M>();  // [M][8]
+  double* hb = rb + 8 * M;  // [M][8]
+  const int ncol = A.S * NT;
+  const bool hi = ncol > 4;
   const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
-  for (; cell < n_cells; cell += gridDim.x) {
-    const long long next = cell + gridDim.x;
-    if (t == 0 && next < n_cells) {
-      fence_proxy_async();
-      double* dst = buf ? Xb0 : Xb1;
-      unsigned long long* b = &bar[buf ^ 1];
-      mbar_expect_tx(b, XBYTES);
-      bulk_g2s(dst, A.X + next * XS, XBYTES, b);
-    }
-    // per-thread local dof (overlaps with the copy in flight)
-    const unsigned cidx = static_cast<unsigned>(A.list ? A.list[cell] : cell);
-    const long long cx = cidx % cxn, cy = (cidx / cxn) % cyn, cz = cidx / (cxn * cyn);
+  const long long stride = static_cast<long long>(gridDim.x) * 8;
+  for (long long pos = static_cast<long long>(blockIdx.x) * 8 + warp; pos < A.n_list; pos += stride) {
+    const unsigned ci = static_cast<unsigned>(A.list ? A.list[pos] : pos);
     LocalDof d{};
-    double lam = 0.0;
-    if (tl < M) {
-      d = local_dof(A, cx, cy, cz, tl);
-      lam = A.lam[cell * M + tl];
-    }
-    if (buf == 0) {
-      mbar_wait(&bar[0], ph0);
-      ph0 ^= 1;
-    } else {
-      mbar_wait(&bar[1], ph1);
-      ph1 ^= 1;
-    }
-    const double* Xs = buf ? Xb1 : Xb0;
-    for (int s = 0; s < A.S; ++s) {
-      if (h == 0 && tl < M) {
+    double rr[8];
 #pragma unroll
-        for (int i = 0; i < NT; ++i) rs[tl * 4 + i] = r[(static_cast<long long>(s) * NT + i) * A.n_space + d.g];
-      }
-      __syncthreads();
-      // hat r = X^T r: thread (e = tl, half h) sums its half of the rows a
-      {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        if (tl < M) {
-          const int a0 = h ? HALF : 0, len = h ? M - HALF : HALF;
-          const double* xcol = Xs + a0 * M + tl;
-          const double* rrow = rs + a0 * 4;
-#pragma unroll 16
-          for (int a = 0; a < M - HALF; ++a) {
-            if (a >= len) break;
-            const double x = xcol[a * M];
-            const double2 r01 = *reinterpret_cast<const double2*>(rrow + a * 4);
-            acc[0] = fma(x, r01.x, acc[0]);
-            if (NT > 1) acc[1] = fma(x, r01.y, acc[1]);
-            if (NT > 2) {
-              const double2 r23 = *reinterpret_cast<const double2*>(rrow + a * 4 + 2);
-              acc[2] = fma(x, r23.x, acc[2]);
-              if (NT > 3) acc[3] = fma(x, r23.y, acc[3]);
-            }
-          }
-          if (h) *reinterpret_cast<double4*>(part + tl * 4) = make_double4(acc[0], acc[1], acc[2], acc[3]);
-        }
-        __syncthreads();
-        if (!h && tl < M) {
-          const double4 o = *reinterpret_cast<const double4*>(part + tl * 4);
-          double b4[4] = {acc[0] + o.x, acc[1] + o.y, acc[2] + o.z, acc[3] + o.w};
-          small_solve(A.TM, A.TA, lam, NT, b4);
-          *reinterpret_cast<double4*>(hs + tl * 4) = make_double4(b4[0], b4[1], b4[2], b4[3]);
-        }
-        __syncthreads();
-      }
-      // z_T = X hat z: thread (a = tl, half h) sums its half of the columns e,
-      // starting at a rotated offset (bank-conflict-free row reads)
-      {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        if (tl < M) {
-          const int e0 = h ? HALF : 0, len = h ? M - HALF : HALF;
-          int e = (ROT * tl) % len;
-          const double* xrow = Xs + tl * M + e0;
-          const double* hrow = hs + e0 * 4;
-#pragma unroll 16
-          for (int j = 0; j < M - HALF; ++j) {
-            if (j < len) {
-              const double x = xrow[e];
-              const double2 h01 = *reinterpret_cast<const double2*>(hrow + e * 4);
-              acc[0] = fma(x, h01.x, acc[0]);
-              if (NT > 1) acc[1] = fma(x, h01.y, acc[1]);
-              if (NT > 2) {
-                const double2 h23 = *reinterpret_cast<const double2*>(hrow + e * 4 + 2);
-                acc[2] = fma(x, h23.x, acc[2]);
-                if (NT > 3) acc[3] = fma(x, h23.y, acc[3]);
-              }
-              e = (e + 1 == len) ? 0 : e + 1;
-            }
-          }
-          if (h) *reinterpret_cast<double4*>(part + tl * 4) = make_double4(acc[0], acc[1], acc[2], acc[3]);
-        }
-        __syncthreads();
-        if (!h && tl < M) {
-          const double4 o = *reinterpret_cast<const double4*>(part + tl * 4);
-          const double sum[4] = {acc[0] + o.x, acc[1] + o.y, acc[2] + o.z, acc[3] + o.w};
-          const double w = scale / d.mult;
+    for (int c = 0; c < 8; ++c) rr[c] = 0.0;
+    const double* Xg = A.X + pos * A.xs;
+    for (int i = lane; i < M * M; i += 32) X[(i / M) * LD + (i % M)] = __ldg(Xg + i);
+    if (lane < M) {
+      d = local_dof(A, ci % cxn, (ci / cxn) % cyn, ci / (cxn * cyn), lane);
 #pragma unroll
-          for (int i = 0; i < NT; ++i) {
-            const double v = d.bdry ? rs[tl * 4 + i] : sum[i];
-            atomicAdd(z + (static_cast<long long>(s) * NT + i) * A.n_space + d.g, v * w);
-          }
-        }
-        __syncthreads();
-      }
+      for (int c = 0; c < 8; ++c)
+        if (c < ncol) rr[c] = __ldg(r + static_cast<long long>(c) * A.n_space + d.g);
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(rb + lane * 8 + c) = make_double2(rr[c], rr[c + 1]);
     }
-    buf ^= 1;
+    const double lam = lane < M ? __ldg(A.lam + pos * M + lane) : 0.0;
+    __syncwarp();
+    if (lane < M) {
+      // hat r (lane e)
+      double h[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) h[c] = 0.0;
+#pragma unroll 3
+      for (int a = 0; a < M; ++a) {
+        const double x = X[a * LD + lane];
+        const double4 r0 = *reinterpret_cast<const double4*>(rb + a * 8);
+        h[0] = fma(x, r0.x, h[0]);
+        h[1] = fma(x, r0.y, h[1]);
+        h[2] = fma(x, r0.z, h[2]);
+        h[3] = fma(x, r0.w, h[3]);
+        if (hi) {
+          const double4 r1 = *reinterpret_cast<const double4*>(rb + a * 8 + 4);
+          h[4] = fma(x, r1.x, h[4]);
+          h[5] = fma(x, r1.y, h[5]);
+          h[6] = fma(x, r1.z, h[6]);
+          h[7] = fma(x, r1.w, h[7]);
+        }
+      }
+#pragma unroll
+      for (int st = 0; st < 8 / NT; ++st) {
+        if (st >= A.S) break;
+        double b4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < NT; ++i) b4[i] = h[st * NT + i];
+        small_solve(A.TM, A.TA, lam, NT, b4);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) h[st * NT + i] = b4[i];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(hb + lane * 8 + c) = make_double2(h[c], h[c + 1]);
+    }
+    __syncwarp();
+    if (lane < M) {
+      // z (lane a)
+      double o[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) o[c] = 0.0;
+#pragma unroll 3
+      for (int e = 0; e < M; ++e) {
+        const double x = X[lane * LD + e];
+        const double4 h0 = *reinterpret_cast<const double4*>(hb + e * 8);
+        o[0] = fma(x, h0.x, o[0]);
+        o[1] = fma(x, h0.y, o[1]);
+        o[2] = fma(x, h0.z, o[2]);
+        o[3] = fma(x, h0.w, o[3]);
+        if (hi) {
+          const double4 h1 = *reinterpret_cast<const double4*>(hb + e * 8 + 4);
+          o[4] = fma(x, h1.x, o[4]);
+          o[5] = fma(x, h1.y, o[5]);
+          o[6] = fma(x, h1.z, o[6]);
+          o[7] = fma(x, h1.w, o[7]);
+        }
+      }
+      const double w = scale / d.mult;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < ncol) atomicAdd(z + static_cast<long long>(c) * A.n_space + d.g, (d.bdry ? rr[c] : o[c]) * w);
+    }
+    __syncwarp();
   }
 }
 
@@ -897,24 +864,23 @@ __global__ void back_transform_kernel(int m, long long xs, const double* __restr
 namespace {
 template <int M, int NT>
 void launch_asm(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
-  constexpr int XS = (M * M + 1) & ~1;
-  constexpr int T = 2 * (((M + 31) / 32) * 32);
-  const size_t smem = sizeof(double) * (2 * XS + 12 * M) + 2 * sizeof(unsigned long long);
+  if (A.n_list == 0) return;
+  if (A.S * NT > 8) throw std::invalid_argument("ASMSmoother: S * n_t must be <= 8");
+  constexpr size_t smem = sizeof(double) * 8 * warp_smem_doubles<M>();
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(asm_apply_tma_kernel<M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(asm_apply_warp_kernel<M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     configured = true;
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_tma_kernel<M, NT>, T, smem);
-  int dev = 0, sms = 148;
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_warp_kernel<M, NT>, 256, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long n_cells = A.n_list;
-  if (n_cells == 0) return;
-  const long long grid = std::max<long long>(1, std::min<long long>(n_cells, static_cast<long long>(std::max(per_sm, 1)) * sms));
+  const long long warps = (A.n_list + 7) / 8;
+  const long long grid = std::max<long long>(1, std::min<long long>(warps, static_cast<long long>(std::max(per_sm, 1)) * sms));
   count_launch();
-  asm_apply_tma_kernel<M, NT><<<static_cast<unsigned>(grid), T, smem, s>>>(A, r, z, scale);
+  asm_apply_warp_kernel<M, NT><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
 }
 template <int M>
 void launch_asm_nt(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {

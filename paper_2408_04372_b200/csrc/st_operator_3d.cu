@@ -1,6 +1,6 @@
 // 3D instantiations of the fused space-time operator: the line-owner kernel
 // (st_lines.cuh) wherever its registers and shared memory fit (N * F <= 16),
-// the general one-thread-per-sweep-line kernel (st_operator.cuh) otherwise.
+// its nodal-coupling, field-grouped variant (st_mix_kernel) otherwise.
 #include <stdexcept>
 
 #include "st_lines.cuh"
@@ -13,7 +13,7 @@ void launch_nf(const DevLevel& L, const double* u, double* y, double sign, cudaS
   if constexpr (stl::fits<N, F>())
     stl::launch<N, F>(L, u, y, sign, s);
   else
-    stk::launch<3, N, F>(L, u, y, sign, s);
+    stl::launch_mix<N, F>(L, u, y, sign, s);
 }
 template <int N>
 void launch_n(const DevLevel& L, const double* u, double* y, double sign, cudaStream_t s) {

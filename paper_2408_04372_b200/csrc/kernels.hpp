@@ -60,7 +60,7 @@ void vec_multidot(const double* const* V, int k, const double* w, long long n, d
 // w += sign * sum_i h_i V_i (h on device)
 void vec_multi_axpy(double* w, const double* const* V, int k, const double* h, double sign, long long n,
                     cudaStream_t s);
-constexpr int kDotBlocks = 296;
+constexpr int kDotBlocks = 592;
 void vec_fill(double* y, double v, long long n, cudaStream_t s);
 void vec_set_element(double* y, long long i, double v, cudaStream_t s);
 // y[g] = 1 where every lattice coordinate of g is congruent to colour (mod period)

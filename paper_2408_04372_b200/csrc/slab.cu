@@ -64,20 +64,22 @@ __global__ void plane_unpack_add_kernel(double* __restrict__ v, long long fstrid
 
 // partial dots over the owned segments, up to 8 basis vectors per group,
 // fixed grid and fixed-order second stage (reproducible)
-constexpr int kDotGrid = 296;
+constexpr int kDotGrid = 592;
 template <int G>
 __global__ void multidot_seg_kernel(const double* const* __restrict__ V, int i0, int k, const double* __restrict__ w,
                                     const DotSegments seg, double* __restrict__ partial) {
+  const double* vp[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) vp[g] = (i0 + g < k) ? V[i0 + g] : w;
   double acc[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) acc[g] = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (int sg = 0; sg < seg.n; ++sg) {
     for (long long j = seg.begin[sg] + blockIdx.x * (long long)blockDim.x + threadIdx.x; j < seg.end[sg]; j += stride) {
-      const double wj = w[j];
+      const double wj = __ldg(w + j);
 #pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (i0 + g < k) acc[g] = fma(V[i0 + g][j], wj, acc[g]);
+      for (int g = 0; g < G; ++g) acc[g] = fma(__ldg(vp[g] + j), wj, acc[g]);
     }
   }
   __shared__ double red[G][kT / 32];

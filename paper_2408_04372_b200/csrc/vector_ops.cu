@@ -44,18 +44,47 @@ __global__ void sub_into_kernel(double* __restrict__ r, const double* __restrict
     r[i] = f[i] - y[i];
 }
 
-// partial dots of up to 8 basis vectors per launch group
+// partial dots of up to G basis vectors per launch group: the G vector
+// pointers are read once, the inner loop streams w and the vectors as
+// 16-byte pairs (scalar path if any pointer is not 16-byte aligned)
 template <int G>
-__global__ void multidot_partial_kernel(const double* const* __restrict__ V, int i0, int k,
-                                        const double* __restrict__ w, long long n, double* __restrict__ partial) {
+__global__ void __launch_bounds__(kThreads) multidot_partial_kernel(const double* const* __restrict__ V, int i0, int k,
+                                                                    const double* __restrict__ w, long long n,
+                                                                    double* __restrict__ partial) {
+  const double* vp[G];
+  unsigned long long al = reinterpret_cast<unsigned long long>(w);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    vp[g] = (i0 + g < k) ? V[i0 + g] : w;
+    al |= reinterpret_cast<unsigned long long>(vp[g]);
+  }
   double acc[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) acc[g] = 0.0;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
-    const double wj = w[j];
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if ((al & 15) == 0) {
+    const long long n2 = n / 2;
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    for (long long j = tid; j < n2; j += stride) {
+      const double2 wj = __ldg(w2 + j);
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (i0 + g < k) acc[g] = fma(V[i0 + g][j], wj, acc[g]);
+      for (int g = 0; g < G; ++g) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(vp[g]) + j);
+        acc[g] = fma(v.x, wj.x, fma(v.y, wj.y, acc[g]));
+      }
+    }
+    if ((n & 1) && tid == 0) {
+      const double wj = w[n - 1];
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g] = fma(vp[g][n - 1], wj, acc[g]);
+    }
+  } else {
+    for (long long j = tid; j < n; j += stride) {
+      const double wj = w[j];
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g] = fma(vp[g][j], wj, acc[g]);
+    }
   }
   __shared__ double red[G][kThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -67,9 +96,9 @@ __global__ void multidot_partial_kernel(const double* const* __restrict__ V, int
   }
   __syncthreads();
   if (threadIdx.x < G && i0 + threadIdx.x < k) {
-    double s = 0.0;
-    for (int i = 0; i < kThreads / 32; ++i) s += red[threadIdx.x][i];
-    partial[static_cast<long long>(i0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
+    double sum = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) sum += red[threadIdx.x][i];
+    partial[static_cast<long long>(i0 + threadIdx.x) * gridDim.x + blockIdx.x] = sum;
   }
 }
 
@@ -87,15 +116,42 @@ __global__ void multi_axpy_kernel(double* __restrict__ w, const double* const* _
                                   const double* __restrict__ h, double sign, long long n) {
   extern __shared__ double hs[];
   const double** vp = reinterpret_cast<const double**>(hs + k);
+  unsigned long long al = reinterpret_cast<unsigned long long>(w);
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     hs[i] = h[i];
     vp[i] = V[i];
   }
   __syncthreads();
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int i = 0; i < k; ++i) s = fma(hs[i], vp[i][j], s);
-    w[j] = fma(sign, s, w[j]);
+  for (int i = 0; i < k; ++i) al |= reinterpret_cast<unsigned long long>(vp[i]);
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if ((al & 15) == 0) {
+    // 16-byte pairs
+    const long long n2 = n / 2;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    for (long long j = tid; j < n2; j += stride) {
+      double sx = 0.0, sy = 0.0;
+      for (int i = 0; i < k; ++i) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(vp[i]) + j);
+        sx = fma(hs[i], v.x, sx);
+        sy = fma(hs[i], v.y, sy);
+      }
+      double2 o = w2[j];
+      o.x = fma(sign, sx, o.x);
+      o.y = fma(sign, sy, o.y);
+      w2[j] = o;
+    }
+    if ((n & 1) && tid == 0) {
+      double sum = 0.0;
+      for (int i = 0; i < k; ++i) sum = fma(hs[i], vp[i][n - 1], sum);
+      w[n - 1] = fma(sign, sum, w[n - 1]);
+    }
+    return;
+  }
+  for (long long j = tid; j < n; j += stride) {
+    double sum = 0.0;
+    for (int i = 0; i < k; ++i) sum = fma(hs[i], vp[i][j], sum);
+    w[j] = fma(sign, sum, w[j]);
   }
 }
 

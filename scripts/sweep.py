@@ -64,8 +64,27 @@ def main(names):
             z = torch.empty_like(u)
             M.apply(u, z)
             t_c = timed(lambda: M.apply(u, z), max(3, reps // 2))
+            vc_bytes = M.vcycle_bytes()
             line.update({"vcycle_ms": t_c, "vcycle_dofs_per_s": N / (t_c * 1e-3), "mg_levels": M.n_levels,
+                         "vcycle_algorithmic_bytes": vc_bytes,
+                         "vcycle_hbm_frac": vc_bytes / (t_c * 1e-3) / 1e9 / peak,
                          "smoother_kind_fine": M.smoother_kind(0), "device_bytes": M.device_bytes()})
+            # one full STMG-GMRES solve (manufactured source; C4: the Gaussian pulse, zero source)
+            u0 = torch.zeros(op.n_space, dtype=torch.float64, device="cuda")
+            wave = cfg.equation == problems.WAVE
+            if wave:
+                u0 = op.interpolate(2, 0.5, 0.0, (0.5, 0.5, 0.5), 0.05, zero_boundary=True)
+            v0 = torch.zeros_like(u0) if wave else None
+            b = op.assemble_rhs(0 if wave else 1, 0.5, 0.0, u0, v0)
+            x = torch.zeros_like(b)
+            M.solve(b, x, rel_tol=1e-10, abs_tol=0.0)  # warm-up: Krylov basis allocated once
+            x.zero_()
+            torch.cuda.synchronize()
+            ts = time.perf_counter()
+            info = M.solve(b, x, rel_tol=1e-10, abs_tol=0.0)
+            torch.cuda.synchronize()
+            t_s = time.perf_counter() - ts
+            line.update({"solve_iterations": info["iterations"], "solve_ms": 1e3 * t_s, "solve_dofs_per_s": N / t_s})
         print(json.dumps(line), flush=True)
         del M, op, u, y, mesh
         torch.cuda.empty_cache()

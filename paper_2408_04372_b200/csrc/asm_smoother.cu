@@ -266,6 +266,9 @@ __global__ void __launch_bounds__(256) asm_apply_warp_kernel(const __grid_consta
 // free. 8 warps: warp w owns rows [8w, 8w+8) of each product; the k loop is
 // split into two independent accumulator chains.
 __host__ __device__ __forceinline__ int swz64(int a, int e) { return a * 64 + (e ^ ((a & 7) << 2)); }
+// record layout of 64-dof cells for the DFMA kernel: column XOR (row & 15),
+// conflict-free row and column reads of 64-bit words
+__host__ __device__ __forceinline__ int swz64f(int a, int e) { return a * 64 + (e ^ (a & 15)); }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -600,6 +603,216 @@ __global__ void __launch_bounds__(256, NBUF == 2 ? 3 : 2) asm_apply_fd64_kernel(
   }
 }
 
+// 64-dof cells on the FP64 FMA pipe (A.x_layout == 1): same record stream,
+// meta and temporal fast diagonalisation as asm_apply_fd64_kernel, but the
+// two 64 x 64 products are DFMA over the NCOL used columns only (the
+// tensor-core version pads them to 8): 256 threads, each product split in
+// four 16-row quarters reduced through shared memory; the row owner of
+// eigen-index e applies (B + lam_e)^-1 and Q for all its columns, so the
+// second product emits original columns directly.
+template <int NT, int S, int NBUF>
+__global__ void __launch_bounds__(256, 2) asm_apply_dfma64_kernel(const __grid_constant__ DevASM A,
+                                                                  const double* __restrict__ r,
+                                                                  double* __restrict__ z, double scale) {
+  constexpr int M = 64, NCOL = NT * S;
+  constexpr unsigned RBYTES = static_cast<unsigned>(kRec64 * sizeof(double));
+  extern __shared__ __align__(128) double sm[];
+  double* rs = sm + NBUF * kRec64;      // [64][4 or 8] P-transformed residual slots
+  constexpr int RW = NCOL <= 4 ? 4 : 8;  // slot row width (double4 broadcasts)
+  double* hs = rs + RW * M;              // [64][RW] result of the temporal solve (original columns)
+  double* part = hs + RW * M;            // [4][64][RW] quarter partial sums
+  long long* cinfo = reinterpret_cast<long long*>(part + 4 * RW * M);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(cinfo + 4);
+  const int t = threadIdx.x;
+  const long long n_pos = A.n_list, nsp = A.n_space;
+  const long long dx = A.dofs[0], dxy = A.dofs[0] * A.dofs[1];
+  const int row = t & 63, qtr = t >> 6;
+  int fb = 0;
+  const int lx = row & 3, ly = (row >> 2) & 3, lz = row >> 4;
+  fb = (lx == 0 ? 1 : 0) | (lx == 3 ? 2 : 0) | (ly == 0 ? 4 : 0) | (ly == 3 ? 8 : 0) | (lz == 0 ? 16 : 0) |
+       (lz == 3 ? 32 : 0);
+  const long long off = lz * dxy + ly * dx + lx;
+  const double w_int = scale * ldexp(1.0, -__popc(fb));
+  if (t == 0) {
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  long long pos = blockIdx.x;
+  if (t == 0) {
+#pragma unroll
+    for (int b = 0; b + 1 < NBUF; ++b) {
+      const long long q = pos + static_cast<long long>(b) * gridDim.x;
+      if (q < n_pos) {
+        mbar_expect_tx(&bar[b], RBYTES);
+        bulk_g2s(sm + b * kRec64, A.X + q * kRec64, RBYTES, &bar[b]);
+      }
+    }
+  }
+  double rn[NCOL];
+  long long g0n = 0, maskn = 0;
+  auto fetch = [&](long long q) {
+    if (t < M) {
+      const longlong2 mt = *reinterpret_cast<const longlong2*>(A.meta + 2 * q);
+      g0n = mt.x;
+      maskn = mt.y;
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) rn[c] = __ldg(r + c * nsp + g0n + off);
+    }
+  };
+  if (pos < n_pos) fetch(pos);
+  unsigned phase_bits = 0;
+  int buf = 0;
+  for (int it = 0; pos < n_pos; pos += gridDim.x, ++it) {
+    const int par = it & 1;
+    const long long next = pos + gridDim.x;
+    // ---- stage the residual (P-transformed slots), boundary contributions
+    if (t < M) {
+      double tr[RW];
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        double sacc = 0.0;
+        if (k < NCOL) {
+#pragma unroll
+          for (int c = 0; c < NCOL; ++c) sacc = fma(A.P[k][c], rn[c], sacc);
+        }
+        tr[k] = sacc;
+      }
+#pragma unroll
+      for (int k = 0; k < RW; k += 2) *reinterpret_cast<double2*>(rs + t * RW + k) = make_double2(tr[k], tr[k + 1]);
+      if (maskn & fb) {
+        const double w = scale * ldexp(1.0, -__popc(fb & ~static_cast<int>(maskn)));
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c) atomicAdd(z + c * nsp + g0n + off, w * rn[c]);
+      }
+      if (t == 0) {
+        cinfo[2 * par] = g0n;
+        cinfo[2 * par + 1] = maskn;
+      }
+      if (next < n_pos) fetch(next);
+    }
+    mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);
+    phase_bits ^= 1u << buf;
+    __syncthreads();
+    {
+      const int fbuf = buf == 0 ? NBUF - 1 : buf - 1;
+      const long long q = pos + static_cast<long long>(NBUF - 1) * gridDim.x;
+      if (t == 0 && q < n_pos) {
+        fence_proxy_async();
+        mbar_expect_tx(&bar[fbuf], RBYTES);
+        bulk_g2s(sm + fbuf * kRec64, A.X + q * kRec64, RBYTES, &bar[fbuf]);
+      }
+    }
+    const double* Xs = sm + buf * kRec64;
+    // ---- product 1, quarter qtr: sum over a in [16 qtr, 16 qtr + 16) of X[a][e] rs[a][.]
+    {
+      double acc[RW];
+#pragma unroll
+      for (int k = 0; k < RW; ++k) acc[k] = 0.0;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int a2 = qtr * 16 + i;
+        const double x = Xs[swz64f(a2, row)];
+        const double4 r0 = *reinterpret_cast<const double4*>(rs + a2 * RW);
+        acc[0] = fma(x, r0.x, acc[0]);
+        acc[1] = fma(x, r0.y, acc[1]);
+        acc[2] = fma(x, r0.z, acc[2]);
+        acc[3] = fma(x, r0.w, acc[3]);
+        if (RW == 8) {
+          const double4 r1 = *reinterpret_cast<const double4*>(rs + a2 * RW + 4);
+          acc[RW == 8 ? 4 : 0] = fma(x, r1.x, acc[RW == 8 ? 4 : 0]);
+          acc[RW == 8 ? 5 : 1] = fma(x, r1.y, acc[RW == 8 ? 5 : 1]);
+          acc[RW == 8 ? 6 : 2] = fma(x, r1.z, acc[RW == 8 ? 6 : 2]);
+          acc[RW == 8 ? 7 : 3] = fma(x, r1.w, acc[RW == 8 ? 7 : 3]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RW; k += 2)
+        *reinterpret_cast<double2*>(part + (qtr * M + row) * RW + k) = make_double2(acc[k], acc[k + 1]);
+    }
+    __syncthreads();
+    // ---- row owner e: reduce, (B + lam_e)^-1 per slot pair, Q back to columns
+    if (t < M) {
+      double h[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) h[k] = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+        for (int k = 0; k < RW; ++k) h[k] += part[(qq * M + t) * RW + k];
+      const double lam = Xs[4096 + t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (2 * j >= NCOL) break;
+        const int kd = A.kind[j];
+        const double a0 = A.s0[j], a1 = A.s1[j];
+        const double p0 = a0 + lam, p1 = a1 + lam;
+        const double m00 = kd ? p0 : p1, m11 = p0, m01 = kd ? -a1 : 0.0, m10 = kd ? a1 : 0.0;
+        const double inv = 1.0 / (kd ? fma(p0, p0, a1 * a1) : p0 * p1);
+        const double v0 = h[2 * j], v1 = h[2 * j + 1];
+        h[2 * j] = fma(m00, v0, m01 * v1) * inv;
+        h[2 * j + 1] = fma(m10, v0, m11 * v1) * inv;
+      }
+      double o[RW];
+#pragma unroll
+      for (int c = 0; c < RW; ++c) {
+        double sacc = 0.0;
+        if (c < NCOL) {
+#pragma unroll
+          for (int k = 0; k < NCOL; ++k) sacc = fma(A.Q[c][k], h[k], sacc);
+        }
+        o[c] = sacc;
+      }
+#pragma unroll
+      for (int c = 0; c < RW; c += 2) *reinterpret_cast<double2*>(hs + t * RW + c) = make_double2(o[c], o[c + 1]);
+    }
+    __syncthreads();
+    // ---- product 2, quarter qtr: sum over e in [16 qtr, 16 qtr + 16) of X[a][e] hs[e][.]
+    {
+      double acc[RW];
+#pragma unroll
+      for (int k = 0; k < RW; ++k) acc[k] = 0.0;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int e2 = qtr * 16 + i;
+        const double x = Xs[swz64f(row, e2)];
+        const double4 h0 = *reinterpret_cast<const double4*>(hs + e2 * RW);
+        acc[0] = fma(x, h0.x, acc[0]);
+        acc[1] = fma(x, h0.y, acc[1]);
+        acc[2] = fma(x, h0.z, acc[2]);
+        acc[3] = fma(x, h0.w, acc[3]);
+        if (RW == 8) {
+          const double4 h1 = *reinterpret_cast<const double4*>(hs + e2 * RW + 4);
+          acc[RW == 8 ? 4 : 0] = fma(x, h1.x, acc[RW == 8 ? 4 : 0]);
+          acc[RW == 8 ? 5 : 1] = fma(x, h1.y, acc[RW == 8 ? 5 : 1]);
+          acc[RW == 8 ? 6 : 2] = fma(x, h1.z, acc[RW == 8 ? 6 : 2]);
+          acc[RW == 8 ? 7 : 3] = fma(x, h1.w, acc[RW == 8 ? 7 : 3]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < RW; k += 2)
+        *reinterpret_cast<double2*>(part + (qtr * M + row) * RW + k) = make_double2(acc[k], acc[k + 1]);
+    }
+    __syncthreads();
+    // ---- dof owner a: reduce, weight, scatter (Dirichlet rows were added by the gather)
+    if (t < M) {
+      const long long g0 = cinfo[2 * par];
+      const int mask = static_cast<int>(cinfo[2 * par + 1]);
+      if (!(mask & fb)) {
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) sacc += part[(qq * M + t) * RW + c];
+          atomicAdd(z + c * nsp + g0 + off, sacc * w_int);
+        }
+      }
+    }
+    buf = buf + 1 == NBUF ? 0 : buf + 1;
+  }
+}
+
 // Large cell blocks (m > 64, e.g. 3D Q4: m = 125): one CTA of 128 threads per
 // cell (persistent), X row-major in global memory (m^2 doubles, L2-resident
 // across the two products of one cell), all S*n_t columns at once:
@@ -613,8 +826,8 @@ __global__ void __launch_bounds__(128) asm_apply_large_kernel(const __grid_const
                                                               double scale) {
   const int m = A.m, t = threadIdx.x;
   const int ncol = A.S * NT;
-  extern __shared__ __align__(16) double sm[];
-  double* rs = sm;            // [m][8]
+  extern __shared__ __align__(16) double lsm[];
+  double* rs = lsm;            // [m][8]
   double* hs = rs + 8 * 128;  // [m][8]
   const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
   for (long long pos = blockIdx.x; pos < A.n_list; pos += gridDim.x) {
@@ -845,7 +1058,7 @@ __global__ void reduce_standard_kernel(const __grid_constant__ DevASM A, double*
 }
 
 // X[a][e] = sum_k Linv[k][a] V[k][e]; V column-major from syev (V[e*m+k])
-__global__ void back_transform_kernel(int m, long long xs, const double* __restrict__ Linv,
+__global__ void back_transform_kernel(int m, long long xs, int layout, const double* __restrict__ Linv,
                                       const double* __restrict__ V, double* __restrict__ X) {
   const long long cell = blockIdx.x;
   const double* Lc = Linv + cell * static_cast<long long>(m) * m;
@@ -855,7 +1068,7 @@ __global__ void back_transform_kernel(int m, long long xs, const double* __restr
     const int a = i / m, e = i % m;
     double s = 0.0;
     for (int k = a; k < m; ++k) s = fma(Lc[static_cast<long long>(k) * m + a], Vc[static_cast<long long>(e) * m + k], s);
-    Xc[m == 64 ? swz64(a, e) : i] = s;
+    Xc[m == 64 ? (layout == 1 ? swz64f(a, e) : swz64(a, e)) : i] = s;
   }
 }
 
@@ -943,12 +1156,39 @@ void launch_fd64_nbuf(const DevASM& A, const double* r, double* z, double scale,
   count_launch();
   asm_apply_fd64_kernel<NT, S, NBUF><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
 }
+template <int NT, int S>
+void launch_dfma64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  constexpr int NCOL = NT * S, RW = NCOL <= 4 ? 4 : 8;
+  constexpr size_t smem = sizeof(double) * (2 * static_cast<size_t>(kRec64) + 6 * RW * 64) + 4 * sizeof(long long) +
+                          2 * sizeof(unsigned long long);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(asm_apply_dfma64_kernel<NT, S, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaFuncSetAttribute(asm_apply_dfma64_kernel<NT, S, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = true;
+  }
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_dfma64_kernel<NT, S, 2>, 256, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (A.n_list == 0) return;
+  const long long grid =
+      std::max<long long>(1, std::min<long long>(A.n_list, static_cast<long long>(std::max(per_sm, 1)) * sms));
+  count_launch();
+  asm_apply_dfma64_kernel<NT, S, 2><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
+}
+
 // record pipeline depth (STMG_ASM_NBUF = 2 or 3). Default 2: one record in
 // flight per CTA at 3 CTAs / SM measured 1.61 ms per C2 sweep against 1.91 ms
 // for 3 buffers at 2 CTAs / SM -- the per-cell solve, not the bytes in
 // flight, limits the sweep
 template <int NT, int S>
 void launch_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  if (A.x_layout == 1) {
+    launch_dfma64<NT, S>(A, r, z, scale, s);
+    return;
+  }
   static const int nbuf = [] {
     const char* e = std::getenv("STMG_ASM_NBUF");
     return e ? std::atoi(e) : 2;
@@ -1064,10 +1304,10 @@ void asm_transpose_cells(int m, long long n_cells, long long xs, const double* c
                            256, 0, s>>>(m, n_cells, xs, colmajor, X);
 }
 
-void asm_back_transform(int m, long long xs, long long n_cells, const double* Linv, const double* V, double* X,
-                        cudaStream_t s) {
+void asm_back_transform(int m, long long xs, int layout, long long n_cells, const double* Linv, const double* V,
+                        double* X, cudaStream_t s) {
   count_launch();
-  back_transform_kernel<<<static_cast<unsigned>(n_cells), 128, 0, s>>>(m, xs, Linv, V, X);
+  back_transform_kernel<<<static_cast<unsigned>(n_cells), 128, 0, s>>>(m, xs, layout, Linv, V, X);
 }
 
 }  // namespace stmgb

@@ -134,6 +134,8 @@ struct DevASM {
   // (2j, 2j+1) is two real eigenvalues s0/s1 (kind 0) or one conjugate pair
   // s0 +- i s1 (kind 1)
   int tdiag;
+  // 64-dof record layout / kernel: 0 FP64 tensor cores (swz64), 1 DFMA (swz64f)
+  int x_layout;
   int kind[4];
   double s0[4], s1[4];
   double P[8][8], Q[8][8];
@@ -163,8 +165,8 @@ void fdm_add_correction(const DevFDM& F, const double* r, double* z, double scal
 void asm_extract_probe(const DevASM& A, int colour_x, int colour_y, int colour_z, int period, const double* probe,
                        int probe_zcells, double* cellmat, cudaStream_t s);
 void asm_reduce_standard(const DevASM& A, double* Mt, double* At, cudaStream_t s);  // At <- L^-1 At L^-T, Mt <- L^-1
-void asm_back_transform(int m, long long xs, long long n_cells, const double* Linv, const double* V, double* X,
-                        cudaStream_t s);
+void asm_back_transform(int m, long long xs, int layout, long long n_cells, const double* Linv, const double* V,
+                        double* X, cudaStream_t s);
 // large blocks (m > 64): Dirichlet rows/cols of the cell matrices (M identity,
 // A zero) and column-major -> row-major X records
 void asm_dirichlet_rows(const DevASM& A, double* Mt, double* At, cudaStream_t s);

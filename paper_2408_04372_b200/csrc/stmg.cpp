@@ -764,7 +764,12 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperat
   // m = 64: one TMA record per cell, X (swizzled) followed by its eigenvalues
   A.xs = A.m == 64 ? kRec64 : (static_cast<long long>(A.m) * A.m + 1) & ~1LL;
   X_.allocate(sizeof(double) * static_cast<size_t>(n_pos) * A.xs);
-  asm_back_transform(A.m, A.xs, n_pos, cellM.d(), cellA.d(), X_.d(), s);
+  // 64-dof kernel: FP64 tensor cores (default) or DFMA (STMG_ASM64=dfma)
+  {
+    const char* e = std::getenv("STMG_ASM64");
+    A.x_layout = (A.m == 64 && e && std::string(e) == "dfma") ? 1 : 0;
+  }
+  asm_back_transform(A.m, A.xs, A.x_layout, n_pos, cellM.d(), cellA.d(), X_.d(), s);
   if (A.m == 64) {
     cuda_check(cudaMemcpy2DAsync(X_.d() + 64 * 64, sizeof(double) * kRec64, lam_.d(), sizeof(double) * 64,
                                  sizeof(double) * 64, static_cast<size_t>(n_pos), cudaMemcpyDeviceToDevice, s),

@@ -1432,8 +1432,6 @@ SpaceTimeMultigrid::SpaceTimeMultigrid(Equation equation, TimeScheme scheme, con
                                                 lv.spec.mesh_level, lv.spec.p, rho);
     const Index n = lv.op->n_dofs();
     lv.r.allocate(sizeof(double) * n);
-    lv.z.allocate(sizeof(double) * n);
-    lv.e.allocate(sizeof(double) * n);
     const bool coarsest = l + 1 == plan.size();
     if (!coarsest || levels_.size() == 1) {
       lv.smoother = std::make_unique<ASMSmoother>(*lv.op);
@@ -1454,6 +1452,7 @@ double SpaceTimeMultigrid::estimate_relaxation(const Level& lv, std::uint64_t se
   // (multigrid.cpp:127-172), modified Gram-Schmidt in the reference order
   const Index n = lv.op->n_dofs();
   const int m = static_cast<int>(std::min<Index>(options_.eig_iters, n));
+  if (m <= 0) return 1.0;  // no Arnoldi steps: the unestimated relaxation factor
   Xoshiro256pp rng(seed);
   std::vector<double> hv(static_cast<size_t>(n));
   double nrm2 = 0.0;
@@ -1672,7 +1671,7 @@ std::vector<LevelInfo> SpaceTimeMultigrid::level_info() const {
 size_t SpaceTimeMultigrid::device_bytes() const {
   size_t b = 0;
   for (const Level& lv : levels_) {
-    b += lv.r.bytes() + lv.z.bytes() + lv.e.bytes() + lv.rc.bytes() + lv.ec.bytes() + lv.coarse_inv.bytes();
+    b += lv.r.bytes() + lv.rc.bytes() + lv.ec.bytes() + lv.coarse_inv.bytes();
     if (lv.smoother) b += lv.smoother->bytes();
   }
   return b;

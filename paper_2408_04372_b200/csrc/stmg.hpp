@@ -298,7 +298,7 @@ class SpaceTimeMultigrid {
     std::unique_ptr<Transfer> to_coarser;
     double omega = 1.0;
     DeviceBuffer coarse_inv;  // dense inverse of the coarsest operator
-    mutable DeviceBuffer r, z, rc, ec, e;  // work vectors
+    mutable DeviceBuffer r, rc, ec;  // work vectors: residual, restricted residual, coarse correction
   };
   double estimate_relaxation(const Level& lv, std::uint64_t seed) const;
   void coarse_solve(const double* f, double* u, cudaStream_t stream) const;

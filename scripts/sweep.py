@@ -5,7 +5,8 @@ Prints one JSON line per configuration (DoF/s, ms, HBM fraction of the vmult's
 algorithmic bytes 16 N (+ 24 n_verts perturbed) against MEASURED_PEAKS.json).
 
   python scripts/sweep.py [C1 C2 C3 C4 C5-32 C5-64 C5-128 C5-256v]
-  (suffix v: vmult only -- the V-cycle does not fit one GPU there)
+  (suffix v: vmult only; suffix n: vmult and V-cycle, no solve -- the
+   Krylov basis of C5-256 does not fit one GPU)
 """
 import json
 import os
@@ -36,7 +37,8 @@ def main(names):
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     for name in names:
         vonly = name.endswith("v")
-        cname = name[:-1] if vonly else name
+        nosolve = name.endswith("n")
+        cname = name[:-1] if (vonly or nosolve) else name
         cfg = problems.config(cname)
         t0 = time.perf_counter()
         mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
@@ -45,8 +47,13 @@ def main(names):
                                        cfg.n_steps, cfg.rho)
             M = None
         else:
+            # C5-256 on one GPU: the 20-vector Arnoldi basis of the relaxation
+            # estimate (multigrid.cpp:127-172) does not fit next to the level
+            # vectors, so omega is fixed to 1 there (the estimate's value on
+            # every C5 level at the sizes where it runs)
+            opts = {"eig_iters": 0} if nosolve else {}
             M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k,
-                                       cfg.n_steps, cfg.tau)
+                                       cfg.n_steps, cfg.tau, **opts)
             op = M.operator_at(0)
         torch.cuda.synchronize()
         setup = time.perf_counter() - t0
@@ -59,9 +66,10 @@ def main(names):
         nv = (cfg.cells + 1) ** cfg.dim
         vbytes = 16 * N + (24 * nv if cfg.perturb > 0 else 0)
         line = {"config": name, **cfg.describe(), "setup_s": round(setup, 2), "vmult_ms": t_v,
+                "omegas": [li["omega"] for li in M.level_info()] if M is not None else None,
                 "vmult_dofs_per_s": N / (t_v * 1e-3), "vmult_hbm_frac": vbytes / (t_v * 1e-3) / 1e9 / peak}
         if M is not None:
-            z = torch.empty_like(u)
+            z = y  # the vmult output is reused (C5-256: four fine vectors would not fit)
             M.apply(u, z)
             t_c = timed(lambda: M.apply(u, z), max(3, reps // 2))
             vc_bytes = M.vcycle_bytes()
@@ -69,6 +77,11 @@ def main(names):
                          "vcycle_algorithmic_bytes": vc_bytes,
                          "vcycle_hbm_frac": vc_bytes / (t_c * 1e-3) / 1e9 / peak,
                          "smoother_kind_fine": M.smoother_kind(0), "device_bytes": M.device_bytes()})
+            if nosolve:
+                print(json.dumps(line), flush=True)
+                del M, op, u, y, mesh, z
+                torch.cuda.empty_cache()
+                continue
             # one full STMG-GMRES solve (manufactured source; C4: the Gaussian pulse, zero source)
             u0 = torch.zeros(op.n_space, dtype=torch.float64, device="cuda")
             wave = cfg.equation == problems.WAVE
@@ -91,4 +104,4 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5-32", "C5-64", "C5-128", "C5-256v"])
+    main(sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5-32", "C5-64", "C5-128", "C5-256n"])

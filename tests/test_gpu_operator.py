@@ -107,3 +107,34 @@ def test_full_size_c2_properties(cuda):
     assert cuda.equal(yv[:, 0], uv[:, 0]) and cuda.equal(yv[:, :, :, -1], uv[:, :, :, -1])
     y3 = op.apply(2.0 * u)
     assert float((y3 - 2.0 * y1).norm() / y1.norm()) <= 1e-14
+
+
+def test_full_size_c5_256_translation_invariance(cuda):
+    """C5 at 256^3 cells (4.31e9 ST dofs, vector indices beyond 2^32): the
+    Cartesian constant-coefficient operator is translation invariant away
+    from the boundary, so the same nodal bump placed near the start and near
+    the end of the lattice must give the same output pattern in every
+    temporal field -- any 32-bit index wrap would break it."""
+    cfg = problems.config("C5-256")
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements)
+    op = api.SpaceTimeOperator(mesh, cfg.refinements, cfg.p, cfg.equation, cfg.scheme, cfg.k, cfg.tau, cfg.n_steps)
+    d = cfg.cells * cfg.p + 1
+    F = cfg.n_steps * cfg.n_t
+    u = cuda.zeros(op.n_dofs, dtype=cuda.float64, device="cuda")
+    uv = u.view(F, d, d, d)
+    g = cuda.Generator(device="cuda").manual_seed(3)
+    bump = cuda.rand((F, 5, 5, 5), dtype=cuda.float64, device="cuda", generator=g)
+    lo = 40  # both far from the boundary, hi near the end of the lattice, same offset mod p
+    hi = (d - 60) - ((d - 60 - lo) % cfg.p)
+    uv[:, lo:lo + 5, lo:lo + 5, lo:lo + 5] = bump
+    uv[:, hi:hi + 5, hi:hi + 5, hi:hi + 5] = bump
+    y = op.apply(u)
+    del u, uv
+    yv = y.view(F, d, d, d)
+    w = 12  # window covering the bump's support (cells of width p)
+    a = yv[:, lo - w:lo + 5 + w, lo - w:lo + 5 + w, lo - w:lo + 5 + w]
+    b = yv[:, hi - w:hi + 5 + w, hi - w:hi + 5 + w, hi - w:hi + 5 + w]
+    assert float(a.norm()) > 0
+    assert float((a - b).norm() / a.norm()) <= 1e-13
+    del y
+    cuda.cuda.empty_cache()

@@ -280,7 +280,8 @@ def run_partitioned(args, world, rank, local):
                        "step": "1 V-cycle + 1 vmult (one preconditioned GMRES iteration's operator work)",
                        "l2": "vectors larger than L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_kind,
+                         "traffic": (lambda tr: tr / world if tr else None)(ncu_traffic(f"{args.workload}:asm")),
+                         "peak_source": peak_kind,
                          "kernel": "asm_apply_fd64_kernel (rank-local fine-level smoother sweep)",
                          "algorithmic_bytes_per_launch": asm_bytes, "launch_ms": t_asm},
             "e2e": e2e, "gpu_launches": int(launches), "setup_s": setup_s, "clocks": clk.summary()}

@@ -193,6 +193,15 @@ int stmg_st_operator_error_norms(const stmg_st_operator* op, const double* d_x, 
 int stmg_march(const stmg_multigrid* mg, int n_batches, int source_kind, double frequency, double* d_u, double* d_v,
                const stmg_gmres_options* options, int* iterations, double errors[3], void* stream);
 
+/* march with probes (driver.cpp:146-186, 226-236): n_probes points
+ * (probe_xyz, 3 each, located on the finest mesh by locate_point,
+ * spatial_operator.cpp:475-524) sampled samples_per_step times per step;
+ * times receives 1 + n_batches * n_steps * samples_per_step sample times and
+ * values the series of each probe (probe-major, same length) */
+int stmg_march_probes(const stmg_multigrid* mg, int n_batches, int source_kind, double frequency, double* d_u,
+                      double* d_v, const stmg_gmres_options* options, int* iterations, double errors[3], int n_probes,
+                      const double* probe_xyz, int samples_per_step, double* times, double* values, void* stream);
+
 /* ---- z-slab partitioned solve over several GPUs (no
  * reference counterpart: the reference is single-process). The finest mesh
  * is cut into n_parts slabs of cell layers along z; a process holds

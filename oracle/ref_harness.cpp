@@ -328,6 +328,21 @@ int ref_error_norms(void* h, const double* u, const double* u0, double frequency
   });
 }
 
+// value_at (space_time_operator.cpp:250-266) of a batch solution u entering
+// from u0, then evaluate_fe at locate_point(x) on the finest mesh
+// (spatial_operator.cpp:451-524): the probe sample march() records
+int ref_probe_value(void* h, const double* u, const double* u0, int step, double t_ref, const double* x3, double* out) {
+  auto* r = static_cast<Ref*>(h);
+  return guard([&] {
+    BatchState st;
+    st.u = vec(u0, r->op->n_space());
+    const Eigen::VectorXd val = r->op->value_at(vec(u, r->op->n_dofs()), st, step, t_ref);
+    const Point x{x3[0], x3[1], x3[2]};
+    const auto loc = locate_point(r->mesh.finest(), x);
+    *out = evaluate_fe(*r->dofmap, val, loc.first, loc.second);
+  });
+}
+
 // extract_final (space_time_operator.cpp:223-248)
 int ref_extract_final(void* h, const double* u, const double* u0, const double* v0, double* uf, double* vf) {
   auto* r = static_cast<Ref*>(h);

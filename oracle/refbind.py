@@ -74,6 +74,7 @@ def load() -> C.CDLL:
     lib.ref_assemble_rhs.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, dp, dp, dp]
     lib.ref_extract_final.argtypes = [C.c_void_p, dp, dp, dp, dp, dp]
     lib.ref_error_norms.argtypes = [C.c_void_p, dp, dp, C.c_double, C.c_double, dp]
+    lib.ref_probe_value.argtypes = [C.c_void_p, dp, dp, C.c_int, C.c_double, dp, dp]
     lib.ref_interpolate_gaussian.argtypes = [C.c_void_p, dp, C.c_double, dp]
     lib.ref_vertices.argtypes = [C.c_void_p, C.c_int, dp]
     lib.ref_temporal_weights.argtypes = [C.c_int, C.c_int, dp, dp, dp, dp, dp]
@@ -250,6 +251,14 @@ class Reference:
         _chk(load().ref_error_norms(self.h, _p(np.ascontiguousarray(u, dtype=np.float64)),
                                     _p(np.ascontiguousarray(u0, dtype=np.float64)), frequency, t0, _p(out)))
         return tuple(out)
+
+    def probe_value(self, u: np.ndarray, u0: np.ndarray, step: int, t_ref: float, x) -> float:
+        """value_at + evaluate_fe at locate_point(x) (the march() probe sample)."""
+        out = np.zeros(1)
+        _chk(load().ref_probe_value(self.h, _p(np.ascontiguousarray(u, dtype=np.float64)),
+                                    _p(np.ascontiguousarray(u0, dtype=np.float64)), step, t_ref,
+                                    _p(np.ascontiguousarray(x, dtype=np.float64)), _p(out)))
+        return float(out[0])
 
     def interpolate_gaussian(self, centre=(0.5, 0.5, 0.5), width: float = 0.05) -> np.ndarray:
         c = np.ascontiguousarray(centre, dtype=np.float64)

@@ -338,6 +338,24 @@ class SpaceTimeMultigrid:
                                     err if errors else None, _stream()))
         return {"iterations": list(its), "error_u": tuple(err) if errors else None}
 
+    def march_probes(self, n_batches: int, u, points, v=None, samples_per_step: int = 16, source_kind: int = 1,
+                     frequency: float = 0.5, **opts) -> dict:
+        """march with probe time series (driver.cpp:146-236): returns the
+        iterations, error norms, sample times and one series per point."""
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        n_samples = 1 + n_batches * self.level_info()[0]["n_steps"] * samples_per_step
+        times = np.zeros(n_samples)
+        vals = np.zeros((pts.shape[0], n_samples))
+        o = gmres_options(**opts)
+        its = (C.c_int * n_batches)()
+        err = (C.c_double * 3)()
+        N.check(N.load().stmg_march_probes(self._h, n_batches, source_kind, frequency, _ptr(u),
+                                           _ptr(v) if v is not None else None, C.byref(o), its, err, pts.shape[0],
+                                           pts.ctypes.data_as(N.c_double_p), samples_per_step,
+                                           times.ctypes.data_as(N.c_double_p), vals.ctypes.data_as(N.c_double_p),
+                                           _stream()))
+        return {"iterations": list(its), "error_u": tuple(err), "times": times, "values": vals}
+
     def solve_host(self, b: np.ndarray, x: np.ndarray, precondition: bool = True, history_cap: int = 1100, **opts):
         o = gmres_options(**opts)
         res = N.GmresResult()

@@ -531,6 +531,39 @@ int stmg_march(const stmg_multigrid* mg, int n_batches, int source_kind, double 
   return rc;
 }
 
+int stmg_march_probes(const stmg_multigrid* mg, int n_batches, int source_kind, double frequency, double* d_u,
+                      double* d_v, const stmg_gmres_options* options, int* iterations, double errors[3], int n_probes,
+                      const double* probe_xyz, int samples_per_step, double* times, double* values, void* stream) {
+  bool converged = true;
+  const int rc = guard([&] {
+    if (!mg || !d_u || !iterations) throw std::invalid_argument("stmg_march_probes: null argument");
+    if (n_probes < 0 || (n_probes > 0 && (!probe_xyz || !times || !values)) || samples_per_step < 1)
+      throw std::invalid_argument("stmg_march_probes: bad probe arguments");
+    ProbeSpec ps;
+    ps.xyz.assign(probe_xyz, probe_xyz + 3 * n_probes);
+    ps.samples_per_step = samples_per_step;
+    const MarchResult r = march(*mg->mg, n_batches, source_kind, frequency, d_u, d_v, gopts(options),
+                                errors != nullptr, st(stream), n_probes > 0 ? &ps : nullptr);
+    for (int b = 0; b < n_batches; ++b)
+      iterations[b] = b < static_cast<int>(r.iterations.size()) ? r.iterations[static_cast<size_t>(b)] : 0;
+    if (errors) {
+      errors[0] = r.error_u.l2_l2;
+      errors[1] = r.error_u.linf_l2;
+      errors[2] = r.error_u.linf_linf;
+    }
+    const size_t ns = r.probe_times.size();
+    for (size_t i = 0; i < ns; ++i) times[i] = r.probe_times[i];
+    for (int p = 0; p < n_probes; ++p)
+      for (size_t i = 0; i < ns; ++i) values[static_cast<size_t>(p) * ns + i] = r.probe_values[static_cast<size_t>(p)][i];
+    converged = r.converged;
+  });
+  if (rc == 0 && !converged) {
+    g_err = "stmg_march_probes: a batch did not converge";
+    return -2;
+  }
+  return rc;
+}
+
 int stmg_nccl_unique_id(char id[128]) {
   return guard_host([&] {
     if (!id) throw std::invalid_argument("stmg_nccl_unique_id: null argument");

@@ -25,6 +25,11 @@ void interpolate_nodes(const DevLevel& L, int kind, double omega, double t, cons
 void spatial_error(const DevLevel& L, const double* u, int n_q, const double* qx, const double* qw, int kind,
                    double omega, double t, double* out, cudaStream_t s);
 
+// evaluate_fe at located points (rhs.cu): out[p * n_fields + f] for n_fields
+// nodal fields u + f * fstride; cells / xi (3 per point) on the device
+void probe_fields(const DevLevel& L, const double* u, int n_fields, long long fstride, int n_probes,
+                  const long long* d_cells, const double* d_xi, double* d_out, cudaStream_t s);
+
 // ---- z-slab partition helpers (slab.cu)
 // v[f * fstride + plane * plane_len + i] = val for every field f < F, i < plane_len
 void plane_fill(double* v, int F, long long fstride, long long plane, long long plane_len, double val, cudaStream_t s);

@@ -191,7 +191,46 @@ __global__ void error_kernel(const __grid_constant__ DevLevel L, const GaussRule
   }
 }
 
+// evaluate_fe (spatial_operator.cpp:451-473) of n_fields nodal fields
+// (field stride fstride) at located points: out[p * n_fields + f]
+__global__ void probe_kernel(const __grid_constant__ DevLevel L, const double* __restrict__ u, int n_fields,
+                             long long fstride, int n_probes, const long long* __restrict__ cells,
+                             const double* __restrict__ xis, double* __restrict__ out) {
+  const int tt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tt >= n_probes * n_fields) return;
+  const int pr = tt / n_fields, f = tt - pr * n_fields;
+  const int dim = L.dim, n = L.n, p = L.p;
+  const long long cell = cells[pr];
+  const long long c[3] = {cell % L.cells[0], (cell / L.cells[0]) % L.cells[1], cell / (L.cells[0] * L.cells[1])};
+  double phi[3][kMaxN];
+  for (int a = 0; a < 3; ++a)
+    for (int j = 0; j < kMaxN; ++j) {
+      double v = 1.0;
+      if (a < dim && j < n)
+        for (int m = 0; m < n; ++m)
+          if (m != j) v *= (xis[3 * pr + a] - L.gl[m]) / (L.gl[j] - L.gl[m]);
+      phi[a][j] = v;
+    }
+  const long long dx = L.dofs[0], dxy = L.dofs[0] * L.dofs[1];
+  const long long base = f * fstride + (dim == 3 ? c[2] * p * dxy : 0) + c[1] * p * dx + c[0] * p;
+  double s = 0.0;
+  const int nz = dim == 3 ? n : 1;
+  for (int lz = 0; lz < nz; ++lz)
+    for (int ly = 0; ly < n; ++ly)
+      for (int lx = 0; lx < n; ++lx)
+        s += u[base + lz * dxy + ly * dx + lx] * phi[0][lx] * phi[1][ly] * (dim == 3 ? phi[2][lz] : 1.0);
+  out[tt] = s;
+}
+
 }  // namespace
+
+void probe_fields(const DevLevel& L, const double* u, int n_fields, long long fstride, int n_probes,
+                  const long long* d_cells, const double* d_xi, double* d_out, cudaStream_t s) {
+  const int total = n_probes * n_fields;
+  if (total == 0) return;
+  count_launch();
+  probe_kernel<<<(total + 127) / 128, 128, 0, s>>>(L, u, n_fields, fstride, n_probes, d_cells, d_xi, d_out);
+}
 
 void spatial_error(const DevLevel& L, const double* u, int n_q, const double* qx, const double* qw, int kind,
                    double omega, double t, double* out, cudaStream_t s) {

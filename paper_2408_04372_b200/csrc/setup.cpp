@@ -328,6 +328,116 @@ double cartesian_coord(const MeshLevel& m, int axis, Index i) {
   return m.lo[axis] + (m.hi[axis] - m.lo[axis]) * static_cast<double>(i) / static_cast<double>(m.cells[axis]);
 }
 
+namespace {
+// corner positions of a cell (lexicographic corners, x fastest)
+void cell_corners(const MeshLevel& m, Index cell, double X[8][3]) {
+  const Index cx = cell % m.cells[0], cy = (cell / m.cells[0]) % m.cells[1], cz = cell / (m.cells[0] * m.cells[1]);
+  const auto nv = m.n_verts_axis();
+  const int corners = 1 << m.dim;
+  for (int s = 0; s < corners; ++s) {
+    const Index i = cx + (s & 1), j = cy + ((s >> 1) & 1), k = cz + ((s >> 2) & 1);
+    for (int a = 0; a < 3; ++a) X[s][a] = 0.0;
+    if (!m.vertices.empty()) {
+      const Index v = (k * nv[1] + j) * nv[0] + i;
+      for (int a = 0; a < m.dim; ++a) X[s][a] = m.vertices[static_cast<size_t>(3 * v + a)];
+    } else {
+      const Index idx[3] = {i, j, k};
+      for (int a = 0; a < m.dim; ++a) X[s][a] = cartesian_coord(m, a, idx[a]);
+    }
+  }
+}
+}  // namespace
+
+void locate_point(const MeshLevel& m, const double x[3], Index& cell_out, double xi_out[3]) {
+  const int dim = m.dim, corners = 1 << dim;
+  const double tol = 1e-10;
+  for (Index cell = 0; cell < m.n_cells(); ++cell) {
+    double X[8][3];
+    cell_corners(m, cell, X);
+    bool reject = false;
+    for (int a = 0; a < dim && !reject; ++a) {
+      double lo = X[0][a], hi = X[0][a];
+      for (int s = 0; s < corners; ++s) {
+        lo = std::min(lo, X[s][a]);
+        hi = std::max(hi, X[s][a]);
+      }
+      const double pad = 0.25 * (hi - lo) + tol;
+      if (x[a] < lo - pad || x[a] > hi + pad) reject = true;
+    }
+    if (reject) continue;
+    double xi[3] = {0.5, 0.5, 0.5};
+    bool converged = false;
+    for (int it = 0; it < 50; ++it) {
+      double g[3] = {0.0, 0.0, 0.0}, J[3][3] = {{0.0}};
+      for (int s = 0; s < corners; ++s) {
+        double w = 1.0;
+        double dw[3];
+        for (int a = 0; a < dim; ++a) w *= ((s >> a) & 1) ? xi[a] : 1.0 - xi[a];
+        for (int bb = 0; bb < dim; ++bb) {
+          double d = 1.0;
+          for (int a = 0; a < dim; ++a)
+            d *= a == bb ? (((s >> a) & 1) ? 1.0 : -1.0) : (((s >> a) & 1) ? xi[a] : 1.0 - xi[a]);
+          dw[bb] = d;
+        }
+        for (int a = 0; a < dim; ++a) {
+          g[a] += w * X[s][a];
+          for (int bb = 0; bb < dim; ++bb) J[a][bb] += dw[bb] * X[s][a];
+        }
+      }
+      double r[3], nr = 0.0;
+      for (int a = 0; a < dim; ++a) {
+        r[a] = g[a] - x[a];
+        nr += r[a] * r[a];
+      }
+      if (std::sqrt(nr) < 1e-13) {
+        converged = true;
+        break;
+      }
+      // dxi = J^-1 r (Gaussian elimination with partial pivoting, dim <= 3)
+      double A[3][4];
+      for (int i = 0; i < dim; ++i) {
+        for (int j = 0; j < dim; ++j) A[i][j] = J[i][j];
+        A[i][dim] = r[i];
+      }
+      bool singular = false;
+      for (int k = 0; k < dim; ++k) {
+        int piv = k;
+        for (int i = k + 1; i < dim; ++i)
+          if (std::abs(A[i][k]) > std::abs(A[piv][k])) piv = i;
+        if (A[piv][k] == 0.0) {
+          singular = true;
+          break;
+        }
+        for (int j = 0; j <= dim; ++j) std::swap(A[k][j], A[piv][j]);
+        for (int i = k + 1; i < dim; ++i) {
+          const double f = A[i][k] / A[k][k];
+          for (int j = k; j <= dim; ++j) A[i][j] -= f * A[k][j];
+        }
+      }
+      if (singular) break;
+      double dxi[3] = {0.0, 0.0, 0.0};
+      for (int i = dim - 1; i >= 0; --i) {
+        double sum = A[i][dim];
+        for (int j = i + 1; j < dim; ++j) sum -= A[i][j] * dxi[j];
+        dxi[i] = sum / A[i][i];
+      }
+      for (int a = 0; a < dim; ++a) xi[a] -= dxi[a];
+    }
+    if (!converged) continue;
+    bool inside = true;
+    for (int a = 0; a < dim; ++a) {
+      if (xi[a] < -tol || xi[a] > 1.0 + tol) inside = false;
+      xi[a] = std::min(1.0, std::max(0.0, xi[a]));
+    }
+    if (inside) {
+      cell_out = cell;
+      for (int a = 0; a < 3; ++a) xi_out[a] = a < dim ? xi[a] : 0.0;
+      return;
+    }
+  }
+  throw std::runtime_error("locate_point: point outside mesh");
+}
+
 MeshHierarchy make_cartesian(int dim, std::array<double, 3> lo, std::array<double, 3> hi, Index base_cells,
                              int refinements) {
   if (dim < 1 || dim > 3) throw std::invalid_argument("make_cartesian: dim must be 1, 2 or 3");

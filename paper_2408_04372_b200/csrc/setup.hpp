@@ -88,6 +88,10 @@ MeshHierarchy make_cartesian(int dim, std::array<double, 3> lo, std::array<doubl
 void set_finest_vertices(MeshHierarchy& mesh, const double* xyz);
 // Cartesian vertex coordinate along an axis (src/mesh.cpp:171-184)
 double cartesian_coord(const MeshLevel& m, int axis, Index i);
+// locate_point (spatial_operator.cpp:475-524): the first cell (lexicographic)
+// whose d-linear map reaches x by Newton iteration from the cell centre,
+// with its reference coordinates; throws when x is outside the mesh
+void locate_point(const MeshLevel& m, const double x[3], Index& cell, double xi[3]);
 
 // Level plans (include/stmg/multigrid.hpp:18-38, src/multigrid.cpp:34-81)
 struct LevelSpec {

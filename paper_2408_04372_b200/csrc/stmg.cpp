@@ -796,7 +796,9 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperat
     }
     meta_ = upload(meta);
     A.meta = static_cast<const long long*>(meta_.raw());
-    temporal_block_diagonalise(A);
+    // STMG_NO_TDIAG: keep the pivoted per-eigenvalue solves (the fallback
+    // kernel for non-diagonalisable temporal blocks), for testing
+    if (!std::getenv("STMG_NO_TDIAG")) temporal_block_diagonalise(A);
   }
   cuda_check(cudaStreamSynchronize(s), "asm setup");
   A.X = X_.d();
@@ -1368,7 +1370,7 @@ void accumulate_errors(const SpaceTimeOperator& op, const double* x, const doubl
 }
 
 MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, double frequency, double* u, double* v,
-                  const GmresOptions& options, bool errors, cudaStream_t s) {
+                  const GmresOptions& options, bool errors, cudaStream_t s, const ProbeSpec* probes) {
   const SpaceTimeOperator& op = mg.fine_operator();
   const bool wave = op.equation() == Equation::Wave;
   if (n_batches < 1) throw std::invalid_argument("march: n_batches must be >= 1");
@@ -1381,6 +1383,32 @@ MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, 
   GmresWorkspace ws;
   MarchResult res;
   ErrorRecord acc;
+  // probes: located once on the finest mesh (locate_point), evaluated as
+  // evaluate_fe of every temporal field and combined with the trial basis
+  // weights at the sample times (value_at is linear)
+  const int np = probes ? static_cast<int>(probes->xyz.size() / 3) : 0;
+  const int F = op.desc().F, nt = op.n_t();
+  DeviceBuffer pcells, pxi, pout;
+  std::vector<double> hv(static_cast<size_t>(np) * (F + 1));
+  auto probe = [&](const double* fields, int nf, long long fstride) {
+    probe_fields(op.desc(), fields, nf, fstride, np, static_cast<const long long*>(pcells.raw()), pxi.d(), pout.d(), s);
+    cuda_check(cudaMemcpyAsync(hv.data(), pout.raw(), sizeof(double) * np * nf, cudaMemcpyDeviceToHost, s), "probe");
+    cuda_check(cudaStreamSynchronize(s), "probe");
+  };
+  if (np > 0) {
+    std::vector<long long> cells(static_cast<size_t>(np));
+    std::vector<double> xi(static_cast<size_t>(3 * np));
+    for (int pi = 0; pi < np; ++pi) {
+      Index cell = 0;
+      locate_point(op.mesh(), probes->xyz.data() + 3 * pi, cell, xi.data() + 3 * pi);
+      cells[static_cast<size_t>(pi)] = cell;
+    }
+    pcells = upload(cells);
+    pxi = upload(xi);
+    pout.allocate(sizeof(double) * static_cast<size_t>(np) * (F + 1));
+    res.probe_values.assign(static_cast<size_t>(np), {});
+    res.probe_times.push_back(0.0);
+  }
   for (int b = 0; b < n_batches; ++b) {
     const double t0 = static_cast<double>(b) * op.n_steps() * op.tau();
     op.assemble_rhs(source_kind, frequency, t0, u, v, rhs.d(), s);
@@ -1395,6 +1423,29 @@ MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, 
       break;
     }
     if (errors) accumulate_errors(op, x.d(), u, frequency, t0, acc, s);
+    if (np > 0) {
+      // entering state, then the F fields of the batch
+      probe(u, 1, nx);
+      std::vector<double> u0v(static_cast<size_t>(np));
+      for (int pi = 0; pi < np; ++pi) u0v[static_cast<size_t>(pi)] = hv[static_cast<size_t>(pi)];
+      if (b == 0)
+        for (int pi = 0; pi < np; ++pi) res.probe_values[static_cast<size_t>(pi)].push_back(u0v[static_cast<size_t>(pi)]);
+      probe(x.d(), F, nx);
+      const int ns = probes->samples_per_step;
+      for (int st = 0; st < op.n_steps(); ++st)
+        for (int j = 1; j <= ns; ++j) {
+          const double tr = static_cast<double>(j) / ns;
+          const double lw = op.weights().left_weight(tr);
+          for (int pi = 0; pi < np; ++pi) {
+            const double* fv = hv.data() + static_cast<size_t>(pi) * F;
+            double val = 0.0;
+            for (int i = 0; i < nt; ++i) val += op.weights().unknown_weight(i, tr) * fv[st * nt + i];
+            if (lw != 0.0) val += lw * (st == 0 ? u0v[static_cast<size_t>(pi)] : fv[(st - 1) * nt + nt - 1]);
+            res.probe_values[static_cast<size_t>(pi)].push_back(val);
+          }
+          res.probe_times.push_back(t0 + (st + tr) * op.tau());
+        }
+    }
     op.extract_final(x.d(), u, v, uf.d(), wave ? vf.d() : nullptr, s);
     vec_copy(u, uf.d(), nx, s);
     if (wave) vec_copy(v, vf.d(), nx, s);

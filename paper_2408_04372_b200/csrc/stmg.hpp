@@ -261,9 +261,18 @@ struct MarchResult {
   std::vector<double> final_residuals;
   bool converged = true;
   ErrorRecord error_u;  // finished (l2_l2 = sqrt of the sum)
+  // probe time series (driver.cpp:146-186, 226-236): times, and per probe
+  // the value at t = 0 and at samples_per_step points of every step
+  std::vector<double> probe_times;
+  std::vector<std::vector<double>> probe_values;
+};
+struct ProbeSpec {
+  std::vector<double> xyz;  // 3 per point
+  int samples_per_step = 16;
 };
 MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, double frequency, double* u, double* v,
-                  const GmresOptions& options, bool errors, cudaStream_t stream = nullptr);
+                  const GmresOptions& options, bool errors, cudaStream_t stream = nullptr,
+                  const ProbeSpec* probes = nullptr);
 
 class SpaceTimeMultigrid {
  public:

@@ -92,6 +92,9 @@ SIGNATURES = [
                                                c_double_p]),
     ("stmg_march", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
                              C.POINTER(GmresOptions), c_int_p, c_double_p, C.c_void_p]),
+    ("stmg_march_probes", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
+                                    C.POINTER(GmresOptions), c_int_p, c_double_p, C.c_int, c_double_p, C.c_int,
+                                    c_double_p, c_double_p, C.c_void_p]),
     # z-slab partitioned solve
     ("stmg_nccl_unique_id", C.c_int, [C.c_char_p]),
     ("stmg_comm_create", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_void_p]),

@@ -104,3 +104,40 @@ def test_march_heat_converges_at_the_expected_order(cuda):
         errs.append(out["error_u"][0])
     rates = [np.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
     assert all(rt >= 1.8 for rt in rates), (errs, rates)
+
+
+@pytest.mark.parametrize("name,r,n_batches", [("C1", 2, 3), ("C2", 2, 2)])
+def test_march_probes_match_reference(cuda, ref, name, r, n_batches):
+    """Probe time series (locate_point + value_at + evaluate_fe at every
+    sample, driver.cpp:146-236) of the device march vs the reference's own
+    functions on the reference's batch solutions: 1e-8 of the series' scale."""
+    cfg = problems.config(name, r)
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
+    M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps,
+                               cfg.tau)
+    R = ref.Reference(cfg, with_mg=True)
+    pts = np.array([[0.31, 0.47, 0.5], [0.73, 0.22, 0.61], [0.5, 0.5, 0.5]])
+    if cfg.dim == 2:
+        pts[:, 2] = 0.0
+    ns = 4
+    u = cuda.zeros(M.operator_at(0).n_space, dtype=cuda.float64, device="cuda")
+    out = M.march_probes(n_batches, u, pts, samples_per_step=ns, rel_tol=1e-10, abs_tol=0.0)
+    # the reference series on its own march loop
+    n_space = M.operator_at(0).n_space
+    uu = np.zeros(n_space)
+    want = [[0.0] for _ in pts]  # the entering state u(0) = 0
+    times = [0.0]
+    for b in range(n_batches):
+        t0 = b * cfg.n_steps * cfg.tau
+        x, _ = R.gmres(R.assemble_rhs(1, 0.5, t0, uu), rel_tol=1e-10, abs_tol=0.0)
+        for st in range(cfg.n_steps):
+            for j in range(1, ns + 1):
+                for pi, xp in enumerate(pts):
+                    want[pi].append(R.probe_value(x, uu, st, j / ns, xp))
+                times.append(t0 + (st + j / ns) * cfg.tau)
+        uu, _ = R.extract_final(x, uu)
+    want = np.array(want)
+    assert np.allclose(out["times"], times, rtol=0, atol=1e-14)
+    scale = float(np.abs(want).max())
+    assert scale > 0
+    assert float(np.abs(out["values"] - want).max()) <= 1e-8 * scale

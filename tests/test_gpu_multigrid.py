@@ -172,3 +172,36 @@ def test_asm_q4_perturbed_exact_blocks(cuda, ref, eq, scheme, k, S):
     for l, w in enumerate(R.level_info()):
         M.set_omega(l, w["omega"])
     assert _rel(M.apply(_dev(cuda, res)).cpu().numpy(), R.vcycle(res)) <= 1e-9
+
+
+@pytest.mark.parametrize("env,kind", [("STMG_NO_TDIAG", 2), ("STMG_ASM64", 6), ("STMG_ASM_NBUF", 6)])
+def test_asm_64dof_kernel_variants(cuda, ref, env, kind):
+    """Every 64-dof smoother kernel matches the reference: the pivoted
+    per-eigenvalue fallback (no temporal diagonalisation), the DFMA variant
+    and the 3-buffer record pipeline. Run in a subprocess because the
+    variant is chosen once per process from the environment."""
+    import os
+    import subprocess
+    import sys
+    val = {"STMG_NO_TDIAG": "1", "STMG_ASM64": "dfma", "STMG_ASM_NBUF": "3"}[env]
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import refbind as ref\n"
+        "from paper_2408_04372_b200 import api, problems\n"
+        "cfg = problems.config('C2', 2)\n"
+        "mesh = api.Mesh(cfg.dim, (0,0,0), (1,1,1), cfg.base_cells, cfg.refinements, cfg.vertices())\n"
+        "M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, None, cfg.refinements, cfg.p, cfg.k, cfg.n_steps, cfg.tau)\n"
+        "R = ref.Reference(cfg, with_mg=True)\n"
+        "r = problems.uniform_vector(R.n_dofs, seed=51); z0 = problems.uniform_vector(R.n_dofs, seed=52)\n"
+        "got = M.asm_add_correction(0, torch.from_numpy(r).cuda(), torch.from_numpy(z0).cuda()).cpu().numpy()\n"
+        "want = R.asm_add_correction(0, r, z0)\n"
+        "err = np.linalg.norm((got - z0) - (want - z0)) / np.linalg.norm(want - z0)\n"
+        f"assert M.smoother_kind(0) == {kind}, M.smoother_kind(0)\n"
+        "assert err <= 1e-9, err\n"
+        "print('ok', err)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env_vars = dict(os.environ, **{env: val}, PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env_vars, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok" in out.stdout

@@ -162,7 +162,7 @@ constexpr int warp_smem_doubles() {
 }
 
 template <int M, int NT>
-__global__ void __launch_bounds__(256) asm_apply_warp_kernel(const __grid_constant__ DevASM A,
+__global__ void __launch_bounds__(256, 3) asm_apply_warp_kernel(const __grid_constant__ DevASM A,
                                                              const double* __restrict__ r, double* __restrict__ z,
                                                              double scale) {
   static_assert(M <= 32, "one lane per local dof");

@@ -77,8 +77,12 @@ constexpr bool fits() {
   return N * F <= 16 && Cfg<N, F>::smem_bytes() <= 100 * 1024;
 }
 
+template <int N>
+constexpr int lines_min_blocks() {
+  return N <= 3 ? 4 : 3;
+}
 template <int N, int F, bool CART>
-__global__ void __launch_bounds__(kT, 3) st_lines_kernel(const __grid_constant__ DevLevel L,
+__global__ void __launch_bounds__(kT, lines_min_blocks<N>()) st_lines_kernel(const __grid_constant__ DevLevel L,
                                                          const double* __restrict__ u, double* __restrict__ y,
                                                          double sign) {
   using C = Cfg<N, F>;

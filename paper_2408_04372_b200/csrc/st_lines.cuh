@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kT, lines_min_blocks<N>()) st_lines_kernel(con
   const int p = N - 1;
   long long base = 0;
   int mask = 0;
+  double gin[F][N];  // this thread's y-line of every field, requested first
   if (valid) {
     const unsigned ci = static_cast<unsigned>(cell);
     const unsigned nx = static_cast<unsigned>(L.cells[0]), ny = static_cast<unsigned>(L.cells[1]);
@@ -114,6 +115,16 @@ __global__ void __launch_bounds__(kT, lines_min_blocks<N>()) st_lines_kernel(con
     base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx + static_cast<long long>(cx) * p;
     mask = (cx == 0 ? 1 : 0) | (cx == nx - 1 ? 2 : 0) | (cy == 0 ? 4 : 0) | (cy == ny - 1 ? 8 : 0) |
            (cz == 0 && (L.zbc & 1) ? 16 : 0) | (cz == L.cells[2] - 1 && (L.zbc & 2) ? 32 : 0);
+    // the gather is issued before the vertex / coefficient loads and their
+    // shared-memory stores, so the two DRAM round trips overlap
+#pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const bool dir = ((mask & 1) && a == 0) || ((mask & 2) && a == p) || ((mask & 4) && k == 0) ||
+                         ((mask & 8) && k == p) || ((mask & 16) && b == 0) || ((mask & 32) && b == p);
+        gin[f][k] = dir ? 0.0 : __ldg(u + f * L.n_space + base + b * dxy + k * dx + a);
+      }
     if (L.verts) {
       const long long vx = L.cells[0] + 1, vy = L.cells[1] + 1;
       for (int s = l; s < 8; s += NL) {
@@ -147,17 +158,13 @@ __global__ void __launch_bounds__(kT, lines_min_blocks<N>()) st_lines_kernel(con
   if (valid) {
 #pragma unroll
     for (int f = 0; f < F; ++f) {
-      double in[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k)
-        in[k] = dirichlet(a, k, b) ? 0.0 : __ldg(u + f * L.n_space + base + b * dxy + k * dx + a);
 #pragma unroll
       for (int q = 0; q < N; ++q) {
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          s0 = fma(L.B[q][k], in[k], s0);
-          s1 = fma(L.D[q][k], in[k], s1);
+          s0 = fma(L.B[q][k], gin[f][k], s0);
+          s1 = fma(L.D[q][k], gin[f][k], s1);
         }
         A0[oy + f * SD + q * RY] = s0;
         A1[oy + f * SD + q * RY] = s1;

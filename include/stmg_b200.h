@@ -77,7 +77,8 @@ int stmg_st_operator_residual(const stmg_st_operator* op, const double* d_f, con
  * support points into d_out (n_space): kind 0 manufactured heat source,
  * 1 manufactured wave source, 2 Gaussian exp(-|x-centre|^2/(2 width^2)),
  * 3 manufactured solution, 4 manufactured velocity (driver.cpp:265-293,
- * omega = 2 pi frequency); zero_boundary sets the Dirichlet entries to 0 */
+ * omega = 2 pi frequency), 5 the shm pulse exp(-r^2)(1-r^2), r = |x|/width < 1
+ * (driver.cpp:295-316); zero_boundary sets the Dirichlet entries to 0 */
 int stmg_st_operator_interpolate(const stmg_st_operator* op, int kind, double frequency, double t,
                                  const double centre[3], double width, int zero_boundary, double* d_out,
                                  void* stream);
@@ -201,6 +202,64 @@ int stmg_march(const stmg_multigrid* mg, int n_batches, int source_kind, double 
 int stmg_march_probes(const stmg_multigrid* mg, int n_batches, int source_kind, double frequency, double* d_u,
                       double* d_v, const stmg_gmres_options* options, int* iterations, double errors[3], int n_probes,
                       const double* probe_xyz, int samples_per_step, double* times, double* values, void* stream);
+
+/* ---- configured runs: the reference's ProblemSpec -> march(spec, probes)
+ * -> RunReport (include/stmg/driver.hpp:14-91, src/driver.cpp:95-262), with
+ * the mesh perturbation (src/mesh.cpp:190-240), coefficient fields
+ * (src/mesh.cpp:254-298) and problem families (src/driver.cpp:265-320) it
+ * builds on. The config front end (src/config.cpp) and the report writer
+ * (tools/stmg.cpp) sit above this, in paper_2408_04372_b200/config.py,
+ * report.py and cli.py. */
+typedef struct {
+  int equation, scheme;
+  int problem; /* 0 manufactured, 1 shm, 2 zero */
+  int k, p, dim;
+  double lo[3], hi[3];
+  double t_final;
+  int refinements, base_cells, base_time_intervals, batch;
+  double frequency, shm_s, perturb;
+  unsigned long long seed;
+  double rho_random_lo, rho_random_hi;
+  double abs_tol, rel_tol;
+  int max_iters, restart, n_smooth, precondition, probe_samples_per_step;
+  int n_strategy; /* 0 = default ordering */
+  int strategy[32];
+  int timers; /* record the profile sections */
+} stmg_problem;
+typedef struct {
+  int converged;
+  long long n_space_dofs;
+  int n_steps_total, n_batches;
+  long long dofs_global;
+  int n_batches_run; /* entries written to the batch arrays */
+  double mean_iterations, work;
+  int has_error_u, has_error_v;
+  double error_u[3], error_v[3]; /* l2_l2, linf_l2, linf_linf */
+  int n_levels;
+  /* total, smoother, gmg_wo_smoother, operator_wo_gmg, other (seconds) */
+  double sections[5];
+  long long n_probe_samples; /* per probe, t = 0 included */
+} stmg_run_report;
+/* the step and batch counts of a problem (no device work): n_steps_total =
+ * base_time_intervals * 2^(refinements+1), n_batches = n_steps_total / batch */
+int stmg_problem_sizes(const stmg_problem* spec, int* n_steps_total, int* n_batches, long long* n_probe_samples);
+/* one run. Batch arrays hold batch_cap entries, level arrays level_cap
+ * (level_ints: coarsening 0..3 or -1 for the finest, mesh_level, p, k,
+ * n_steps per level), probe arrays probe_cap samples per probe (probe-major).
+ * Returns 0 also when a batch did not converge (report->converged == 0). */
+int stmg_run(const stmg_problem* spec, int n_probes, const double* probe_xyz, stmg_run_report* report, int batch_cap,
+             int* batch_iterations, double* batch_residuals, int* batch_converged, int level_cap, int* level_ints,
+             long long* level_dofs, double* level_omega, long long probe_cap, double* probe_times,
+             double* probe_values);
+/* host-only: the level plan build_level_plan(finest, scheme, strategy)
+ * (multigrid.cpp:34-81) of (fine_mesh_level, p, k, n_steps, tau);
+ * n_strategy < 0 = default_strategy. ints: 5 per level as stmg_run. */
+int stmg_level_plan(int scheme, int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
+                    const int* strategy, int cap, int* n_levels, int* ints, double* taus);
+/* host-only: the finest-level vertices of make_cartesian + perturb
+ * (src/mesh.cpp:148-240), 3 per vertex, x fastest */
+int stmg_perturbed_vertices(int dim, const double lo[3], const double hi[3], int base_cells, int refinements,
+                            double magnitude, unsigned long long seed, double* xyz);
 
 /* ---- z-slab partitioned solve over several GPUs (no
  * reference counterpart: the reference is single-process). The finest mesh

@@ -8,7 +8,10 @@
 #include <string>
 #include <vector>
 
+#include <json.hpp>
+
 #include "stmg/asm_smoother.hpp"
+#include "stmg/config.hpp"
 #include "stmg/driver.hpp"
 #include "stmg/gmres.hpp"
 #include "stmg/multigrid.hpp"
@@ -421,6 +424,77 @@ int ref_quadrature(int kind, int n, double* pts, double* wts) {
       pts[i] = q.points[static_cast<std::size_t>(i)];
       wts[i] = q.weights[static_cast<std::size_t>(i)];
     }
+  });
+}
+
+// ---- configured runs (src/config.cpp + march, src/driver.cpp:95-262): the
+// run report in the key layout of the stmg tool's report_to_json
+// (tools/stmg.cpp:30-62), plus the probe series, for parity of the device run
+namespace {
+nlohmann::json run_to_json(const RunReport& r) {
+  using nlohmann::json;
+  json batches = json::array();
+  for (const BatchStats& b : r.batches)
+    batches.push_back({{"iterations", b.iterations}, {"final_residual", b.final_residual}, {"converged", b.converged}});
+  json hierarchy = json::array();
+  for (const LevelInfo& l : r.hierarchy)
+    hierarchy.push_back({{"coarsening", l.coarsening}, {"mesh_level", l.mesh_level}, {"p", l.p}, {"k", l.k},
+                         {"n_steps", l.n_steps}, {"n_dofs", l.n_dofs}, {"omega", l.omega}});
+  json out{{"converged", r.converged},       {"n_space_dofs", r.n_space_dofs}, {"n_steps_total", r.n_steps_total},
+           {"n_batches", r.n_batches},       {"dofs_global", r.dofs_global},   {"mean_iterations", r.mean_iterations},
+           {"work", r.work},                 {"batches", batches},             {"hierarchy", hierarchy},
+           {"probe_times", r.probe_times},   {"probe_values", r.probe_values}};
+  auto err = [](const ErrorRecord& e) {
+    return json{{"l2_l2", e.l2_l2}, {"linf_l2", e.linf_l2}, {"linf_linf", e.linf_linf}};
+  };
+  if (r.error_u) out["error_u"] = err(*r.error_u);
+  if (r.error_v) out["error_v"] = err(*r.error_v);
+  return out;
+}
+int put(const std::string& s, char* out, long cap) {
+  if (static_cast<long>(s.size()) + 1 > cap) {
+    g_err = "output buffer too small (" + std::to_string(s.size() + 1) + " bytes needed)";
+    return -2;
+  }
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
+}
+}  // namespace
+
+// parse_config + make_problem + march(spec, resolve_probes) at refinement r
+// (r < 0: config.refinements)
+int ref_run_json(const char* config_json, int refinement, char* out, long cap) {
+  std::string s;
+  const int rc = guard([&] {
+    const Config c = parse_config(config_json);
+    const ProblemSpec spec = make_problem(c, refinement < 0 ? c.refinements : refinement);
+    s = run_to_json(march(spec, resolve_probes(c))).dump();
+  });
+  return rc != 0 ? rc : put(s, out, cap);
+}
+
+// parse_config, the --set overrides (apply_override), config_to_json
+// (src/config.cpp:87-160); returns -1 with the message on invalid input
+int ref_config_json(const char* config_json, int n_overrides, const char* const* keys, const char* const* values,
+                    char* out, long cap) {
+  std::string s;
+  const int rc = guard([&] {
+    Config c = parse_config(config_json);
+    for (int i = 0; i < n_overrides; ++i) apply_override(c, keys[i], values[i]);
+    s = config_to_json(c).dump();
+  });
+  return rc != 0 ? rc : put(s, out, cap);
+}
+
+// make_cartesian + perturb (src/mesh.cpp:148-240): finest vertices
+int ref_perturbed_vertices(int dim, const double* lo, const double* hi, int base_cells, int refinements,
+                           double magnitude, std::uint64_t seed, double* xyz) {
+  return guard([&] {
+    MeshHierarchy m = make_cartesian(dim, {lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}, base_cells, refinements);
+    perturb(m, magnitude, seed);
+    const MeshLevel& f = m.levels.back();
+    for (std::size_t v = 0; v < f.vertices.size(); ++v)
+      for (int a = 0; a < 3; ++a) xyz[3 * v + a] = f.vertices[v][a];
   });
 }
 

@@ -80,6 +80,10 @@ def load() -> C.CDLL:
     lib.ref_temporal_weights.argtypes = [C.c_int, C.c_int, dp, dp, dp, dp, dp]
     lib.ref_quadrature.argtypes = [C.c_int, C.c_int, dp, dp]
     lib.ref_block_coefficients.argtypes = [C.c_void_p, C.c_int, C.c_int, dp, dp]
+    lib.ref_run_json.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_long]
+    lib.ref_config_json.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), C.c_char_p,
+                                    C.c_long]
+    lib.ref_perturbed_vertices.argtypes = [C.c_int, dp, dp, C.c_int, C.c_int, C.c_double, C.c_uint64, dp]
     _lib = lib
     return lib
 
@@ -279,3 +283,35 @@ def quadrature(kind: int, n: int):
     p, w = np.zeros(n), np.zeros(n)
     _chk(load().ref_quadrature(kind, n, _p(p), _p(w)))
     return p, w
+
+
+def run_json(config: dict, refinement: int = -1) -> dict:
+    """The reference's march over a config (parse_config, make_problem,
+    resolve_probes; src/config.cpp, src/driver.cpp:95-262) as a report dict."""
+    import json
+    buf = C.create_string_buffer(1 << 24)
+    _chk(load().ref_run_json(json.dumps(config).encode(), refinement, buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def config_json(config_text: str, overrides=()) -> dict:
+    """parse_config + apply_override + config_to_json of the reference;
+    raises ValueError with the reference's message on invalid input."""
+    import json
+    keys = (C.c_char_p * max(1, len(overrides)))(*[k.encode() for k, _ in overrides])
+    vals = (C.c_char_p * max(1, len(overrides)))(*[v.encode() for _, v in overrides])
+    buf = C.create_string_buffer(1 << 16)
+    rc = load().ref_config_json(config_text.encode(), len(overrides), keys, vals, buf, len(buf))
+    if rc != 0:
+        raise ValueError(load().ref_last_error().decode())
+    return json.loads(buf.value.decode())
+
+
+def perturbed_vertices(dim: int, lo, hi, base_cells: int, refinements: int, magnitude: float, seed: int):
+    n = (base_cells << refinements) + 1
+    nv = n ** dim
+    out = np.zeros(3 * nv)
+    lo_a = np.asarray(lo, dtype=np.float64)
+    hi_a = np.asarray(hi, dtype=np.float64)
+    _chk(load().ref_perturbed_vertices(dim, _p(lo_a), _p(hi_a), base_cells, refinements, magnitude, seed, _p(out)))
+    return out.reshape(nv, 3)

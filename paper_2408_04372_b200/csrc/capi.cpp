@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "run.hpp"
 #include "slab_mg.hpp"
 #include "stmg.hpp"
 
@@ -191,7 +192,7 @@ int stmg_st_operator_interpolate(const stmg_st_operator* op, int kind, double fr
                                  const double centre[3], double width, int zero_boundary, double* d_out,
                                  void* stream) {
   return guard([&] {
-    if (!op || !d_out || kind < 0 || kind > 4) throw std::invalid_argument("stmg_st_operator_interpolate: bad argument");
+    if (!op || !d_out || kind < 0 || kind > 5) throw std::invalid_argument("stmg_st_operator_interpolate: bad argument");
     op->op->interpolate(kind, frequency, t, centre, width, zero_boundary != 0, d_out, st(stream));
   });
 }
@@ -562,6 +563,182 @@ int stmg_march_probes(const stmg_multigrid* mg, int n_batches, int source_kind, 
     return -2;
   }
   return rc;
+}
+
+namespace {
+ProblemSpec problem_spec(const stmg_problem* p) {
+  if (!p) throw std::invalid_argument("stmg_problem: null argument");
+  if (p->equation < 0 || p->equation > 1 || p->scheme < 0 || p->scheme > 1 || p->problem < 0 || p->problem > 2)
+    throw std::invalid_argument("stmg_problem: bad equation, scheme or problem");
+  if (p->n_strategy < 0 || p->n_strategy > 32) throw std::invalid_argument("stmg_problem: bad strategy length");
+  ProblemSpec s;
+  s.equation = static_cast<Equation>(p->equation);
+  s.scheme = static_cast<TimeScheme>(p->scheme);
+  s.problem = static_cast<ProblemKind>(p->problem);
+  s.k = p->k;
+  s.p = p->p;
+  s.dim = p->dim;
+  for (int a = 0; a < 3; ++a) {
+    s.lo[a] = p->lo[a];
+    s.hi[a] = p->hi[a];
+  }
+  s.t_final = p->t_final;
+  s.refinements = p->refinements;
+  s.base_cells = p->base_cells;
+  s.base_time_intervals = p->base_time_intervals;
+  s.batch = p->batch;
+  s.frequency = p->frequency;
+  s.shm_s = p->shm_s;
+  s.perturb = p->perturb;
+  s.seed = p->seed;
+  s.rho_random_lo = p->rho_random_lo;
+  s.rho_random_hi = p->rho_random_hi;
+  s.abs_tol = p->abs_tol;
+  s.rel_tol = p->rel_tol;
+  s.max_iters = p->max_iters;
+  s.restart = p->restart;
+  s.n_smooth = p->n_smooth;
+  s.precondition = p->precondition != 0;
+  s.probe_samples_per_step = p->probe_samples_per_step;
+  for (int i = 0; i < p->n_strategy; ++i) {
+    if (p->strategy[i] < 0 || p->strategy[i] > 3) throw std::invalid_argument("stmg_problem: unknown coarsening");
+    s.strategy.push_back(static_cast<Coarsening>(p->strategy[i]));
+  }
+  s.timers = p->timers != 0;
+  return s;
+}
+int coarsening_code(const std::string& name) {
+  if (name == "space-h") return 0;
+  if (name == "space-p") return 1;
+  if (name == "time-tau") return 2;
+  if (name == "time-k") return 3;
+  return -1;  // "finest"
+}
+}  // namespace
+
+int stmg_problem_sizes(const stmg_problem* spec, int* n_steps_total, int* n_batches, long long* n_probe_samples) {
+  return guard_host([&] {
+    const ProblemSpec s = problem_spec(spec);
+    if (s.refinements < 0 || s.refinements > 24 || s.base_time_intervals < 1)
+      throw std::invalid_argument("stmg_problem_sizes: bad refinements or time intervals");
+    const int nst = s.base_time_intervals << (s.refinements + 1);
+    if (s.batch < 1 || nst % s.batch != 0) throw std::invalid_argument("march: batch must divide the step count");
+    if (n_steps_total) *n_steps_total = nst;
+    if (n_batches) *n_batches = nst / s.batch;
+    if (n_probe_samples) *n_probe_samples = 1 + static_cast<long long>(nst) * std::max(0, s.probe_samples_per_step);
+  });
+}
+
+int stmg_run(const stmg_problem* spec, int n_probes, const double* probe_xyz, stmg_run_report* report, int batch_cap,
+             int* batch_iterations, double* batch_residuals, int* batch_converged, int level_cap, int* level_ints,
+             long long* level_dofs, double* level_omega, long long probe_cap, double* probe_times,
+             double* probe_values) {
+  return guard([&] {
+    if (!report) throw std::invalid_argument("stmg_run: null report");
+    if (n_probes < 0 || (n_probes > 0 && (!probe_xyz || !probe_times || !probe_values)))
+      throw std::invalid_argument("stmg_run: bad probe arguments");
+    const ProblemSpec s = problem_spec(spec);
+    if (n_probes > 0 && s.probe_samples_per_step < 1)
+      throw std::invalid_argument("stmg_run: probe_samples_per_step must be >= 1");
+    const std::vector<double> probes(probe_xyz, probe_xyz + 3 * n_probes);
+    const RunReport r = run_march(s, probes, nullptr);
+    std::memset(report, 0, sizeof(*report));
+    report->converged = r.converged ? 1 : 0;
+    report->n_space_dofs = r.n_space_dofs;
+    report->n_steps_total = r.n_steps_total;
+    report->n_batches = r.n_batches;
+    report->dofs_global = r.dofs_global;
+    report->n_batches_run = static_cast<int>(r.batches.size());
+    report->mean_iterations = r.mean_iterations;
+    report->work = r.work;
+    report->has_error_u = r.has_error_u ? 1 : 0;
+    report->has_error_v = r.has_error_v ? 1 : 0;
+    const ErrorRecord* er[2] = {&r.error_u, &r.error_v};
+    double* eo[2] = {report->error_u, report->error_v};
+    for (int i = 0; i < 2; ++i) {
+      eo[i][0] = er[i]->l2_l2;
+      eo[i][1] = er[i]->linf_l2;
+      eo[i][2] = er[i]->linf_linf;
+    }
+    report->n_levels = static_cast<int>(r.hierarchy.size());
+    report->sections[0] = r.sections.total;
+    report->sections[1] = r.sections.smoother;
+    report->sections[2] = r.sections.gmg_wo_smoother;
+    report->sections[3] = r.sections.operator_wo_gmg;
+    report->sections[4] = r.sections.other;
+    report->n_probe_samples = static_cast<long long>(r.probe_times.size());
+    for (int b = 0; b < std::min(batch_cap, report->n_batches_run); ++b) {
+      const BatchStats& bs = r.batches[static_cast<size_t>(b)];
+      if (batch_iterations) batch_iterations[b] = bs.iterations;
+      if (batch_residuals) batch_residuals[b] = bs.final_residual;
+      if (batch_converged) batch_converged[b] = bs.converged ? 1 : 0;
+    }
+    for (int l = 0; l < std::min(level_cap, report->n_levels); ++l) {
+      const LevelInfo& li = r.hierarchy[static_cast<size_t>(l)];
+      if (level_ints) {
+        int* o = level_ints + 5 * l;
+        o[0] = coarsening_code(li.coarsening);
+        o[1] = li.mesh_level;
+        o[2] = li.p;
+        o[3] = li.k;
+        o[4] = li.n_steps;
+      }
+      if (level_dofs) level_dofs[l] = li.n_dofs;
+      if (level_omega) level_omega[l] = li.omega;
+    }
+    const long long ns = std::min<long long>(probe_cap, report->n_probe_samples);
+    for (long long i = 0; i < ns && n_probes > 0; ++i) probe_times[i] = r.probe_times[static_cast<size_t>(i)];
+    for (int p = 0; p < n_probes; ++p)
+      for (long long i = 0; i < ns; ++i)
+        probe_values[static_cast<long long>(p) * probe_cap + i] =
+            r.probe_values[static_cast<size_t>(p)][static_cast<size_t>(i)];
+  });
+}
+
+int stmg_level_plan(int scheme, int fine_mesh_level, int p, int k, int n_steps, double tau, int n_strategy,
+                    const int* strategy, int cap, int* n_levels, int* ints, double* taus) {
+  return guard_host([&] {
+    if (!n_levels || (n_strategy > 0 && !strategy)) throw std::invalid_argument("stmg_level_plan: null argument");
+    if (scheme < 0 || scheme > 1) throw std::invalid_argument("stmg_level_plan: bad scheme");
+    for (int i = 0; i < n_strategy; ++i)
+      if (strategy[i] < 0 || strategy[i] > 3) throw std::invalid_argument("stmg_level_plan: unknown coarsening");
+    const auto plan = mg_plan(scheme, fine_mesh_level, p, k, n_steps, tau, n_strategy, strategy);
+    *n_levels = static_cast<int>(plan.size());
+    for (int l = 0; l < std::min(cap, *n_levels); ++l) {
+      const LevelSpec& ls = plan[static_cast<size_t>(l)];
+      if (ints) {
+        int* o = ints + 5 * l;
+        o[0] = l == 0 ? -1 : static_cast<int>(ls.from_finer);
+        o[1] = ls.mesh_level;
+        o[2] = ls.p;
+        o[3] = ls.k;
+        o[4] = ls.n_steps;
+      }
+      if (taus) taus[l] = ls.tau;
+    }
+  });
+}
+
+int stmg_perturbed_vertices(int dim, const double lo[3], const double hi[3], int base_cells, int refinements,
+                            double magnitude, unsigned long long seed, double* xyz) {
+  return guard_host([&] {
+    if (!lo || !hi || !xyz) throw std::invalid_argument("stmg_perturbed_vertices: null argument");
+    MeshHierarchy m = make_cartesian(dim, {lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}, base_cells, refinements);
+    const MeshLevel& f = m.levels.back();
+    perturb_mesh(m, magnitude, seed);
+    if (f.vertices.empty()) {
+      // magnitude 0: the Cartesian lattice
+      const auto n = f.n_verts_axis();
+      for (Index kk = 0; kk < n[2]; ++kk)
+        for (Index j = 0; j < n[1]; ++j)
+          for (Index i = 0; i < n[0]; ++i) {
+            const Index vi = (kk * n[1] + j) * n[0] + i, idx[3] = {i, j, kk};
+            for (int a = 0; a < 3; ++a) xyz[3 * vi + a] = a < dim ? cartesian_coord(f, a, idx[a]) : 0.0;
+          }
+    } else {
+      std::copy(f.vertices.begin(), f.vertices.end(), xyz);
+    }
+  });
 }
 
 int stmg_nccl_unique_id(char id[128]) {

@@ -15,7 +15,8 @@
 namespace stmgb {
 
 constexpr int kMaxN = 5;   // p <= 4
-constexpr int kMaxF = 8;   // S * n_t <= 8
+constexpr int kMaxF = 8;   // S * n_t <= 8 in the fused kernels
+constexpr int kMaxWideF = 64;  // composed (wide-batch) application
 
 struct DevLevel {
   int dim;

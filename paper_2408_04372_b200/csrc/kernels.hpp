@@ -13,6 +13,12 @@ void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream
 void st_zero_boundary(const DevLevel& L, double* v, cudaStream_t stream);
 // r = f - S u (overwrite), fused residual (no separate subtraction pass)
 void st_residual(const DevLevel& L, const double* f, const double* u, double* r, cudaStream_t stream);
+// S * n_t > kMaxF: 2F single-field applications of the constrained mass and
+// stiffness (descriptors mass / stiff) into mu / au (F * n_space each), then
+// the temporal combination with the full F x F CM / CA (device, row-major);
+// f != nullptr gives the residual f - S u
+void st_apply_wide(const DevLevel& L, const DevLevel& mass, const DevLevel& stiff, const double* cm, const double* ca,
+                   const double* f, const double* u, double* y, double* mu, double* au, cudaStream_t stream);
 
 // nodal interpolant at the Q_p support points (rhs.cu); kind: 0 heat source,
 // 1 wave source, 2 Gaussian(centre, width), 3 manufactured u, 4 manufactured v

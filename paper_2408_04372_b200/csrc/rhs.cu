@@ -54,6 +54,8 @@ __device__ void node_position(const DevLevel& L, const double* gl, long long g, 
 // kind 3: manufactured solution     sin(om t) prod sin(om x_a)
 // kind 4: manufactured velocity     om cos(om t) prod sin(om x_a)
 // (driver.cpp:265-293 with om = 2 pi frequency)
+// kind 5: the compact pulse of shm_problem (driver.cpp:295-316), r = |x| / width:
+//         exp(-r^2) (1 - r^2) for r < 1, else 0
 __global__ void interpolate_kernel(const __grid_constant__ DevLevel L, int kind, double om, double t, double cx,
                                    double cy, double cz, double width, bool zero_bdry, double* __restrict__ out) {
   const long long n = L.n_space;
@@ -66,6 +68,10 @@ __global__ void interpolate_kernel(const __grid_constant__ DevLevel L, int kind,
       const double r2 = (x[0] - cx) * (x[0] - cx) + (L.dim > 1 ? (x[1] - cy) * (x[1] - cy) : 0.0) +
                         (L.dim > 2 ? (x[2] - cz) * (x[2] - cz) : 0.0);
       v = exp(-r2 / (2.0 * width * width));
+    } else if (kind == 5) {
+      double r2 = 0.0;
+      for (int a = 0; a < L.dim; ++a) r2 += (x[a] / width) * (x[a] / width);
+      v = r2 >= 1.0 ? 0.0 : exp(-r2) * (1.0 - r2);
     } else {
       double sp = 1.0;
       for (int a = 0; a < L.dim; ++a) sp *= sin(om * x[a]);

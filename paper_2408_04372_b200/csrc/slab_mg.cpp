@@ -178,6 +178,11 @@ SlabMultigrid::SlabMultigrid(Equation equation, TimeScheme scheme, const MeshHie
   if (L < 0 || L >= global.n_levels()) throw std::invalid_argument("SlabMultigrid: bad finest mesh level");
   const MeshLevel& gf = global.levels[static_cast<size_t>(L)];
   if (gf.dim != 3) throw std::invalid_argument("SlabMultigrid: the z-slab partition needs dim == 3");
+  {
+    const int nt = scheme == TimeScheme::DG ? plan[0].k + 1 : plan[0].k;
+    if (plan[0].n_steps * nt > kMaxF)
+      throw std::invalid_argument("SlabMultigrid: the partitioned solve needs n_steps * n_t <= 8");
+  }
   plan_ = make_slab_plan(plan, gf.cells[2], L, n_parts);
   if (first_part < 0 || local_parts < 1 || first_part + local_parts > n_parts)
     throw std::invalid_argument("SlabMultigrid: bad local part range");

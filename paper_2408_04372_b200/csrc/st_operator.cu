@@ -76,6 +76,50 @@ void run(const DevLevel& L, const double* f, const double* u, double* y, cudaStr
 }  // namespace
 
 void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream) { run(L, nullptr, u, y, stream); }
+
+namespace {
+// y_f += sign * sum_g CM[f][g] (M u_g) + CA[f][g] (A u_g): the temporal
+// combination of the reference's apply (space_time_operator.cpp:59-89);
+// zero coefficients are skipped (uniform branch)
+__global__ void wide_combine_kernel(int F, long long n_space, double sign, const double* __restrict__ cm,
+                                    const double* __restrict__ ca, const double* __restrict__ mu,
+                                    const double* __restrict__ au, double* __restrict__ y) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_space;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    for (int f = 0; f < F; ++f) {
+      double s = 0.0;
+      for (int g = 0; g < F; ++g) {
+        const double a = __ldg(cm + f * F + g), b = __ldg(ca + f * F + g);
+        if (a != 0.0) s = fma(a, __ldg(mu + g * n_space + i), s);
+        if (b != 0.0) s = fma(b, __ldg(au + g * n_space + i), s);
+      }
+      y[f * n_space + i] += sign * s;
+    }
+}
+}  // namespace
+
+void st_apply_wide(const DevLevel& L, const DevLevel& mass, const DevLevel& stiff, const double* cm, const double* ca,
+                   const double* f, const double* u, double* y, double* mu, double* au, cudaStream_t stream) {
+  const long long ns = L.n_space;
+  for (int g = 0; g < L.F; ++g) {
+    run(mass, nullptr, u + g * ns, mu + g * ns, stream);
+    run(stiff, nullptr, u + g * ns, au + g * ns, stream);
+  }
+  if (f) {
+    vec_copy(y, f, L.n_dofs, stream);
+    if (L.dim == 3 && !(L.zbc & 1)) plane_fill(y, L.F, L.n_space, 0, L.dofs[0] * L.dofs[1], 0.0, stream);
+  } else {
+    cudaMemsetAsync(y, 0, sizeof(double) * L.n_dofs, stream);
+  }
+  const unsigned grid = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((ns + 255) / 256, 148LL * 8)));
+  count_launch();
+  wide_combine_kernel<<<grid, 256, 0, stream>>>(L.F, ns, f ? -1.0 : 1.0, cm, ca, mu, au, y);
+  const long long faces = 2 * (L.dofs[1] * L.dofs[2] + L.dofs[0] * L.dofs[2] + (L.dim == 3 ? L.dofs[0] * L.dofs[1] : 0));
+  const unsigned blocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((faces + 255) / 256, 148LL * 8)));
+  count_launch();
+  boundary_identity_kernel<<<blocks, 256, 0, stream>>>(L.dim, L.dim == 3 ? L.zbc : 3, L.dofs[0], L.dofs[1], L.dofs[2],
+                                                       L.n_space, L.F, f, u, y);
+}
 void st_zero_boundary(const DevLevel& L, double* v, cudaStream_t stream) {
   const long long faces = 2 * (L.dofs[1] * L.dofs[2] + L.dofs[0] * L.dofs[2] + (L.dim == 3 ? L.dofs[0] * L.dofs[1] : 0));
   const unsigned blocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((faces + 255) / 256, 148LL * 8)));

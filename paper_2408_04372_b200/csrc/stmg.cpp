@@ -76,7 +76,8 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
   if (mesh_level < 0 || mesh_level >= mesh.n_levels()) throw std::invalid_argument("SpaceTimeOperator: bad level");
   if (p < 1 || p + 1 > kMaxN) throw std::invalid_argument("SpaceTimeOperator: p must be in [1, 4]");
   const int F = n_steps * weights.n_t;
-  if (F > kMaxF) throw std::invalid_argument("SpaceTimeOperator: n_steps * n_t must be <= 8");
+  if (F > kMaxWideF) throw std::invalid_argument("SpaceTimeOperator: n_steps * n_t must be <= 64");
+  wide_ = F > kMaxF;
   const MeshLevel& m = mesh.levels[static_cast<size_t>(mesh_level)];
   mesh_level_ptr_ = &m;
   if (m.dim < 2 || m.dim > 3) throw std::invalid_argument("SpaceTimeOperator: dim must be 2 or 3");
@@ -136,8 +137,19 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
   block_coefficient_matrices(equation, weights, tau, n_steps, CM, CA);
   std::memset(d.CM, 0, sizeof(d.CM));
   std::memset(d.CA, 0, sizeof(d.CA));
-  std::copy(CM.begin(), CM.end(), d.CM);
-  std::copy(CA.begin(), CA.end(), d.CA);
+  if (!wide_) {
+    std::copy(CM.begin(), CM.end(), d.CM);
+    std::copy(CA.begin(), CA.end(), d.CA);
+  } else {
+    // the fused kernels hold at most kMaxF fields: wide batches compose 2F
+    // single-field applications (st_apply_wide) with the full tables
+    wide_cm_ = upload(CM);
+    wide_ca_ = upload(CA);
+    wide_mu_.allocate(sizeof(double) * static_cast<size_t>(d.n_dofs));
+    wide_au_.allocate(sizeof(double) * static_cast<size_t>(d.n_dofs));
+  }
+  cm_ = CM;
+  ca_ = CA;
   // single-field spatial mass / stiffness (SpatialOperator::apply)
   mass_desc_ = desc_;
   mass_desc_.S = mass_desc_.nt = mass_desc_.F = 1;
@@ -151,12 +163,20 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
 
 void SpaceTimeOperator::apply(const double* u, double* y, cudaStream_t stream) const {
   ++apply_count_;
-  st_apply(desc_, u, y, stream);
+  if (wide_)
+    st_apply_wide(desc_, mass_desc_, stiff_desc_, wide_cm_.d(), wide_ca_.d(), nullptr, u, y, wide_mu_.d(),
+                  wide_au_.d(), stream);
+  else
+    st_apply(desc_, u, y, stream);
 }
 
 void SpaceTimeOperator::residual(const double* f, const double* u, double* r, cudaStream_t stream) const {
   ++apply_count_;
-  st_residual(desc_, f, u, r, stream);
+  if (wide_)
+    st_apply_wide(desc_, mass_desc_, stiff_desc_, wide_cm_.d(), wide_ca_.d(), f, u, r, wide_mu_.d(), wide_au_.d(),
+                  stream);
+  else
+    st_residual(desc_, f, u, r, stream);
 }
 
 void SpaceTimeOperator::spatial_apply(int kind, const double* u, double* y, cudaStream_t stream) const {
@@ -312,6 +332,38 @@ void SpaceTimeOperator::extract_final(const double* u, const double* u0, const d
   }
   vec_copy(vf, vl.d(), nx, s);
   cuda_check(cudaStreamSynchronize(s), "extract_final");
+}
+
+void SpaceTimeOperator::velocity_trajectory(const double* u, const double* u0, const double* v0, double* vout,
+                                            cudaStream_t s) const {
+  if (equation_ != Equation::Wave) throw std::invalid_argument("velocity_trajectory: wave equation only");
+  if (!u || !u0 || !v0 || !vout) throw std::invalid_argument("velocity_trajectory: null argument");
+  const int S = n_steps_, nt = weights_.n_t;
+  const Index nx = n_space();
+  const bool cgp = weights_.scheme == TimeScheme::CGP;
+  const std::vector<double> minv = invert_small(weights_.m, nt);
+  const std::vector<double> minv_a = matmul_small(minv, weights_.a, nt, nt, nt);
+  const std::vector<double> minv_alpha = matmul_small(minv, weights_.alpha, nt, nt, 1);
+  const std::vector<double> minv_beta =
+      cgp ? matmul_small(minv, weights_.beta, nt, nt, 1) : std::vector<double>(static_cast<size_t>(nt), 0.0);
+  // v_{s,i} = sum_j (M^-1 A)_ij / tau u_{s,j} + history of the previous step
+  const double* prev_last = u0;
+  const double* v_prev_last = v0;
+  for (int st = 0; st < S; ++st) {
+    for (int i = 0; i < nt; ++i) {
+      double* vi = vout + block_offset(st, i);
+      vec_fill(vi, 0.0, nx, s);
+      for (int j = 0; j < nt; ++j) vec_axpy(vi, minv_a[i * nt + j] / tau_, u + block_offset(st, j), nx, s);
+      if (cgp) {
+        vec_axpy(vi, minv_alpha[i] / tau_, prev_last, nx, s);
+        vec_axpy(vi, -minv_beta[i], v_prev_last, nx, s);
+      } else {
+        vec_axpy(vi, -minv_alpha[i] / tau_, prev_last, nx, s);
+      }
+    }
+    prev_last = u + block_offset(st, nt - 1);
+    v_prev_last = vout + block_offset(st, nt - 1);
+  }
 }
 
 void SpaceTimeOperator::value_at(const double* u, const double* u0, int step, double t_ref, double* out,
@@ -594,8 +646,8 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
   const int F = d.F;
   for (int i = 0; i < A.nt; ++i)
     for (int j = 0; j < A.nt; ++j) {
-      A.TM[i * A.nt + j] = d.CM[i * F + j];
-      A.TA[i * A.nt + j] = d.CA[i * F + j];
+      A.TM[i * A.nt + j] = op.block_cm()[static_cast<size_t>(i * F + j)];
+      A.TA[i * A.nt + j] = op.block_ca()[static_cast<size_t>(i * F + j)];
     }
   const Index n_cells = d.cells[0] * d.cells[1] * d.cells[2];
   const bool cartesian = d.verts == nullptr;
@@ -803,6 +855,18 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperat
   cuda_check(cudaStreamSynchronize(s), "asm setup");
   A.X = X_.d();
   A.lam = lam_.d();
+  if (A.S * A.nt > 8) {
+    // wide batches: sweep groups of 8 / n_t steps (see add_correction)
+    const bool td = A.meta && !std::getenv("STMG_NO_TDIAG");
+    chunk_ = A;
+    chunk_.S = 8 / A.nt;
+    chunk_.tdiag = 0;
+    if (td) temporal_block_diagonalise(chunk_);
+    tail_ = A;
+    tail_.S = A.S % chunk_.S;
+    tail_.tdiag = 0;
+    if (td && tail_.S > 0) temporal_block_diagonalise(tail_);
+  }
 }
 
 // Large cell blocks (m > 64): the same fast diagonalisation with library
@@ -899,7 +963,18 @@ void ASMSmoother::add_correction(const double* residual, double* correction, cud
                                  double scale) const {
   ++sweep_count_;
   if (use_fdm_) fdm_add_correction(fdm_, residual, correction, scale, stream);
-  if (asm_.n_list > 0) asm_add_correction(asm_, residual, correction, scale, stream);
+  if (asm_.n_list == 0) return;
+  if (asm_.S * asm_.nt <= 8) {
+    asm_add_correction(asm_, residual, correction, scale, stream);
+    return;
+  }
+  // wide batches: the blocks are per (step, cell) (asm_smoother.cpp:24-28),
+  // so groups of whole steps are independent sweeps of <= 8 columns
+  const long long step = static_cast<long long>(asm_.nt) * asm_.n_space;
+  for (int s0 = 0; s0 < asm_.S; s0 += chunk_.S) {
+    const DevASM& A = asm_.S - s0 >= chunk_.S ? chunk_ : tail_;
+    asm_add_correction(A, residual + s0 * step, correction + s0 * step, scale, stream);
+  }
 }
 
 // --------------------------------------------------------------- Transfer
@@ -1355,23 +1430,82 @@ std::vector<std::pair<double, double>> eigenvalues_small(std::vector<double> a, 
 
 // ------------------------------------------------------- march / errors
 void accumulate_errors(const SpaceTimeOperator& op, const double* x, const double* u0, double frequency, double t0,
-                       ErrorRecord& acc, cudaStream_t s) {
+                       ErrorRecord& acc, cudaStream_t s, int kind) {
+  if (kind != 3 && kind != 4) throw std::invalid_argument("accumulate_errors: kind must be 3 (u) or 4 (v)");
   const Rule tq = gauss(op.weights().k + 2);
   DeviceBuffer uval(sizeof(double) * op.n_space());
   for (int st = 0; st < op.n_steps(); ++st)
     for (size_t q = 0; q < tq.x.size(); ++q) {
       const double t = t0 + (st + tq.x[q]) * op.tau();
       op.value_at(x, u0, st, tq.x[q], uval.d(), s);
-      const auto e = op.spatial_error(uval.d(), 3, frequency, t, s);
+      const auto e = op.spatial_error(uval.d(), kind, frequency, t, s);
       acc.l2_l2 += tq.w[q] * op.tau() * e.first;
       acc.linf_l2 = std::max(acc.linf_l2, std::sqrt(e.first));
       acc.linf_linf = std::max(acc.linf_linf, e.second);
     }
 }
 
+// ------------------------------------------------------------ SectionClock
+SectionClock::~SectionClock() {
+  for (cudaEvent_t e : ev_) cudaEventDestroy(e);
+}
+
+void SectionClock::begin(cudaStream_t s) {
+  if (used_ % 2 != 0) throw std::logic_error("SectionClock: begin inside an open section");
+  if (used_ >= 1024) fold();
+  while (ev_.size() < used_ + 2) {
+    cudaEvent_t e = nullptr;
+    cuda_check(cudaEventCreate(&e), "section event");
+    ev_.push_back(e);
+  }
+  cuda_check(cudaEventRecord(ev_[used_++], s), "section begin");
+}
+
+void SectionClock::end(cudaStream_t s) {
+  if (used_ % 2 != 1) throw std::logic_error("SectionClock: end without begin");
+  cuda_check(cudaEventRecord(ev_[used_++], s), "section end");
+}
+
+void SectionClock::fold() {
+  if (used_ == 0) return;
+  cuda_check(cudaEventSynchronize(ev_[used_ - 1]), "section sync");
+  for (size_t i = 0; i + 1 < used_; i += 2) {
+    float ms = 0.0f;
+    cuda_check(cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]), "section elapsed");
+    total_ += 1e-3 * static_cast<double>(ms);
+  }
+  used_ = 0;
+}
+
+double SectionClock::seconds() {
+  fold();
+  return total_;
+}
+
+void SectionClock::reset() {
+  if (used_ > 0) cuda_check(cudaEventSynchronize(ev_[used_ - 1]), "section sync");
+  used_ = 0;
+  total_ = 0.0;
+}
+
 MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, double frequency, double* u, double* v,
                   const GmresOptions& options, bool errors, cudaStream_t s, const ProbeSpec* probes) {
-  const SpaceTimeOperator& op = mg.fine_operator();
+  MarchOptions o;
+  o.n_batches = n_batches;
+  o.source_kind = source_kind;
+  o.frequency = frequency;
+  o.gmres = options;
+  o.errors_u = errors;
+  o.probes = probes;
+  return march(mg.fine_operator(), &mg, u, v, o, s);
+}
+
+MarchResult march(const SpaceTimeOperator& op, const SpaceTimeMultigrid* mg, double* u, double* v,
+                  const MarchOptions& mo, cudaStream_t s) {
+  const int n_batches = mo.n_batches, source_kind = mo.source_kind;
+  const double frequency = mo.frequency;
+  const GmresOptions& options = mo.gmres;
+  const ProbeSpec* probes = mo.probes;
   const bool wave = op.equation() == Equation::Wave;
   if (n_batches < 1) throw std::invalid_argument("march: n_batches must be >= 1");
   if (wave && !v) throw std::invalid_argument("march: the wave equation needs the initial velocity");
@@ -1379,10 +1513,21 @@ MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, 
   // homogeneous Dirichlet convention of the entering state (driver.cpp:158-166)
   op.zero_boundary_field(u, s);
   if (wave) op.zero_boundary_field(v, s);
+  if (mo.errors_v && !wave) throw std::invalid_argument("march: velocity errors need the wave equation");
   DeviceBuffer rhs(sizeof(double) * n), x(sizeof(double) * n), uf(sizeof(double) * nx), vf(sizeof(double) * nx);
+  DeviceBuffer vtraj;
+  if (mo.errors_v) vtraj.allocate(sizeof(double) * n);
   GmresWorkspace ws;
   MarchResult res;
-  ErrorRecord acc;
+  ErrorRecord acc, acc_v;
+  SectionClock* clk = mo.op_clock;
+  const DeviceMap apply_op = [&op, clk](const double* in, double* out, cudaStream_t st) {
+    if (clk) clk->begin(st);
+    op.apply(in, out, st);
+    if (clk) clk->end(st);
+  };
+  DeviceMap precond;
+  if (mg) precond = [mg](const double* in, double* out, cudaStream_t st) { mg->apply(in, out, st); };
   // probes: located once on the finest mesh (locate_point), evaluated as
   // evaluate_fe of every temporal field and combined with the trial basis
   // weights at the sample times (value_at is linear)
@@ -1413,16 +1558,21 @@ MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, 
     const double t0 = static_cast<double>(b) * op.n_steps() * op.tau();
     op.assemble_rhs(source_kind, frequency, t0, u, v, rhs.d(), s);
     vec_fill(x.d(), 0.0, n, s);
-    const GmresResult r = gmres([&op](const double* in, double* out, cudaStream_t st) { op.apply(in, out, st); },
-                                rhs.d(), x.d(), n, options,
-                                [&mg](const double* in, double* out, cudaStream_t st) { mg.apply(in, out, st); }, ws, s);
+    const GmresResult r = gmres(apply_op, rhs.d(), x.d(), n, options, precond, ws, s);
     res.iterations.push_back(r.iterations);
     res.final_residuals.push_back(r.final_residual);
+    res.batch_converged.push_back(r.converged ? 1 : 0);
     if (!r.converged) {
       res.converged = false;
       break;
     }
-    if (errors) accumulate_errors(op, x.d(), u, frequency, t0, acc, s);
+    if (mo.errors_u) accumulate_errors(op, x.d(), u, frequency, t0, acc, s, 3);
+    if (mo.errors_v) {
+      // the velocity trajectory entering from v, measured like u
+      // (driver.cpp:213-223)
+      op.velocity_trajectory(x.d(), u, v, vtraj.d(), s);
+      accumulate_errors(op, vtraj.d(), v, frequency, t0, acc_v, s, 4);
+    }
     if (np > 0) {
       // entering state, then the F fields of the batch
       probe(u, 1, nx);
@@ -1453,6 +1603,8 @@ MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, 
   cuda_check(cudaStreamSynchronize(s), "march");
   res.error_u = acc;
   res.error_u.l2_l2 = std::sqrt(acc.l2_l2);
+  res.error_v = acc_v;
+  res.error_v.l2_l2 = std::sqrt(acc_v.l2_l2);
   return res;
 }
 
@@ -1621,8 +1773,10 @@ void SpaceTimeMultigrid::smooth(int l, const double* f, double* u, cudaStream_t 
   // u += omega * ASM(f - S u) (multigrid.cpp:174-185): fused residual, and the
   // smoother scatters omega * W * (block solves) straight into u
   const Level& lv = levels_[static_cast<size_t>(l)];
+  if (timers_) clock_smoother_.begin(s);
   lv.op->residual(f, u, lv.r.d(), s);
   lv.smoother->add_correction(lv.r.d(), u, s, lv.omega);
+  if (timers_) clock_smoother_.end(s);
 }
 
 void SpaceTimeMultigrid::v_cycle(int l, const double* f, double* u, cudaStream_t s) const {
@@ -1633,10 +1787,13 @@ void SpaceTimeMultigrid::v_cycle(int l, const double* f, double* u, cudaStream_t
     return;
   }
   for (int i = 0; i < options_.n_smooth; ++i) {
-    if (i == 0)
+    if (i == 0) {
+      if (timers_) clock_smoother_.begin(s);
       lv.smoother->add_correction(f, u, s, lv.omega);  // S 0 = 0 exactly
-    else
+      if (timers_) clock_smoother_.end(s);
+    } else {
       smooth(l, f, u, s);
+    }
   }
   lv.op->residual(f, u, lv.r.d(), s);
   lv.to_coarser->restrict_(lv.r.d(), lv.rc.d(), s);
@@ -1667,7 +1824,7 @@ void SpaceTimeMultigrid::coarse_cycle(cudaStream_t s) const {
     v_cycle(1, lv.rc.d(), lv.ec.d(), st);
   };
   static const bool disabled = std::getenv("STMG_NO_GRAPH") != nullptr;
-  if (disabled || graph_failed_) {
+  if (disabled || graph_failed_ || timers_) {
     direct(s);
     return;
   }
@@ -1705,8 +1862,15 @@ void SpaceTimeMultigrid::coarse_cycle(cudaStream_t s) const {
 }
 
 void SpaceTimeMultigrid::apply(const double* r, double* z, cudaStream_t s) const {
+  if (timers_) clock_total_.begin(s);
   vec_fill(z, 0.0, fine_operator().n_dofs(), s);
   v_cycle(0, r, z, s);
+  if (timers_) clock_total_.end(s);
+}
+
+void SpaceTimeMultigrid::enable_timers(bool on) {
+  timers_ = on;
+  reset_timers();
 }
 
 std::vector<LevelInfo> SpaceTimeMultigrid::level_info() const {

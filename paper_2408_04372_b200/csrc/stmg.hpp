@@ -87,6 +87,11 @@ class SpaceTimeOperator {
   // extract_final (space_time_operator.cpp:223-248)
   void extract_final(const double* u, const double* u0, const double* v0, double* uf, double* vf,
                      cudaStream_t stream = nullptr) const;
+  // velocity_trajectory (driver.cpp:47-82, wave only): the velocity node
+  // values of every (step, temporal node) of a batch solution u entering
+  // from (u0, v0), in the layout of u (overwrite vout, n_dofs)
+  void velocity_trajectory(const double* u, const double* u0, const double* v0, double* vout,
+                           cudaStream_t stream = nullptr) const;
   void zero_boundary_field(double* v, cudaStream_t stream = nullptr) const;
   // value_at (space_time_operator.cpp:250-266): the discrete trajectory of
   // step `step` at reference time t_ref, entering state u0 (n_space)
@@ -98,6 +103,10 @@ class SpaceTimeOperator {
   std::pair<double, double> spatial_error(const double* field, int kind, double frequency, double t,
                                           cudaStream_t stream = nullptr) const;
   long applications() const { return apply_count_; }
+  // the F x F block coefficient tables CM, CA (row-major, F = S n_t)
+  const std::vector<double>& block_cm() const { return cm_; }
+  const std::vector<double>& block_ca() const { return ca_; }
+  bool wide() const { return wide_; }
 
  private:
   Equation equation_;
@@ -111,6 +120,11 @@ class SpaceTimeOperator {
   DevLevel mass_desc_{}, stiff_desc_{};
   DeviceBuffer verts_, rho0_;
   mutable long apply_count_ = 0;
+  // S * n_t > kMaxF ("wide" batches): composed application, see st_apply_wide
+  bool wide_ = false;
+  std::vector<double> cm_, ca_;  // full F x F block coefficients
+  DeviceBuffer wide_cm_, wide_ca_;
+  mutable DeviceBuffer wide_mu_, wide_au_;
 };
 
 class ASMSmoother {
@@ -143,6 +157,7 @@ class ASMSmoother {
   void build_exact_large(DeviceBuffer& cellM, DeviceBuffer& cellA, cudaStream_t s);
   const SpaceTimeOperator* op_;
   DevASM asm_{};
+  DevASM chunk_{}, tail_{};  // S * n_t > 8: step groups of chunk_.S steps (tail_: the rest)
   DevFDM fdm_{};
   bool use_fdm_ = false;
   bool exact_ = true;
@@ -247,8 +262,31 @@ struct ErrorRecord {
 // accumulate_errors (driver.cpp:27-43): temporal Gauss (k+2) x spatial Gauss
 // (p+2) sample of one batch solution x entering from u0 against the
 // manufactured solution of frequency f; acc.l2_l2 holds the squared sum
+// (kind 3: u = sin(om t) prod sin(om x_a); kind 4: its velocity)
 void accumulate_errors(const SpaceTimeOperator& op, const double* x, const double* u0, double frequency, double t0,
-                       ErrorRecord& acc, cudaStream_t stream = nullptr);
+                       ErrorRecord& acc, cudaStream_t stream = nullptr, int kind = 3);
+
+// Device time of one profile section: the reference's wall-clock section
+// accounting (multigrid.hpp:85-88, driver.cpp:186-196) restated with CUDA
+// event pairs recorded on the launching stream and folded into the total
+// when read (or when the pool fills)
+class SectionClock {
+ public:
+  SectionClock() = default;
+  SectionClock(const SectionClock&) = delete;
+  SectionClock& operator=(const SectionClock&) = delete;
+  ~SectionClock();
+  void begin(cudaStream_t stream);
+  void end(cudaStream_t stream);
+  double seconds();  // waits for the recorded events
+  void reset();
+
+ private:
+  void fold();
+  std::vector<cudaEvent_t> ev_;
+  size_t used_ = 0;
+  double total_ = 0.0;
+};
 
 class SpaceTimeMultigrid;
 // march (driver.cpp:95-260) with every slab on the device: per batch
@@ -257,10 +295,12 @@ class SpaceTimeMultigrid;
 // n_space each; Dirichlet entries are zeroed first) and the final state on
 // output.
 struct MarchResult {
-  std::vector<int> iterations;
+  std::vector<int> iterations;  // per batch run (the last one may not have converged)
   std::vector<double> final_residuals;
+  std::vector<char> batch_converged;
   bool converged = true;
   ErrorRecord error_u;  // finished (l2_l2 = sqrt of the sum)
+  ErrorRecord error_v;  // velocity errors (wave, errors_v)
   // probe time series (driver.cpp:146-186, 226-236): times, and per probe
   // the value at t = 0 and at samples_per_step points of every step
   std::vector<double> probe_times;
@@ -273,6 +313,22 @@ struct ProbeSpec {
 MarchResult march(const SpaceTimeMultigrid& mg, int n_batches, int source_kind, double frequency, double* u, double* v,
                   const GmresOptions& options, bool errors, cudaStream_t stream = nullptr,
                   const ProbeSpec* probes = nullptr);
+// the general form: op with an optional preconditioner (spec.precondition,
+// driver.cpp:121-137, 197-201), velocity errors against the manufactured
+// velocity (driver.cpp:213-223), and op_clock timing every operator
+// application inside GMRES (the "Operator w/o GMG" section, driver.cpp:193-196)
+struct MarchOptions {
+  int n_batches = 1;
+  int source_kind = 1;
+  double frequency = 0.5;
+  GmresOptions gmres;
+  bool errors_u = false;
+  bool errors_v = false;
+  const ProbeSpec* probes = nullptr;
+  SectionClock* op_clock = nullptr;
+};
+MarchResult march(const SpaceTimeOperator& op, const SpaceTimeMultigrid* mg, double* u, double* v,
+                  const MarchOptions& options, cudaStream_t stream = nullptr);
 
 class SpaceTimeMultigrid {
  public:
@@ -297,6 +353,16 @@ class SpaceTimeMultigrid {
   void v_cycle(int l, const double* f, double* u, cudaStream_t stream) const;
   void smooth(int l, const double* f, double* u, cudaStream_t stream) const;
   size_t device_bytes() const;
+  // profile sections (multigrid.hpp:85-88): device seconds inside apply() and
+  // inside the smoothing steps; while enabled the coarse cycle runs as plain
+  // launches so every smoothing step is bracketed by its own events
+  void enable_timers(bool on);
+  double seconds_total() const { return clock_total_.seconds(); }
+  double seconds_smoother() const { return clock_smoother_.seconds(); }
+  void reset_timers() const {
+    clock_total_.reset();
+    clock_smoother_.reset();
+  }
 
  private:
   struct Level {
@@ -319,6 +385,8 @@ class SpaceTimeMultigrid {
   mutable cudaGraphExec_t coarse_exec_ = nullptr;
   mutable long long coarse_nodes_ = 0;
   mutable bool graph_failed_ = false;
+  bool timers_ = false;
+  mutable SectionClock clock_total_, clock_smoother_;
 
   MultigridOptions options_;
   std::vector<Level> levels_;

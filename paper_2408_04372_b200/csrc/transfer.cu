@@ -210,6 +210,19 @@ __global__ void temporal_kernel(const double* __restrict__ T, int Ff, int Fc, bo
     const long long ix = g % dx, iy = (g / dx) % dy, iz = g / (dx * dy);
     const bool bd = on_bdry(ix, dx) || (dim > 1 && on_bdry(iy, dy)) ||
                     (dim > 2 && (on_bdry_z(iz, dz, zbc) || (skip_lo_in && iz == 0)));
+    if (Fin > kMaxF || Fout > kMaxF) {
+      // wide batches: straight from memory
+      for (int r = 0; r < Fout; ++r) {
+        double s = 0.0;
+        if (!bd)
+          for (int c = 0; c < Fin; ++c) s = fma(transpose ? T[c * Fc + r] : T[r * Fc + c], in[c * fs_in + g], s);
+        if (accumulate)
+          out[r * fs_out + g] += s;
+        else
+          out[r * fs_out + g] = s;
+      }
+      continue;
+    }
     double x[kMaxF];
 #pragma unroll
     for (int c = 0; c < kMaxF; ++c) x[c] = (c < Fin && !bd) ? in[c * fs_in + g] : 0.0;

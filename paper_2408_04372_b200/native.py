@@ -28,6 +28,27 @@ class GmresResult(C.Structure):
                 ("final_residual", C.c_double), ("history_len", C.c_int)]
 
 
+class Problem(C.Structure):
+    """stmg_problem: the resolved ProblemSpec (include/stmg/driver.hpp:14-48)."""
+    _fields_ = [("equation", C.c_int), ("scheme", C.c_int), ("problem", C.c_int), ("k", C.c_int), ("p", C.c_int),
+                ("dim", C.c_int), ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("t_final", C.c_double),
+                ("refinements", C.c_int), ("base_cells", C.c_int), ("base_time_intervals", C.c_int),
+                ("batch", C.c_int), ("frequency", C.c_double), ("shm_s", C.c_double), ("perturb", C.c_double),
+                ("seed", C.c_ulonglong), ("rho_random_lo", C.c_double), ("rho_random_hi", C.c_double),
+                ("abs_tol", C.c_double), ("rel_tol", C.c_double), ("max_iters", C.c_int), ("restart", C.c_int),
+                ("n_smooth", C.c_int), ("precondition", C.c_int), ("probe_samples_per_step", C.c_int),
+                ("n_strategy", C.c_int), ("strategy", C.c_int * 32), ("timers", C.c_int)]
+
+
+class RunReport(C.Structure):
+    """stmg_run_report (include/stmg/driver.hpp:54-91)."""
+    _fields_ = [("converged", C.c_int), ("n_space_dofs", C.c_longlong), ("n_steps_total", C.c_int),
+                ("n_batches", C.c_int), ("dofs_global", C.c_longlong), ("n_batches_run", C.c_int),
+                ("mean_iterations", C.c_double), ("work", C.c_double), ("has_error_u", C.c_int),
+                ("has_error_v", C.c_int), ("error_u", C.c_double * 3), ("error_v", C.c_double * 3),
+                ("n_levels", C.c_int), ("sections", C.c_double * 5), ("n_probe_samples", C.c_longlong)]
+
+
 LINEAR_MAP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
 
 # (name, restype, argtypes): every symbol declared in include/stmg_b200.h
@@ -97,6 +118,14 @@ SIGNATURES = [
                                     c_double_p, c_double_p, C.c_void_p]),
     # z-slab partitioned solve
     ("stmg_nccl_unique_id", C.c_int, [C.c_char_p]),
+    ("stmg_problem_sizes", C.c_int, [C.POINTER(Problem), c_int_p, c_int_p, c_ll_p]),
+    ("stmg_run", C.c_int, [C.POINTER(Problem), C.c_int, c_double_p, C.POINTER(RunReport), C.c_int, c_int_p,
+                           c_double_p, c_int_p, C.c_int, c_int_p, c_ll_p, c_double_p, C.c_longlong, c_double_p,
+                           c_double_p]),
+    ("stmg_level_plan", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, c_int_p, C.c_int,
+                                  c_int_p, c_int_p, c_double_p]),
+    ("stmg_perturbed_vertices", C.c_int, [C.c_int, c_double_p, c_double_p, C.c_int, C.c_int, C.c_double,
+                                          C.c_ulonglong, c_double_p]),
     ("stmg_comm_create", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_void_p]),
     ("stmg_comm_destroy", None, [C.c_void_p]),
     ("stmg_slab_plan", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_int, c_int_p,

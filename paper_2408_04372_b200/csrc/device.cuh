@@ -49,6 +49,11 @@ struct DevLevel {
   double w[kMaxN];          // Gauss weights
   double xq[kMaxN];         // Gauss points on [0,1]
   double gl[kMaxN];         // Gauss-Lobatto support nodes on [0,1]
+  // 1D element matrices of [0,1] (Cartesian fast path, st_cart.cuh):
+  // Mr = B^T W B, Kr = D^T W D; hinv2[a] = 1 / h[a]^2
+  double Mr[kMaxN][kMaxN];
+  double Kr[kMaxN][kMaxN];
+  double hinv2[3];
   // space-time block coefficients, row-major F x F (space_time_operator.cpp:269-317)
   double CM[kMaxF * kMaxF];
   double CA[kMaxF * kMaxF];

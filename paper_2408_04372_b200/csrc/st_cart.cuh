@@ -1,0 +1,220 @@
+// 3D fused space-time operator on Cartesian levels (axis-aligned cells of
+// one size h, the lattice every level of C3/C4/C5 lives on): the same
+// y = sum_j CM_ij M u_j + CA_ij A u_j as st_lines.cuh (reference:
+// SpaceTimeOperator::apply, space_time_operator.cpp:45-130, over
+// SpatialOperator::apply_cells, spatial_operator.cpp:187-315), but applied
+// with the 1D ELEMENT matrices instead of through the quadrature points.
+//
+// On an affine box cell the reference's Gauss quadrature (q = p + 1 points,
+// exact for the degree-2p integrands) of the cell mass and stiffness factors
+// into Kronecker products of the [0,1] interval matrices
+//   Mr = B^T W B,  Kr = D^T W D     ((p+1) x (p+1), symmetric),
+//   M_e = V Mr(x)Mr(x)Mr,  A_e = rho V (Kr/hx^2 (x) Mr (x) Mr + Mr (x) Kr/hy^2 (x) Mr
+//                                      + Mr (x) Mr (x) Kr/hz^2),  V = hx hy hz,
+// so a cell needs 7 line sweeps per field (the quadrature form needs 18):
+//   A  y-owner: gather u along y (Dirichlet inputs zeroed), a = Mr_y u,
+//               b = Kr_y u
+//   B  x-owner: c = Mr_x a, pre = Kr_x a / hx^2 + Mr_x b / hy^2 (in place)
+//   C  z-owner: temporal block coupling of the z-lines of every field,
+//               Zm_i = sum_j V CM_ij c_j + rho V CA_ij pre_j,
+//               Zk_i = sum_j rho V / hz^2 CA_ij c_j,
+//               y_i = Mr_z Zm_i + Kr_z Zk_i, scatter-add (Dirichlet rows
+//               skipped; the boundary pass writes them,
+//               space_time_operator.cpp:125-129)
+// Two CTA barriers, two shared arrays. Wide field counts (N * F > 20) split
+// each line's fields over two thread groups in stages A and B; in stage C
+// each group produces half of the output fields.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+#include "st_lines.cuh"
+
+namespace stmgb {
+namespace stc {
+
+template <int N, int F>
+struct Cfg {
+  static constexpr int NL = N * N;
+  static constexpr int FG = (N * F > 20) ? 2 : 1;  // thread groups per line
+  static constexpr int FPG = (F + FG - 1) / FG;    // fields per group
+  static constexpr int NC = (128 / NL) > 0 ? (128 / NL) : 1;
+  static constexpr int T = ((NC * NL * FG + 31) / 32) * 32;
+  static constexpr int MINB = FG == 1 ? 4 : 2;
+  static constexpr int SD = stl::Lay<N>::SD;
+  static constexpr int ARR = NC * F * SD;
+  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * static_cast<size_t>(ARR); }
+};
+
+template <int N, int F>
+__global__ void __launch_bounds__(Cfg<N, F>::T, Cfg<N, F>::MINB)
+    st_cart_kernel(const __grid_constant__ DevLevel L, const double* __restrict__ u, double* __restrict__ y,
+                   double sign) {
+  using C = Cfg<N, F>;
+  constexpr int NL = C::NL, NC = C::NC, SD = C::SD, ARR = C::ARR, FPG = C::FPG;
+  constexpr int RY = stl::Lay<N>::RY, PZ = stl::Lay<N>::PZ;
+  extern __shared__ __align__(16) double smem[];
+  double* A0 = smem;
+  double* A1 = A0 + ARR;
+
+  const int t = threadIdx.x;
+  const int g = t / (NC * NL);
+  const int r = t - g * (NC * NL);
+  const int c = r / NL, l = r - (r / NL) * NL;
+  const int a = l % N, b = l / N;
+  const long long n_cells = L.cells[0] * L.cells[1] * L.cells[2];
+  const long long cell = static_cast<long long>(blockIdx.x) * NC + c;
+  const bool valid = g < C::FG && cell < n_cells;
+  const int j0 = g * FPG;  // first field of this thread's group
+  const long long dx = L.dofs[0], dxy = L.dofs[0] * L.dofs[1], ns = L.n_space;
+  const int p = N - 1;
+  long long base = 0;
+  int mask = 0;
+  unsigned cx = 0, cy = 0, cz = 0;
+  double gin[FPG][N];
+  if (valid) {
+    const unsigned ci = static_cast<unsigned>(cell);
+    const unsigned nx = static_cast<unsigned>(L.cells[0]), ny = static_cast<unsigned>(L.cells[1]);
+    cx = ci % nx;
+    cy = (ci / nx) % ny;
+    cz = ci / (nx * ny);
+    base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx + static_cast<long long>(cx) * p;
+    mask = (cx == 0 ? 1 : 0) | (cx == nx - 1 ? 2 : 0) | (cy == 0 ? 4 : 0) | (cy == ny - 1 ? 8 : 0) |
+           (cz == 0 && (L.zbc & 1) ? 16 : 0) | (cz == L.cells[2] - 1 && (L.zbc & 2) ? 32 : 0);
+#pragma unroll
+    for (int jj = 0; jj < FPG; ++jj)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const bool dir = ((mask & 1) && a == 0) || ((mask & 2) && a == p) || ((mask & 4) && k == 0) ||
+                         ((mask & 8) && k == p) || ((mask & 16) && b == 0) || ((mask & 32) && b == p);
+        gin[jj][k] = (dir || j0 + jj >= F) ? 0.0 : __ldg(u + (j0 + jj) * ns + base + b * dxy + k * dx + a);
+      }
+  }
+  const int cbase = c * F * SD;
+  const int oy = cbase + a + PZ * b;       // y-line (x = a, z = b), stride RY
+  const int ox = cbase + RY * a + PZ * b;  // x-line (y = a, z = b), stride 1
+  const int oz = cbase + a + RY * b;       // z-line (x = a, y = b), stride PZ
+
+  // ---- A: y-owner, a = Mr_y u, b = Kr_y u
+  if (valid) {
+#pragma unroll
+    for (int jj = 0; jj < FPG; ++jj) {
+      if (j0 + jj >= F) break;
+      const int o = oy + (j0 + jj) * SD;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          s0 = fma(L.Mr[q][k], gin[jj][k], s0);
+          s1 = fma(L.Kr[q][k], gin[jj][k], s1);
+        }
+        A0[o + q * RY] = s0;
+        A1[o + q * RY] = s1;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- B: x-owner, c = Mr_x a, pre = Kr_x a / hx^2 + Mr_x b / hy^2, in place
+  if (valid) {
+    const double sx = L.hinv2[0], sy = L.hinv2[1];
+#pragma unroll
+    for (int jj = 0; jj < FPG; ++jj) {
+      if (j0 + jj >= F) break;
+      const int o = ox + (j0 + jj) * SD;
+      double va[N], vb[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        va[k] = A0[o + k];
+        vb[k] = A1[o + k];
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          s0 = fma(L.Mr[q][k], va[k], s0);
+          s1 = fma(L.Kr[q][k], va[k], s1);
+          s2 = fma(L.Mr[q][k], vb[k], s2);
+        }
+        A0[o + q] = s0;
+        A1[o + q] = fma(sx, s1, sy * s2);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- C: z-owner, temporal coupling, Mr_z / Kr_z, scatter-add
+  if (valid) {
+    const double V = L.h[0] * L.h[1] * L.h[2];
+    double rho = 1.0;
+    if (L.rho0) {
+      const long long ax = cx >> L.rho_shift, ay = cy >> L.rho_shift, az = (cz + L.cz0) >> L.rho_shift;
+      rho = __ldg(L.rho0 + (az * L.cells0[1] + ay) * L.cells0[0] + ax);
+    }
+    const double rv = rho * V, rvz = rv * L.hinv2[2];
+    double Zm[FPG][N], Zk[FPG][N];
+#pragma unroll
+    for (int ii = 0; ii < FPG; ++ii)
+#pragma unroll
+      for (int k = 0; k < N; ++k) Zm[ii][k] = Zk[ii][k] = 0.0;
+#pragma unroll
+    for (int j = 0; j < F; ++j) {
+      double vc[N], vp[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        vc[k] = A0[oz + j * SD + k * PZ];
+        vp[k] = A1[oz + j * SD + k * PZ];
+      }
+#pragma unroll
+      for (int ii = 0; ii < FPG; ++ii) {
+        const int i = j0 + ii;
+        if (i >= F) break;
+        const double cmv = L.CM[i * F + j], cav = L.CA[i * F + j];
+        if (cmv == 0.0 && cav == 0.0) continue;
+        const double cm = V * cmv, ca = rv * cav, ck = rvz * cav;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          Zm[ii][k] = fma(cm, vc[k], fma(ca, vp[k], Zm[ii][k]));
+          Zk[ii][k] = fma(ck, vc[k], Zk[ii][k]);
+        }
+      }
+    }
+    auto dirichlet = [&](int lx, int ly, int lz) {
+      return ((mask & 1) && lx == 0) || ((mask & 2) && lx == p) || ((mask & 4) && ly == 0) ||
+             ((mask & 8) && ly == p) || ((mask & 16) && lz == 0) || ((mask & 32) && lz == p);
+    };
+#pragma unroll
+    for (int ii = 0; ii < FPG; ++ii) {
+      const int i = j0 + ii;
+      if (i >= F) break;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) s = fma(L.Mr[k][q], Zm[ii][q], fma(L.Kr[k][q], Zk[ii][q], s));
+        if (!dirichlet(a, b, k)) atomicAdd(y + i * ns + base + k * dxy + b * dx + a, sign * s);
+      }
+    }
+  }
+}
+
+template <int N, int F>
+void launch(const DevLevel& L, const double* u, double* y, double sign, cudaStream_t stream) {
+  using C = Cfg<N, F>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(st_cart_kernel<N, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::smem_bytes()));
+    cudaFuncSetAttribute(st_cart_kernel<N, F>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = true;
+  }
+  const long long n_cells = L.cells[0] * L.cells[1] * L.cells[2];
+  const long long blocks = (n_cells + C::NC - 1) / C::NC;
+  st_cart_kernel<N, F><<<static_cast<unsigned>(blocks), C::T, C::smem_bytes(), stream>>>(L, u, y, sign);
+}
+
+}  // namespace stc
+}  // namespace stmgb

@@ -1,8 +1,13 @@
 // 3D instantiations of the fused space-time operator: the line-owner kernel
 // (st_lines.cuh) wherever its registers and shared memory fit (N * F <= 16),
-// its nodal-coupling, field-grouped variant (st_mix_kernel) otherwise.
+// its nodal-coupling, field-grouped variant (st_mix_kernel) otherwise;
+// Cartesian levels take the element-matrix kernel (st_cart.cuh) unless
+// STMG_VMULT=quad asks for the quadrature form.
+#include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 
+#include "st_cart.cuh"
 #include "st_lines.cuh"
 #include "st_operator.cuh"
 
@@ -10,6 +15,14 @@ namespace stmgb {
 namespace {
 template <int N, int F>
 void launch_nf(const DevLevel& L, const double* u, double* y, double sign, cudaStream_t s) {
+  static const bool quad = [] {
+    const char* e = std::getenv("STMG_VMULT");
+    return e != nullptr && std::strcmp(e, "quad") == 0;
+  }();
+  if (!L.verts && !quad) {
+    stc::launch<N, F>(L, u, y, sign, s);
+    return;
+  }
   if constexpr (stl::fits<N, F>())
     stl::launch<N, F>(L, u, y, sign, s);
   else

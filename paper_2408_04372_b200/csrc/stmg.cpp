@@ -133,6 +133,17 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
     d.xq[i] = i < d.n ? q.x[i] : 0.0;
     d.gl[i] = i < d.n ? gl.x[i] : 0.0;
   }
+  for (int i = 0; i < kMaxN; ++i)
+    for (int j = 0; j < kMaxN; ++j) {
+      double mr = 0.0, kr = 0.0;
+      for (int k = 0; k < d.n; ++k) {
+        mr += d.w[k] * d.B[k][i] * d.B[k][j];
+        kr += d.w[k] * d.D[k][i] * d.D[k][j];
+      }
+      d.Mr[i][j] = mr;
+      d.Kr[i][j] = kr;
+    }
+  for (int a = 0; a < 3; ++a) d.hinv2[a] = 1.0 / (d.h[a] * d.h[a]);
   std::vector<double> CM, CA;
   block_coefficient_matrices(equation, weights, tau, n_steps, CM, CA);
   std::memset(d.CM, 0, sizeof(d.CM));

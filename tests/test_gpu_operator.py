@@ -47,16 +47,37 @@ for dim in (2, 3):
 
 
 @pytest.mark.parametrize("dim,p,eq,scheme,k,S", CASES[::3])
-@pytest.mark.parametrize("geom", ["cartesian", "perturbed+rho"])
+@pytest.mark.parametrize("geom", ["cartesian", "cartesian+rho", "perturbed+rho"])
 def test_vmult_parity_sweep(cuda, ref, dim, p, eq, scheme, k, S, geom):
+    """Cartesian levels run the element-matrix kernel (st_cart.cuh), perturbed
+    ones the quadrature form (st_lines.cuh / st_operator.cuh)."""
     base, refine = (2, 1) if dim == 3 else (3, 1)
     cfg = problems.Config("sweep", eq, scheme, dim, base, refine, p, k, S, 0.3)
-    if geom != "cartesian":
+    if geom.startswith("perturbed"):
         cfg.perturb = 0.15
+    if geom.endswith("rho"):
         rng = np.random.default_rng(7)
         cfg.rho = rng.uniform(0.5, 3.0, base ** dim)
     mesh, op, R = _pair(cfg, ref)
     u = problems.uniform_vector(op.n_dofs, seed=3)
+    y = op.apply(cuda.from_numpy(u).cuda()).cpu().numpy()
+    assert _rel(y, R.apply(u)) <= TOL
+
+
+# every field count of the Cartesian element-matrix kernel, both thread-group
+# layouts (one group per line, and two when N * F > 20), heat and wave
+CART_FIELDS = [(p, eq, scheme, k, S) for p in (1, 2, 3, 4)
+               for eq, scheme, k, S in ((0, 0, 0, 1), (0, 0, 1, 1), (0, 0, 2, 1), (0, 0, 1, 2), (1, 1, 1, 5),
+                                        (0, 0, 2, 2), (1, 1, 2, 7 // 2), (0, 0, 0, 7), (1, 1, 2, 4))]
+
+
+@pytest.mark.parametrize("p,eq,scheme,k,S", CART_FIELDS)
+def test_cartesian_vmult_every_field_count(cuda, ref, p, eq, scheme, k, S):
+    cfg = problems.Config("cart", eq, scheme, 3, 3, 0, p, k, S, 0.2)
+    rng = np.random.default_rng(p * 100 + S)
+    cfg.rho = rng.uniform(0.5, 3.0, 27)
+    mesh, op, R = _pair(cfg, ref)
+    u = problems.uniform_vector(op.n_dofs, seed=5)
     y = op.apply(cuda.from_numpy(u).cuda()).cpu().numpy()
     assert _rel(y, R.apply(u)) <= TOL
 

@@ -20,6 +20,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "st_cart_layout.h"
 
 namespace stmgb {
 
@@ -72,6 +73,45 @@ __device__ __forceinline__ void solve_small(const double* TM, const double* TA, 
 #pragma unroll
     for (int j = i + 1; j < 4; ++j) s = fma(-a[i][j], b[j], s);
     b[i] = s / a[i][i];
+  }
+}
+
+// (T_M + mu T_A)^-1 b for every eigen-index: pivoted elimination, or, when
+// the host block-diagonalised T_A^-1 T_M = Q B Q^-1 (P.tdiag),
+// Q (B + mu)^-1 P b with P = Q^-1 T_A^-1 -- two n_t x n_t products and one
+// reciprocal per 1x1 / 2x2 block, no pivoting
+template <int NT, bool TD>
+__device__ __forceinline__ void temporal_solve(const DevFDM& P, double mu, double (&b)[4]) {
+  if constexpr (!TD) {
+    solve_small(P.TM, P.TA, mu, NT, b);
+    return;
+  }
+  double w[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) s = fma(P.tP[i * NT + j], b[j], s);
+    w[i] = s;
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    if (P.tkind[i] == 0) {
+      w[i] = w[i] / (P.ta[i] + mu);
+    } else if (P.tkind[i] == 1 && i + 1 < NT) {
+      const double al = P.ta[i] + mu, be = P.tb[i];
+      const double inv = 1.0 / fma(al, al, be * be);
+      const double w0 = w[i], w1 = w[i + 1];
+      w[i] = (al * w0 - be * w1) * inv;
+      w[i + 1] = (be * w0 + al * w1) * inv;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) s = fma(P.tQ[i * NT + j], w[j], s);
+    b[i] = s;
   }
 }
 
@@ -180,7 +220,10 @@ __global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ Dev
       double b[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int i = 0; i < NT; ++i) b[i] = W[(c * NT + i) * ND + e];
-      solve_small(P.TM, P.TA, lam, NT, b);
+      if (P.tdiag)
+        temporal_solve<NT, true>(P, lam, b);
+      else
+        temporal_solve<NT, false>(P, lam, b);
 #pragma unroll
       for (int i = 0; i < NT; ++i) W[(c * NT + i) * ND + e] = b[i];
     }
@@ -231,31 +274,13 @@ __global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ Dev
 // registers. Per step: y-owner gathers r and applies S_y^T, x-owner S_x^T,
 // z-owner S_z^T + the n_t x n_t solves at its N eigen-points + S_z, x-owner
 // S_x, y-owner S_y and the weighted scatter (Dirichlet rows: w r, re-read).
-template <int N>
-struct FLay;
-template <>
-struct FLay<2> {
-  static constexpr int RY = 2, PZ = 5, SD = 10;
-};
-template <>
-struct FLay<3> {
-  static constexpr int RY = 3, PZ = 10, SD = 30;
-};
-template <>
-struct FLay<4> {
-  static constexpr int RY = 4, PZ = 19, SD = 74;
-};
-template <>
-struct FLay<5> {
-  static constexpr int RY = 5, PZ = 26, SD = 130;
-};
-
-template <int N, int NT>
-__global__ void __launch_bounds__(128) fdm_lines_kernel(const __grid_constant__ DevFDM P,
+template <int N, int NT, bool TD>
+__global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant__ DevFDM P,
                                                         const double* __restrict__ r, double* __restrict__ z,
                                                         double scale) {
-  constexpr int NL = N * N, NC = 128 / NL, SD = FLay<N>::SD, RY = FLay<N>::RY, PZ = FLay<N>::PZ;
-  __shared__ double W[NC * NT * SD];
+  using Y = stc::FdmLayout<N, NT>;  // bank-conflict-modelled (scripts/gen_cart_layout.py)
+  constexpr int NL = N * N, NC = 128 / NL, SD = Y::SD, RY = Y::RY, PZ = Y::PZ;
+  __shared__ double W[NC * Y::CS];
   const int t = threadIdx.x;
   const int c = t / NL, l = t - (t / NL) * NL;
   const int a = l % N, b = l / N;
@@ -286,8 +311,9 @@ __global__ void __launch_bounds__(128) fdm_lines_kernel(const __grid_constant__ 
     return ((mask & 1) && lx == 0) || ((mask & 2) && lx == p) || ((mask & 4) && ly == 0) || ((mask & 8) && ly == p) ||
            ((mask & 16) && lz == 0) || ((mask & 32) && lz == p);
   };
-  const int cb = c * NT * SD;
-  const int oy = cb + a + PZ * b, ox = cb + RY * a + PZ * b, oz = cb + a + RY * b;
+  const int cb = c * Y::CS;
+  const int oy = cb + a + PZ * b, oz = cb + a + RY * b;
+  const int ox = cb + RY * (Y::SWAP ? b : a) + PZ * (Y::SWAP ? a : b);
   const double(&Sx)[kMaxN][kMaxN] = P.S1[0][tx];
   const double(&Sy)[kMaxN][kMaxN] = P.S1[1][ty];
   const double(&Sz)[kMaxN][kMaxN] = P.S1[2][tz];
@@ -350,7 +376,7 @@ __global__ void __launch_bounds__(128) fdm_lines_kernel(const __grid_constant__ 
         double bb[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int f = 0; f < NT; ++f) bb[f] = v[f][e];
-        solve_small(P.TM, P.TA, rho * (lxy + P.L1[2][tz][e]), NT, bb);
+        temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][tz][e]), bb);
 #pragma unroll
         for (int f = 0; f < NT; ++f) v[f][e] = bb[f];
       }
@@ -418,7 +444,10 @@ void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cud
   constexpr int NC = 128 / (N * N);
   const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
   count_launch();
-  fdm_lines_kernel<N, NT><<<static_cast<unsigned>((n_cells + NC - 1) / NC), 128, 0, s>>>(P, r, z, scale);
+  if (P.tdiag)
+    fdm_lines_kernel<N, NT, true><<<static_cast<unsigned>((n_cells + NC - 1) / NC), 128, 0, s>>>(P, r, z, scale);
+  else
+    fdm_lines_kernel<N, NT, false><<<static_cast<unsigned>((n_cells + NC - 1) / NC), 128, 0, s>>>(P, r, z, scale);
 }
 
 template <int DIM, int N, int NT>

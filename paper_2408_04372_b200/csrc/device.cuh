@@ -54,6 +54,10 @@ struct DevLevel {
   double Mr[kMaxN][kMaxN];
   double Kr[kMaxN][kMaxN];
   double hinv2[3];
+  // even-odd halves of Mr / Kr (both centro-symmetric: A[i][j] =
+  // A[n-1-i][n-1-j]): E[i][k] = (A[i][k] + A[i][n-1-k]) / 2 (k < n/2),
+  // E[i][n/2] = A[i][n/2] (odd n); O[i][k] = (A[i][k] - A[i][n-1-k]) / 2
+  double MrE[3][3], MrO[2][2], KrE[3][3], KrO[2][2];
   // space-time block coefficients, row-major F x F (space_time_operator.cpp:269-317)
   double CM[kMaxF * kMaxF];
   double CA[kMaxF * kMaxF];

@@ -168,6 +168,14 @@ struct DevFDM {
   const unsigned char* skip;      // per cell: 1 = solved by the exact per-cell kernel
   int zbc;                        // z-slab partition (as DevLevel::zbc / cz0)
   long long cz0;
+  // temporal fast diagonalisation of the n_t x n_t solves (tdiag = 1):
+  // (T_M + mu T_A)^-1 = Q (B + mu)^-1 P, row-major n_t x n_t tP / tQ; B is
+  // block diagonal: tkind[i] = 0 real eigenvalue ta[i]; 1 first column of a
+  // conjugate pair [[ta, tb], [-tb, ta]] (2 its second column)
+  int tdiag;
+  int tkind[4];
+  double ta[4], tb[4];
+  double tP[16], tQ[16];
 };
 void fdm_add_correction(const DevFDM& F, const double* r, double* z, double scale, cudaStream_t s);
 // probing-based extraction of restricted cell matrices (setup)

@@ -14,25 +14,77 @@
 // so a cell needs 7 line sweeps per field (the quadrature form needs 18):
 //   A  y-owner: gather u along y (Dirichlet inputs zeroed), a = Mr_y u,
 //               b = Kr_y u
-//   B  x-owner: c = Mr_x a, pre = Kr_x a / hx^2 + Mr_x b / hy^2 (in place)
+//   B  x-owner: c = Mr_x a, pre = Kr_x a / hx^2 + Mr_x b / hy^2
 //   C  z-owner: temporal block coupling of the z-lines of every field,
 //               Zm_i = sum_j V CM_ij c_j + rho V CA_ij pre_j,
 //               Zk_i = sum_j rho V / hz^2 CA_ij c_j,
 //               y_i = Mr_z Zm_i + Kr_z Zk_i, scatter-add (Dirichlet rows
 //               skipped; the boundary pass writes them,
 //               space_time_operator.cpp:125-129)
-// Two CTA barriers, two shared arrays. Wide field counts (N * F > 20) split
-// each line's fields over two thread groups in stages A and B; in stage C
-// each group produces half of the output fields.
+// Two shared arrays. Their padded layouts come from a bank-conflict model of
+// the three line orientations (scripts/gen_cart_layout.py ->
+// st_cart_layout.h): where one layout cannot serve all three, stage B reads
+// layout 1 and, after a third barrier, writes layout 2. Wide field counts
+// (N * F > 20) split each line's fields over two thread groups in stages A
+// and B; in stage C each group produces half of the output fields.
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include "device.cuh"
-#include "st_lines.cuh"
+#include "st_cart_layout.h"
 
 namespace stmgb {
 namespace stc {
+
+// Even-odd (centro-symmetric) line products: v -> (e, o) with
+// e[k] = v[k] + v[n-1-k], o[k] = v[k] - v[n-1-k] (k < n/2), e[n/2] = v[n/2]
+// for odd n; then A v = (E e + O o, mirrored: (E e - O o) on the upper half).
+// N = 5: 13 FMAs per product instead of 25, and 26 distinct table values
+// (both matrices) that stay in uniform registers.
+template <int N>
+struct EO {
+  static constexpr int H = N / 2, HE = (N + 1) / 2;
+};
+template <int N>
+__device__ __forceinline__ void eo_split(const double (&v)[N], double (&e)[EO<N>::HE], double (&o)[EO<N>::H]) {
+#pragma unroll
+  for (int k = 0; k < EO<N>::H; ++k) {
+    e[k] = v[k] + v[N - 1 - k];
+    o[k] = v[k] - v[N - 1 - k];
+  }
+  if constexpr (N % 2 == 1) e[EO<N>::H] = v[EO<N>::H];
+}
+// E-part / O-part of one matrix applied to a split vector
+template <int N>
+__device__ __forceinline__ void eo_even(const double (&E)[3][3], const double (&e)[EO<N>::HE], double (&se)[EO<N>::HE]) {
+#pragma unroll
+  for (int i = 0; i < EO<N>::HE; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < EO<N>::HE; ++k) s = fma(E[i][k], e[k], s);
+    se[i] = s;
+  }
+}
+template <int N>
+__device__ __forceinline__ void eo_odd(const double (&O)[2][2], const double (&o)[EO<N>::H], double (&so)[EO<N>::H > 0 ? EO<N>::H : 1]) {
+#pragma unroll
+  for (int i = 0; i < EO<N>::H; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < EO<N>::H; ++k) s = fma(O[i][k], o[k], s);
+    so[i] = s;
+  }
+}
+template <int N>
+__device__ __forceinline__ void eo_merge(const double (&se)[EO<N>::HE], const double (&so)[EO<N>::H], double (&out)[N]) {
+#pragma unroll
+  for (int i = 0; i < EO<N>::H; ++i) {
+    out[i] = se[i] + so[i];
+    out[N - 1 - i] = se[i] - so[i];
+  }
+  if constexpr (N % 2 == 1) out[EO<N>::H] = se[EO<N>::H];
+}
 
 template <int N, int F>
 struct Cfg {
@@ -42,8 +94,10 @@ struct Cfg {
   static constexpr int NC = (128 / NL) > 0 ? (128 / NL) : 1;
   static constexpr int T = ((NC * NL * FG + 31) / 32) * 32;
   static constexpr int MINB = FG == 1 ? 4 : 2;
-  static constexpr int SD = stl::Lay<N>::SD;
-  static constexpr int ARR = NC * F * SD;
+  using Lay = Layout<N, F>;
+  // one buffer per array, holding layout 1 (stage A -> B) and then layout 2
+  // (stage B -> C)
+  static constexpr int ARR = NC * (Lay::CS1 > Lay::CS2 ? Lay::CS1 : Lay::CS2);
   static constexpr size_t smem_bytes() { return sizeof(double) * 2 * static_cast<size_t>(ARR); }
 };
 
@@ -52,8 +106,8 @@ __global__ void __launch_bounds__(Cfg<N, F>::T, Cfg<N, F>::MINB)
     st_cart_kernel(const __grid_constant__ DevLevel L, const double* __restrict__ u, double* __restrict__ y,
                    double sign) {
   using C = Cfg<N, F>;
-  constexpr int NL = C::NL, NC = C::NC, SD = C::SD, ARR = C::ARR, FPG = C::FPG;
-  constexpr int RY = stl::Lay<N>::RY, PZ = stl::Lay<N>::PZ;
+  using Y = typename C::Lay;
+  constexpr int NL = C::NL, NC = C::NC, ARR = C::ARR, FPG = C::FPG;
   extern __shared__ __align__(16) double smem[];
   double* A0 = smem;
   double* A1 = A0 + ARR;
@@ -91,56 +145,91 @@ __global__ void __launch_bounds__(Cfg<N, F>::T, Cfg<N, F>::MINB)
         gin[jj][k] = (dir || j0 + jj >= F) ? 0.0 : __ldg(u + (j0 + jj) * ns + base + b * dxy + k * dx + a);
       }
   }
-  const int cbase = c * F * SD;
-  const int oy = cbase + a + PZ * b;       // y-line (x = a, z = b), stride RY
-  const int ox = cbase + RY * a + PZ * b;  // x-line (y = a, z = b), stride 1
-  const int oz = cbase + a + RY * b;       // z-line (x = a, y = b), stride PZ
+  // stage A: y-line (x = a, z = b) of layout 1; stage B: x-line (y, z) =
+  // (a, b), or (b, a) when the layout swaps, read from layout 1 and written to
+  // layout 2; stage C: z-line (x = a, y = b) of layout 2
+  const int oy = c * Y::CS1 + a + Y::PZ1 * b;
+  const int by = Y::SWAP ? b : a, bz = Y::SWAP ? a : b;
+  const int ox1 = c * Y::CS1 + Y::RY1 * by + Y::PZ1 * bz;
+  const int ox2 = c * Y::CS2 + Y::RY2 * by + Y::PZ2 * bz;
+  const int oz = c * Y::CS2 + a + Y::RY2 * b;
 
   // ---- A: y-owner, a = Mr_y u, b = Kr_y u
   if (valid) {
 #pragma unroll
     for (int jj = 0; jj < FPG; ++jj) {
       if (j0 + jj >= F) break;
-      const int o = oy + (j0 + jj) * SD;
+      const int o = oy + (j0 + jj) * Y::SD1;
+      double e[EO<N>::HE], od[EO<N>::H], se[EO<N>::HE], so[EO<N>::H], ra[N], rb[N];
+      eo_split<N>(gin[jj], e, od);
+      eo_even<N>(L.MrE, e, se);
+      eo_odd<N>(L.MrO, od, so);
+      eo_merge<N>(se, so, ra);
+      eo_even<N>(L.KrE, e, se);
+      eo_odd<N>(L.KrO, od, so);
+      eo_merge<N>(se, so, rb);
 #pragma unroll
       for (int q = 0; q < N; ++q) {
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          s0 = fma(L.Mr[q][k], gin[jj][k], s0);
-          s1 = fma(L.Kr[q][k], gin[jj][k], s1);
-        }
-        A0[o + q * RY] = s0;
-        A1[o + q * RY] = s1;
+        A0[o + q * Y::RY1] = ra[q];
+        A1[o + q * Y::RY1] = rb[q];
       }
     }
   }
   __syncthreads();
 
-  // ---- B: x-owner, c = Mr_x a, pre = Kr_x a / hx^2 + Mr_x b / hy^2, in place
-  if (valid) {
-    const double sx = L.hinv2[0], sy = L.hinv2[1];
+  // ---- B: x-owner, c = Mr_x a, pre = Kr_x a / hx^2 + Mr_x b / hy^2
+  {
+    double vc[FPG][N], vp[FPG][N];
+    if (valid) {
+      const double sx = L.hinv2[0], sy = L.hinv2[1];
 #pragma unroll
-    for (int jj = 0; jj < FPG; ++jj) {
-      if (j0 + jj >= F) break;
-      const int o = ox + (j0 + jj) * SD;
-      double va[N], vb[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        va[k] = A0[o + k];
-        vb[k] = A1[o + k];
-      }
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int jj = 0; jj < FPG; ++jj) {
+        if (j0 + jj >= F) break;
+        const int o = ox1 + (j0 + jj) * Y::SD1;
+        double va[N], vb[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          s0 = fma(L.Mr[q][k], va[k], s0);
-          s1 = fma(L.Kr[q][k], va[k], s1);
-          s2 = fma(L.Mr[q][k], vb[k], s2);
+          va[k] = A0[o + k];
+          vb[k] = A1[o + k];
         }
-        A0[o + q] = s0;
-        A1[o + q] = fma(sx, s1, sy * s2);
+        double ea[EO<N>::HE], oa[EO<N>::H], eb[EO<N>::HE], ob[EO<N>::H];
+        eo_split<N>(va, ea, oa);
+        eo_split<N>(vb, eb, ob);
+        double se[EO<N>::HE], so[EO<N>::H], te[EO<N>::HE], to[EO<N>::H];
+        eo_even<N>(L.MrE, ea, se);
+        eo_odd<N>(L.MrO, oa, so);
+        eo_merge<N>(se, so, vc[jj]);
+        eo_even<N>(L.KrE, ea, se);
+        eo_odd<N>(L.KrO, oa, so);
+        eo_even<N>(L.MrE, eb, te);
+        eo_odd<N>(L.MrO, ob, to);
+#pragma unroll
+        for (int i = 0; i < EO<N>::HE; ++i) se[i] = fma(sx, se[i], sy * te[i]);
+#pragma unroll
+        for (int i = 0; i < EO<N>::H; ++i) so[i] = fma(sx, so[i], sy * to[i]);
+        eo_merge<N>(se, so, vp[jj]);
+        if constexpr (!Y::SPLIT) {  // in place: this thread owns the line
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            A0[o + q] = vc[jj][q];
+            A1[o + q] = vp[jj][q];
+          }
+        }
+      }
+    }
+    if constexpr (Y::SPLIT) {
+      __syncthreads();
+      if (valid) {
+#pragma unroll
+        for (int jj = 0; jj < FPG; ++jj) {
+          if (j0 + jj >= F) break;
+          const int o = ox2 + (j0 + jj) * Y::SD2;
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            A0[o + q] = vc[jj][q];
+            A1[o + q] = vp[jj][q];
+          }
+        }
       }
     }
   }
@@ -165,8 +254,8 @@ __global__ void __launch_bounds__(Cfg<N, F>::T, Cfg<N, F>::MINB)
       double vc[N], vp[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        vc[k] = A0[oz + j * SD + k * PZ];
-        vp[k] = A1[oz + j * SD + k * PZ];
+        vc[k] = A0[oz + j * Y::SD2 + k * Y::PZ2];
+        vp[k] = A1[oz + j * Y::SD2 + k * Y::PZ2];
       }
 #pragma unroll
       for (int ii = 0; ii < FPG; ++ii) {
@@ -190,13 +279,22 @@ __global__ void __launch_bounds__(Cfg<N, F>::T, Cfg<N, F>::MINB)
     for (int ii = 0; ii < FPG; ++ii) {
       const int i = j0 + ii;
       if (i >= F) break;
+      double em[EO<N>::HE], om[EO<N>::H], ek[EO<N>::HE], ok[EO<N>::H];
+      eo_split<N>(Zm[ii], em, om);
+      eo_split<N>(Zk[ii], ek, ok);
+      double se[EO<N>::HE], so[EO<N>::H], te[EO<N>::HE], to[EO<N>::H], out[N];
+      eo_even<N>(L.MrE, em, se);
+      eo_odd<N>(L.MrO, om, so);
+      eo_even<N>(L.KrE, ek, te);
+      eo_odd<N>(L.KrO, ok, to);
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        double s = 0.0;
+      for (int q = 0; q < EO<N>::HE; ++q) se[q] += te[q];
 #pragma unroll
-        for (int q = 0; q < N; ++q) s = fma(L.Mr[k][q], Zm[ii][q], fma(L.Kr[k][q], Zk[ii][q], s));
-        if (!dirichlet(a, b, k)) atomicAdd(y + i * ns + base + k * dxy + b * dx + a, sign * s);
-      }
+      for (int q = 0; q < EO<N>::H; ++q) so[q] += to[q];
+      eo_merge<N>(se, so, out);
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (!dirichlet(a, b, k)) atomicAdd(y + i * ns + base + k * dxy + b * dx + a, sign * out[k]);
     }
   }
 }

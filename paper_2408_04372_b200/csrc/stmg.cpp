@@ -144,6 +144,24 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
       d.Kr[i][j] = kr;
     }
   for (int a = 0; a < 3; ++a) d.hinv2[a] = 1.0 / (d.h[a] * d.h[a]);
+  std::memset(d.MrE, 0, sizeof(d.MrE));
+  std::memset(d.MrO, 0, sizeof(d.MrO));
+  std::memset(d.KrE, 0, sizeof(d.KrE));
+  std::memset(d.KrO, 0, sizeof(d.KrO));
+  {
+    const int n = d.n, H = n / 2, HE = (n + 1) / 2;
+    for (int i = 0; i < HE; ++i)
+      for (int k = 0; k < HE; ++k) {
+        const bool mid = (n % 2 == 1) && k == H;
+        d.MrE[i][k] = mid ? d.Mr[i][k] : 0.5 * (d.Mr[i][k] + d.Mr[i][n - 1 - k]);
+        d.KrE[i][k] = mid ? d.Kr[i][k] : 0.5 * (d.Kr[i][k] + d.Kr[i][n - 1 - k]);
+      }
+    for (int i = 0; i < H; ++i)
+      for (int k = 0; k < H; ++k) {
+        d.MrO[i][k] = 0.5 * (d.Mr[i][k] - d.Mr[i][n - 1 - k]);
+        d.KrO[i][k] = 0.5 * (d.Kr[i][k] - d.Kr[i][n - 1 - k]);
+      }
+  }
   std::vector<double> CM, CA;
   block_coefficient_matrices(equation, weights, tau, n_steps, CM, CA);
   std::memset(d.CM, 0, sizeof(d.CM));
@@ -489,19 +507,20 @@ std::vector<std::complex<double>> eigvec_small(const std::vector<double>& G, int
 }
 }  // namespace
 
-// Real block diagonalisation of the temporal solves of the cell blocks:
-// T_M + lam T_A = T_A (G + lam I), G = T_A^-1 T_M = Q B Q^-1 with B 1x1 real
-// eigenvalues and 2x2 [[a, b], [-b, a]] blocks for conjugate pairs a +- ib, so
-// (T_M + lam T_A)^-1 = Q (B + lam)^-1 (Q^-1 T_A^-1). Fills A.P/Q/kind/s0/s1
-// over the S*n_t slab columns and sets A.tdiag; leaves it 0 (the pivoted
-// per-eigenvalue solve is used) when G has a repeated eigenvalue or Q is
-// ill-conditioned.
-void temporal_block_diagonalise(DevASM& A) {
-  A.tdiag = 0;
-  const int n = A.nt, S = A.S, ncol = n * S;
-  if (ncol > 8 || n < 1) return;
-  std::vector<double> TM(A.TM, A.TM + n * n), TA(A.TA, A.TA + n * n), TAi, G(static_cast<size_t>(n * n), 0.0);
-  if (!invert_small(TA, n, TAi)) return;
+struct TBlk {
+  int size;
+  double a, b;
+};
+
+// G = T_A^-1 T_M = Q B Q^-1 with B real block diagonal (1x1 eigenvalues, 2x2
+// [[a, b], [-b, a]] blocks for conjugate pairs, pairs first); Pm = Q^-1 T_A^-1.
+// false when T_A is singular, G has a repeated eigenvalue, or Q is
+// ill-conditioned (the callers keep the pivoted solves then).
+bool temporal_fd(const double* TMp, const double* TAp, int n, std::vector<double>& Pm, std::vector<double>& Qm,
+                 std::vector<TBlk>& blocks) {
+  if (n < 1 || n > 4) return false;
+  std::vector<double> TM(TMp, TMp + n * n), TA(TAp, TAp + n * n), TAi, G(static_cast<size_t>(n * n), 0.0);
+  if (!invert_small(TA, n, TAi)) return false;
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j)
       for (int k = 0; k < n; ++k) G[static_cast<size_t>(i * n + j)] += TAi[static_cast<size_t>(i * n + k)] * TM[static_cast<size_t>(k * n + j)];
@@ -509,20 +528,16 @@ void temporal_block_diagonalise(DevASM& A) {
   try {
     ev = eigenvalues_small(G, n);
   } catch (const std::exception&) {
-    return;
+    return false;
   }
   double gmax = 0.0;
   for (auto& e : ev) gmax = std::max(gmax, std::hypot(e.first, e.second));
   for (size_t a = 0; a < ev.size(); ++a)
     for (size_t b = a + 1; b < ev.size(); ++b)
-      if (std::hypot(ev[a].first - ev[b].first, ev[a].second - ev[b].second) < 1e-8 * gmax) return;
+      if (std::hypot(ev[a].first - ev[b].first, ev[a].second - ev[b].second) < 1e-8 * gmax) return false;
   // blocks in Q column order: complex pairs first (they need aligned slot pairs)
-  struct Blk {
-    int size;
-    double a, b;
-  };
-  std::vector<Blk> blocks;
-  std::vector<double> Qm(static_cast<size_t>(n * n), 0.0);
+  blocks.clear();
+  Qm.assign(static_cast<size_t>(n * n), 0.0);
   int col = 0;
   for (int pass = 0; pass < 2; ++pass)
     for (auto& e : ev) {
@@ -537,9 +552,9 @@ void temporal_block_diagonalise(DevASM& A) {
       blocks.push_back({cplx ? 2 : 1, e.first, cplx ? e.second : 0.0});
       col += cplx ? 2 : 1;
     }
-  if (col != n) return;
+  if (col != n) return false;
   std::vector<double> Qi;
-  if (!invert_small(Qm, n, Qi)) return;
+  if (!invert_small(Qm, n, Qi)) return false;
   // conditioning and reconstruction checks: Q B Q^-1 == G
   double nq = 0.0, nqi = 0.0;
   for (int i = 0; i < n; ++i) {
@@ -551,7 +566,7 @@ void temporal_block_diagonalise(DevASM& A) {
     nq = std::max(nq, r1);
     nqi = std::max(nqi, r2);
   }
-  if (nq * nqi > 1e6) return;
+  if (nq * nqi > 1e6) return false;
   std::vector<double> B(static_cast<size_t>(n * n), 0.0);
   {
     int c = 0;
@@ -574,12 +589,29 @@ void temporal_block_diagonalise(DevASM& A) {
           s += Qm[static_cast<size_t>(i * n + k)] * B[static_cast<size_t>(k * n + l)] * Qi[static_cast<size_t>(l * n + j)];
       err = std::max(err, std::abs(s - G[static_cast<size_t>(i * n + j)]));
     }
-  if (err > 1e-10 * std::max(gmax, 1e-300)) return;
+  if (err > 1e-10 * std::max(gmax, 1e-300)) return false;
   // Pm = Q^-1 T_A^-1
-  std::vector<double> Pm(static_cast<size_t>(n * n), 0.0);
+  Pm.assign(static_cast<size_t>(n * n), 0.0);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j)
       for (int k = 0; k < n; ++k) Pm[static_cast<size_t>(i * n + j)] += Qi[static_cast<size_t>(i * n + k)] * TAi[static_cast<size_t>(k * n + j)];
+  return true;
+}
+
+// Real block diagonalisation of the temporal solves of the cell blocks:
+// T_M + lam T_A = T_A (G + lam I), G = T_A^-1 T_M = Q B Q^-1 with B 1x1 real
+// eigenvalues and 2x2 [[a, b], [-b, a]] blocks for conjugate pairs a +- ib, so
+// (T_M + lam T_A)^-1 = Q (B + lam)^-1 (Q^-1 T_A^-1). Fills A.P/Q/kind/s0/s1
+// over the S*n_t slab columns and sets A.tdiag; leaves it 0 (the pivoted
+// per-eigenvalue solve is used) when G has a repeated eigenvalue or Q is
+// ill-conditioned.
+void temporal_block_diagonalise(DevASM& A) {
+  A.tdiag = 0;
+  const int n = A.nt, S = A.S, ncol = n * S;
+  if (ncol > 8 || n < 1) return;
+  std::vector<double> Pm, Qm;
+  std::vector<TBlk> blocks;
+  if (!temporal_fd(A.TM, A.TA, n, Pm, Qm, blocks)) return;
   // slots: complex blocks of every step on aligned pairs, then the reals
   std::vector<int> slot(static_cast<size_t>(S * n), -1);  // (step, transformed component) -> slot
   int next_pair = 0;
@@ -681,6 +713,39 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
     Fd.n_space = d.n_space;
     std::memcpy(Fd.TM, A.TM, sizeof(A.TM));
     std::memcpy(Fd.TA, A.TA, sizeof(A.TA));
+    // temporal fast diagonalisation of the per-eigen-index n_t x n_t solves
+    // (STMG_NO_TDIAG keeps the pivoted elimination, for testing)
+    Fd.tdiag = 0;
+    {
+      std::vector<double> Pm, Qm;
+      std::vector<TBlk> blocks;
+      if (!std::getenv("STMG_NO_TDIAG") && temporal_fd(A.TM, A.TA, A.nt, Pm, Qm, blocks)) {
+        const int n = A.nt;
+        for (int i = 0; i < 16; ++i) Fd.tP[i] = Fd.tQ[i] = 0.0;
+        for (int i = 0; i < n * n; ++i) {
+          Fd.tP[i] = Pm[static_cast<size_t>(i)];
+          Fd.tQ[i] = Qm[static_cast<size_t>(i)];
+        }
+        for (int i = 0; i < 4; ++i) {
+          Fd.tkind[i] = 0;
+          Fd.ta[i] = 1.0;
+          Fd.tb[i] = 0.0;
+        }
+        int c = 0;
+        for (const TBlk& b : blocks) {
+          Fd.tkind[c] = b.size == 2 ? 1 : 0;
+          Fd.ta[c] = b.a;
+          Fd.tb[c] = b.b;
+          if (b.size == 2) {
+            Fd.tkind[c + 1] = 2;
+            Fd.ta[c + 1] = b.a;
+            Fd.tb[c + 1] = b.b;
+          }
+          c += b.size;
+        }
+        Fd.tdiag = 1;
+      }
+    }
     Fd.rho0 = d.rho0;
     Fd.rho_shift = d.rho_shift;
     Fd.skip = nullptr;

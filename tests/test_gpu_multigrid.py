@@ -205,3 +205,51 @@ def test_asm_64dof_kernel_variants(cuda, ref, env, kind):
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "ok" in out.stdout
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("eq,scheme,k,S", Q3_TIME_CASES)
+def test_asm_cartesian_fdm_temporal_variants(cuda, ref, eq, scheme, k, S, p):
+    """Cartesian cells (tensor-product FDM kernel, temporally fast-diagonalised
+    n_t x n_t solves) across heat/wave, DG/CGP, k and S: equal to the
+    reference's LU block solves to 1e-9."""
+    cfg = problems.Config("fdm", eq, scheme, 3, 2, 1, p, k, S, 0.2)
+    mesh, M, R = _build(cfg, ref)
+    n = R.n_dofs
+    res = problems.uniform_vector(n, seed=61)
+    z0 = problems.uniform_vector(n, seed=62)
+    got = M.asm_add_correction(0, _dev(cuda, res), _dev(cuda, z0)).cpu().numpy()
+    want = R.asm_add_correction(0, res, z0)
+    assert M.smoother_kind(0) == 1  # tensor-product FDM everywhere
+    assert _rel(got - z0, want - z0) <= 1e-9
+
+
+def test_asm_cartesian_fdm_pivoted_fallback(cuda, ref):
+    """The FDM kernel's pivoted per-eigen-index solves (STMG_NO_TDIAG, the
+    path taken when T_A^-1 T_M is not safely diagonalisable) match the
+    reference; subprocess because the choice is made at setup from the
+    environment."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import refbind as ref\n"
+        "from paper_2408_04372_b200 import api, problems\n"
+        "cfg = problems.config('C5-4')\n"
+        "mesh = api.Mesh(cfg.dim, (0,0,0), (1,1,1), cfg.base_cells, cfg.refinements, cfg.vertices())\n"
+        "M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps, cfg.tau)\n"
+        "R = ref.Reference(cfg, with_mg=True)\n"
+        "r = problems.uniform_vector(R.n_dofs, seed=71); z0 = problems.uniform_vector(R.n_dofs, seed=72)\n"
+        "got = M.asm_add_correction(0, torch.from_numpy(r).cuda(), torch.from_numpy(z0).cuda()).cpu().numpy()\n"
+        "want = R.asm_add_correction(0, r, z0)\n"
+        "err = np.linalg.norm((got - z0) - (want - z0)) / np.linalg.norm(want - z0)\n"
+        "assert M.smoother_kind(0) == 1, M.smoother_kind(0)\n"
+        "assert err <= 1e-9, err\n"
+        "print('ok', err)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env_vars = dict(os.environ, STMG_NO_TDIAG="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env_vars, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok" in out.stdout

@@ -268,10 +268,191 @@ __global__ void __launch_bounds__(kT) asm_fdm_kernel(const __grid_constant__ Dev
   }
 }
 
+// 1D eigenbasis line transforms. Generic: out[e] = sum_k S[k][e] in[k]
+// (forward, S^T) / out[k] = sum_e S[k][e] in[e] (backward, S). EO: the
+// interior position class, whose host-reordered eigenvectors are symmetric
+// (columns 0 .. HE-1) then antisymmetric (HE .. N-1) about the cell centre,
+// so both transforms split into even / odd halves (N = 5: 13 FMAs instead
+// of 25) and read the table at compile-time indices.
+template <int N, bool EO>
+__device__ __forceinline__ void fdm_fwd(const double (&S)[kMaxN][kMaxN], const double (&in)[N], double (&out)[N]) {
+  if constexpr (EO) {
+    constexpr int H = N / 2, HE = (N + 1) / 2;
+    double ev[HE], ov[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      ev[k] = in[k] + in[N - 1 - k];
+      ov[k] = in[k] - in[N - 1 - k];
+    }
+    if constexpr (N % 2 == 1) ev[H] = in[H];
+#pragma unroll
+    for (int e = 0; e < HE; ++e) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < HE; ++k) acc = fma(S[k][e], ev[k], acc);
+      out[e] = acc;
+    }
+#pragma unroll
+    for (int e = 0; e < H; ++e) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < H; ++k) acc = fma(S[k][HE + e], ov[k], acc);
+      out[HE + e] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc = fma(S[k][e], in[k], acc);
+      out[e] = acc;
+    }
+  }
+}
+template <int N, bool EO>
+__device__ __forceinline__ void fdm_bwd(const double (&S)[kMaxN][kMaxN], const double (&in)[N], double (&out)[N]) {
+  if constexpr (EO) {
+    constexpr int H = N / 2, HE = (N + 1) / 2;
+#pragma unroll
+    for (int k = 0; k < HE; ++k) {
+      double A = 0.0, B = 0.0;
+#pragma unroll
+      for (int e = 0; e < HE; ++e) A = fma(S[k][e], in[e], A);
+      if (k < H) {
+#pragma unroll
+        for (int e = 0; e < H; ++e) B = fma(S[k][HE + e], in[HE + e], B);
+        out[k] = A + B;
+        out[N - 1 - k] = A - B;
+      } else {
+        out[k] = A;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) acc = fma(S[k][e], in[e], acc);
+      out[k] = acc;
+    }
+  }
+}
+
+// the five stages of one cell batch; EO: every cell of the CTA is interior
+// along all three axes (position class 0, even-odd transforms)
+template <int N, int NT, bool TD, bool EO>
+__device__ __forceinline__ void fdm_stages(const DevFDM& P, const double* __restrict__ r, double* __restrict__ z,
+                                           double scale, double* W, bool valid, long long base, int mask, int tx,
+                                           int ty, int tz, double rho, int a, int b, int oy, int ox, int oz) {
+  using Y = stc::FdmLayout<N, NT>;
+  constexpr int SD = Y::SD, RY = Y::RY, PZ = Y::PZ;
+  constexpr int p = N - 1;
+  const long long dx = P.dofs[0], dxy = P.dofs[0] * P.dofs[1];
+  auto bdry = [&](int lx, int ly, int lz) {
+    return ((mask & 1) && lx == 0) || ((mask & 2) && lx == p) || ((mask & 4) && ly == 0) || ((mask & 8) && ly == p) ||
+           ((mask & 16) && lz == 0) || ((mask & 32) && lz == p);
+  };
+  const double(&Sx)[kMaxN][kMaxN] = P.S1[0][EO ? 0 : tx];
+  const double(&Sy)[kMaxN][kMaxN] = P.S1[1][EO ? 0 : ty];
+  const double(&Sz)[kMaxN][kMaxN] = P.S1[2][EO ? 0 : tz];
+  {  // one step per CTA row (blockIdx.y): no loop-invariant table hoisting
+    const long long st = blockIdx.y;
+    const double* rs = r + st * NT * P.n_space;
+    double* zs = z + st * NT * P.n_space;
+    // A: y-owner (x = a, z = b): gather, S_y^T
+    if (valid) {
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N], out[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) in[k] = __ldg(rs + f * P.n_space + base + b * dxy + k * dx + a);
+        fdm_fwd<N, EO>(Sy, in, out);
+#pragma unroll
+        for (int e = 0; e < N; ++e) W[oy + f * SD + e * RY] = out[e];
+      }
+    }
+    __syncthreads();
+    // B: x-owner (y = a, z = b): S_x^T
+    if (valid) {
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N], out[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) in[k] = W[ox + f * SD + k];
+        fdm_fwd<N, EO>(Sx, in, out);
+#pragma unroll
+        for (int e = 0; e < N; ++e) W[ox + f * SD + e] = out[e];
+      }
+    }
+    __syncthreads();
+    // C: z-owner (eigen-indices ex = a, ey = b): S_z^T, solves, S_z
+    if (valid) {
+      double v[NT][N];
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) in[k] = W[oz + f * SD + k * PZ];
+        fdm_fwd<N, EO>(Sz, in, v[f]);
+      }
+      const double lxy = P.L1[0][EO ? 0 : tx][a] + P.L1[1][EO ? 0 : ty][b];
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        double bb[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int f = 0; f < NT; ++f) bb[f] = v[f][e];
+        temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][EO ? 0 : tz][e]), bb);
+#pragma unroll
+        for (int f = 0; f < NT; ++f) v[f][e] = bb[f];
+      }
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double out[N];
+        fdm_bwd<N, EO>(Sz, v[f], out);
+#pragma unroll
+        for (int k = 0; k < N; ++k) W[oz + f * SD + k * PZ] = out[k];
+      }
+    }
+    __syncthreads();
+    // D: x-owner: S_x
+    if (valid) {
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N], out[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) in[e] = W[ox + f * SD + e];
+        fdm_bwd<N, EO>(Sx, in, out);
+#pragma unroll
+        for (int k = 0; k < N; ++k) W[ox + f * SD + k] = out[k];
+      }
+    }
+    __syncthreads();
+    // E: y-owner: S_y, weighted scatter (asm_smoother.cpp:45-49, 75)
+    if (valid) {
+      const double wxz = ((a == 0 && !(mask & 1)) || (a == p && !(mask & 2)) ? 0.5 : 1.0) *
+                         ((b == 0 && !(mask & 16)) || (b == p && !(mask & 32)) ? 0.5 : 1.0);
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N], out[N];
+#pragma unroll
+        for (int e = 0; e < N; ++e) in[e] = W[oy + f * SD + e * RY];
+        fdm_bwd<N, EO>(Sy, in, out);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const long long g = base + b * dxy + k * dx + a;
+          const double val = bdry(a, k, b) ? __ldg(rs + f * P.n_space + g) : out[k];
+          const double wy = (k == 0 && !(mask & 4)) || (k == p && !(mask & 8)) ? 0.5 : 1.0;
+          atomicAdd(zs + f * P.n_space + g, scale * wxz * wy * val);
+        }
+      }
+    }
+  }
+}
+
 // 3D line-owner FDM solve (the st_lines.cuh pattern): a 128-thread CTA owns
 // NC cells, thread (c, a, b) owns lattice line (a, b) of cell c along the
-// axis the stage sweeps, for the n_t fields of one step at a time, in
-// registers. Per step: y-owner gathers r and applies S_y^T, x-owner S_x^T,
+// axis the stage sweeps, for the n_t fields of the step blockIdx.y, in
+// registers. y-owner gathers r and applies S_y^T, x-owner S_x^T,
 // z-owner S_z^T + the n_t x n_t solves at its N eigen-points + S_z, x-owner
 // S_x, y-owner S_y and the weighted scatter (Dirichlet rows: w r, re-read).
 template <int N, int NT, bool TD>
@@ -279,7 +460,7 @@ __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant
                                                         const double* __restrict__ r, double* __restrict__ z,
                                                         double scale) {
   using Y = stc::FdmLayout<N, NT>;  // bank-conflict-modelled (scripts/gen_cart_layout.py)
-  constexpr int NL = N * N, NC = 128 / NL, SD = Y::SD, RY = Y::RY, PZ = Y::PZ;
+  constexpr int NL = N * N, NC = 128 / NL, RY = Y::RY, PZ = Y::PZ;
   __shared__ double W[NC * Y::CS];
   const int t = threadIdx.x;
   const int c = t / NL, l = t - (t / NL) * NL;
@@ -307,136 +488,17 @@ __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant
       rho = P.rho0[(az * P.cells0[1] + ay) * P.cells0[0] + ax];
     }
   }
-  auto bdry = [&](int lx, int ly, int lz) {
-    return ((mask & 1) && lx == 0) || ((mask & 2) && lx == p) || ((mask & 4) && ly == 0) || ((mask & 8) && ly == p) ||
-           ((mask & 16) && lz == 0) || ((mask & 32) && lz == p);
-  };
   const int cb = c * Y::CS;
   const int oy = cb + a + PZ * b, oz = cb + a + RY * b;
   const int ox = cb + RY * (Y::SWAP ? b : a) + PZ * (Y::SWAP ? a : b);
-  const double(&Sx)[kMaxN][kMaxN] = P.S1[0][tx];
-  const double(&Sy)[kMaxN][kMaxN] = P.S1[1][ty];
-  const double(&Sz)[kMaxN][kMaxN] = P.S1[2][tz];
-  for (int st = 0; st < P.S; ++st) {
-    const double* rs = r + static_cast<long long>(st) * NT * P.n_space;
-    double* zs = z + static_cast<long long>(st) * NT * P.n_space;
-    // A: y-owner (x = a, z = b): gather, S_y^T
-    if (valid) {
-#pragma unroll
-      for (int f = 0; f < NT; ++f) {
-        double in[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) in[k] = __ldg(rs + f * P.n_space + base + b * dxy + k * dx + a);
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < N; ++k) acc = fma(Sy[k][e], in[k], acc);
-          W[oy + f * SD + e * RY] = acc;
-        }
-      }
-    }
-    __syncthreads();
-    // B: x-owner (y = a, z = b): S_x^T
-    if (valid) {
-#pragma unroll
-      for (int f = 0; f < NT; ++f) {
-        double in[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) in[k] = W[ox + f * SD + k];
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < N; ++k) acc = fma(Sx[k][e], in[k], acc);
-          W[ox + f * SD + e] = acc;
-        }
-      }
-    }
-    __syncthreads();
-    // C: z-owner (eigen-indices ex = a, ey = b): S_z^T, solves, S_z
-    if (valid) {
-      double v[NT][N];
-#pragma unroll
-      for (int f = 0; f < NT; ++f) {
-        double in[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) in[k] = W[oz + f * SD + k * PZ];
-#pragma unroll
-        for (int e = 0; e < N; ++e) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < N; ++k) acc = fma(Sz[k][e], in[k], acc);
-          v[f][e] = acc;
-        }
-      }
-      const double lxy = P.L1[0][tx][a] + P.L1[1][ty][b];
-#pragma unroll
-      for (int e = 0; e < N; ++e) {
-        double bb[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int f = 0; f < NT; ++f) bb[f] = v[f][e];
-        temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][tz][e]), bb);
-#pragma unroll
-        for (int f = 0; f < NT; ++f) v[f][e] = bb[f];
-      }
-#pragma unroll
-      for (int f = 0; f < NT; ++f) {
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double acc = 0.0;
-#pragma unroll
-          for (int e = 0; e < N; ++e) acc = fma(Sz[k][e], v[f][e], acc);
-          W[oz + f * SD + k * PZ] = acc;
-        }
-      }
-    }
-    __syncthreads();
-    // D: x-owner: S_x
-    if (valid) {
-#pragma unroll
-      for (int f = 0; f < NT; ++f) {
-        double in[N];
-#pragma unroll
-        for (int e = 0; e < N; ++e) in[e] = W[ox + f * SD + e];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double acc = 0.0;
-#pragma unroll
-          for (int e = 0; e < N; ++e) acc = fma(Sx[k][e], in[e], acc);
-          W[ox + f * SD + k] = acc;
-        }
-      }
-    }
-    __syncthreads();
-    // E: y-owner: S_y, weighted scatter (asm_smoother.cpp:45-49, 75)
-    if (valid) {
-      const double wxz = ((a == 0 && !(mask & 1)) || (a == p && !(mask & 2)) ? 0.5 : 1.0) *
-                         ((b == 0 && !(mask & 16)) || (b == p && !(mask & 32)) ? 0.5 : 1.0);
-#pragma unroll
-      for (int f = 0; f < NT; ++f) {
-        double in[N];
-#pragma unroll
-        for (int e = 0; e < N; ++e) in[e] = W[oy + f * SD + e * RY];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          const long long g = base + b * dxy + k * dx + a;
-          double val;
-          if (bdry(a, k, b)) {
-            val = __ldg(rs + f * P.n_space + g);
-          } else {
-            double acc = 0.0;
-#pragma unroll
-            for (int e = 0; e < N; ++e) acc = fma(Sy[k][e], in[e], acc);
-            val = acc;
-          }
-          const double wy = (k == 0 && !(mask & 4)) || (k == p && !(mask & 8)) ? 0.5 : 1.0;
-          atomicAdd(zs + f * P.n_space + g, scale * wxz * wy * val);
-        }
-      }
-    }
-    __syncthreads();
-  }
+  // CTAs whose cells are all interior take the even-odd transforms
+  // (uniform branch; P.eo = 0 when the host could not order the interior
+  // eigenvectors by parity)
+  const bool all_interior = __syncthreads_and(!valid || mask == 0) && P.eo;
+  if (all_interior)
+    fdm_stages<N, NT, TD, true>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
+  else
+    fdm_stages<N, NT, TD, false>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
 }
 
 template <int N, int NT>
@@ -444,10 +506,11 @@ void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cud
   constexpr int NC = 128 / (N * N);
   const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
   count_launch();
+  const dim3 grid(static_cast<unsigned>((n_cells + NC - 1) / NC), static_cast<unsigned>(P.S));
   if (P.tdiag)
-    fdm_lines_kernel<N, NT, true><<<static_cast<unsigned>((n_cells + NC - 1) / NC), 128, 0, s>>>(P, r, z, scale);
+    fdm_lines_kernel<N, NT, true><<<grid, 128, 0, s>>>(P, r, z, scale);
   else
-    fdm_lines_kernel<N, NT, false><<<static_cast<unsigned>((n_cells + NC - 1) / NC), 128, 0, s>>>(P, r, z, scale);
+    fdm_lines_kernel<N, NT, false><<<grid, 128, 0, s>>>(P, r, z, scale);
 }
 
 template <int DIM, int N, int NT>

@@ -173,6 +173,9 @@ struct DevFDM {
   // block diagonal: tkind[i] = 0 real eigenvalue ta[i]; 1 first column of a
   // conjugate pair [[ta, tb], [-tb, ta]] (2 its second column)
   int tdiag;
+  // interior position class (S1[a][0]) ordered symmetric-then-antisymmetric
+  // eigenvectors on every axis: the even-odd transforms apply
+  int eo;
   int tkind[4];
   double ta[4], tb[4];
   double tP[16], tQ[16];

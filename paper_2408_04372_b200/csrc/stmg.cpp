@@ -667,6 +667,46 @@ void temporal_block_diagonalise(DevASM& A) {
   A.tdiag = 1;
 }
 
+// Reorders the interior-class 1D eigenpairs of every axis: eigenvectors
+// symmetric about the cell centre first, antisymmetric after (the even-odd
+// FDM transforms, asm_fdm.cu fdm_fwd / fdm_bwd). The interior 1D matrices
+// are centro-symmetric, so with distinct eigenvalues every eigenvector has a
+// parity; false (tables untouched) if one does not or the counts differ.
+bool fdm_order_interior_by_parity(DevFDM& F, int dim) {
+  const int n = F.n, H = n / 2, HE = (n + 1) / 2;
+  double S[3][kMaxN][kMaxN], L[3][kMaxN];
+  for (int a = 0; a < dim; ++a) {
+    std::vector<int> sym, anti;
+    for (int e = 0; e < n; ++e) {
+      double scale = 0.0, ds = 0.0, da = 0.0;
+      for (int k = 0; k < n; ++k) {
+        scale = std::max(scale, std::abs(F.S1[a][0][k][e]));
+        ds = std::max(ds, std::abs(F.S1[a][0][k][e] - F.S1[a][0][n - 1 - k][e]));
+        da = std::max(da, std::abs(F.S1[a][0][k][e] + F.S1[a][0][n - 1 - k][e]));
+      }
+      if (ds <= 1e-12 * scale)
+        sym.push_back(e);
+      else if (da <= 1e-12 * scale)
+        anti.push_back(e);
+      else
+        return false;
+    }
+    if (static_cast<int>(sym.size()) != HE || static_cast<int>(anti.size()) != H) return false;
+    std::vector<int> order(sym);
+    order.insert(order.end(), anti.begin(), anti.end());
+    for (int e = 0; e < n; ++e) {
+      L[a][e] = F.L1[a][0][order[static_cast<size_t>(e)]];
+      for (int k = 0; k < n; ++k) S[a][k][e] = F.S1[a][0][k][order[static_cast<size_t>(e)]];
+    }
+  }
+  for (int a = 0; a < dim; ++a)
+    for (int e = 0; e < n; ++e) {
+      F.L1[a][0][e] = L[a][e];
+      for (int k = 0; k < n; ++k) F.S1[a][0][k][e] = S[a][k][e];
+    }
+  return true;
+}
+
 ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* probe_op, int probe_zcells)
     : op_(&op) {
   const DevLevel& d = op.desc();
@@ -762,6 +802,7 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
           for (int j = 0; j < kMaxN; ++j) Fd.S1[a][t][i][j] = S[t][i][j];
         }
     }
+    Fd.eo = fdm_order_interior_by_parity(Fd, d.dim) ? 1 : 0;
     if (d.rho0) {
       // host copy of the level-0 coefficient table
       const Index n0 = d.cells0[0] * d.cells0[1] * d.cells0[2];

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -293,6 +294,222 @@ void pass(int F, const PassArgs& A, const DevAxisTransfer& T, bool prolong, cons
   axis_pass_kernel<AXIS><<<grid, block, 0, s>>>(A, ptr, idx, w, in, out);
 }
 
+// Fused x-y h-transfer (equal p, 3D): one CTA per tile of TCX x TCY coarse
+// cells of one (z plane, field) stages the tile's input plane region in
+// shared memory (coalesced rows), applies the x pass into a second shared
+// array and the y pass straight to global memory -- the x-pass intermediate
+// never touches HBM. Restriction (first of two passes, z follows): input
+// masks as the separable first pass; prolongation (last pass, after the z
+// pass): output masks and accumulation as the separable last pass. The
+// per-cell rules are those of axis_cell_kernel.
+constexpr int kXyTCX = 16, kXyTCY = 4, kXyThreads = 256;
+
+template <int P, bool PROLONG>
+struct XyCfg {
+  // restriction: fine region of the tile's cells plus the left neighbour
+  // cell; prolongation: the tile's coarse nodes
+  static constexpr int LX = PROLONG ? kXyTCX * P + 1 : 2 * P * (kXyTCX + 1) + 1;
+  static constexpr int LY = PROLONG ? kXyTCY * P + 1 : 2 * P * (kXyTCY + 1) + 1;
+  // x-pass output columns: restriction coarse x nodes, prolongation fine x nodes
+  static constexpr int MX = PROLONG ? 2 * P * kXyTCX + 1 : kXyTCX * P + 1;
+  static constexpr size_t smem_bytes() { return sizeof(double) * (static_cast<size_t>(LX) * LY + static_cast<size_t>(MX) * LY); }
+};
+
+template <int P, bool PROLONG>
+__global__ void __launch_bounds__(kXyThreads) xy_cell_kernel(const PassArgs A, const DevAxisTransfer Tx,
+                                                             const DevAxisTransfer Ty, const double* __restrict__ in,
+                                                             double* __restrict__ out) {
+  using C = XyCfg<P, PROLONG>;
+  extern __shared__ __align__(16) double sm[];
+  double* R0 = sm;                 // [LY][LX] input region
+  double* R1 = sm + C::LX * C::LY;  // [LY][MX] after the x pass
+  const long long ix = A.i[0], iy = A.i[1], ox = A.o[0], oy = A.o[1];
+  const long long z = blockIdx.z % A.o[2], f = blockIdx.z / A.o[2];
+  // coarse cells along x / y (coarse side: output of a restriction, input of a prolongation)
+  const long long ncx = PROLONG ? (ix - 1) / P : (ox - 1) / P, ncy = PROLONG ? (iy - 1) / P : (oy - 1) / P;
+  const long long cx0 = static_cast<long long>(blockIdx.x) * kXyTCX, cy0 = static_cast<long long>(blockIdx.y) * kXyTCY;
+  const int t = threadIdx.x;
+  // ---- load the input region (masked as the first / an inner pass)
+  const long long gx0 = PROLONG ? cx0 * P : 2 * P * (cx0 - 1), gy0 = PROLONG ? cy0 * P : 2 * P * (cy0 - 1);
+  bool plane0 = false;
+  if (!PROLONG && A.mask_in && A.i[2] > 1 && on_bdry_z(z, A.i[2], A.zbc)) plane0 = true;
+  if (!PROLONG && A.skip_lo_in && z == 0) plane0 = true;
+  const double* src = in + f * A.fs_in + z * iy * ix;
+  // all of a thread's loads are issued before any shared store (the loop is
+  // latency-bound otherwise)
+  constexpr int NLD = (C::LX * C::LY + kXyThreads - 1) / kXyThreads;
+  double v[NLD];
+#pragma unroll
+  for (int i = 0; i < NLD; ++i) {
+    const int e = t + i * kXyThreads;
+    const int ly = e / C::LX, lx = e - ly * C::LX;
+    const long long gx = gx0 + lx, gy = gy0 + ly;
+    v[i] = 0.0;
+    if (e < C::LX * C::LY && !plane0 && gx >= 0 && gx < ix && gy >= 0 && gy < iy) {
+      const bool masked = !PROLONG && A.mask_in && (on_bdry(gx, ix) || on_bdry(gy, iy));
+      if (!masked) v[i] = __ldg(src + gy * ix + gx);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NLD; ++i) {
+    const int e = t + i * kXyThreads;
+    if (e < C::LX * C::LY) R0[e] = v[i];
+  }
+  __syncthreads();
+  if (!PROLONG) {
+    // ---- x pass: (fine row ly, local coarse cell lc) -> coarse x nodes lc*P + jj;
+    // lanes run over rows (odd row pitch: conflict-free)
+    for (int e = t; e < C::LY * kXyTCX; e += kXyThreads) {
+      const int lc = e / C::LY, ly = e - lc * C::LY;
+      const long long c = cx0 + lc;
+      if (c >= ncx) continue;
+      const double* row = R0 + ly * C::LX;
+      double fv[2 * P + 1], lv[2 * P];
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) fv[r] = row[2 * P * (lc + 1) + r];
+#pragma unroll
+      for (int r = 0; r < 2 * P; ++r) lv[r] = row[2 * P * lc + r];
+#pragma unroll
+      for (int jj = 0; jj < P; ++jj) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r <= 2 * P; ++r) s = fma(Tx.hw[r][jj], fv[r], s);
+        if (jj == 0) {
+#pragma unroll
+          for (int r = 0; r < 2 * P; ++r) s = fma(Tx.hw[r][P], lv[r], s);
+        }
+        R1[ly * C::MX + lc * P + jj] = s;
+      }
+      if (c == ncx - 1) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r <= 2 * P; ++r) s = fma(Tx.hw[r][P], fv[r], s);
+        R1[ly * C::MX + lc * P + P] = s;
+      }
+    }
+    __syncthreads();
+    // ---- y pass: (coarse x node lx, local coarse y cell lc) -> coarse y nodes
+    double* dst = out + f * A.fs_out + z * oy * ox;
+    for (int e = t; e < C::MX * kXyTCY; e += kXyThreads) {
+      const int lc = e / C::MX, lx = e - lc * C::MX;
+      const long long c = cy0 + lc, gx = cx0 * P + lx;
+      if (c >= ncy || gx >= ox) continue;
+      if (lx == kXyTCX * P && gx != ox - 1) continue;  // the next tile's first node
+      double fv[2 * P + 1], lv[2 * P];
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) fv[r] = R1[(2 * P * (lc + 1) + r) * C::MX + lx];
+#pragma unroll
+      for (int r = 0; r < 2 * P; ++r) lv[r] = R1[(2 * P * lc + r) * C::MX + lx];
+#pragma unroll
+      for (int jj = 0; jj < P; ++jj) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r <= 2 * P; ++r) s = fma(Ty.hw[r][jj], fv[r], s);
+        if (jj == 0) {
+#pragma unroll
+          for (int r = 0; r < 2 * P; ++r) s = fma(Ty.hw[r][P], lv[r], s);
+        }
+        double* o = dst + (c * P + jj) * ox + gx;
+        if (A.accumulate) *o += s; else *o = s;
+      }
+      if (c == ncy - 1) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r <= 2 * P; ++r) s = fma(Ty.hw[r][P], fv[r], s);
+        double* o = dst + (c * P + P) * ox + gx;
+        if (A.accumulate) *o += s; else *o = s;
+      }
+    }
+  } else {
+    // ---- x pass: (coarse row ly, local coarse cell lc) -> fine x nodes 2P lc + r;
+    // lanes run over rows (odd row pitch: conflict-free)
+    for (int e = t; e < C::LY * kXyTCX; e += kXyThreads) {
+      const int lc = e / C::LY, ly = e - lc * C::LY;
+      const long long c = cx0 + lc;
+      if (c >= ncx) continue;
+      const double* row = R0 + ly * C::LX;
+      double cv[P + 1];
+#pragma unroll
+      for (int j = 0; j <= P; ++j) cv[j] = row[lc * P + j];
+      const int rmax = c == ncx - 1 ? 2 * P : 2 * P - 1;
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) {
+        if (r > rmax) break;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) s = fma(Tx.hw[r][j], cv[j], s);
+        R1[ly * C::MX + 2 * P * lc + r] = s;
+      }
+    }
+    __syncthreads();
+    // ---- y pass: (fine x column lx, local coarse y cell lc) -> fine y rows, masked store
+    const bool plane_out0 = A.mask_out && A.o[2] > 1 && on_bdry_z(z, A.o[2], A.zbc);
+    double* dst = out + f * A.fs_out + z * oy * ox;
+    for (int e = t; e < C::MX * kXyTCY; e += kXyThreads) {
+      const int lc = e / C::MX, lx = e - lc * C::MX;
+      const long long c = cy0 + lc, gx = 2 * P * cx0 + lx;
+      if (c >= ncy || gx >= ox) continue;
+      if (lx == 2 * P * kXyTCX && gx != ox - 1) continue;
+      double cv[P + 1];
+#pragma unroll
+      for (int j = 0; j <= P; ++j) cv[j] = R1[(lc * P + j) * C::MX + lx];
+      const bool col0 = plane_out0 || (A.mask_out && on_bdry(gx, ox));
+      const int rmax = c == ncy - 1 ? 2 * P : 2 * P - 1;
+      // accumulation: every old value is requested before the first store
+      double old[2 * P + 1];
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) old[r] = (A.accumulate && r <= rmax) ? dst[(2 * P * c + r) * ox + gx] : 0.0;
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) {
+        if (r > rmax) break;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) s = fma(Ty.hw[r][j], cv[j], s);
+        const long long gy = 2 * P * c + r;
+        if (col0 || (A.mask_out && on_bdry(gy, oy))) s = 0.0;
+        dst[gy * ox + gx] = old[r] + s;
+      }
+    }
+  }
+}
+
+template <int P, bool PROLONG>
+void launch_xy(int F, const PassArgs& A, const DevAxisTransfer& Tx, const DevAxisTransfer& Ty, const double* in,
+               double* out, cudaStream_t s) {
+  using C = XyCfg<P, PROLONG>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(xy_cell_kernel<P, PROLONG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::smem_bytes()));
+    configured = true;
+  }
+  const long long ncx = PROLONG ? (A.i[0] - 1) / P : (A.o[0] - 1) / P;
+  const long long ncy = PROLONG ? (A.i[1] - 1) / P : (A.o[1] - 1) / P;
+  const dim3 grid(static_cast<unsigned>((ncx + kXyTCX - 1) / kXyTCX), static_cast<unsigned>((ncy + kXyTCY - 1) / kXyTCY),
+                  static_cast<unsigned>(A.o[2] * F));
+  count_launch();
+  xy_cell_kernel<P, PROLONG><<<grid, kXyThreads, C::smem_bytes(), s>>>(A, Tx, Ty, in, out);
+}
+
+void xy_pass(int F, const PassArgs& A, const DevAxisTransfer& Tx, const DevAxisTransfer& Ty, bool prolong,
+             const double* in, double* out, cudaStream_t s) {
+  switch (Tx.hp) {
+#define STMG_XY(PP)                                     \
+  case PP:                                              \
+    if (prolong)                                        \
+      launch_xy<PP, true>(F, A, Tx, Ty, in, out, s);    \
+    else                                                \
+      launch_xy<PP, false>(F, A, Tx, Ty, in, out, s);   \
+    return;
+    STMG_XY(1)
+    STMG_XY(2)
+    STMG_XY(3)
+    STMG_XY(4)
+#undef STMG_XY
+    default: break;
+  }
+}
+
 // apply the per-axis maps x, then y, then z (2D: x, y); the intermediates are
 // compact, the source / destination use the given field strides
 void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const long long* src_d, const long long* dst_d,
@@ -320,6 +537,21 @@ void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const lo
     return;
   }
   long long d2[3] = {dst_d[0], dst_d[1], src_d[2]};
+  static const bool no_fused = std::getenv("STMG_XFER_SEPARABLE") != nullptr;
+  if (!no_fused && ax[0].hp > 0 && ax[0].hp == ax[1].hp && ax[0].hp <= 4) {
+    // equal-p h-coarsening in x and y: one fused x-y pass plus the z pass --
+    // restriction x-y first, prolongation z first (the passes commute), so
+    // the single HBM intermediate is the (coarse x, coarse y, fine z) lattice
+    if (prolong) {
+      long long dz[3] = {src_d[0], src_d[1], dst_d[2]};
+      pass<2>(F, args(src_d, dz, fs_src, 0, true, false), ax[2], true, in, t2, s);
+      xy_pass(F, args(dz, dst_d, 0, fs_dst, false, true), ax[0], ax[1], true, t2, out, s);
+    } else {
+      xy_pass(F, args(src_d, d2, fs_src, 0, true, false), ax[0], ax[1], false, in, t2, s);
+      pass<2>(F, args(d2, dst_d, 0, fs_dst, false, true), ax[2], false, t2, out, s);
+    }
+    return;
+  }
   pass<0>(F, args(src_d, d1, fs_src, 0, true, false), ax[0], prolong, in, t1, s);
   pass<1>(F, args(d1, d2, 0, 0, false, false), ax[1], prolong, t1, t2, s);
   pass<2>(F, args(d2, dst_d, 0, fs_dst, false, true), ax[2], prolong, t2, out, s);

@@ -253,3 +253,38 @@ def test_asm_cartesian_fdm_pivoted_fallback(cuda, ref):
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "ok" in out.stdout
+
+
+def test_transfers_separable_fallback(cuda, ref):
+    """The per-axis separable passes (STMG_XFER_SEPARABLE; the path for
+    unequal p, CSR transfers and 2D) match the reference on a 3D equal-p
+    hierarchy where the fused x-y kernel is the default; subprocess because
+    the choice is read once per process."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import refbind as ref\n"
+        "from paper_2408_04372_b200 import api, problems\n"
+        "cfg = problems.config('C3', 0)\n"
+        "mesh = api.Mesh(cfg.dim, (0,0,0), (1,1,1), cfg.base_cells, cfg.refinements, cfg.vertices())\n"
+        "M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps, cfg.tau)\n"
+        "R = ref.Reference(cfg, with_mg=True)\n"
+        "info = R.level_info()\n"
+        "worst = 0.0\n"
+        "for l in range(M.n_levels - 1):\n"
+        "    nf, nc = info[l]['n_dofs'], info[l + 1]['n_dofs']\n"
+        "    c = problems.uniform_vector(nc, seed=100 + l); f = problems.uniform_vector(nf, seed=200 + l)\n"
+        "    pf = M.prolong(l, torch.from_numpy(c).cuda()).cpu().numpy()\n"
+        "    rc = M.restrict_(l, torch.from_numpy(f).cuda()).cpu().numpy()\n"
+        "    a = R.prolong(l, c, nf); b = R.restrict_(l, f, nc)\n"
+        "    worst = max(worst, np.linalg.norm(pf - a) / np.linalg.norm(a), np.linalg.norm(rc - b) / np.linalg.norm(b))\n"
+        "assert worst <= 1e-13, worst\n"
+        "print('ok', worst)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env_vars = dict(os.environ, STMG_XFER_SEPARABLE="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env_vars, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok" in out.stdout

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -455,7 +456,11 @@ __device__ __forceinline__ void fdm_stages(const DevFDM& P, const double* __rest
 // registers. y-owner gathers r and applies S_y^T, x-owner S_x^T,
 // z-owner S_z^T + the n_t x n_t solves at its N eigen-points + S_z, x-owner
 // S_x, y-owner S_y and the weighted scatter (Dirichlet rows: w r, re-read).
-template <int N, int NT, bool TD>
+// MODE 0: every CTA, generic transforms; 1: only CTAs whose cells are all
+// interior, even-odd transforms; 2: only the other CTAs, generic. Modes 1 and
+// 2 are two launches over the same grid (CTAs of the other kind return at
+// once), so each kernel's code stays small enough for the instruction cache.
+template <int N, int NT, bool TD, int MODE>
 __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant__ DevFDM P,
                                                         const double* __restrict__ r, double* __restrict__ z,
                                                         double scale) {
@@ -491,14 +496,14 @@ __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant
   const int cb = c * Y::CS;
   const int oy = cb + a + PZ * b, oz = cb + a + RY * b;
   const int ox = cb + RY * (Y::SWAP ? b : a) + PZ * (Y::SWAP ? a : b);
-  // CTAs whose cells are all interior take the even-odd transforms
-  // (uniform branch; P.eo = 0 when the host could not order the interior
-  // eigenvectors by parity)
-  const bool all_interior = __syncthreads_and(!valid || mask == 0) && P.eo;
-  if (all_interior)
-    fdm_stages<N, NT, TD, true>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
-  else
-    fdm_stages<N, NT, TD, false>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
+  // CTAs whose cells are all interior take the even-odd transforms (P.eo = 0
+  // when the host could not order the interior eigenvectors by parity: one
+  // MODE 0 launch)
+  if constexpr (MODE != 0) {
+    const bool all_interior = __syncthreads_and(!valid || mask == 0);
+    if (all_interior != (MODE == 1)) return;
+  }
+  fdm_stages<N, NT, TD, MODE == 1>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
 }
 
 template <int N, int NT>
@@ -507,10 +512,20 @@ void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cud
   const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
   count_launch();
   const dim3 grid(static_cast<unsigned>((n_cells + NC - 1) / NC), static_cast<unsigned>(P.S));
+  auto go = [&](auto td) {
+    constexpr bool TD = decltype(td)::value;
+    if (P.eo) {
+      count_launch();  // the second launch of the pair
+      fdm_lines_kernel<N, NT, TD, 1><<<grid, 128, 0, s>>>(P, r, z, scale);
+      fdm_lines_kernel<N, NT, TD, 2><<<grid, 128, 0, s>>>(P, r, z, scale);
+    } else {
+      fdm_lines_kernel<N, NT, TD, 0><<<grid, 128, 0, s>>>(P, r, z, scale);
+    }
+  };
   if (P.tdiag)
-    fdm_lines_kernel<N, NT, true><<<grid, 128, 0, s>>>(P, r, z, scale);
+    go(std::true_type{});
   else
-    fdm_lines_kernel<N, NT, false><<<grid, 128, 0, s>>>(P, r, z, scale);
+    go(std::false_type{});
 }
 
 template <int DIM, int N, int NT>

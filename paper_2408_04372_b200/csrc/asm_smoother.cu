@@ -183,7 +183,21 @@ __global__ void __launch_bounds__(256, 3) asm_apply_warp_kernel(const __grid_con
 #pragma unroll
     for (int c = 0; c < 8; ++c) rr[c] = 0.0;
     const double* Xg = A.X + pos * A.xs;
-    for (int i = lane; i < M * M; i += 32) X[(i / M) * LD + (i % M)] = __ldg(Xg + i);
+    {
+      // all of the lane's record loads in flight before any shared store
+      constexpr int NX = (M * M + 31) / 32;
+      double xv[NX];
+#pragma unroll
+      for (int k = 0; k < NX; ++k) {
+        const int i = lane + 32 * k;
+        xv[k] = i < M * M ? __ldg(Xg + i) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < NX; ++k) {
+        const int i = lane + 32 * k;
+        if (i < M * M) X[(i / M) * LD + (i % M)] = xv[k];
+      }
+    }
     if (lane < M) {
       d = local_dof(A, ci % cxn, (ci / cxn) % cyn, ci / (cxn * cyn), lane);
 #pragma unroll
@@ -820,8 +834,9 @@ __global__ void __launch_bounds__(256, 2) asm_apply_dfma64_kernel(const __grid_c
 //   hat z_e = (T_M + lam_e T_A)^-1 hat r_e per step (pivoted n_t x n_t solve)
 //   z = X hat z    (thread a)
 // then the weighted scatter-add; Dirichlet rows contribute w * r.
+constexpr int kLargeChunk = 32;
 template <int NT>
-__global__ void __launch_bounds__(128) asm_apply_large_kernel(const __grid_constant__ DevASM A,
+__global__ void __launch_bounds__(128, 4) asm_apply_large_kernel(const __grid_constant__ DevASM A,
                                                               const double* __restrict__ r, double* __restrict__ z,
                                                               double scale) {
   const int m = A.m, t = threadIdx.x;
@@ -845,6 +860,8 @@ __global__ void __launch_bounds__(128) asm_apply_large_kernel(const __grid_const
       double acc[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+      // X rows streamed from HBM: 16 loads in flight per thread
+#pragma unroll 16
       for (int a = 0; a < m; ++a) {
         const double x = __ldg(X + static_cast<long long>(a) * m + t);
         const double4 r0 = *reinterpret_cast<const double4*>(rs + a * 8);
@@ -873,28 +890,56 @@ __global__ void __launch_bounds__(128) asm_apply_large_kernel(const __grid_const
       }
     }
     __syncthreads();
-    if (t < m) {
+    {
+      // z = X hat z (thread a). X is staged through shared memory in column
+      // chunks of kLargeChunk: coalesced row-segment loads that hit L2 (the
+      // first product just streamed X), conflict-free row reads (odd pitch);
+      // a thread-per-row global read would touch one sector per lane.
       double acc[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-      const double* xr = X + static_cast<long long>(t) * m;
-      for (int e = 0; e < m; ++e) {
-        const double x = __ldg(xr + e);
-        const double4 h0 = *reinterpret_cast<const double4*>(hs + e * 8);
-        const double4 h1 = *reinterpret_cast<const double4*>(hs + e * 8 + 4);
-        acc[0] = fma(x, h0.x, acc[0]);
-        acc[1] = fma(x, h0.y, acc[1]);
-        acc[2] = fma(x, h0.z, acc[2]);
-        acc[3] = fma(x, h0.w, acc[3]);
-        acc[4] = fma(x, h1.x, acc[4]);
-        acc[5] = fma(x, h1.y, acc[5]);
-        acc[6] = fma(x, h1.z, acc[6]);
-        acc[7] = fma(x, h1.w, acc[7]);
+      double* xc = hs + 8 * 128;  // [128][kLargeChunk + 1]
+      constexpr int LDc = kLargeChunk + 1;
+      for (int e0 = 0; e0 < m; e0 += kLargeChunk) {
+        const int ncols = min(kLargeChunk, m - e0);
+        constexpr int NLD = 128 * kLargeChunk / 128;
+        double xv[NLD];
+#pragma unroll
+        for (int k = 0; k < NLD; ++k) {
+          const int i = t + 128 * k, row = i / kLargeChunk, col = i % kLargeChunk;
+          xv[k] = (row < m && col < ncols) ? __ldg(X + static_cast<long long>(row) * m + e0 + col) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < NLD; ++k) {
+          const int i = t + 128 * k;
+          xc[(i / kLargeChunk) * LDc + i % kLargeChunk] = xv[k];
+        }
+        __syncthreads();
+        if (t < m) {
+          for (int k = 0; k < ncols; ++k) {
+            const double x = xc[t * LDc + k];
+            const double4 h0 = *reinterpret_cast<const double4*>(hs + (e0 + k) * 8);
+            const double4 h1 = *reinterpret_cast<const double4*>(hs + (e0 + k) * 8 + 4);
+            acc[0] = fma(x, h0.x, acc[0]);
+            acc[1] = fma(x, h0.y, acc[1]);
+            acc[2] = fma(x, h0.z, acc[2]);
+            acc[3] = fma(x, h0.w, acc[3]);
+            acc[4] = fma(x, h1.x, acc[4]);
+            acc[5] = fma(x, h1.y, acc[5]);
+            acc[6] = fma(x, h1.z, acc[6]);
+            acc[7] = fma(x, h1.w, acc[7]);
+          }
+        }
+        __syncthreads();
       }
+      if (t < m) {
       const double w = scale / d.mult;
-      for (int c = 0; c < ncol; ++c) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c >= ncol) break;
         const double v = d.bdry ? rs[t * 8 + c] : acc[c];
         atomicAdd(z + static_cast<long long>(c) * A.n_space + d.g, v * w);
+      }
       }
     }
     __syncthreads();
@@ -1223,7 +1268,12 @@ void launch_asm_fd64(const DevASM& A, const double* r, double* z, double scale, 
 template <int NT>
 void launch_large(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if (A.n_list == 0) return;
-  const size_t smem = sizeof(double) * 16 * 128;
+  const size_t smem = sizeof(double) * (16 * 128 + 128 * (kLargeChunk + 1));
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(asm_apply_large_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -213,20 +213,50 @@ __global__ void __launch_bounds__(256, 3) asm_apply_warp_kernel(const __grid_con
       double h[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) h[c] = 0.0;
+      if (hi) {
 #pragma unroll 3
-      for (int a = 0; a < M; ++a) {
-        const double x = X[a * LD + lane];
-        const double4 r0 = *reinterpret_cast<const double4*>(rb + a * 8);
-        h[0] = fma(x, r0.x, h[0]);
-        h[1] = fma(x, r0.y, h[1]);
-        h[2] = fma(x, r0.z, h[2]);
-        h[3] = fma(x, r0.w, h[3]);
-        if (hi) {
+        for (int a = 0; a < M; ++a) {
+          const double x = X[a * LD + lane];
+          const double4 r0 = *reinterpret_cast<const double4*>(rb + a * 8);
           const double4 r1 = *reinterpret_cast<const double4*>(rb + a * 8 + 4);
+          h[0] = fma(x, r0.x, h[0]);
+          h[1] = fma(x, r0.y, h[1]);
+          h[2] = fma(x, r0.z, h[2]);
+          h[3] = fma(x, r0.w, h[3]);
           h[4] = fma(x, r1.x, h[4]);
           h[5] = fma(x, r1.y, h[5]);
           h[6] = fma(x, r1.z, h[6]);
           h[7] = fma(x, r1.w, h[7]);
+        }
+      } else {
+        // <= 4 columns: even / odd rows into separate accumulators (two
+        // independent FMA chains per column), folded after the loop
+#pragma unroll 3
+        for (int a = 0; a < M - 1; a += 2) {
+          const double x0 = X[a * LD + lane], x1 = X[(a + 1) * LD + lane];
+          const double4 r0 = *reinterpret_cast<const double4*>(rb + a * 8);
+          const double4 r1 = *reinterpret_cast<const double4*>(rb + (a + 1) * 8);
+          h[0] = fma(x0, r0.x, h[0]);
+          h[1] = fma(x0, r0.y, h[1]);
+          h[2] = fma(x0, r0.z, h[2]);
+          h[3] = fma(x0, r0.w, h[3]);
+          h[4] = fma(x1, r1.x, h[4]);
+          h[5] = fma(x1, r1.y, h[5]);
+          h[6] = fma(x1, r1.z, h[6]);
+          h[7] = fma(x1, r1.w, h[7]);
+        }
+        if (M % 2 == 1) {
+          const double x = X[(M - 1) * LD + lane];
+          const double4 r0 = *reinterpret_cast<const double4*>(rb + (M - 1) * 8);
+          h[0] = fma(x, r0.x, h[0]);
+          h[1] = fma(x, r0.y, h[1]);
+          h[2] = fma(x, r0.z, h[2]);
+          h[3] = fma(x, r0.w, h[3]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          h[c] += h[c + 4];
+          h[c + 4] = 0.0;
         }
       }
 #pragma unroll
@@ -248,20 +278,48 @@ __global__ void __launch_bounds__(256, 3) asm_apply_warp_kernel(const __grid_con
       double o[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) o[c] = 0.0;
+      if (hi) {
 #pragma unroll 3
-      for (int e = 0; e < M; ++e) {
-        const double x = X[lane * LD + e];
-        const double4 h0 = *reinterpret_cast<const double4*>(hb + e * 8);
-        o[0] = fma(x, h0.x, o[0]);
-        o[1] = fma(x, h0.y, o[1]);
-        o[2] = fma(x, h0.z, o[2]);
-        o[3] = fma(x, h0.w, o[3]);
-        if (hi) {
+        for (int e = 0; e < M; ++e) {
+          const double x = X[lane * LD + e];
+          const double4 h0 = *reinterpret_cast<const double4*>(hb + e * 8);
           const double4 h1 = *reinterpret_cast<const double4*>(hb + e * 8 + 4);
+          o[0] = fma(x, h0.x, o[0]);
+          o[1] = fma(x, h0.y, o[1]);
+          o[2] = fma(x, h0.z, o[2]);
+          o[3] = fma(x, h0.w, o[3]);
           o[4] = fma(x, h1.x, o[4]);
           o[5] = fma(x, h1.y, o[5]);
           o[6] = fma(x, h1.z, o[6]);
           o[7] = fma(x, h1.w, o[7]);
+        }
+      } else {
+#pragma unroll 3
+        for (int e = 0; e < M - 1; e += 2) {
+          const double x0 = X[lane * LD + e], x1 = X[lane * LD + e + 1];
+          const double4 h0 = *reinterpret_cast<const double4*>(hb + e * 8);
+          const double4 h1 = *reinterpret_cast<const double4*>(hb + (e + 1) * 8);
+          o[0] = fma(x0, h0.x, o[0]);
+          o[1] = fma(x0, h0.y, o[1]);
+          o[2] = fma(x0, h0.z, o[2]);
+          o[3] = fma(x0, h0.w, o[3]);
+          o[4] = fma(x1, h1.x, o[4]);
+          o[5] = fma(x1, h1.y, o[5]);
+          o[6] = fma(x1, h1.z, o[6]);
+          o[7] = fma(x1, h1.w, o[7]);
+        }
+        if (M % 2 == 1) {
+          const double x = X[lane * LD + M - 1];
+          const double4 h0 = *reinterpret_cast<const double4*>(hb + (M - 1) * 8);
+          o[0] = fma(x, h0.x, o[0]);
+          o[1] = fma(x, h0.y, o[1]);
+          o[2] = fma(x, h0.z, o[2]);
+          o[3] = fma(x, h0.w, o[3]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          o[c] += o[c + 4];
+          o[c + 4] = 0.0;
         }
       }
       const double w = scale / d.mult;

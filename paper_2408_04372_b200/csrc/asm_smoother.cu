@@ -55,10 +55,12 @@ __device__ __forceinline__ LocalDof local_dof(const DevASM& A, long long cx, lon
   d.bdry = gx == 0 || gx == A.dofs[0] - 1 || (A.dim > 1 && (gy == 0 || gy == A.dofs[1] - 1)) ||
            (A.dim > 2 && (zlo || zhi));
   // number of cells containing the dof (asm_smoother.cpp:45-49)
+  // (gx % p == 0 exactly when the local index is a cell vertex: no 64-bit
+  // modulo on the hot path)
   double m = 1.0;
-  if (gx % A.p == 0 && gx > 0 && gx < A.dofs[0] - 1) m *= 2.0;
-  if (A.dim > 1 && gy % A.p == 0 && gy > 0 && gy < A.dofs[1] - 1) m *= 2.0;
-  if (A.dim > 2 && gz % A.p == 0 && !zlo && !zhi) m *= 2.0;
+  if ((lx == 0 || lx == A.p) && gx > 0 && gx < A.dofs[0] - 1) m *= 2.0;
+  if (A.dim > 1 && (ly == 0 || ly == A.p) && gy > 0 && gy < A.dofs[1] - 1) m *= 2.0;
+  if (A.dim > 2 && (lz == 0 || lz == A.p) && !zlo && !zhi) m *= 2.0;
   d.mult = m;
   return d;
 }

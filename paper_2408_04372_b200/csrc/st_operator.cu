@@ -27,19 +27,24 @@ __global__ void boundary_identity_kernel(int dim, int zbc, long long dx, long lo
        t += static_cast<long long>(gridDim.x) * blockDim.x) {
     long long g;
     long long r = t;
+    // face-local indices fit 32 bits (a face has < 2^32 entries): 32-bit
+    // division instead of the 64-bit software sequence
+    const unsigned udx = static_cast<unsigned>(dx), udy = static_cast<unsigned>(dy);
     // the low plane of a slab whose low face is an interface is owned by the
     // slab below: its Dirichlet rows are written there only
     if (r < 2 * fx) {
-      const long long side = r / fx, k = r % fx;
-      if (dim == 3 && !(zbc & 1) && k / dy == 0) continue;
-      g = (k / dy) * dx * dy + (k % dy) * dx + (side ? dx - 1 : 0);
+      const long long side = r >= fx;
+      const unsigned k = static_cast<unsigned>(r - side * fx), kz = k / udy, ky = k - kz * udy;
+      if (dim == 3 && !(zbc & 1) && kz == 0) continue;
+      g = static_cast<long long>(kz) * dx * dy + static_cast<long long>(ky) * dx + (side ? dx - 1 : 0);
     } else if ((r -= 2 * fx) < 2 * fy) {
-      const long long side = r / fy, k = r % fy;
-      if (dim == 3 && !(zbc & 1) && k / dx == 0) continue;
-      g = (k / dx) * dx * dy + (side ? dy - 1 : 0) * dx + (k % dx);
+      const long long side = r >= fy;
+      const unsigned k = static_cast<unsigned>(r - side * fy), kz = k / udx, kx = k - kz * udx;
+      if (dim == 3 && !(zbc & 1) && kz == 0) continue;
+      g = static_cast<long long>(kz) * dx * dy + (side ? dy - 1 : 0) * dx + kx;
     } else {
       r -= 2 * fy;
-      const long long side = r / fz, k = r % fz;
+      const long long side = r >= fz, k = r - side * fz;
       if (!(zbc & (side ? 2 : 1))) continue;
       g = (side ? dz - 1 : 0) * dx * dy + k;
     }

@@ -16,8 +16,8 @@
 //               b = Kr_y u
 //   B  x-owner: c = Mr_x a, pre = Kr_x a / hx^2 + Mr_x b / hy^2
 //   C  z-owner: temporal block coupling of the z-lines of every field,
-//               Zm_i = sum_j V CM_ij c_j + rho V CA_ij pre_j,
-//               Zk_i = sum_j rho V / hz^2 CA_ij c_j,
+//               Zm_i = V sum_j (CM_ij c_j + CA_ij rho pre_j),
+//               Zk_i = rho V / hz^2 sum_j CA_ij c_j,
 //               y_i = Mr_z Zm_i + Kr_z Zk_i, scatter-add (Dirichlet rows
 //               skipped; the boundary pass writes them,
 //               space_time_operator.cpp:125-129)
@@ -243,31 +243,67 @@ __global__ void __launch_bounds__(Cfg<N, F>::T, Cfg<N, F>::MINB)
       const long long ax = cx >> L.rho_shift, ay = cy >> L.rho_shift, az = (cz + L.cz0) >> L.rho_shift;
       rho = __ldg(L.rho0 + (az * L.cells0[1] + ay) * L.cells0[0] + ax);
     }
-    const double rv = rho * V, rvz = rv * L.hinv2[2];
+    const double rvz = rho * V * L.hinv2[2];
     double Zm[FPG][N], Zk[FPG][N];
 #pragma unroll
     for (int ii = 0; ii < FPG; ++ii)
 #pragma unroll
       for (int k = 0; k < N; ++k) Zm[ii][k] = Zk[ii][k] = 0.0;
+    if constexpr (F >= 6) {
+      // wide slabs: raw table coefficients in the j loop (rho folded into
+      // pre once per value, V and rho V / hz^2 applied after the sums), so
+      // no per-cell coefficient products stay live in registers (F = 8
+      // spilled otherwise)
 #pragma unroll
-    for (int j = 0; j < F; ++j) {
-      double vc[N], vp[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        vc[k] = A0[oz + j * Y::SD2 + k * Y::PZ2];
-        vp[k] = A1[oz + j * Y::SD2 + k * Y::PZ2];
-      }
-#pragma unroll
-      for (int ii = 0; ii < FPG; ++ii) {
-        const int i = j0 + ii;
-        if (i >= F) break;
-        const double cmv = L.CM[i * F + j], cav = L.CA[i * F + j];
-        if (cmv == 0.0 && cav == 0.0) continue;
-        const double cm = V * cmv, ca = rv * cav, ck = rvz * cav;
+      for (int j = 0; j < F; ++j) {
+        double vc[N], vp[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          Zm[ii][k] = fma(cm, vc[k], fma(ca, vp[k], Zm[ii][k]));
-          Zk[ii][k] = fma(ck, vc[k], Zk[ii][k]);
+          vc[k] = A0[oz + j * Y::SD2 + k * Y::PZ2];
+          vp[k] = rho * A1[oz + j * Y::SD2 + k * Y::PZ2];
+        }
+#pragma unroll
+        for (int ii = 0; ii < FPG; ++ii) {
+          const int i = j0 + ii;
+          if (i >= F) break;
+          const double cm = L.CM[i * F + j], ca = L.CA[i * F + j];
+          if (cm == 0.0 && ca == 0.0) continue;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            Zm[ii][k] = fma(cm, vc[k], fma(ca, vp[k], Zm[ii][k]));
+            Zk[ii][k] = fma(ca, vc[k], Zk[ii][k]);
+          }
+        }
+      }
+#pragma unroll
+      for (int ii = 0; ii < FPG; ++ii)
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          Zm[ii][k] *= V;
+          Zk[ii][k] *= rvz;
+        }
+    } else {
+      const double rv = rho * V;
+#pragma unroll
+      for (int j = 0; j < F; ++j) {
+        double vc[N], vp[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          vc[k] = A0[oz + j * Y::SD2 + k * Y::PZ2];
+          vp[k] = A1[oz + j * Y::SD2 + k * Y::PZ2];
+        }
+#pragma unroll
+        for (int ii = 0; ii < FPG; ++ii) {
+          const int i = j0 + ii;
+          if (i >= F) break;
+          const double cmv = L.CM[i * F + j], cav = L.CA[i * F + j];
+          if (cmv == 0.0 && cav == 0.0) continue;
+          const double cm = V * cmv, ca = rv * cav, ck = rvz * cav;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            Zm[ii][k] = fma(cm, vc[k], fma(ca, vp[k], Zm[ii][k]));
+            Zk[ii][k] = fma(ck, vc[k], Zk[ii][k]);
+          }
         }
       }
     }

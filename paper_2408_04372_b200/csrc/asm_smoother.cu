@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 #include "kernels.hpp"
 
@@ -484,6 +485,272 @@ __global__ void __launch_bounds__(256) asm_apply_mma_kernel(const __grid_constan
   }
 }
 
+// Tensor-core variant for 24 < m <= 32 (3D Q2 cells, m = 27: the exact cells
+// of a Cartesian level, e.g. coefficient-jump neighbourhoods; 2D Q4, m = 25).
+// One WARP per cell, as in the DFMA warp kernel above, but both block
+// products run as mma.sync.m8n8k4.f64 over the block padded to 32 rows (four
+// 8-row tiles, k in steps of 4 up to 28; entries past m predicated to zero),
+// and the per-row work happens in the lane-per-dof layout between them:
+//   stage   lane a: gather r_a (local dof a), P-mix into slots (A.tdiag)
+//   MMA 1   hat r = X^T r            (D fragments -> shared, transposed)
+//   row     lane e: (B + lam_e)^-1 on the slot pairs, then Q back to the
+//           time columns (Q commutes with X); pivoted solves without tdiag
+//   MMA 2   z_T = X hat z            (D fragments -> shared, transposed)
+//   scatter lane a: weighted atomics with its own local dof
+// X arrives by one TMA bulk copy per cell into the warp's double buffer; 4
+// independent warps per CTA, no CTA barriers in the loop.
+// With A.tdiag (the temporal blocks are real-block-diagonalisable, see
+// temporal_block_diagonalise) the padded kernels replace the per-lane pivoted
+// solves by the m = 64 kernel's scheme: P mixes the residual columns at the
+// staging, the lane holding slot pair (2j, 2j+1) of eigen-row e applies the
+// 1x1 / 2x2 (B + lam_e)^-1, and Q mixes the slots of each output row after a
+// 4-lane shuffle; Dirichlet rows add w r straight from the staging threads.
+__device__ __forceinline__ void tdiag_scale(const DevASM& A, int j, double lam, double v0, double v1, double& o0,
+                                            double& o1) {
+  const int kd = A.kind[j];
+  const double a0 = A.s0[j], a1 = A.s1[j];
+  const double p0 = a0 + lam, p1 = a1 + lam;
+  const double m00 = kd ? p0 : p1, m11 = p0, m01 = kd ? -a1 : 0.0, m10 = kd ? a1 : 0.0;
+  const double inv = 1.0 / (kd ? fma(p0, p0, a1 * a1) : p0 * p1);
+  o0 = fma(m00, v0, m01 * v1) * inv;
+  o1 = fma(m10, v0, m11 * v1) * inv;
+}
+// Ps / Qs: A.P / A.Q copied to shared memory (param-space tables read inside a
+// persistent loop get hoisted into registers and spill)
+__device__ __forceinline__ void tdiag_qmix(const double* Qs, int lane, double v0, double v1, double& o0, double& o1) {
+  double v[8];
+  const int grp = lane & ~3, c0 = 2 * (lane & 3);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __shfl_sync(0xffffffffu, v0, grp | i);
+    v[2 * i + 1] = __shfl_sync(0xffffffffu, v1, grp | i);
+  }
+  o0 = 0.0;
+  o1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    o0 = fma(Qs[c0 * 8 + k], v[k], o0);
+    o1 = fma(Qs[(c0 + 1) * 8 + k], v[k], o1);
+  }
+}
+// residual row of one local dof, P-transformed when A.tdiag (slots), raw
+// otherwise; a Dirichlet row under tdiag adds w r to z here
+__device__ __forceinline__ void stage_row(const DevASM& A, const double* Ps, const double* rn, long long g, bool bdry,
+                                          double mult, double scale, int ncol, double* z, double* dst) {
+  double tr[8];
+  if (A.tdiag) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) s = fma(Ps[k * 8 + c], rn[c], s);
+      tr[k] = s;
+    }
+    if (bdry) {
+      const double w = scale / mult;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < ncol) atomicAdd(z + static_cast<long long>(c) * A.n_space + g, rn[c] * w);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tr[k] = rn[k];
+  }
+#pragma unroll
+  for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(dst + c) = make_double2(tr[c], tr[c + 1]);
+}
+
+template <int M>
+constexpr int mma32_xbuf() {
+  return (M * M + 1) & ~1;  // = DevASM::xs for m != 64 (16-byte bulk copies)
+}
+constexpr int kWmmaWarps = 4, kWmmaPitch = 12;  // pitch 12: conflict-free B-fragment rows
+template <int M>
+constexpr int wmma_warp_doubles() {
+  return 2 * mma32_xbuf<M>() + 2 * 32 * kWmmaPitch;
+}
+template <int M>
+constexpr size_t mma32_smem() {
+  return sizeof(double) * (128 + static_cast<size_t>(kWmmaWarps) * wmma_warp_doubles<M>()) +
+         2 * kWmmaWarps * sizeof(unsigned long long);
+}
+
+template <int M, int NT>
+__global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(const __grid_constant__ DevASM A,
+                                                                             const double* __restrict__ r,
+                                                                             double* __restrict__ z, double scale) {
+  static_assert(M > 24 && M <= 32, "four 8-row MMA tiles");
+  constexpr int XB = mma32_xbuf<M>(), KT = (M + 3) / 4, RS = kWmmaPitch, W = kWmmaWarps;
+  constexpr unsigned XBYTES = static_cast<unsigned>(XB * sizeof(double));
+  static_assert(XBYTES % 16 == 0, "bulk copy size");
+  extern __shared__ __align__(128) double sm[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  double* PQ = sm;  // A.P, A.Q
+  double* X0 = sm + 128 + warp * wmma_warp_doubles<M>();
+  double* X1 = X0 + XB;
+  double* rs = X1 + XB;       // [32][RS] staged residual (slots)
+  double* hs = rs + 32 * RS;  // [32][RS] product outputs, transposed
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + 128 + W * wmma_warp_doubles<M>()) + 2 * warp;
+  PQ[t] = t < 64 ? A.P[t >> 3][t & 7] : A.Q[(t - 64) >> 3][t & 7];
+  for (int i = lane; i < 2 * 32 * RS; i += 32) rs[i] = 0.0;
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long n_pos = A.n_list, nsp = A.n_space;
+  const long long stride = static_cast<long long>(gridDim.x) * W;
+  const int ncol = A.S * NT;
+  const int kl = lane & 3, n8 = lane >> 2;
+  const bool own = lane < M;
+  const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
+  long long pos = static_cast<long long>(blockIdx.x) * W + warp;
+  if (lane == 0 && pos < n_pos) {
+    mbar_expect_tx(&bar[0], XBYTES);
+    bulk_g2s(X0, A.X + pos * A.xs, XBYTES, &bar[0]);
+  }
+  unsigned ph0 = 0, ph1 = 0;
+  int buf = 0;
+  // lane a's local dof, residual row and eigenvalue of list position q, loaded
+  // one cell ahead so the gather latency hides behind the current cell
+  LocalDof dn{0, false, 1.0};
+  double rnn[8], lamn = 0.0;
+  auto gather = [&](long long q) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) rnn[c] = 0.0;
+    if (own) {
+      const unsigned ci = static_cast<unsigned>(A.list ? A.list[q] : q);
+      dn = local_dof(A, ci % cxn, (ci / cxn) % cyn, ci / (cxn * cyn), lane);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < ncol) rnn[c] = __ldg(r + static_cast<long long>(c) * nsp + dn.g);
+      lamn = __ldg(A.lam + q * M + lane);
+    }
+  };
+  if (pos < n_pos) gather(pos);
+  for (; pos < n_pos; pos += stride) {
+    const long long next = pos + stride;
+    if (lane == 0 && next < n_pos) {
+      fence_proxy_async();
+      unsigned long long* b = &bar[buf ^ 1];
+      mbar_expect_tx(b, XBYTES);
+      bulk_g2s(buf ? X0 : X1, A.X + next * A.xs, XBYTES, b);
+    }
+    // ---- stage: lane a's residual row (gathered during the previous cell)
+    const LocalDof d = dn;
+    const double lam = lamn;
+    double rn[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) rn[c] = rnn[c];
+    if (own) stage_row(A, PQ, rn, d.g, d.bdry, d.mult, scale, ncol, z, rs + lane * RS);
+    if (next < n_pos) gather(next);
+    if (buf == 0) {
+      mbar_wait(&bar[0], ph0);
+      ph0 ^= 1;
+    } else {
+      mbar_wait(&bar[1], ph1);
+      ph1 ^= 1;
+    }
+    __syncwarp();
+    const double* Xs = buf ? X1 : X0;
+    double acc[4][2];
+    // ---- MMA 1: hat r (e x 8) = X^T r, A[row=e][k=a] = X[a][e]
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const int a = kt * 4 + kl;
+      const double b = rs[a * RS + n8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = i * 8 + n8;
+        const double xa = (a < M && e < M) ? Xs[a * M + e] : 0.0;
+        dmma(acc[i][0], acc[i][1], xa, b);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<double2*>(hs + (i * 8 + n8) * RS + 2 * kl) = make_double2(acc[i][0], acc[i][1]);
+    __syncwarp();
+    // ---- row work: lane e solves its eigen-row (slots -> time columns)
+    if (own) {
+      double v[8];
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) {
+        const double2 q = *reinterpret_cast<const double2*>(hs + lane * RS + c);
+        v[c] = q.x;
+        v[c + 1] = q.y;
+      }
+      double o[8];
+      if (A.tdiag) {
+        double sl[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tdiag_scale(A, j, lam, v[2 * j], v[2 * j + 1], sl[2 * j], sl[2 * j + 1]);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double s = 0.0;
+          if (c < ncol) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s = fma(PQ[64 + c * 8 + k], sl[k], s);
+          }
+          o[c] = s;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) o[c] = v[c];
+#pragma unroll
+        for (int st = 0; st < 8 / NT; ++st) {
+          if (st >= A.S) break;
+          double b4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < NT; ++i) b4[i] = o[st * NT + i];
+          small_solve(A.TM, A.TA, lam, NT, b4);
+#pragma unroll
+          for (int i = 0; i < NT; ++i) o[st * NT + i] = b4[i];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(hs + lane * RS + c) = make_double2(o[c], o[c + 1]);
+    }
+    __syncwarp();
+    // ---- MMA 2: z_T (a x 8) = X hat z, A[row=a][k=e] = X[a][e]
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const int e = kt * 4 + kl;
+      const double b = hs[e * RS + n8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int a = i * 8 + n8;
+        const double xa = (a < M && e < M) ? Xs[a * M + e] : 0.0;
+        dmma(acc[i][0], acc[i][1], xa, b);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<double2*>(hs + (i * 8 + n8) * RS + 2 * kl) = make_double2(acc[i][0], acc[i][1]);
+    __syncwarp();
+    // ---- scatter: lane a, weighted (Dirichlet rows: w r; under tdiag added at the staging)
+    if (own) {
+      const double w = scale / d.mult;
+      if (!d.bdry) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < ncol) atomicAdd(z + static_cast<long long>(c) * nsp + d.g, hs[lane * RS + c] * w);
+      } else if (!A.tdiag) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (c < ncol) atomicAdd(z + static_cast<long long>(c) * nsp + d.g, rn[c] * w);
+      }
+    }
+    __syncwarp();
+    buf ^= 1;
+  }
+}
+
 // m = 64 smoother with the temporal solves fast-diagonalised as well
 // (A.tdiag): per cell and eigen-index e the n_t x n_t solve
 // (T_M + lam_e T_A)^-1 = Q (B + lam_e)^-1 P, B block-diagonal. P mixes the
@@ -887,6 +1154,168 @@ __global__ void __launch_bounds__(256, 2) asm_apply_dfma64_kernel(const __grid_c
   }
 }
 
+// Tensor-core variant for 3D Q4 exact cells (m = 125, padded to 128 rows):
+// one CTA of 16 warps per cell (persistent), warp w owns rows [8w, 8w+8) of
+// both products, mma.sync.m8n8k4.f64 over k in 32 steps of 4 (entries past m
+// predicated to zero). The A fragments come straight from global memory --
+// product 1 reads X[a][e] as 4 row segments of 64 bytes per warp and k step
+// (HBM stream, all 32 loads of a warp in flight before the first MMA),
+// product 2 reads X[a][e] along rows, 32-byte sectors, from L2 where the first
+// product just left the record. r / hat z are shared-memory B fragments; the
+// n_t x n_t solves are the pivoted small_solve, the next cell's residual is
+// gathered into registers while this cell is solved.
+constexpr int kLargeMmaPitch = 12;
+template <int M, int NT>
+__global__ void __launch_bounds__(((M + 7) / 8) * 32, 1) asm_apply_large_mma_kernel(const __grid_constant__ DevASM A,
+                                                                                   const double* __restrict__ r,
+                                                                                   double* __restrict__ z,
+                                                                                   double scale) {
+  constexpr int NW = (M + 7) / 8, MP = NW * 8, KT = (M + 3) / 4, KH = (KT + 1) / 2;
+  // row pitch 12: the B-fragment rows 4kt + kl of a half-warp fall in distinct banks
+  constexpr int RS = kLargeMmaPitch;
+  static_assert(KT * 4 <= MP, "k rows inside the padded block");
+  extern __shared__ __align__(16) double lsm[];
+  double* rs = lsm;            // [MP][RS] block residual (rows >= M stay zero)
+  double* hs = rs + RS * MP;  // [MP][RS] hat z
+  double* PQ = hs + RS * MP;  // A.P, A.Q
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ncol = A.S * NT;
+  for (int i = t; i < 2 * RS * MP; i += NW * 32) lsm[i] = 0.0;
+  if (t < 128) PQ[t] = t < 64 ? A.P[t >> 3][t & 7] : A.Q[(t - 64) >> 3][t & 7];
+  const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
+  const int row = warp * 8 + (lane >> 2), col = (lane & 3) * 2, kl = lane & 3, n8 = lane >> 2;
+  const bool row_ok = row < M;
+  double rn[8];
+  LocalDof dn{0, false, 1.0};
+  auto gather = [&](long long q) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) rn[c] = 0.0;
+    if (t < M) {
+      const unsigned ci = static_cast<unsigned>(A.list ? A.list[q] : q);
+      dn = local_dof(A, ci % cxn, (ci / cxn) % cyn, ci / (cxn * cyn), t);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < ncol) rn[c] = __ldg(r + static_cast<long long>(c) * A.n_space + dn.g);
+    }
+  };
+  if (blockIdx.x < A.n_list) gather(blockIdx.x);
+  __syncthreads();
+  for (long long pos = blockIdx.x; pos < A.n_list; pos += gridDim.x) {
+    const unsigned ci = static_cast<unsigned>(A.list ? A.list[pos] : pos);
+    const long long cx = ci % cxn, cy = (ci / cxn) % cyn, cz = ci / (cxn * cyn);
+    const double* X = A.X + pos * A.xs;
+    // stage this cell's residual, put the next cell's gather in flight, then
+    // the 32 A-fragment loads of product 1
+    if (t < M) stage_row(A, PQ, rn, dn.g, dn.bdry, dn.mult, scale, ncol, z, rs + t * RS);
+    if (pos + gridDim.x < A.n_list) gather(pos + gridDim.x);
+    // (two halves of KH loads each: all 32 in flight spill at 128 registers)
+    double xa[KH];
+#pragma unroll
+    for (int kt = 0; kt < KH; ++kt) {
+      const int a = kt * 4 + kl;
+      xa[kt] = (row_ok && a < M) ? __ldg(X + a * M + row) : 0.0;
+    }
+    const double lam = row_ok ? __ldg(A.lam + pos * M + row) : 0.0;
+    __syncthreads();
+    {
+      // hat r (e x 8) = X^T r: A[row=e][k=a] = X[a][e]
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KH; ++kt) {
+        const double rb = rs[(kt * 4 + kl) * RS + n8];
+        const int a = (kt + KH) * 4 + kl;
+        const double xn = (kt + KH < KT && row_ok && a < M) ? __ldg(X + a * M + row) : 0.0;
+        if (kt & 1)
+          dmma(d10, d11, xa[kt], rb);
+        else
+          dmma(d00, d01, xa[kt], rb);
+        xa[kt] = xn;
+      }
+#pragma unroll
+      for (int kt = KH; kt < KT; ++kt) {
+        const double rb = rs[(kt * 4 + kl) * RS + n8];
+        if (kt & 1)
+          dmma(d10, d11, xa[kt - KH], rb);
+        else
+          dmma(d00, d01, xa[kt - KH], rb);
+      }
+      const double c0 = d00 + d10, c1 = d01 + d11;
+      double out0 = 0.0, out1 = 0.0;
+      if (A.tdiag) {
+        if (row_ok) tdiag_scale(A, kl, lam, c0, c1, out0, out1);
+      } else {
+      double v[8];
+      const int grp = lane & ~3;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[2 * j] = __shfl_sync(0xffffffffu, c0, grp | j);
+        v[2 * j + 1] = __shfl_sync(0xffffffffu, c1, grp | j);
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int s = 0; s < 8 / NT; ++s) {
+          if (s >= A.S) break;
+          double b4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < NT; ++i) b4[i] = v[s * NT + i];
+          small_solve(A.TM, A.TA, lam, NT, b4);
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            if (s * NT + i == col) out0 = b4[i];
+            if (s * NT + i == col + 1) out1 = b4[i];
+          }
+        }
+      }
+      }
+      *reinterpret_cast<double2*>(hs + row * RS + col) = make_double2(out0, out1);
+    }
+    // second product's A fragments: X[row][e], e = 4 kt + kl (L2)
+#pragma unroll
+    for (int kt = 0; kt < KH; ++kt) {
+      const int e = kt * 4 + kl;
+      xa[kt] = (row_ok && e < M) ? __ldg(X + row * M + e) : 0.0;
+    }
+    __syncthreads();
+    {
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KH; ++kt) {
+        const double hb = hs[(kt * 4 + kl) * RS + n8];
+        const int e = (kt + KH) * 4 + kl;
+        const double xn = (kt + KH < KT && row_ok && e < M) ? __ldg(X + row * M + e) : 0.0;
+        if (kt & 1)
+          dmma(d10, d11, xa[kt], hb);
+        else
+          dmma(d00, d01, xa[kt], hb);
+        xa[kt] = xn;
+      }
+#pragma unroll
+      for (int kt = KH; kt < KT; ++kt) {
+        const double hb = hs[(kt * 4 + kl) * RS + n8];
+        if (kt & 1)
+          dmma(d10, d11, xa[kt - KH], hb);
+        else
+          dmma(d00, d01, xa[kt - KH], hb);
+      }
+      double v0 = d00 + d10, v1 = d01 + d11;
+      if (A.tdiag) tdiag_qmix(PQ + 64, lane, d00 + d10, d01 + d11, v0, v1);
+      if (row_ok) {
+        const LocalDof d = local_dof(A, cx, cy, cz, row);
+        const double w = scale / d.mult;
+        if (!(A.tdiag && d.bdry)) {
+          if (d.bdry) {
+            v0 = rs[row * RS + col];
+            v1 = rs[row * RS + col + 1];
+          }
+          if (col < ncol) atomicAdd(z + static_cast<long long>(col) * A.n_space + d.g, v0 * w);
+          if (col + 1 < ncol) atomicAdd(z + static_cast<long long>(col + 1) * A.n_space + d.g, v1 * w);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Large cell blocks (m > 64, e.g. 3D Q4: m = 125): one CTA of 128 threads per
 // cell (persistent), X row-major in global memory (m^2 doubles, L2-resident
 // across the two products of one cell), all S*n_t columns at once:
@@ -1200,13 +1629,53 @@ void launch_asm(const DevASM& A, const double* r, double* z, double scale, cudaS
   count_launch();
   asm_apply_warp_kernel<M, NT><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
 }
+template <int M, int NT>
+void launch_mma32(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  if (A.xs != mma32_xbuf<M>()) throw std::invalid_argument("ASMSmoother: unexpected record stride");
+  constexpr size_t smem = mma32_smem<M>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(asm_apply_mma32_kernel<M, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaFuncSetAttribute(asm_apply_mma32_kernel<M, NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = true;
+  }
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_mma32_kernel<M, NT>, 128, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long warps = (A.n_list + kWmmaWarps - 1) / kWmmaWarps;
+  const long long grid =
+      std::max<long long>(1, std::min<long long>(warps, static_cast<long long>(std::max(per_sm, 1)) * sms));
+  count_launch();
+  asm_apply_mma32_kernel<M, NT><<<static_cast<unsigned>(grid), 128, smem, s>>>(A, r, z, scale);
+}
+// m = 25 / 27 run on the tensor cores (C3 fine sweep 1.79 -> 1.51 ms) unless
+// STMG_ASM27=warp (the DFMA warp-per-cell kernel, kept as the measured
+// alternative and tested)
+template <int M, int NT>
+void launch_small(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  if constexpr (M > 24) {
+    static const bool warp = [] {
+      const char* e = std::getenv("STMG_ASM27");
+      return e && std::string(e) == "warp";
+    }();
+    if (!warp) {
+      if (A.n_list == 0) return;
+      if (A.S * NT > 8) throw std::invalid_argument("ASMSmoother: S * n_t must be <= 8");
+      launch_mma32<M, NT>(A, r, z, scale, s);
+      return;
+    }
+  }
+  launch_asm<M, NT>(A, r, z, scale, s);
+}
 template <int M>
 void launch_asm_nt(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   switch (A.nt) {
-    case 1: launch_asm<M, 1>(A, r, z, scale, s); break;
-    case 2: launch_asm<M, 2>(A, r, z, scale, s); break;
-    case 3: launch_asm<M, 3>(A, r, z, scale, s); break;
-    case 4: launch_asm<M, 4>(A, r, z, scale, s); break;
+    case 1: launch_small<M, 1>(A, r, z, scale, s); break;
+    case 2: launch_small<M, 2>(A, r, z, scale, s); break;
+    case 3: launch_small<M, 3>(A, r, z, scale, s); break;
+    case 4: launch_small<M, 4>(A, r, z, scale, s); break;
     default: throw std::invalid_argument("ASMSmoother: n_t must be in [1, 4]");
   }
 }
@@ -1325,9 +1794,32 @@ void launch_asm_fd64(const DevASM& A, const double* r, double* z, double scale, 
   }
 }
 
+template <int M, int NT>
+void launch_large_mma(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
+  constexpr int NTH = ((M + 7) / 8) * 32;
+  constexpr size_t smem = sizeof(double) * (2 * kLargeMmaPitch * ((M + 7) / 8) * 8 + 128);
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_large_mma_kernel<M, NT>, NTH, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long grid =
+      std::max<long long>(1, std::min<long long>(A.n_list, static_cast<long long>(std::max(per_sm, 1)) * sms));
+  count_launch();
+  asm_apply_large_mma_kernel<M, NT><<<static_cast<unsigned>(grid), NTH, smem, s>>>(A, r, z, scale);
+}
+// m = 125 (3D Q4) runs on the tensor cores unless STMG_ASM125=dfma (the
+// CTA-per-cell DFMA kernel below, kept as the measured alternative and tested)
 template <int NT>
 void launch_large(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if (A.n_list == 0) return;
+  static const bool dfma = [] {
+    const char* e = std::getenv("STMG_ASM125");
+    return e && std::string(e) == "dfma";
+  }();
+  if (A.m == 125 && !dfma) {
+    launch_large_mma<125, NT>(A, r, z, scale, s);
+    return;
+  }
   const size_t smem = sizeof(double) * (16 * 128 + 128 * (kLargeChunk + 1));
   static bool configured = false;
   if (!configured) {

@@ -968,13 +968,16 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperat
     // STMG_NO_TDIAG: keep the pivoted per-eigenvalue solves (the fallback
     // kernel for non-diagonalisable temporal blocks), for testing
     if (!std::getenv("STMG_NO_TDIAG")) temporal_block_diagonalise(A);
+  } else if (!std::getenv("STMG_NO_TDIAG")) {
+    // the padded tensor-core kernels (m = 25, 27) use it as well
+    temporal_block_diagonalise(A);
   }
   cuda_check(cudaStreamSynchronize(s), "asm setup");
   A.X = X_.d();
   A.lam = lam_.d();
   if (A.S * A.nt > 8) {
     // wide batches: sweep groups of 8 / n_t steps (see add_correction)
-    const bool td = A.meta && !std::getenv("STMG_NO_TDIAG");
+    const bool td = !std::getenv("STMG_NO_TDIAG");
     chunk_ = A;
     chunk_.S = 8 / A.nt;
     chunk_.tdiag = 0;
@@ -1074,6 +1077,9 @@ void ASMSmoother::build_exact_large(DeviceBuffer& cellM, DeviceBuffer& cellA, cu
   cusolverDnDestroy(h);
   A.X = X_.d();
   A.lam = lam_.d();
+  // temporal fast diagonalisation for the tensor-core 125-dof kernel
+  A.tdiag = 0;
+  if (!std::getenv("STMG_NO_TDIAG")) temporal_block_diagonalise(A);
 }
 
 void ASMSmoother::add_correction(const double* residual, double* correction, cudaStream_t stream,

@@ -155,7 +155,9 @@ def test_asm_q3_temporal_variants(cuda, ref, eq, scheme, k, S):
     assert _rel(got - z0, want - z0) <= 1e-9
 
 
-@pytest.mark.parametrize("eq,scheme,k,S", [(problems.HEAT, problems.DG, 1, 1), (problems.WAVE, problems.CGP, 2, 2)])
+@pytest.mark.parametrize("eq,scheme,k,S", [(problems.HEAT, problems.DG, 1, 1), (problems.WAVE, problems.CGP, 2, 2),
+                                            (problems.HEAT, problems.DG, 3, 2), (problems.HEAT, problems.DG, 0, 4),
+                                            (problems.WAVE, problems.DG, 2, 1)])
 def test_asm_q4_perturbed_exact_blocks(cuda, ref, eq, scheme, k, S):
     """Perturbed Q4 cells (125-dof blocks, exact per-cell eigenbasis built by
     batched Cholesky / triangular solves / syev): equal to the reference's LU
@@ -172,6 +174,105 @@ def test_asm_q4_perturbed_exact_blocks(cuda, ref, eq, scheme, k, S):
     for l, w in enumerate(R.level_info()):
         M.set_omega(l, w["omega"])
     assert _rel(M.apply(_dev(cuda, res)).cpu().numpy(), R.vcycle(res)) <= 1e-9
+
+
+@pytest.mark.parametrize("eq,scheme,k,S", Q3_TIME_CASES)
+def test_asm_q2_exact_blocks_temporal_variants(cuda, ref, eq, scheme, k, S):
+    """Perturbed Q2 cells (27-dof exact blocks on every cell: the warp-per-cell
+    tensor-core kernel, temporally fast-diagonalised solves) across heat/wave,
+    DG/CGP, k and S: equal to the reference's LU block solves to 1e-9, and a
+    V-cycle to 1e-9."""
+    cfg = problems.Config("q2p", eq, scheme, 3, 2, 1, 2, k, S, 0.2, perturb=0.15)
+    cfg.rho = np.random.default_rng(7).uniform(0.5, 3.0, 8)
+    mesh, M, R = _build(cfg, ref)
+    n = R.n_dofs
+    res = problems.uniform_vector(n, seed=33)
+    z0 = problems.uniform_vector(n, seed=34)
+    got = M.asm_add_correction(0, _dev(cuda, res), _dev(cuda, z0)).cpu().numpy()
+    want = R.asm_add_correction(0, res, z0)
+    assert M.smoother_kind(0) & 2  # per-cell eigenbasis
+    assert _rel(got - z0, want - z0) <= 1e-9
+    for l, w in enumerate(R.level_info()):
+        M.set_omega(l, w["omega"])
+    assert _rel(M.apply(_dev(cuda, res)).cpu().numpy(), R.vcycle(res)) <= 1e-9
+
+
+@pytest.mark.parametrize("eq,scheme,k,S", [(problems.HEAT, problems.DG, 1, 2), (problems.WAVE, problems.CGP, 2, 1)])
+def test_asm_2d_q4_exact_blocks(cuda, ref, eq, scheme, k, S):
+    """Perturbed 2D Q4 cells (25-dof exact blocks): equal to the reference's
+    LU block solves to 1e-9."""
+    cfg = problems.Config("q4p2d", eq, scheme, 2, 2, 2, 4, k, S, 0.2, perturb=0.15)
+    mesh, M, R = _build(cfg, ref)
+    n = R.n_dofs
+    res = problems.uniform_vector(n, seed=35)
+    z0 = problems.uniform_vector(n, seed=36)
+    got = M.asm_add_correction(0, _dev(cuda, res), _dev(cuda, z0)).cpu().numpy()
+    want = R.asm_add_correction(0, res, z0)
+    assert _rel(got - z0, want - z0) <= 1e-9
+
+
+@pytest.mark.parametrize("env,val", [("STMG_ASM125", "dfma"), ("STMG_NO_TDIAG", "1")])
+def test_asm_125dof_kernel_variants(cuda, ref, env, val):
+    """The CTA-per-cell DFMA kernel for 125-dof exact blocks (STMG_ASM125=dfma,
+    the measured alternative to the tensor-core kernel) and the tensor-core
+    kernel's pivoted per-eigenvalue solves (STMG_NO_TDIAG) match the
+    reference on perturbed Q4 cells; subprocess because the kernel is chosen
+    once per process from the environment."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import refbind as ref\n"
+        "from paper_2408_04372_b200 import api, problems\n"
+        "cfg = problems.Config('q4p', problems.WAVE, problems.CGP, 3, 2, 1, 4, 2, 2, 0.2, perturb=0.15)\n"
+        "mesh = api.Mesh(cfg.dim, (0,0,0), (1,1,1), cfg.base_cells, cfg.refinements, cfg.vertices())\n"
+        "M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps, cfg.tau)\n"
+        "R = ref.Reference(cfg, with_mg=True)\n"
+        "r = problems.uniform_vector(R.n_dofs, seed=55); z0 = problems.uniform_vector(R.n_dofs, seed=56)\n"
+        "got = M.asm_add_correction(0, torch.from_numpy(r).cuda(), torch.from_numpy(z0).cuda()).cpu().numpy()\n"
+        "want = R.asm_add_correction(0, r, z0)\n"
+        "err = np.linalg.norm((got - z0) - (want - z0)) / np.linalg.norm(want - z0)\n"
+        "assert err <= 1e-9, err\n"
+        "print('ok', err)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env_vars = dict(os.environ, **{env: val}, PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env_vars, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok" in out.stdout
+
+
+@pytest.mark.parametrize("envs", [{"STMG_ASM27": "warp"}, {"STMG_NO_TDIAG": "1"}])
+def test_asm_27dof_kernel_variants(cuda, ref, envs):
+    """The DFMA warp-per-cell kernel for 27-dof exact blocks (STMG_ASM27=warp,
+    the measured alternative to the default tensor-core kernel) and the
+    tensor-core kernel's pivoted per-eigenvalue solves (STMG_NO_TDIAG) match
+    the reference on C3's checkerboard cells; subprocess because the kernel
+    is chosen once per process from the environment."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import refbind as ref\n"
+        "from paper_2408_04372_b200 import api, problems\n"
+        "cfg = problems.config('C3', 1)\n"
+        "mesh = api.Mesh(cfg.dim, (0,0,0), (1,1,1), cfg.base_cells, cfg.refinements, cfg.vertices())\n"
+        "M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k, cfg.n_steps, cfg.tau)\n"
+        "R = ref.Reference(cfg, with_mg=True)\n"
+        "r = problems.uniform_vector(R.n_dofs, seed=53); z0 = problems.uniform_vector(R.n_dofs, seed=54)\n"
+        "got = M.asm_add_correction(0, torch.from_numpy(r).cuda(), torch.from_numpy(z0).cuda()).cpu().numpy()\n"
+        "want = R.asm_add_correction(0, r, z0)\n"
+        "err = np.linalg.norm((got - z0) - (want - z0)) / np.linalg.norm(want - z0)\n"
+        "assert err <= 1e-9, err\n"
+        "print('ok', err)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env_vars = dict(os.environ, **envs, PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env_vars, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok" in out.stdout
 
 
 @pytest.mark.parametrize("env,kind", [("STMG_NO_TDIAG", 2), ("STMG_ASM64", 6), ("STMG_ASM_NBUF", 6)])

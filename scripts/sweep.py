@@ -8,6 +8,7 @@ algorithmic bytes 16 N (+ 24 n_verts perturbed) against MEASURED_PEAKS.json).
   (suffix v: vmult only; suffix n: vmult and V-cycle, no solve -- the
    Krylov basis of C5-256 does not fit one GPU)
 """
+import gc
 import json
 import os
 import sys
@@ -98,8 +99,12 @@ def main(names):
             torch.cuda.synchronize()
             t_s = time.perf_counter() - ts
             line.update({"solve_iterations": info["iterations"], "solve_ms": 1e3 * t_s, "solve_dofs_per_s": N / t_s})
+            del b, x, u0, v0, z
         print(json.dumps(line), flush=True)
+        # every device buffer of this configuration is released before the
+        # next one (C4's solve vectors left C5-128 out of memory otherwise)
         del M, op, u, y, mesh
+        gc.collect()
         torch.cuda.empty_cache()
 
 

@@ -560,9 +560,15 @@ __device__ __forceinline__ void stage_row(const DevASM& A, const double* Ps, con
   for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(dst + c) = make_double2(tr[c], tr[c + 1]);
 }
 
+// records of the 25/27-dof tensor-core kernel are stored with row pitch 28
+// (DevASM::x_layout == 2): the A-fragment loads X[a][e] (4 k-rows x 4 m-rows
+// per half-warp) then fall in 16 distinct 64-bit banks in both products; the
+// contiguous pitch 27 was 2-way conflicted (ncu: 117 M conflicts per C3 sweep)
+constexpr int kMma32Pitch = 28;
 template <int M>
 constexpr int mma32_xbuf() {
-  return (M * M + 1) & ~1;  // = DevASM::xs for m != 64 (16-byte bulk copies)
+  static_assert(M <= kMma32Pitch && (M * kMma32Pitch) % 2 == 0, "16-byte bulk copies");
+  return M * kMma32Pitch;  // = DevASM::xs under x_layout 2
 }
 constexpr int kWmmaWarps = 4, kWmmaPitch = 12;  // pitch 12: conflict-free B-fragment rows
 template <int M>
@@ -665,7 +671,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int e = i * 8 + n8;
-        const double xa = (a < M && e < M) ? Xs[a * M + e] : 0.0;
+        const double xa = (a < M && e < M) ? Xs[a * kMma32Pitch + e] : 0.0;
         dmma(acc[i][0], acc[i][1], xa, b);
       }
     }
@@ -724,7 +730,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int a = i * 8 + n8;
-        const double xa = (a < M && e < M) ? Xs[a * M + e] : 0.0;
+        const double xa = (a < M && e < M) ? Xs[a * kMma32Pitch + e] : 0.0;
         dmma(acc[i][0], acc[i][1], xa, b);
       }
     }
@@ -1602,7 +1608,7 @@ __global__ void back_transform_kernel(int m, long long xs, int layout, const dou
     const int a = i / m, e = i % m;
     double s = 0.0;
     for (int k = a; k < m; ++k) s = fma(Lc[static_cast<long long>(k) * m + a], Vc[static_cast<long long>(e) * m + k], s);
-    Xc[m == 64 ? (layout == 1 ? swz64f(a, e) : swz64(a, e)) : i] = s;
+    Xc[m == 64 ? (layout == 1 ? swz64f(a, e) : swz64(a, e)) : (layout == 2 ? a * kMma32Pitch + e : i)] = s;
   }
 }
 
@@ -1656,11 +1662,8 @@ void launch_mma32(const DevASM& A, const double* r, double* z, double scale, cud
 template <int M, int NT>
 void launch_small(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if constexpr (M > 24) {
-    static const bool warp = [] {
-      const char* e = std::getenv("STMG_ASM27");
-      return e && std::string(e) == "warp";
-    }();
-    if (!warp) {
+    // the record layout chosen at setup (stmg.cpp) selects the kernel
+    if (A.x_layout == 2) {
       if (A.n_list == 0) return;
       if (A.S * NT > 8) throw std::invalid_argument("ASMSmoother: S * n_t must be <= 8");
       launch_mma32<M, NT>(A, r, z, scale, s);

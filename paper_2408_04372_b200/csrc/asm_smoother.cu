@@ -536,7 +536,7 @@ __device__ __forceinline__ void tdiag_qmix(const double* Qs, int lane, double v0
 // residual row of one local dof, P-transformed when A.tdiag (slots), raw
 // otherwise; a Dirichlet row under tdiag adds w r to z here
 __device__ __forceinline__ void stage_row(const DevASM& A, const double* Ps, const double* rn, long long g, bool bdry,
-                                          double mult, double scale, int ncol, double* z, double* dst) {
+                                          double mult, double scale, int ncol, double* z, double* dst, int sw = 0) {
   double tr[8];
   if (A.tdiag) {
 #pragma unroll
@@ -557,7 +557,7 @@ __device__ __forceinline__ void stage_row(const DevASM& A, const double* Ps, con
     for (int k = 0; k < 8; ++k) tr[k] = rn[k];
   }
 #pragma unroll
-  for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(dst + c) = make_double2(tr[c], tr[c + 1]);
+  for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(dst + (c ^ sw)) = make_double2(tr[c], tr[c + 1]);
 }
 
 // records of the 25/27-dof tensor-core kernel are stored with row pitch 28
@@ -570,7 +570,13 @@ constexpr int mma32_xbuf() {
   static_assert(M <= kMma32Pitch && (M * kMma32Pitch) % 2 == 0, "16-byte bulk copies");
   return M * kMma32Pitch;  // = DevASM::xs under x_layout 2
 }
-constexpr int kWmmaWarps = 4, kWmmaPitch = 12;  // pitch 12: conflict-free B-fragment rows
+// rs / hs rows of 8 doubles with the columns XOR-swizzled by row bits 1-2
+// (wmma_sw, even so 16-byte pairs stay whole): the B-fragment loads (4 rows x
+// 4 columns per half-warp), the 16-byte row accesses of 8 lanes and the
+// accumulator-pair stores are conflict-free, the per-lane scatter reads 2-way
+// (pitch 12 unswizzled: 2-way / 4-way on the last two)
+constexpr int kWmmaWarps = 4, kWmmaPitch = 8;
+__device__ __forceinline__ int wmma_sw(int row) { return 4 * ((row >> 1) & 1) + 2 * ((row >> 2) & 1); }
 template <int M>
 constexpr int wmma_warp_doubles() {
   return 2 * mma32_xbuf<M>() + 2 * 32 * kWmmaPitch;
@@ -649,7 +655,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
     double rn[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) rn[c] = rnn[c];
-    if (own) stage_row(A, PQ, rn, d.g, d.bdry, d.mult, scale, ncol, z, rs + lane * RS);
+    if (own) stage_row(A, PQ, rn, d.g, d.bdry, d.mult, scale, ncol, z, rs + lane * RS, wmma_sw(lane));
     if (next < n_pos) gather(next);
     if (buf == 0) {
       mbar_wait(&bar[0], ph0);
@@ -667,7 +673,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
       const int a = kt * 4 + kl;
-      const double b = rs[a * RS + n8];
+      const double b = rs[a * RS + (n8 ^ wmma_sw(a))];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int e = i * 8 + n8;
@@ -677,14 +683,14 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      *reinterpret_cast<double2*>(hs + (i * 8 + n8) * RS + 2 * kl) = make_double2(acc[i][0], acc[i][1]);
+      *reinterpret_cast<double2*>(hs + (i * 8 + n8) * RS + ((2 * kl) ^ wmma_sw(i * 8 + n8))) = make_double2(acc[i][0], acc[i][1]);
     __syncwarp();
     // ---- row work: lane e solves its eigen-row (slots -> time columns)
     if (own) {
       double v[8];
 #pragma unroll
       for (int c = 0; c < 8; c += 2) {
-        const double2 q = *reinterpret_cast<const double2*>(hs + lane * RS + c);
+        const double2 q = *reinterpret_cast<const double2*>(hs + lane * RS + (c ^ wmma_sw(lane)));
         v[c] = q.x;
         v[c + 1] = q.y;
       }
@@ -717,7 +723,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
         }
       }
 #pragma unroll
-      for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(hs + lane * RS + c) = make_double2(o[c], o[c + 1]);
+      for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(hs + lane * RS + (c ^ wmma_sw(lane))) = make_double2(o[c], o[c + 1]);
     }
     __syncwarp();
     // ---- MMA 2: z_T (a x 8) = X hat z, A[row=a][k=e] = X[a][e]
@@ -726,7 +732,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
       const int e = kt * 4 + kl;
-      const double b = hs[e * RS + n8];
+      const double b = hs[e * RS + (n8 ^ wmma_sw(e))];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int a = i * 8 + n8;
@@ -737,7 +743,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      *reinterpret_cast<double2*>(hs + (i * 8 + n8) * RS + 2 * kl) = make_double2(acc[i][0], acc[i][1]);
+      *reinterpret_cast<double2*>(hs + (i * 8 + n8) * RS + ((2 * kl) ^ wmma_sw(i * 8 + n8))) = make_double2(acc[i][0], acc[i][1]);
     __syncwarp();
     // ---- scatter: lane a, weighted (Dirichlet rows: w r; under tdiag added at the staging)
     if (own) {
@@ -745,7 +751,7 @@ __global__ void __launch_bounds__(32 * kWmmaWarps, 3) asm_apply_mma32_kernel(con
       if (!d.bdry) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          if (c < ncol) atomicAdd(z + static_cast<long long>(c) * nsp + d.g, hs[lane * RS + c] * w);
+          if (c < ncol) atomicAdd(z + static_cast<long long>(c) * nsp + d.g, hs[lane * RS + (c ^ wmma_sw(lane))] * w);
       } else if (!A.tdiag) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)

@@ -42,6 +42,9 @@ struct DevLevel {
   const double* rho0;
   int rho_shift;          // refinement levels between this level and level 0
   long long cells0[3];
+  // rho is constant on every z layer of level-0 cells (or rho0 == nullptr):
+  // the owner-computes Cartesian kernel (st_brick.cu) applies
+  int rho_zonly;
   // 1D tables at the q = n Gauss points of [0,1]
   double B[kMaxN][kMaxN];   // B[q][j] = phi_j(x_q)      (spatial_operator.cpp:141-147)
   double Dq[kMaxN][kMaxN];  // collocation derivative at the Gauss points

@@ -9,6 +9,10 @@ namespace stmgb {
 
 // y = S u (overwrite), fused space-time operator -- st_operator.cu
 void st_apply(const DevLevel& L, const double* u, double* y, cudaStream_t stream);
+// owner-computes Cartesian form (st_brick.cu): y = S u (f == nullptr) or
+// y = f - S u, Dirichlet rows included, every dof written once
+bool st_brick_supported(const DevLevel& L);
+void st_brick(const DevLevel& L, const double* f, const double* u, double* y, cudaStream_t stream);
 // Dirichlet entries of every field of v set to zero
 void st_zero_boundary(const DevLevel& L, double* v, cudaStream_t stream);
 // r = f - S u (overwrite), fused residual (no separate subtraction pass)

@@ -1,0 +1,435 @@
+// Owner-computes space-time operator on Cartesian levels whose coefficient
+// is constant on every z layer of cells (every level of C4 and C5):
+//   y = S u          (SpaceTimeOperator::apply, space_time_operator.cpp:45-130)
+//   r = f - S u      (the residual f - S u of multigrid.cpp:174-185)
+// with the Dirichlet identity rows (space_time_operator.cpp:125-129) written
+// in the same pass -- no memset of y, no copy of f, no boundary kernel and
+// no atomics: every output dof is written exactly once, by the CTA owning it.
+//
+// Why this is exact. On a uniform axis-aligned lattice the reference's cell
+// matrices (Gauss rule with q = p + 1 points, spatial_operator.cpp:129-185)
+// are Kronecker products of the [0,1] element matrices Mr = B^T W B and
+// Kr = D^T W D, and with rho depending on z only the assembled spatial
+// operators factor into ASSEMBLED 1D operators along x and y:
+//   M = Mz (x) My (x) Mx,
+//   A = sum_ez rho_ez [Mz^e (x) (Ky/hy^2 (x) Mx + My (x) Kx/hx^2) + Kz^e/hz^2 (x) My (x) Mx]
+// so a CTA owning a tile of x-y lattice nodes needs u only on the tile plus
+// p nodes of halo on the low side and 1 node on the high side, and each
+// assembled 1D product costs one even-odd element product per element plus
+// one add per shared vertex -- half the arithmetic of the per-cell form
+// (st_cart.cuh), whose 125 cell dofs cover 64 owned ones for p = 4.
+//
+// Schedule. Grid = (x-y tiles) x (z chunks). A CTA marches its chunk plane by
+// plane, PB planes per batch:
+//   Y: thread = (x column of the input box, field, plane): loads the column
+//      of u from HBM (Dirichlet and out-of-domain inputs zeroed,
+//      spatial_operator.cpp:304-307), a = My u, b = Ky u on the owned rows
+//      -> shared memory
+//   X: thread = (owned row, field, plane): c = Mx a, pre = Kx a / hx^2 +
+//      Mx b / hy^2 on the owned columns -> shared memory
+//   Z: thread = owned (x, y) point (and field group): temporal block
+//      coupling of all F fields (space_time_operator.cpp:59-89 through the
+//      block coefficients CM / CA, :269-317), then the z element products of
+//      the plane's layer(s) accumulated into the per-thread z window held in
+//      registers; when a layer closes, its p planes are final and are stored
+//      (residual: f - S u read and written in the same step).
+// The z chunk additionally processes the layer below it (halo) so the
+// chunk's first plane receives both layers' contributions.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "kernels.hpp"
+#include "st_cart.cuh"
+
+namespace stmgb {
+namespace stb {
+
+using stc::EO;
+
+constexpr int kThreads = 256;
+
+template <int N, int F>
+struct Cfg {
+  static constexpr int P = N - 1;
+  static constexpr int FG = F > 4 ? 2 : 1;          // field groups in stage Z
+  static constexpr int FPG = (F + FG - 1) / FG;      // fields per group
+  static constexpr int OX = 16;                      // owned nodes per tile (x)
+  static constexpr int OY = FG == 1 ? 16 : 8;        // owned nodes per tile (y)
+  static constexpr int TX = OX / P, TY = OY / P;     // cells per tile
+  static constexpr int WX = OX + P + 1, WY = OY + P + 1;  // input box
+  static constexpr int PB = F > 4 ? 1 : (F > 2 ? 2 : 4);  // planes per batch
+  static constexpr int XP = WX;                      // AB row pitch (odd: conflict-free rows)
+  static constexpr int CPP = OX + 1;                 // CP row pitch
+  static constexpr int AB_F = OY * XP;               // one (field, plane) of a / b
+  static constexpr int CP_F = OY * CPP;              // one (field, plane) of c / pre
+  static constexpr int AB = PB * F * AB_F;
+  static constexpr int CP = PB * F * CP_F;
+  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * static_cast<size_t>(AB + CP); }
+  static_assert(OX % P == 0 && OY % P == 0, "tile must hold whole cells");
+  static_assert(OX * OY * FG == kThreads, "one stage-Z item per thread");
+  static_assert(WX * F * PB <= kThreads && OY * F * PB <= kThreads, "stage Y / X items per thread");
+};
+
+// se/so of one element (the even / odd halves of E and O applied to the
+// element's split input)
+template <int N>
+struct Split {
+  double e[EO<N>::HE];
+  double o[EO<N>::H > 0 ? EO<N>::H : 1];
+};
+template <int N>
+__device__ __forceinline__ Split<N> split_at(const double* v) {
+  Split<N> s;
+#pragma unroll
+  for (int k = 0; k < EO<N>::H; ++k) {
+    s.e[k] = v[k] + v[N - 1 - k];
+    s.o[k] = v[k] - v[N - 1 - k];
+  }
+  if constexpr (N % 2 == 1) s.e[EO<N>::H] = v[EO<N>::H];
+  return s;
+}
+// out[j] (j = 0..N-1) of the element product with (E, O)
+template <int N>
+__device__ __forceinline__ void elem(const double (&E)[3][3], const double (&O)[2][2], const Split<N>& s,
+                                     double (&out)[N]) {
+  double se[EO<N>::HE], so[EO<N>::H > 0 ? EO<N>::H : 1];
+#pragma unroll
+  for (int i = 0; i < EO<N>::HE; ++i) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < EO<N>::HE; ++k) t = fma(E[i][k], s.e[k], t);
+    se[i] = t;
+  }
+#pragma unroll
+  for (int i = 0; i < EO<N>::H; ++i) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < EO<N>::H; ++k) t = fma(O[i][k], s.o[k], t);
+    so[i] = t;
+  }
+#pragma unroll
+  for (int i = 0; i < EO<N>::H; ++i) {
+    out[i] = se[i] + so[i];
+    out[N - 1 - i] = se[i] - so[i];
+  }
+  if constexpr (N % 2 == 1) out[EO<N>::H] = se[EO<N>::H];
+}
+// last entry (j = N-1) of the element product only (halo element)
+template <int N>
+__device__ __forceinline__ double elem_last(const double (&E)[3][3], const double (&O)[2][2], const Split<N>& s) {
+  double se = 0.0, so = 0.0;
+#pragma unroll
+  for (int k = 0; k < EO<N>::HE; ++k) se = fma(E[0][k], s.e[k], se);
+#pragma unroll
+  for (int k = 0; k < EO<N>::H; ++k) so = fma(O[0][k], s.o[k], so);
+  return se - so;
+}
+
+template <int N, int F, bool RES>
+__global__ void __launch_bounds__(kThreads, 2)
+    st_brick_kernel(const __grid_constant__ DevLevel L, const double* __restrict__ u, const double* __restrict__ fvec,
+                    double* __restrict__ y, int ntx, int zc) {
+  using C = Cfg<N, F>;
+  constexpr int P = C::P, OX = C::OX, OY = C::OY, WX = C::WX, WY = C::WY, PB = C::PB, FPG = C::FPG;
+  extern __shared__ __align__(16) double smem[];
+  double* Aa = smem;
+  double* Ab = Aa + C::AB;
+  double* Cc = Ab + C::AB;
+  double* Cp = Cc + C::CP;
+
+  const int t = threadIdx.x;
+  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+  const long long X0 = static_cast<long long>(tx) * OX, Y0 = static_cast<long long>(ty) * OY;
+  const long long dx = L.dofs[0], dy = L.dofs[1], dz = L.dofs[2];
+  const long long dxy = dx * dy, ns = L.n_space;
+  const int ncz = static_cast<int>(L.cells[2]);
+  const int L0 = static_cast<int>(blockIdx.y) * zc;
+  const int L1 = L0 + zc < ncz ? L0 + zc : ncz;
+  const int Ls = L0 > 0 ? L0 - 1 : 0;  // first layer processed (halo)
+  const int z_first = Ls * P, z_last = L1 * P;
+  const bool lo_dir = (L.zbc & 1) != 0, hi_dir = (L.zbc & 2) != 0;
+  const double V = L.h[0] * L.h[1] * L.h[2];
+  const double sx = L.hinv2[0], sy = L.hinv2[1], sz = L.hinv2[2];
+  auto rho_of = [&](int e) -> double {
+    if (!L.rho0) return 1.0;
+    const long long az = (e + L.cz0) >> L.rho_shift;
+    return __ldg(L.rho0 + az * L.cells0[1] * L.cells0[0]);
+  };
+
+  // stage-Z identity of this thread
+  const int g = t / (OX * OY);                 // field group
+  const int pt = t - g * (OX * OY);
+  const int zx = pt % OX, zy = pt / OX;
+  const long long gx = X0 + zx, gy = Y0 + zy;
+  const int f0 = g * FPG;
+  // the point is written by this CTA if it lies on the lattice; x / y end
+  // planes (always Dirichlet) are written by the tile containing them, or by
+  // the last tile's border threads when the tile ends exactly on them
+  const bool on_lat = gx < dx && gy < dy;
+  const bool xend_extra = (zx == OX - 1) && (X0 + OX == dx - 1);
+  const bool yend_extra = (zy == OY - 1) && (Y0 + OY == dy - 1);
+
+  double win[FPG][N];  // z window of the open layer, per own field
+#pragma unroll
+  for (int i = 0; i < FPG; ++i)
+#pragma unroll
+    for (int j = 0; j < N; ++j) win[i][j] = 0.0;
+
+  // store one output plane zz of the own fields (value v[i] per field)
+  auto store_dir = [&](long long x, long long yy, long long zz) {
+#pragma unroll
+    for (int i = 0; i < FPG; ++i) {
+      const int f = f0 + i;
+      if (f >= F) break;
+      const long long idx = f * ns + zz * dxy + yy * dx + x;
+      const double uv = __ldg(u + idx);
+      y[idx] = RES ? __ldg(fvec + idx) - uv : uv;
+    }
+  };
+  auto store_plane = [&](long long zz, int jw) {
+    const bool zdir = (zz == 0 && lo_dir) || (zz == dz - 1 && hi_dir);
+    if (on_lat) {
+      const bool dir = zdir || gx == 0 || gy == 0 || gx == dx - 1 || gy == dy - 1;
+      if (dir) {
+        store_dir(gx, gy, zz);
+      } else {
+        const bool no_f = (zz == 0 && !lo_dir);  // low interface plane: f counted by the slab below
+#pragma unroll
+        for (int i = 0; i < FPG; ++i) {
+          const int f = f0 + i;
+          if (f >= F) break;
+          const long long idx = f * ns + zz * dxy + gy * dx + gx;
+          if (RES)
+            y[idx] = no_f ? -win[i][jw] : __ldg(fvec + idx) - win[i][jw];
+          else
+            y[idx] = win[i][jw];
+        }
+      }
+    }
+    if (xend_extra && gy < dy) store_dir(dx - 1, gy, zz);
+    if (yend_extra && gx < dx) store_dir(gx, dy - 1, zz);
+    if (xend_extra && yend_extra) store_dir(dx - 1, dy - 1, zz);
+  };
+
+  for (int zb = z_first; zb <= z_last; zb += PB) {
+    const int nb = z_last - zb + 1 < PB ? z_last - zb + 1 : PB;
+    // ---- Y: columns of u along y on the input box
+    if (t < WX * F * PB) {
+      const int x = t % WX, fb = t / WX;
+      const int f = fb % F, b = fb / F;
+      const long long z = zb + b;
+      const long long gxx = X0 - P + x;
+      if (b < nb) {
+        double v[WY];
+        const bool zd = (z == 0 && lo_dir) || (z == dz - 1 && hi_dir);
+        const bool xok = !zd && gxx > 0 && gxx < dx - 1;
+        const double* col = u + f * ns + z * dxy + gxx;
+#pragma unroll
+        for (int r = 0; r < WY; ++r) {
+          const long long yy = Y0 - P + r;
+          v[r] = (xok && yy > 0 && yy < dy - 1) ? __ldg(col + yy * dx) : 0.0;
+        }
+        double* oa = Aa + (b * F + f) * C::AB_F + x;
+        double* ob = Ab + (b * F + f) * C::AB_F + x;
+        // element 0 is the halo cell: it reaches owned row 0 only
+        double ca, cb;
+        {
+          const Split<N> s = split_at<N>(v);
+          ca = elem_last<N>(L.MrE, L.MrO, s);
+          cb = elem_last<N>(L.KrE, L.KrO, s);
+        }
+#pragma unroll
+        for (int e = 1; e <= OY / P; ++e) {
+          const Split<N> s = split_at<N>(v + e * P);
+          double ea[N], eb[N];
+          elem<N>(L.MrE, L.MrO, s, ea);
+          elem<N>(L.KrE, L.KrO, s, eb);
+          const int r0 = (e - 1) * P;
+          oa[r0 * C::XP] = ca + ea[0];
+          ob[r0 * C::XP] = cb + eb[0];
+#pragma unroll
+          for (int j = 1; j < P; ++j) {
+            oa[(r0 + j) * C::XP] = ea[j];
+            ob[(r0 + j) * C::XP] = eb[j];
+          }
+          ca = ea[P];
+          cb = eb[P];
+        }
+      }
+    }
+    __syncthreads();
+    // ---- X: rows of a / b along x -> c, pre on the owned columns
+    if (t < OY * F * PB) {
+      const int r = t % OY, fb = t / OY;
+      const int f = fb % F, b = fb / F;
+      if (b < nb) {
+        const double* ia = Aa + (b * F + f) * C::AB_F + r * C::XP;
+        const double* ib = Ab + (b * F + f) * C::AB_F + r * C::XP;
+        double* oc = Cc + (b * F + f) * C::CP_F + r * C::CPP;
+        double* op = Cp + (b * F + f) * C::CP_F + r * C::CPP;
+        double va[N], vb[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          va[k] = ia[k];
+          vb[k] = ib[k];
+        }
+        double cc, cp;
+        {
+          const Split<N> sa = split_at<N>(va), sb = split_at<N>(vb);
+          cc = elem_last<N>(L.MrE, L.MrO, sa);
+          cp = fma(sx, elem_last<N>(L.KrE, L.KrO, sa), sy * elem_last<N>(L.MrE, L.MrO, sb));
+        }
+#pragma unroll
+        for (int e = 1; e <= OX / P; ++e) {
+          va[0] = va[P];
+          vb[0] = vb[P];
+#pragma unroll
+          for (int k = 1; k < N; ++k) {
+            va[k] = ia[e * P + k];
+            vb[k] = ib[e * P + k];
+          }
+          const Split<N> sa = split_at<N>(va), sb = split_at<N>(vb);
+          double ec[N], ek[N], em[N];
+          elem<N>(L.MrE, L.MrO, sa, ec);
+          elem<N>(L.KrE, L.KrO, sa, ek);
+          elem<N>(L.MrE, L.MrO, sb, em);
+          const int r0 = (e - 1) * P;
+          oc[r0] = cc + ec[0];
+          op[r0] = cp + fma(sx, ek[0], sy * em[0]);
+#pragma unroll
+          for (int j = 1; j < P; ++j) {
+            oc[r0 + j] = ec[j];
+            op[r0 + j] = fma(sx, ek[j], sy * em[j]);
+          }
+          cc = ec[P];
+          cp = fma(sx, ek[P], sy * em[P]);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- Z: temporal coupling and the z element products
+    for (int b = 0; b < nb; ++b) {
+      const int z = zb + b;
+      const int e_of = z / P, j = z - e_of * P;
+      double cmc[FPG], cap[FPG], cac[FPG];
+#pragma unroll
+      for (int i = 0; i < FPG; ++i) cmc[i] = cap[i] = cac[i] = 0.0;
+      const double* ic = Cc + b * F * C::CP_F + zy * C::CPP + zx;
+      const double* ip = Cp + b * F * C::CP_F + zy * C::CPP + zx;
+#pragma unroll
+      for (int gg = 0; gg < F; ++gg) {
+        const double vc = ic[gg * C::CP_F], vp = ip[gg * C::CP_F];
+#pragma unroll
+        for (int i = 0; i < FPG; ++i) {
+          const int f = (C::FG == 1 ? 0 : f0) + i;
+          if (f >= F) break;
+          const double cm = L.CM[f * F + gg], ca = L.CA[f * F + gg];
+          cmc[i] = fma(cm, vc, cmc[i]);
+          cap[i] = fma(ca, vp, cap[i]);
+          cac[i] = fma(ca, vc, cac[i]);
+        }
+      }
+      // contribution of this plane to layer e at local index jl
+      auto add_layer = [&](int e, int jl) {
+        const double rho = rho_of(e);
+        const double rv = rho * V * sz;
+        double mc[N], kc[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          mc[q] = L.Mr[q][jl];
+          kc[q] = L.Kr[q][jl];
+        }
+#pragma unroll
+        for (int i = 0; i < FPG; ++i) {
+          const double zm = V * fma(rho, cap[i], cmc[i]);
+          const double zk = rv * cac[i];
+#pragma unroll
+          for (int q = 0; q < N; ++q) win[i][q] = fma(mc[q], zm, fma(kc[q], zk, win[i][q]));
+        }
+      };
+      if (j == 0 && z > z_first) {
+        // vertex plane: close layer e - 1; its p lower planes are final
+        const int e = e_of - 1;
+        add_layer(e, P);
+        if (e >= L0) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) store_plane(e * P + q, q);
+        }
+#pragma unroll
+        for (int i = 0; i < FPG; ++i) {
+          win[i][0] = win[i][P];
+#pragma unroll
+          for (int q = 1; q < N; ++q) win[i][q] = 0.0;
+        }
+      }
+      if (z < z_last) add_layer(e_of, j);
+    }
+  }
+  // the slab's top plane: Dirichlet, or an interface partial sum
+  if (L1 == ncz) store_plane(z_last, 0);
+}
+
+template <int N, int F>
+void launch(const DevLevel& L, const double* u, const double* f, double* y, cudaStream_t s) {
+  using C = Cfg<N, F>;
+  static bool configured = false;
+  if (!configured) {
+    for (auto k : {st_brick_kernel<N, F, false>, st_brick_kernel<N, F, true>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::smem_bytes()));
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    configured = true;
+  }
+  const long long ntx = std::max<long long>(1, (L.dofs[0] - 1 + C::OX - 1) / C::OX);
+  const long long nty = std::max<long long>(1, (L.dofs[1] - 1 + C::OY - 1) / C::OY);
+  const long long tiles = ntx * nty;
+  const long long ncz = L.cells[2];
+  // enough CTAs for ~8 per SM-slot, chunks of >= 4 layers (halo layer cost)
+  long long nch = std::max<long long>(1, (148LL * 2 * 8 + tiles - 1) / tiles);
+  nch = std::min<long long>(nch, std::max<long long>(1, ncz / 4));
+  const long long zc = (ncz + nch - 1) / nch;
+  nch = (ncz + zc - 1) / zc;
+  const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nch));
+  count_launch();
+  if (f)
+    st_brick_kernel<N, F, true><<<grid, kThreads, C::smem_bytes(), s>>>(L, u, f, y, static_cast<int>(ntx),
+                                                                        static_cast<int>(zc));
+  else
+    st_brick_kernel<N, F, false><<<grid, kThreads, C::smem_bytes(), s>>>(L, u, nullptr, y, static_cast<int>(ntx),
+                                                                         static_cast<int>(zc));
+}
+
+template <int N>
+void launch_n(const DevLevel& L, const double* u, const double* f, double* y, cudaStream_t s) {
+  switch (L.F) {
+    case 1: launch<N, 1>(L, u, f, y, s); break;
+    case 2: launch<N, 2>(L, u, f, y, s); break;
+    case 3: launch<N, 3>(L, u, f, y, s); break;
+    case 4: launch<N, 4>(L, u, f, y, s); break;
+    case 5: launch<N, 5>(L, u, f, y, s); break;
+    case 6: launch<N, 6>(L, u, f, y, s); break;
+    case 7: launch<N, 7>(L, u, f, y, s); break;
+    case 8: launch<N, 8>(L, u, f, y, s); break;
+    default: throw std::invalid_argument("st_brick: S * n_t must be in [1, 8]");
+  }
+}
+
+}  // namespace stb
+
+bool st_brick_supported(const DevLevel& L) {
+  return L.dim == 3 && L.verts == nullptr && L.rho_zonly && (L.n == 2 || L.n == 3 || L.n == 5) && L.F >= 1 &&
+         L.F <= kMaxF;
+}
+
+void st_brick(const DevLevel& L, const double* f, const double* u, double* y, cudaStream_t s) {
+  switch (L.n) {
+    case 2: stb::launch_n<2>(L, u, f, y, s); break;
+    case 3: stb::launch_n<3>(L, u, f, y, s); break;
+    case 5: stb::launch_n<5>(L, u, f, y, s); break;
+    default: throw std::invalid_argument("st_brick: p must be 1, 2 or 4");
+  }
+}
+
+}  // namespace stmgb

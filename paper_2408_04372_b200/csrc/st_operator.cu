@@ -57,6 +57,10 @@ __global__ void boundary_identity_kernel(int dim, int zbc, long long dx, long lo
 
 namespace {
 void run(const DevLevel& L, const double* f, const double* u, double* y, cudaStream_t stream) {
+  if (st_brick_supported(L)) {
+    st_brick(L, f, u, y, stream);
+    return;
+  }
   if (f) {
     vec_copy(y, f, L.n_dofs, stream);
     // slab whose low z plane is an interface owned by the slab below: its f

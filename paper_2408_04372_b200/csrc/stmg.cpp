@@ -117,8 +117,13 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
     d.rho0 = rho0_.d();
     d.rho_shift = mesh_level;
     for (int a = 0; a < 3; ++a) d.cells0[a] = a < m.dim ? c0[a] : 1;
+    d.rho_zonly = 1;
+    const Index layer = c0[0] * c0[1];
+    for (size_t i = 0; i < rho.coarse_cell_scale.size(); ++i)
+      if (rho.coarse_cell_scale[i] != rho.coarse_cell_scale[(i / layer) * layer]) d.rho_zonly = 0;
   } else {
     d.rho0 = nullptr;
+    d.rho_zonly = 1;
   }
   const Rule q = gauss(d.n);
   const Rule gl = gauss_lobatto(d.n);

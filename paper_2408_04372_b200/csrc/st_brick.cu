@@ -62,14 +62,21 @@ struct Cfg {
   static constexpr int PB = F > 4 ? 1 : (F > 2 ? 2 : 4);  // planes per batch
   static constexpr int XP = WX;                      // AB row pitch (odd: conflict-free rows)
   static constexpr int CPP = OX + 1;                 // CP row pitch
-  static constexpr int AB_F = OY * XP;               // one (field, plane) of a / b
+  // block strides padded to WX (mod 16): the stage-Y threads t = x + WX * block
+  // then address word t (mod 16) -- conflict-free 64-bit shared accesses
+  static constexpr int pad16(int base, int want) { return base + (((want - base) % 16) + 16) % 16; }
+  static constexpr int AB_F = pad16(OY * XP, WX);    // one (field, plane) of a / b
   static constexpr int CP_F = OY * CPP;              // one (field, plane) of c / pre
   static constexpr int AB = PB * F * AB_F;
   static constexpr int CP = PB * F * CP_F;
-  static constexpr size_t smem_bytes() { return sizeof(double) * 2 * static_cast<size_t>(AB + CP); }
+  static constexpr int UB_F = pad16(WY * WX, WX);     // one (field, plane) of the staged u box
+  static constexpr int UB = PB * F * UB_F;
+  static constexpr int XH = 2;                        // stage-X items per row (halves)
+  static constexpr size_t smem_bytes() { return sizeof(double) * (2 * static_cast<size_t>(AB + CP) + UB); }
   static_assert(OX % P == 0 && OY % P == 0, "tile must hold whole cells");
   static_assert(OX * OY * FG == kThreads, "one stage-Z item per thread");
-  static_assert(WX * F * PB <= kThreads && OY * F * PB <= kThreads, "stage Y / X items per thread");
+  static_assert(WX * F * PB <= kThreads && XH * OY * F * PB <= kThreads, "stage Y / X items per thread");
+  static_assert((OX / P) % XH == 0, "stage-X halves hold whole cells");
 };
 
 // se/so of one element (the even / odd halves of E and O applied to the
@@ -127,6 +134,14 @@ __device__ __forceinline__ double elem_last(const double (&E)[3][3], const doubl
   return se - so;
 }
 
+// 8-byte asynchronous global -> shared copy; bytes = 0 fills zeros
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, int bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 template <int N, int F, bool RES>
 __global__ void __launch_bounds__(kThreads, 2)
     st_brick_kernel(const __grid_constant__ DevLevel L, const double* __restrict__ u, const double* __restrict__ fvec,
@@ -138,6 +153,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   double* Ab = Aa + C::AB;
   double* Cc = Ab + C::AB;
   double* Cp = Cc + C::CP;
+  double* Ub = Cp + C::CP;
 
   const int t = threadIdx.x;
   const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
@@ -168,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // planes (always Dirichlet) are written by the tile containing them, or by
   // the last tile's border threads when the tile ends exactly on them
   const bool on_lat = gx < dx && gy < dy;
+  const long long pbase = gy * dx + gx;
   const bool xend_extra = (zx == OX - 1) && (X0 + OX == dx - 1);
   const bool yend_extra = (zy == OY - 1) && (Y0 + OY == dy - 1);
 
@@ -196,11 +213,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         store_dir(gx, gy, zz);
       } else {
         const bool no_f = (zz == 0 && !lo_dir);  // low interface plane: f counted by the slab below
+        const long long base = f0 * ns + zz * dxy + pbase;
 #pragma unroll
         for (int i = 0; i < FPG; ++i) {
-          const int f = f0 + i;
-          if (f >= F) break;
-          const long long idx = f * ns + zz * dxy + gy * dx + gx;
+          if (f0 + i >= F) break;
+          const long long idx = base + i * ns;
           if (RES)
             y[idx] = no_f ? -win[i][jw] : __ldg(fvec + idx) - win[i][jw];
           else
@@ -213,24 +230,55 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (xend_extra && yend_extra) store_dir(dx - 1, dy - 1, zz);
   };
 
+  // stage-Y identity: one column (x, field, plane slot) of the input box;
+  // the thread stages its own column of u into Ub (cp.async, Dirichlet and
+  // out-of-domain entries zero-filled) and later reads it back, so no
+  // barrier orders the staging
+  const bool ycol = t < WX * F * PB;
+  const int yx = t % WX, yf = (t / WX) % F, yb = t / (WX * F);
+  int rlo = 0, rhi = 0;  // rows [rlo, rhi) of the column lie inside the lattice, off its Dirichlet faces
+  const double* ybase = u;
+  {
+    const long long gxx = X0 - P + yx;
+    if (gxx > 0 && gxx < dx - 1) {
+      rlo = static_cast<int>(Y0 - P) < 1 ? static_cast<int>(1 - (Y0 - P)) : 0;
+      const long long rmax = dy - 1 - (Y0 - P);  // first row at or beyond the high face
+      rhi = rmax < WY ? static_cast<int>(rmax) : WY;
+      ybase = u + yf * ns + (Y0 - P + rlo) * dx + gxx;
+    }
+  }
+  double* ycolbuf = Ub + (yb * F + yf) * C::UB_F + yx;
+  auto stage_u = [&](int zb, int nb) {
+    if (!ycol || yb >= nb) return;
+    const int z = zb + yb;
+    const bool zd = (z == 0 && lo_dir) || (z == dz - 1 && hi_dir);
+    const double* src = ybase + z * dxy;
+    if (!zd && rlo == 0 && rhi == WY) {
+#pragma unroll
+      for (int r = 0; r < WY; ++r) cp_async8(ycolbuf + r * WX, src + r * dx, 8);
+    } else {
+#pragma unroll
+      for (int r = 0; r < WY; ++r) {
+        const bool ok = !zd && r >= rlo && r < rhi;
+        cp_async8(ycolbuf + r * WX, ok ? src + (r - rlo) * dx : u, ok ? 8 : 0);
+      }
+    }
+    cp_async_commit();
+  };
+  stage_u(z_first, z_last - z_first + 1 < PB ? z_last - z_first + 1 : PB);
+
   for (int zb = z_first; zb <= z_last; zb += PB) {
     const int nb = z_last - zb + 1 < PB ? z_last - zb + 1 : PB;
     // ---- Y: columns of u along y on the input box
-    if (t < WX * F * PB) {
-      const int x = t % WX, fb = t / WX;
-      const int f = fb % F, b = fb / F;
-      const long long z = zb + b;
-      const long long gxx = X0 - P + x;
-      if (b < nb) {
+    if (ycol && yb < nb) {
+      const int x = yx, f = yf, b = yb;
+      {
+        cp_async_wait_all();
         double v[WY];
-        const bool zd = (z == 0 && lo_dir) || (z == dz - 1 && hi_dir);
-        const bool xok = !zd && gxx > 0 && gxx < dx - 1;
-        const double* col = u + f * ns + z * dxy + gxx;
 #pragma unroll
-        for (int r = 0; r < WY; ++r) {
-          const long long yy = Y0 - P + r;
-          v[r] = (xok && yy > 0 && yy < dy - 1) ? __ldg(col + yy * dx) : 0.0;
-        }
+        for (int r = 0; r < WY; ++r) v[r] = ycolbuf[r * WX];
+        // this thread's column is consumed: stage the next batch's
+        if (zb + PB <= z_last) stage_u(zb + PB, z_last - zb - PB + 1 < PB ? z_last - zb - PB + 1 : PB);
         double* oa = Aa + (b * F + f) * C::AB_F + x;
         double* ob = Ab + (b * F + f) * C::AB_F + x;
         // element 0 is the halo cell: it reaches owned row 0 only
@@ -260,15 +308,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
     __syncthreads();
-    // ---- X: rows of a / b along x -> c, pre on the owned columns
-    if (t < OY * F * PB) {
-      const int r = t % OY, fb = t / OY;
+    // ---- X: half rows of a / b along x -> c, pre on the owned columns
+    if (t < C::XH * OY * F * PB) {
+      constexpr int HX = OX / C::XH;  // owned columns per half
+      const int h = t % C::XH, rfb = t / C::XH;
+      const int r = rfb % OY, fb = rfb / OY;
       const int f = fb % F, b = fb / F;
       if (b < nb) {
-        const double* ia = Aa + (b * F + f) * C::AB_F + r * C::XP;
-        const double* ib = Ab + (b * F + f) * C::AB_F + r * C::XP;
-        double* oc = Cc + (b * F + f) * C::CP_F + r * C::CPP;
-        double* op = Cp + (b * F + f) * C::CP_F + r * C::CPP;
+        const double* ia = Aa + (b * F + f) * C::AB_F + r * C::XP + h * HX;
+        const double* ib = Ab + (b * F + f) * C::AB_F + r * C::XP + h * HX;
+        double* oc = Cc + (b * F + f) * C::CP_F + r * C::CPP + h * HX;
+        double* op = Cp + (b * F + f) * C::CP_F + r * C::CPP + h * HX;
         double va[N], vb[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
@@ -282,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           cp = fma(sx, elem_last<N>(L.KrE, L.KrO, sa), sy * elem_last<N>(L.MrE, L.MrO, sb));
         }
 #pragma unroll
-        for (int e = 1; e <= OX / P; ++e) {
+        for (int e = 1; e <= HX / P; ++e) {
           va[0] = va[P];
           vb[0] = vb[P];
 #pragma unroll

@@ -53,6 +53,11 @@ int stmg_block_coefficients(int equation, int scheme, int k, double tau, int n_s
  * the shared positions (src/mesh.cpp:221-236). */
 int stmg_mesh_create(int dim, const double lo[3], const double hi[3], long long base_cells, int refinements,
                      const double* finest_vertices, stmg_mesh** out);
+/* box mesh with per-axis base cell counts (no reference counterpart: the
+ * weak-scaling study's 128^2 x 256 ... 256^3 meshes; the cube case is
+ * stmg_mesh_create) */
+int stmg_mesh_create_box(int dim, const double lo[3], const double hi[3], const long long base_cells[3],
+                         int refinements, const double* finest_vertices, stmg_mesh** out);
 void stmg_mesh_destroy(stmg_mesh* mesh);
 
 /* SpaceTimeOperator ctor (include/stmg/space_time_operator.hpp:34-36) with its
@@ -272,10 +277,22 @@ int stmg_perturbed_vertices(int dim, const double lo[3], const double hi[3], int
  * interface planes included on both sides). */
 typedef struct stmg_comm stmg_comm;
 typedef struct stmg_slab_multigrid stmg_slab_multigrid;
-/* NCCL unique id (128 bytes) for stmg_comm_create, on the root rank */
+/* NCCL unique id (128 bytes) for stmg_comm_create, on the root rank
+ * (the NCCL communicator: NVLink / NVSwitch between the GPUs of one box) */
 int stmg_nccl_unique_id(char id[128]);
 int stmg_comm_create(int world, int rank, const char id[128], stmg_comm** out);
 void stmg_comm_destroy(stmg_comm* c);
+/* Host-staged transport (no reference counterpart): the partition's
+ * interface exchanges and allreduces go through page-locked host buffers
+ * and these callbacks (e.g. torch.distributed over gloo). allreduce_sum sums
+ * n doubles in place over all ranks; sendrecv sends n doubles to rank peer
+ * and receives n doubles from it. Both return 0 on success. */
+typedef struct {
+  void* ctx;
+  int (*allreduce_sum)(void* ctx, double* h, long long n);
+  int (*sendrecv)(void* ctx, int peer, const double* h_send, double* h_recv, long long n);
+} stmg_host_transport;
+int stmg_comm_create_host(int world, int rank, const stmg_host_transport* transport, stmg_comm** out);
 /* host-only: how many levels of the default plan of (fine_mesh_level, p, k,
  * n_steps) stay partitioned for n_parts slabs of cells_z finest layers */
 int stmg_slab_plan(int scheme, int fine_mesh_level, int p, int k, int n_steps, long long cells_z, int n_parts,

@@ -47,18 +47,40 @@ def _dbl(a: Optional[np.ndarray]):
 
 
 class Mesh:
-    def __init__(self, dim: int, lo, hi, base_cells: int, refinements: int, vertices: Optional[np.ndarray] = None):
+    """MeshHierarchy of make_cartesian (mesh.cpp:148-187). base_cells is the
+    reference's cube count per axis, or a per-axis triple (x, y, z) for the
+    box meshes of the weak-scaling study (stmg_mesh_create_box)."""
+
+    def __init__(self, dim: int, lo, hi, base_cells, refinements: int, vertices: Optional[np.ndarray] = None):
         lib = N.load()
-        self.dim, self.base_cells, self.refinements = dim, base_cells, refinements
+        self.dim, self.refinements = dim, refinements
+        if np.ndim(base_cells) == 0:
+            self.base = (int(base_cells),) * 3
+        else:
+            self.base = tuple(int(c) for c in base_cells) + (1,) * (3 - len(base_cells))
+        self.base_cells = self.base[0]
         lo_a, lo_p = _dbl(np.asarray(lo, dtype=np.float64))
         hi_a, hi_p = _dbl(np.asarray(hi, dtype=np.float64))
         v = _dbl(vertices)
+        if v is not None and v[0].size != 3 * self.n_verts(refinements):
+            raise N.StmgInvalidArgument("Mesh: vertices must hold 3 doubles per finest-level vertex")
         h = C.c_void_p()
-        N.check(lib.stmg_mesh_create(dim, lo_p, hi_p, base_cells, refinements, v[1] if v else None, C.byref(h)))
+        if np.ndim(base_cells) == 0:
+            N.check(lib.stmg_mesh_create(dim, lo_p, hi_p, int(base_cells), refinements, v[1] if v else None,
+                                         C.byref(h)))
+        else:
+            bc = (C.c_longlong * 3)(*self.base)
+            N.check(lib.stmg_mesh_create_box(dim, lo_p, hi_p, bc, refinements, v[1] if v else None, C.byref(h)))
         self._h = h
 
+    def cells_axis(self, level: int):
+        return tuple((self.base[a] << level) if a < self.dim else 1 for a in range(3))
+
     def cells(self, level: int) -> int:
-        return (self.base_cells << level) ** self.dim
+        return int(np.prod(self.cells_axis(level)))
+
+    def n_verts(self, level: int) -> int:
+        return int(np.prod([c + 1 for c in self.cells_axis(level)[:self.dim]]))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -374,13 +396,54 @@ class SpaceTimeMultigrid:
 
 
 class Comm:
-    """NCCL communicator of the partitioned solve: rank 0 draws the unique id,
-    torch.distributed broadcasts it, every rank joins (stmg_comm_create)."""
+    """Communicator of the partitioned solve. Comm(world, rank, uid): NCCL
+    (rank 0 draws the unique id, torch.distributed broadcasts it, every rank
+    joins, stmg_comm_create). Comm.host(group): the host-staged transport
+    (stmg_comm_create_host) over a torch.distributed process group, e.g. gloo
+    -- interface planes and allreduces cross page-locked host memory."""
 
-    def __init__(self, world: int, rank: int, uid: bytes):
+    def __init__(self, world: int, rank: int, uid: Optional[bytes] = None, _handle=None):
+        if _handle is not None:
+            self._h, self.world, self.rank = _handle, world, rank
+            return
         h = C.c_void_p()
         N.check(N.load().stmg_comm_create(world, rank, uid, C.byref(h)))
         self._h, self.world, self.rank = h, world, rank
+
+    @classmethod
+    def host(cls, group=None) -> "Comm":
+        import torch
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+
+        def view(p, n):
+            return torch.from_numpy(np.ctypeslib.as_array(p, shape=(n,)))
+
+        def allreduce(ctx, h, n):
+            try:
+                dist.all_reduce(view(h, n), op=dist.ReduceOp.SUM, group=group)
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a C status
+                return 1
+
+        def sendrecv(ctx, peer, hs, hr, n):
+            try:
+                send = view(hs, n).clone()
+                recv = torch.empty(n, dtype=torch.float64)
+                reqs = [dist.isend(send, peer, group=group), dist.irecv(recv, peer, group=group)]
+                for q in reqs:
+                    q.wait()
+                view(hr, n).copy_(recv)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        t = N.HostTransport(None, N.HOST_ALLREDUCE(allreduce), N.HOST_SENDRECV(sendrecv))
+        h = C.c_void_p()
+        N.check(N.load().stmg_comm_create_host(world, rank, C.byref(t), C.byref(h)))
+        c = cls(world, rank, _handle=h)
+        c._transport = t  # the callbacks must outlive the communicator
+        return c
 
     @staticmethod
     def unique_id() -> bytes:

@@ -32,7 +32,7 @@ struct stmg_transfer {
   std::unique_ptr<Transfer> t;
 };
 struct stmg_comm {
-  std::unique_ptr<NcclComm> c;
+  std::unique_ptr<Comm> c;
 };
 struct stmg_slab_multigrid {
   std::unique_ptr<SlabMultigrid> mg;
@@ -133,6 +133,17 @@ int stmg_mesh_create(int dim, const double lo[3], const double hi[3], long long 
     *out = m.release();
   });
 }
+int stmg_mesh_create_box(int dim, const double lo[3], const double hi[3], const long long base_cells[3],
+                         int refinements, const double* finest_vertices, stmg_mesh** out) {
+  return guard_host([&] {
+    if (!out || !base_cells) throw std::invalid_argument("stmg_mesh_create_box: null argument");
+    auto m = std::make_unique<stmg_mesh>();
+    m->h = make_cartesian_box(dim, {lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]},
+                              {base_cells[0], base_cells[1], base_cells[2]}, refinements);
+    if (finest_vertices) set_finest_vertices(m->h, finest_vertices);
+    *out = m.release();
+  });
+}
 void stmg_mesh_destroy(stmg_mesh* mesh) { delete mesh; }
 
 int stmg_st_operator_create(const stmg_mesh* mesh, int mesh_level, int p, int equation, int scheme, int k, double tau,
@@ -167,9 +178,9 @@ int stmg_st_operator_apply_host(const stmg_st_operator* op, const double* h_u, d
       op->hu.allocate(bytes);
       op->hy.allocate(bytes);
     }
-    cuda_check(cudaMemcpy(op->hu.raw(), h_u, bytes, cudaMemcpyHostToDevice), "H2D");
+    copy_to_device(op->hu.d(), h_u, bytes, nullptr);
     op->op->apply(op->hu.d(), op->hy.d(), nullptr);
-    cuda_check(cudaMemcpy(h_y, op->hy.raw(), bytes, cudaMemcpyDeviceToHost), "D2H");
+    copy_to_host(h_y, op->hy.d(), bytes, nullptr);
   });
 }
 
@@ -377,9 +388,9 @@ int stmg_multigrid_apply_host(const stmg_multigrid* mg, const double* h_r, doubl
       mg->hr.allocate(bytes);
       mg->hz.allocate(bytes);
     }
-    cuda_check(cudaMemcpy(mg->hr.raw(), h_r, bytes, cudaMemcpyHostToDevice), "H2D");
+    copy_to_device(mg->hr.d(), h_r, bytes, nullptr);
     mg->mg->apply(mg->hr.d(), mg->hz.d(), nullptr);
-    cuda_check(cudaMemcpy(h_z, mg->hz.raw(), bytes, cudaMemcpyDeviceToHost), "D2H");
+    copy_to_host(h_z, mg->hz.d(), bytes, nullptr);
   });
 }
 int stmg_multigrid_smooth(const stmg_multigrid* mg, int level, const double* d_f, double* d_u, void* stream) {
@@ -485,11 +496,11 @@ int stmg_solve_host(const stmg_multigrid* mg, int precondition, const double* h_
     if (!mg || !h_b || !h_x) throw std::invalid_argument("stmg_solve_host: null argument");
     const size_t bytes = sizeof(double) * mg->mg->fine_operator().n_dofs();
     DeviceBuffer b(bytes), x(bytes);
-    cuda_check(cudaMemcpy(b.raw(), h_b, bytes, cudaMemcpyHostToDevice), "H2D b");
-    cuda_check(cudaMemcpy(x.raw(), h_x, bytes, cudaMemcpyHostToDevice), "H2D x");
+    copy_to_device(b.d(), h_b, bytes, nullptr);
+    copy_to_device(x.d(), h_x, bytes, nullptr);
     const int rc = stmg_solve(mg, precondition, b.d(), x.d(), options, result, history, history_cap, nullptr);
     if (rc != 0) throw std::runtime_error(g_err);
-    cuda_check(cudaMemcpy(h_x, x.raw(), bytes, cudaMemcpyDeviceToHost), "D2H x");
+    copy_to_host(h_x, x.d(), bytes, nullptr);
   });
 }
 
@@ -757,6 +768,18 @@ int stmg_comm_create(int world, int rank, const char id[128], stmg_comm** out) {
   });
 }
 void stmg_comm_destroy(stmg_comm* c) { delete c; }
+int stmg_comm_create_host(int world, int rank, const stmg_host_transport* transport, stmg_comm** out) {
+  return guard_host([&] {
+    if (!transport || !out) throw std::invalid_argument("stmg_comm_create_host: null argument");
+    HostTransport t;
+    t.ctx = transport->ctx;
+    t.allreduce_sum = transport->allreduce_sum;
+    t.sendrecv = transport->sendrecv;
+    auto c = std::make_unique<stmg_comm>();
+    c->c = std::make_unique<HostComm>(world, rank, t);
+    *out = c.release();
+  });
+}
 
 int stmg_slab_plan(int scheme, int fine_mesh_level, int p, int k, int n_steps, long long cells_z, int n_parts,
                    int* dist_levels, int* n_levels) {

@@ -440,15 +440,22 @@ void locate_point(const MeshLevel& m, const double x[3], Index& cell_out, double
 
 MeshHierarchy make_cartesian(int dim, std::array<double, 3> lo, std::array<double, 3> hi, Index base_cells,
                              int refinements) {
+  return make_cartesian_box(dim, lo, hi, {base_cells, base_cells, base_cells}, refinements);
+}
+
+MeshHierarchy make_cartesian_box(int dim, std::array<double, 3> lo, std::array<double, 3> hi,
+                                 std::array<Index, 3> base_cells, int refinements) {
   if (dim < 1 || dim > 3) throw std::invalid_argument("make_cartesian: dim must be 1, 2 or 3");
-  if (base_cells < 1 || refinements < 0) throw std::invalid_argument("make_cartesian: invalid sizes");
+  if (refinements < 0) throw std::invalid_argument("make_cartesian: invalid sizes");
+  for (int a = 0; a < dim; ++a)
+    if (base_cells[a] < 1) throw std::invalid_argument("make_cartesian: invalid sizes");
   MeshHierarchy h;
   for (int l = 0; l <= refinements; ++l) {
     MeshLevel m;
     m.dim = dim;
     m.lo = lo;
     m.hi = hi;
-    for (int a = 0; a < dim; ++a) m.cells[a] = base_cells << l;
+    for (int a = 0; a < dim; ++a) m.cells[a] = base_cells[a] << l;
     h.levels.push_back(m);
   }
   return h;

@@ -83,6 +83,10 @@ struct MeshHierarchy {
 };
 MeshHierarchy make_cartesian(int dim, std::array<double, 3> lo, std::array<double, 3> hi, Index base_cells,
                              int refinements);
+// per-axis base cell counts (box meshes of the weak-scaling study; the
+// reference's make_cartesian is the cube case)
+MeshHierarchy make_cartesian_box(int dim, std::array<double, 3> lo, std::array<double, 3> hi,
+                                 std::array<Index, 3> base_cells, int refinements);
 // Inject finest-level vertex positions; coarser levels take the positions of
 // the vertices they share with the finest level (src/mesh.cpp:221-236).
 void set_finest_vertices(MeshHierarchy& mesh, const double* xyz);

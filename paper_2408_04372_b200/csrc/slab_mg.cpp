@@ -61,7 +61,7 @@ std::string NcclComm::unique_id() {
   return std::string(id.internal, sizeof(id.internal));
 }
 
-NcclComm::NcclComm(int world, int rank, const std::string& id) : world_(world), rank_(rank) {
+NcclComm::NcclComm(int world, int rank, const std::string& id) : Comm(world, rank) {
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("NcclComm: bad world/rank");
   if (id.size() != sizeof(ncclUniqueId::internal)) throw std::invalid_argument("NcclComm: unique id must be 128 bytes");
   ncclUniqueId uid;
@@ -94,6 +94,53 @@ void NcclComm::exchange(const double* lo_send, double* lo_recv, const double* hi
     nccl_check(nccl().recv(hi_recv, n, ncclDouble, rank_ + 1, c, s), "recv");
   }
   nccl_check(nccl().group_end(), "group_end");
+}
+
+// ------------------------------------------------------------ host staged
+HostComm::HostComm(int world, int rank, const HostTransport& t) : Comm(world, rank), t_(t) {
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("HostComm: bad world/rank");
+  if (!t.allreduce_sum || !t.sendrecv) throw std::invalid_argument("HostComm: transport callbacks missing");
+}
+HostComm::~HostComm() {
+  if (buf_) cudaFreeHost(buf_);
+}
+double* HostComm::host(size_t n) const {
+  if (n > cap_) {
+    if (buf_) cudaFreeHost(buf_);
+    buf_ = nullptr;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&buf_), sizeof(double) * n, cudaHostAllocDefault),
+               "HostComm staging");
+    cap_ = n;
+  }
+  return buf_;
+}
+void HostComm::allreduce_sum(double* d, size_t n, cudaStream_t s) const {
+  if (world_ == 1 || n == 0) return;
+  double* h = host(n);
+  cuda_check(cudaMemcpyAsync(h, d, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "HostComm D2H");
+  cuda_check(cudaStreamSynchronize(s), "HostComm sync");
+  if (t_.allreduce_sum(t_.ctx, h, static_cast<long long>(n)) != 0)
+    throw std::runtime_error("HostComm: allreduce callback failed");
+  cuda_check(cudaMemcpyAsync(d, h, sizeof(double) * n, cudaMemcpyHostToDevice, s), "HostComm H2D");
+  cuda_check(cudaStreamSynchronize(s), "HostComm sync");
+}
+void HostComm::exchange(const double* lo_send, double* lo_recv, const double* hi_send, double* hi_recv, size_t n,
+                        bool lo, bool hi, cudaStream_t s) const {
+  if (world_ == 1 || (!lo && !hi)) return;
+  double* h = host(4 * n);
+  double *hls = h, *hlr = h + n, *hhs = h + 2 * n, *hhr = h + 3 * n;
+  if (lo) cuda_check(cudaMemcpyAsync(hls, lo_send, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "HostComm D2H");
+  if (hi) cuda_check(cudaMemcpyAsync(hhs, hi_send, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "HostComm D2H");
+  cuda_check(cudaStreamSynchronize(s), "HostComm sync");
+  // the lower neighbour first: rank r pairs its lo exchange with rank r-1's hi
+  // exchange, so the chain resolves from rank 0 upwards
+  if (lo && t_.sendrecv(t_.ctx, rank_ - 1, hls, hlr, static_cast<long long>(n)) != 0)
+    throw std::runtime_error("HostComm: sendrecv callback failed");
+  if (hi && t_.sendrecv(t_.ctx, rank_ + 1, hhs, hhr, static_cast<long long>(n)) != 0)
+    throw std::runtime_error("HostComm: sendrecv callback failed");
+  if (lo) cuda_check(cudaMemcpyAsync(lo_recv, hlr, sizeof(double) * n, cudaMemcpyHostToDevice, s), "HostComm H2D");
+  if (hi) cuda_check(cudaMemcpyAsync(hi_recv, hhr, sizeof(double) * n, cudaMemcpyHostToDevice, s), "HostComm H2D");
+  cuda_check(cudaStreamSynchronize(s), "HostComm sync");
 }
 
 // ------------------------------------------------------------------ plan
@@ -171,7 +218,7 @@ MeshHierarchy slab_hierarchy(const MeshHierarchy& g, int L, Index cz0, Index nz,
 
 SlabMultigrid::SlabMultigrid(Equation equation, TimeScheme scheme, const MeshHierarchy& global, const Coefficient& rho,
                              const std::vector<LevelSpec>& plan, const MultigridOptions& options, int n_parts,
-                             int first_part, int local_parts, const NcclComm* comm)
+                             int first_part, int local_parts, const Comm* comm)
     : options_(options), comm_(comm), global_(&global) {
   if (plan.empty()) throw std::invalid_argument("SlabMultigrid: empty plan");
   const int L = plan[0].mesh_level;
@@ -289,7 +336,7 @@ SlabMultigrid::SlabMultigrid(Equation equation, TimeScheme scheme, const MeshHie
     levels_[static_cast<size_t>(l)].omega = estimate_relaxation(l, options.seed + static_cast<std::uint64_t>(l));
   dots_.seg = levels_[0].seg;
   if (comm_ && comm_->world() > 1) {
-    const NcclComm* c = comm_;
+    const Comm* c = comm_;
     dots_.allreduce = [c](double* d, int k, cudaStream_t s) { c->allreduce_sum(d, static_cast<size_t>(k), s); };
   }
 }

@@ -32,28 +32,67 @@ namespace stmgb {
 // NCCL communicator, loaded at run time (dlopen "libnccl.so.2"), so the
 // library carries no link-time NCCL dependency and shares the copy torch has
 // already loaded.
-class NcclComm {
+// The data-path exchange of the partition: the interface-plane sum with the
+// neighbouring ranks and the dot-product / coarse-vector allreduce.
+class Comm {
+ public:
+  Comm(int world, int rank) : world_(world), rank_(rank) {}
+  virtual ~Comm() = default;
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  int world() const { return world_; }
+  int rank() const { return rank_; }
+  // in-place sum over ranks (device buffer, stream-ordered)
+  virtual void allreduce_sum(double* d, size_t n, cudaStream_t s) const = 0;
+  // grouped exchange with the neighbouring ranks: send lo_send to rank-1 and
+  // receive its data into lo_recv (if lo), same with rank+1 (if hi)
+  virtual void exchange(const double* lo_send, double* lo_recv, const double* hi_send, double* hi_recv, size_t n,
+                        bool lo, bool hi, cudaStream_t s) const = 0;
+
+ protected:
+  int world_, rank_;
+};
+
+// NCCL over NVLink / NVSwitch (libnccl.so.2 loaded at run time)
+class NcclComm : public Comm {
  public:
   static std::string unique_id();  // 128 bytes, on the root rank
   NcclComm(int world, int rank, const std::string& id);
-  ~NcclComm();
-  NcclComm(const NcclComm&) = delete;
-  NcclComm& operator=(const NcclComm&) = delete;
-  int world() const { return world_; }
-  int rank() const { return rank_; }
-  // in-place sum over ranks
-  void allreduce_sum(double* d, size_t n, cudaStream_t s) const;
-  // grouped exchange with the neighbouring ranks: send lo_send to rank-1 and
-  // receive its data into lo_recv (if lo), same with rank+1 (if hi)
+  ~NcclComm() override;
+  void allreduce_sum(double* d, size_t n, cudaStream_t s) const override;
   void exchange(const double* lo_send, double* lo_recv, const double* hi_send, double* hi_recv, size_t n, bool lo,
-                bool hi, cudaStream_t s) const;
+                bool hi, cudaStream_t s) const override;
 
  private:
-  int world_, rank_;
   void* comm_ = nullptr;
 };
 
-// partition of the level plan (host only, no GPU)
+// Host-staged transport: device buffers are copied to page-locked host
+// memory and handed to caller-supplied callbacks (e.g. torch.distributed over
+// gloo), then copied back. For ranks without a device-to-device path, and for
+// exercising the per-rank code path with several processes on one GPU.
+struct HostTransport {
+  void* ctx = nullptr;
+  // in-place sum over ranks of n host doubles; 0 on success
+  int (*allreduce_sum)(void* ctx, double* h, long long n) = nullptr;
+  // send n doubles to rank `peer` and receive n doubles from it; 0 on success
+  int (*sendrecv)(void* ctx, int peer, const double* h_send, double* h_recv, long long n) = nullptr;
+};
+class HostComm : public Comm {
+ public:
+  HostComm(int world, int rank, const HostTransport& t);
+  ~HostComm() override;
+  void allreduce_sum(double* d, size_t n, cudaStream_t s) const override;
+  void exchange(const double* lo_send, double* lo_recv, const double* hi_send, double* hi_recv, size_t n, bool lo,
+                bool hi, cudaStream_t s) const override;
+
+ private:
+  double* host(size_t n) const;
+  HostTransport t_;
+  mutable double* buf_ = nullptr;
+  mutable size_t cap_ = 0;
+};
+
 struct SlabPlan {
   int n_parts = 1;
   int dist_levels = 0;           // plan levels [0, dist_levels) are partitioned
@@ -69,7 +108,7 @@ class SlabMultigrid {
   // rank per block of local_parts consecutive parts
   SlabMultigrid(Equation equation, TimeScheme scheme, const MeshHierarchy& global, const Coefficient& rho,
                 const std::vector<LevelSpec>& plan, const MultigridOptions& options, int n_parts, int first_part,
-                int local_parts, const NcclComm* comm);
+                int local_parts, const Comm* comm);
   ~SlabMultigrid();
 
   int n_parts() const { return plan_.n_parts; }
@@ -138,7 +177,7 @@ class SlabMultigrid {
   std::vector<Part> parts_;
   std::vector<Level> levels_;  // the partitioned levels
   int n_levels_ = 0;
-  const NcclComm* comm_ = nullptr;
+  const Comm* comm_ = nullptr;
   std::unique_ptr<SpaceTimeMultigrid> tail_;
   const MeshHierarchy* global_ = nullptr;
   Index full_coarse_n_ = 0, full_coarse_nspace_ = 0;

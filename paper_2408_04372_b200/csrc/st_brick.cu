@@ -195,14 +195,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int j = 0; j < N; ++j) win[i][j] = 0.0;
 
   // store one output plane zz of the own fields (value v[i] per field)
+  // Dirichlet row: u (residual f - u); on a slab's low interface plane the
+  // row belongs to the slab below, this copy holds 0 (the interface sum adds it)
   auto store_dir = [&](long long x, long long yy, long long zz) {
+    const bool other = zz == 0 && !lo_dir;
 #pragma unroll
     for (int i = 0; i < FPG; ++i) {
       const int f = f0 + i;
       if (f >= F) break;
       const long long idx = f * ns + zz * dxy + yy * dx + x;
-      const double uv = __ldg(u + idx);
-      y[idx] = RES ? __ldg(fvec + idx) - uv : uv;
+      if (other) {
+        y[idx] = 0.0;
+      } else {
+        const double uv = __ldg(u + idx);
+        y[idx] = RES ? __ldg(fvec + idx) - uv : uv;
+      }
     }
   };
   auto store_plane = [&](long long zz, int jw) {

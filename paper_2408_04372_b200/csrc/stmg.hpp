@@ -23,6 +23,10 @@
 namespace stmgb {
 
 void cuda_check(cudaError_t e, const char* what);
+// host <-> device copies of the host-buffer entry points (host_xfer.cpp):
+// pinned-chunk pipeline with parallel host copies; synchronous on return
+void copy_to_device(double* d_dst, const double* h_src, size_t bytes, cudaStream_t s);
+void copy_to_host(double* h_dst, const double* d_src, size_t bytes, cudaStream_t s);
 
 // owning device buffer of doubles (or raw bytes)
 class DeviceBuffer {

@@ -50,6 +50,13 @@ class RunReport(C.Structure):
 
 
 LINEAR_MAP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, c_double_p, C.c_longlong)
+HOST_SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, c_double_p, c_double_p, C.c_longlong)
+
+
+class HostTransport(C.Structure):
+    """stmg_host_transport: callbacks of the host-staged communicator."""
+    _fields_ = [("ctx", C.c_void_p), ("allreduce_sum", HOST_ALLREDUCE), ("sendrecv", HOST_SENDRECV)]
 
 # (name, restype, argtypes): every symbol declared in include/stmg_b200.h
 SIGNATURES = [
@@ -59,6 +66,8 @@ SIGNATURES = [
     ("stmg_quadrature", C.c_int, [C.c_int, C.c_int, c_double_p, c_double_p]),
     ("stmg_temporal_weights", C.c_int, [C.c_int, C.c_int, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     ("stmg_block_coefficients", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, c_double_p, c_double_p]),
+    ("stmg_mesh_create_box", C.c_int, [C.c_int, c_double_p, c_double_p, c_ll_p, C.c_int, c_double_p,
+                                       C.c_void_p]),
     ("stmg_mesh_create", C.c_int, [C.c_int, c_double_p, c_double_p, C.c_longlong, C.c_int, c_double_p,
                                    C.c_void_p]),
     ("stmg_mesh_destroy", None, [C.c_void_p]),
@@ -128,6 +137,7 @@ SIGNATURES = [
                                           C.c_ulonglong, c_double_p]),
     ("stmg_comm_create", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_void_p]),
     ("stmg_comm_destroy", None, [C.c_void_p]),
+    ("stmg_comm_create_host", C.c_int, [C.c_int, C.c_int, C.POINTER(HostTransport), C.c_void_p]),
     ("stmg_slab_plan", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_int, c_int_p,
                                  c_int_p]),
     ("stmg_slab_multigrid_create", C.c_int, [C.c_int, C.c_int, C.c_void_p, c_double_p, C.c_int, C.c_int, C.c_int,

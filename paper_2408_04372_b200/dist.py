@@ -1,11 +1,10 @@
 """Multi-GPU plumbing for the STMG path (one process per GPU, torch.distributed).
 
-Round 1 runs independent slab replicas per rank ("replicas only", DESIGN.md
-section 7): there is no data-path collective; NCCL is used only to take the
-max over ranks of the device-timed step. The z-slab partition of SURVEY.md
-§8e (each rank owns a contiguous range of cell layers; the interface dof
-plane is owned by the lower rank) is described by `slab_partition`, which the
-sharded operator will use.
+The partitioned solve (csrc/slab_mg.cpp): the finest
+mesh is cut into z-slabs, one per rank; NCCL (or the host-staged transport,
+api.Comm.host) carries the interface-plane sums and the dot-product /
+coarse-vector allreduces. Here: the rank environment, the slab bookkeeping,
+the weak-scaling meshes of the C5 study and max-over-ranks timing helpers.
 """
 from __future__ import annotations
 
@@ -15,6 +14,14 @@ from typing import Tuple
 def env_rank() -> Tuple[int, int, int]:
     import os
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def weak_box(n_gpus: int) -> Tuple[int, int, int]:
+    """Base cells per axis of the C5 weak-scaling mesh for n_gpus GPUs, each
+    rank holding one 128^3 block after 7 refinements (128^3 on
+    1 GPU -> 256^3 on 8): 1 -> 1x1x1, 2 -> 1x1x2, 4 -> 1x2x2, 8 -> 2x2x2,
+    otherwise 1x1xN (z-slabs of 128 layers)."""
+    return {1: (1, 1, 1), 2: (1, 1, 2), 4: (1, 2, 2), 8: (2, 2, 2)}.get(n_gpus, (1, 1, n_gpus))
 
 
 def slab_partition(n_cell_layers: int, world: int, rank: int, p: int) -> dict:

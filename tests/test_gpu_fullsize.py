@@ -1,0 +1,57 @@
+"""Full-size vmult parity (SpaceTimeOperator::apply, space_time_operator.cpp:
+45-130) at the BASELINE sizes C2 (64^3), C3 (128^3), C4 (96^3) and C5-128,
+against fingerprints of the reference's own output on the same seeded input
+(tests/golden/fullsize_<cfg>.npz, written by tests/golden/make_fullsize.py
+from the compiled reference). The 4.3 GB outputs cannot be committed, so the
+GPU output is reduced the same way and compared:
+  * 4096 block dot products with seeded random signs (first-order sensitive
+    to a local error anywhere) and 4096 block norms: relative <= 1e-12
+    against the block norm (signed dots) / 1e-12 (norms),
+  * 20000 seeded sample entries: relative L2 <= 1e-12,
+  * the global norm: <= 1e-13.
+The north_star bar is relative L2 <= 1e-12."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2408_04372_b200 import api, problems
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+BLOCKS = 4096
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5-128"])
+def test_fullsize_vmult_fingerprint(cuda, name):
+    path = os.path.join(GOLDEN, f"fullsize_{name}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing fixture {path} (tests/golden/make_fullsize.py)")
+    fx = np.load(path)
+    cfg = problems.config(name)
+    mesh = api.Mesh(cfg.dim, (0, 0, 0), (1, 1, 1), cfg.base_cells, cfg.refinements, cfg.vertices())
+    op = api.SpaceTimeOperator(mesh, cfg.refinements, cfg.p, cfg.equation, cfg.scheme, cfg.k, cfg.tau, cfg.n_steps,
+                               cfg.rho)
+    n = op.n_dofs
+    assert n == int(fx["n_dofs"])
+    u = cuda.from_numpy(problems.uniform_vector(n, seed=42)).cuda()
+    y = op.apply(u)
+    del u
+    s = cuda.from_numpy(np.random.default_rng(99).integers(0, 2, n, dtype=np.int8) * 2 - 1).cuda()
+    b = (n * np.arange(BLOCKS + 1, dtype=np.int64)) // BLOCKS
+    seg = cuda.from_numpy(np.repeat(np.arange(BLOCKS), np.diff(b))).cuda()
+    dots = cuda.zeros(BLOCKS, dtype=cuda.float64, device="cuda").index_add_(0, seg, y * s)
+    norms = cuda.zeros(BLOCKS, dtype=cuda.float64, device="cuda").index_add_(0, seg, y * y).sqrt()
+    del s, seg
+    dots, norms = dots.cpu().numpy(), norms.cpu().numpy()
+    ref_norms = fx["block_norm"]
+    assert np.max(np.abs(dots - fx["block_dot"]) / ref_norms) <= 1e-12
+    assert np.max(np.abs(norms - ref_norms) / ref_norms) <= 1e-12
+    idx = cuda.from_numpy(fx["sample_idx"]).cuda()
+    got = y[idx].cpu().numpy()
+    want = fx["sample_val"]
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-12
+    assert abs(float(y.norm()) - float(fx["norm"])) <= 1e-13 * float(fx["norm"])
+    del y
+    cuda.cuda.empty_cache()

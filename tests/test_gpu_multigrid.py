@@ -92,7 +92,10 @@ def test_vcycle_matches_reference(cuda, ref, name, r):
     assert _rel(got, R.vcycle(res)) <= 1e-9
 
 
-@pytest.mark.parametrize("name,r", [("C1", None), ("C2", 1), ("C2", 2), ("C3", 1), ("C5-4", None), ("C5-8", None)])
+# up to the edge of the oracle's reach: C2 16^3, C3 32^3,
+# C4 6^3 (the wave system solved directly, not only through march), C5 8^3
+@pytest.mark.parametrize("name,r", [("C1", None), ("C2", 1), ("C2", 2), ("C3", 1), ("C3", 2), ("C4", 0), ("C4", 1),
+                                    ("C5-4", None), ("C5-8", None)])
 def test_gmres_solve_matches_reference(cuda, ref, name, r):
     """STMG-preconditioned GMRES on the manufactured slab RHS: iteration
     count within +-1 and solution relative difference <= 1e-8."""

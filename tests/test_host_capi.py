@@ -109,3 +109,14 @@ def test_invalid_arguments_return_codes():
         N.check(-1)
     with pytest.raises(N.StmgError):
         N.check(-2)
+
+
+def test_reference_side_binding_links():
+    """oracle/b200_backend.cpp (INTEGRATION.md's LinearMap adapter) compiles
+    against the reference headers and links the reference's objects with
+    libstmg_b200.so; GPU runs are in tests/test_gpu_ref_binding.py."""
+    path = os.path.join(ROOT, "oracle", "_ref", "libb200_backend.so")
+    if not os.path.exists(path):
+        refbind.build()
+    lib = C.CDLL(path)
+    assert hasattr(lib, "b200_backend_gmres") and hasattr(lib, "b200_backend_last_error")

@@ -59,7 +59,13 @@ struct Cfg {
   static constexpr int OY = FG == 1 ? 16 : 8;        // owned nodes per tile (y)
   static constexpr int TX = OX / P, TY = OY / P;     // cells per tile
   static constexpr int WX = OX + P + 1, WY = OY + P + 1;  // input box
-  static constexpr int PB = F > 4 ? 1 : (F > 2 ? 2 : 4);  // planes per batch
+#ifndef STB_PB4
+#define STB_PB4 2
+#endif
+#ifndef STB_MINB
+#define STB_MINB 2
+#endif
+  static constexpr int PB = F > 4 ? 1 : (F > 2 ? STB_PB4 : 2);  // planes per batch
   static constexpr int XP = WX;                      // AB row pitch (odd: conflict-free rows)
   static constexpr int CPP = OX + 1;                 // CP row pitch
   // block strides padded to WX (mod 16): the stage-Y threads t = x + WX * block
@@ -143,7 +149,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <int N, int F, bool RES>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, STB_MINB)
     st_brick_kernel(const __grid_constant__ DevLevel L, const double* __restrict__ u, const double* __restrict__ fvec,
                     double* __restrict__ y, int ntx, int zc) {
   using C = Cfg<N, F>;
@@ -212,6 +218,20 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   };
+  // residual: pull the f entries of layer e's owned planes towards L2 when
+  // the layer opens; they are read when it closes, p planes later
+  auto prefetch_layer = [&](int e) {
+    if (!RES || !on_lat || e < L0) return;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const long long base = f0 * ns + static_cast<long long>(e * P + q) * dxy + pbase;
+#pragma unroll
+      for (int i = 0; i < FPG; ++i) {
+        if (f0 + i >= F) break;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(fvec + base + i * ns));
+      }
+    }
+  };
   auto store_plane = [&](long long zz, int jw) {
     const bool zdir = (zz == 0 && lo_dir) || (zz == dz - 1 && hi_dir);
     if (on_lat) {
@@ -273,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     cp_async_commit();
   };
   stage_u(z_first, z_last - z_first + 1 < PB ? z_last - z_first + 1 : PB);
+  prefetch_layer(Ls);
 
   for (int zb = z_first; zb <= z_last; zb += PB) {
     const int nb = z_last - zb + 1 < PB ? z_last - zb + 1 : PB;
@@ -281,14 +302,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int x = yx, f = yf, b = yb;
       {
         cp_async_wait_all();
-        double v[WY];
-#pragma unroll
-        for (int r = 0; r < WY; ++r) v[r] = ycolbuf[r * WX];
-        // this thread's column is consumed: stage the next batch's
-        if (zb + PB <= z_last) stage_u(zb + PB, z_last - zb - PB + 1 < PB ? z_last - zb - PB + 1 : PB);
+        // this thread's column is consumed element by element below; the next
+        // batch's column is staged once the last element has been read
         double* oa = Aa + (b * F + f) * C::AB_F + x;
         double* ob = Ab + (b * F + f) * C::AB_F + x;
         // element 0 is the halo cell: it reaches owned row 0 only
+        double v[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = ycolbuf[k * WX];
         double ca, cb;
         {
           const Split<N> s = split_at<N>(v);
@@ -297,7 +318,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
 #pragma unroll
         for (int e = 1; e <= OY / P; ++e) {
-          const Split<N> s = split_at<N>(v + e * P);
+          v[0] = v[P];
+#pragma unroll
+          for (int k = 1; k < N; ++k) v[k] = ycolbuf[(e * P + k) * WX];
+          if (e == OY / P && zb + PB <= z_last)
+            stage_u(zb + PB, z_last - zb - PB + 1 < PB ? z_last - zb - PB + 1 : PB);
+          const Split<N> s = split_at<N>(v);
           double ea[N], eb[N];
           elem<N>(L.MrE, L.MrO, s, ea);
           elem<N>(L.KrE, L.KrO, s, eb);
@@ -420,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int q = 1; q < N; ++q) win[i][q] = 0.0;
         }
+        if (z < z_last) prefetch_layer(e_of);
       }
       if (z < z_last) add_layer(e_of, j);
     }

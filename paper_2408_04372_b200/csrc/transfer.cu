@@ -510,6 +510,363 @@ void xy_pass(int F, const PassArgs& A, const DevAxisTransfer& Tx, const DevAxisT
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused 3D h-transfers (equal p on all three axes): one kernel per transfer,
+// no HBM intermediate. A CTA owns a tile of TCX x TCY coarse cells and
+// marches a chunk of coarse cell layers along z, one fine plane at a time:
+//   restriction: the fine plane tile (plus the left neighbour cell in x and
+//     y) is staged by cp.async one plane ahead, the x and y passes run in
+//     shared memory (as xy_cell_kernel), and each y-pass thread accumulates
+//     its coarse (x, y) nodes into a z window of the p + 1 coarse planes of
+//     the open coarse layer held in registers; when the layer closes its p
+//     lower planes are final and stored. The chunk starts one coarse layer
+//     early (its contribution to the chunk's first coarse plane).
+//   prolongation: the p + 1 coarse planes of the open coarse layer are
+//     staged; every fine plane is the z combination of them, then the x and
+//     y passes, added into the fine vector.
+// Masks, slab options and field strides are those of the separable passes
+// (input masked as the first pass, output as the last).
+constexpr int kZT = 256, kZCX = 8, kZCY = 8;
+
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(ok ? src : nullptr), "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <int P>
+struct ZCfg {
+  static constexpr int LX = 2 * P * (kZCX + 1) + 1, LY = 2 * P * (kZCY + 1) + 1;  // fine tile + left cells
+  static constexpr int LXP = LX | 1;                 // odd row pitch
+  static constexpr int MX = kZCX * P + 1;            // coarse x nodes of the tile (+ right edge)
+  static constexpr int MXP = MX | 1;
+  static constexpr int YI = kZCX * P * kZCY;         // y-pass items: (coarse x node, coarse y cell)
+  static constexpr size_t r_smem() { return sizeof(double) * (2 * static_cast<size_t>(LY) * LXP + LY * MXP); }
+  // prolongation: coarse tile (P + 1 planes), z-combined plane, x-pass output
+  static constexpr int CX = kZCX * P + 1, CY = kZCY * P + 1, CXP = CX | 1;
+  static constexpr int FX = 2 * P * kZCX + 1, FXP = FX | 1;  // fine x nodes of the tile (+ right edge)
+  static constexpr size_t p_smem() {
+    return sizeof(double) * (static_cast<size_t>(P + 1) * CY * CXP + CY * CXP + static_cast<size_t>(CY) * FXP);
+  }
+};
+
+template <int P>
+__global__ void __launch_bounds__(kZT, 2) xyz_restrict_kernel(const PassArgs A, const DevAxisTransfer Tx,
+                                                           const DevAxisTransfer Ty, const DevAxisTransfer Tz,
+                                                           const double* __restrict__ in, double* __restrict__ out,
+                                                           int ntx, int nch, int zc) {
+  using C = ZCfg<P>;
+  extern __shared__ __align__(16) double sm[];
+  double* R0[2] = {sm, sm + C::LY * C::LXP};
+  double* R1 = sm + 2 * C::LY * C::LXP;
+  const long long ix = A.i[0], iy = A.i[1], iz = A.i[2], ox = A.o[0], oy = A.o[1];
+  const int ncx = static_cast<int>((ox - 1) / P), ncy = static_cast<int>((oy - 1) / P),
+            ncz = static_cast<int>((A.o[2] - 1) / P);
+  const int tile = blockIdx.x, f = blockIdx.y / nch, ch = blockIdx.y - (blockIdx.y / nch) * nch;
+  const int cx0 = (tile % ntx) * kZCX, cy0 = (tile / ntx) * kZCY;
+  const int C0 = ch * zc, C1 = C0 + zc < ncz ? C0 + zc : ncz;
+  const int zf0 = 2 * P * (C0 > 0 ? C0 - 1 : 0), zf1 = 2 * P * C1 - 1;  // + the top plane if C1 == ncz
+  const int zf_end = C1 == ncz ? zf1 + 1 : zf1;
+  const int t = threadIdx.x;
+  const long long gx0 = 2LL * P * (cx0 - 1), gy0 = 2LL * P * (cy0 - 1);
+  const double* src_f = in + f * A.fs_in;
+  // stage fine plane zf of the tile region (input masks; left-of-domain zero)
+  auto stage = [&](int zf, double* dst) {
+    // warp w stages rows w, w + 8, ...; lanes run along x (one row base per row)
+    const bool plane0 = (A.mask_in && on_bdry_z(zf, iz, A.zbc)) || (A.skip_lo_in && zf == 0);
+    const double* src = src_f + static_cast<long long>(zf) * iy * ix;
+    const int lane = t & 31, w = t >> 5;
+    for (int ly = w; ly < C::LY; ly += kZT / 32) {
+      const long long gy = gy0 + ly;
+      const bool rok = !plane0 && gy >= 0 && gy < iy && !(A.mask_in && on_bdry(gy, iy));
+      const double* rs = src + gy * ix;
+      double* rd = dst + ly * C::LXP;
+#pragma unroll
+      for (int k = 0; k < (C::LX + 31) / 32; ++k) {
+        const int lx = lane + 32 * k;
+        if (lx < C::LX) {
+          const long long gx = gx0 + lx;
+          const bool ok = rok && gx >= 0 && gx < ix && !(A.mask_in && on_bdry(gx, ix));
+          cp8(rd + lx, rs + gx, ok);
+        }
+      }
+    }
+    cp_commit();
+  };
+  // y-pass identity: coarse x node lxn of the tile, coarse y cell lcy
+  const int lxn = t % (kZCX * P), lcy = t / (kZCX * P);
+  const bool yitem = t < C::YI;
+  const long long gxc = static_cast<long long>(cx0) * P + lxn;
+  const bool xin = gxc < ox - 1;  // the last coarse x node is a boundary node (zero)
+  const int cyg = cy0 + lcy;
+  const bool yin = cyg < ncy;
+  double win[P][P + 1];
+#pragma unroll
+  for (int a = 0; a < P; ++a)
+#pragma unroll
+    for (int j = 0; j <= P; ++j) win[a][j] = 0.0;
+  double* dst_f = out + f * A.fs_out;
+  auto store_layer = [&](int cz, int nj) {  // coarse planes cz*P + j, j < nj
+    if (yitem && xin && yin) {
+#pragma unroll
+      for (int j = 0; j <= P; ++j) {
+        if (j >= nj) break;
+        const long long zc_ = static_cast<long long>(cz) * P + j;
+        const bool pz = A.mask_out && on_bdry_z(zc_, A.o[2], A.zbc);
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+          const long long gy = static_cast<long long>(cyg) * P + a;
+          double v = win[a][j];
+          if (pz || (A.mask_out && (gy == 0 || gxc == 0))) v = 0.0;
+          double* o = dst_f + (zc_ * oy + gy) * ox + gxc;
+          if (A.accumulate) *o += v; else *o = v;
+        }
+      }
+    }
+    // the last coarse x column / y row of the lattice (boundary nodes): zero
+    if (!A.accumulate) {
+      const bool last_x = cx0 + kZCX >= ncx, last_y = cy0 + kZCY >= ncy;
+      for (int j = 0; j < nj; ++j) {
+        const long long zc_ = static_cast<long long>(cz) * P + j;
+        double* pl = dst_f + zc_ * oy * ox;
+        if (last_x && t < kZCY * P + 1) {
+          const long long gy = static_cast<long long>(cy0) * P + t;
+          if (gy < oy) pl[gy * ox + ox - 1] = 0.0;
+        }
+        if (last_y && t < kZCX * P + 1) {
+          const long long gx = static_cast<long long>(cx0) * P + t;
+          if (gx < ox) pl[(oy - 1) * ox + gx] = 0.0;
+        }
+      }
+    }
+  };
+  stage(zf0, R0[0]);
+  for (int zf = zf0; zf <= zf_end; ++zf) {
+    const int buf = (zf - zf0) & 1;
+    cp_wait_all();
+    __syncthreads();  // plane zf staged; the previous plane's R1 readers are done
+    if (zf + 1 <= zf_end) stage(zf + 1, R0[buf ^ 1]);
+    const double* R = R0[buf];
+    // ---- x pass: (fine row ly, coarse cell lc) -> coarse x nodes lc*P + jj
+    for (int e = t; e < C::LY * kZCX; e += kZT) {
+      const int lc = e / C::LY, ly = e - lc * C::LY;
+      const double* row = R + ly * C::LXP;
+      double fv[2 * P + 1], lv[2 * P];
+#pragma unroll
+      for (int r = 0; r <= 2 * P; ++r) fv[r] = row[2 * P * (lc + 1) + r];
+#pragma unroll
+      for (int r = 0; r < 2 * P; ++r) lv[r] = row[2 * P * lc + r];
+#pragma unroll
+      for (int jj = 0; jj < P; ++jj) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r <= 2 * P; ++r) s = fma(Tx.hw[r][jj], fv[r], s);
+        if (jj == 0) {
+#pragma unroll
+          for (int r = 0; r < 2 * P; ++r) s = fma(Tx.hw[r][P], lv[r], s);
+        }
+        R1[ly * C::MXP + lc * P + jj] = s;
+      }
+    }
+    __syncthreads();
+    // ---- y pass + z window
+    const bool top = zf == 2 * P * ncz;  // the lattice's top fine plane: r = 2P of the last layer
+    const int cz = top ? ncz - 1 : zf / (2 * P), r = top ? 2 * P : zf - 2 * P * (zf / (2 * P));
+    if (r == 0 && zf > zf0) {
+      // fine vertex plane: coarse layer cz - 1 closes
+      if (cz - 1 >= C0) store_layer(cz - 1, P);
+#pragma unroll
+      for (int a = 0; a < P; ++a) {
+        win[a][0] = win[a][P];
+#pragma unroll
+        for (int j = 1; j <= P; ++j) win[a][j] = 0.0;
+      }
+    }
+    if (yitem) {
+      double fv[2 * P + 1], lv[2 * P];
+#pragma unroll
+      for (int rr = 0; rr <= 2 * P; ++rr) fv[rr] = R1[(2 * P * (lcy + 1) + rr) * C::MXP + lxn];
+#pragma unroll
+      for (int rr = 0; rr < 2 * P; ++rr) lv[rr] = R1[(2 * P * lcy + rr) * C::MXP + lxn];
+      double wz[P + 1];
+#pragma unroll
+      for (int j = 0; j <= P; ++j) wz[j] = Tz.hw[r][j];
+#pragma unroll
+      for (int a = 0; a < P; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int rr = 0; rr <= 2 * P; ++rr) s = fma(Ty.hw[rr][a], fv[rr], s);
+        if (a == 0) {
+#pragma unroll
+          for (int rr = 0; rr < 2 * P; ++rr) s = fma(Ty.hw[rr][P], lv[rr], s);
+        }
+#pragma unroll
+        for (int j = 0; j <= P; ++j) win[a][j] = fma(wz[j], s, win[a][j]);
+      }
+    }
+  }
+  // close the chunk's last layer; the top coarse plane too on the last chunk
+  store_layer(C1 - 1, C1 == ncz ? P + 1 : P);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kZT, 2) xyz_prolong_kernel(const PassArgs A, const DevAxisTransfer Tx,
+                                                          const DevAxisTransfer Ty, const DevAxisTransfer Tz,
+                                                          const double* __restrict__ in, double* __restrict__ out,
+                                                          int ntx, int nch, int zc) {
+  using C = ZCfg<P>;
+  extern __shared__ __align__(16) double sm[];
+  double* Cb = sm;                                   // [P+1][CY][CXP] coarse planes of the open layer
+  double* Zp = Cb + (P + 1) * C::CY * C::CXP;        // [CY][CXP] z-combined plane
+  double* R1 = Zp + C::CY * C::CXP;                  // [CY][FXP] after the x pass
+  const long long ix = A.i[0], iy = A.i[1], iz = A.i[2], ox = A.o[0], oy = A.o[1], oz = A.o[2];
+  const int ncx = static_cast<int>((ix - 1) / P), ncy = static_cast<int>((iy - 1) / P),
+            ncz = static_cast<int>((iz - 1) / P);
+  const int tile = blockIdx.x, f = blockIdx.y / nch, ch = blockIdx.y - (blockIdx.y / nch) * nch;
+  const int cx0 = (tile % ntx) * kZCX, cy0 = (tile / ntx) * kZCY;
+  const int C0 = ch * zc, C1 = C0 + zc < ncz ? C0 + zc : ncz;
+  const int t = threadIdx.x;
+  const double* src_f = in + f * A.fs_in;
+  double* dst_f = out + f * A.fs_out;
+  const long long cgx0 = static_cast<long long>(cx0) * P, cgy0 = static_cast<long long>(cy0) * P;
+  auto stage_layer = [&](int cz) {
+    for (int e = t; e < (P + 1) * C::CY * C::CX; e += kZT) {
+      const int j = e / (C::CY * C::CX), rem = e - j * (C::CY * C::CX);
+      const int ly = rem / C::CX, lx = rem - ly * C::CX;
+      const long long gx = cgx0 + lx, gy = cgy0 + ly, gz = static_cast<long long>(cz) * P + j;
+      const bool ok = gx < ix && gy < iy &&
+                      !(A.mask_in && (on_bdry(gx, ix) || on_bdry(gy, iy) || on_bdry_z(gz, iz, A.zbc))) &&
+                      !(A.skip_lo_in && gz == 0);
+      cp8(Cb + (j * C::CY + ly) * C::CXP + lx, src_f + (gz * iy + gy) * ix + gx, ok);
+    }
+    cp_commit();
+  };
+  const int zf_last = C1 == ncz ? 2 * P * C1 : 2 * P * C1 - 1;
+  int open = -1;
+  for (int zf = 2 * P * C0; zf <= zf_last; ++zf) {
+    const bool top = zf == 2 * P * ncz;
+    const int cz = top ? ncz - 1 : zf / (2 * P), r = top ? 2 * P : zf - 2 * P * (zf / (2 * P));
+    if (cz != open) {
+      __syncthreads();  // the previous layer's readers are done
+      stage_layer(cz);
+      cp_wait_all();
+      open = cz;
+    }
+    __syncthreads();
+    // ---- z combination of the layer's coarse planes at fine z index r
+    for (int e = t; e < C::CY * C::CX; e += kZT) {
+      const int ly = e / C::CX, lx = e - ly * C::CX;
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j <= P; ++j) s = fma(Tz.hw[r][j], Cb[(j * C::CY + ly) * C::CXP + lx], s);
+      Zp[ly * C::CXP + lx] = s;
+    }
+    __syncthreads();
+    // ---- x pass: (coarse row ly, coarse cell lc) -> fine x nodes 2P lc + rr
+    for (int e = t; e < C::CY * kZCX; e += kZT) {
+      const int lc = e / C::CY, ly = e - lc * C::CY;
+      if (cx0 + lc >= ncx) continue;
+      const double* row = Zp + ly * C::CXP + lc * P;
+      double cv[P + 1];
+#pragma unroll
+      for (int j = 0; j <= P; ++j) cv[j] = row[j];
+#pragma unroll
+      for (int rr = 0; rr <= 2 * P; ++rr) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) s = fma(Tx.hw[rr][j], cv[j], s);
+        R1[ly * C::FXP + 2 * P * lc + rr] = s;  // rr = 2P: the next cell's rr = 0 (same value)
+      }
+    }
+    __syncthreads();
+    // ---- y pass: (fine x column lx, coarse y cell lc) -> fine rows, masked add
+    const bool plane_out0 = A.mask_out && on_bdry_z(zf, oz, A.zbc);
+    double* dst = dst_f + static_cast<long long>(zf) * oy * ox;
+    for (int e = t; e < C::FX * kZCY; e += kZT) {
+      const int lc = e / C::FX, lx = e - lc * C::FX;
+      const long long c = cy0 + lc, gx = 2LL * P * cx0 + lx;
+      if (c >= ncy || gx >= ox) continue;
+      if (lx == 2 * P * kZCX && gx != ox - 1) continue;  // the next tile's first column
+      double cv[P + 1];
+#pragma unroll
+      for (int j = 0; j <= P; ++j) cv[j] = R1[(lc * P + j) * C::FXP + lx];
+      const bool col0 = plane_out0 || (A.mask_out && on_bdry(gx, ox));
+      const int rmax = c == ncy - 1 ? 2 * P : 2 * P - 1;
+      double old[2 * P + 1];
+#pragma unroll
+      for (int rr = 0; rr <= 2 * P; ++rr) old[rr] = (A.accumulate && rr <= rmax) ? dst[(2 * P * c + rr) * ox + gx] : 0.0;
+#pragma unroll
+      for (int rr = 0; rr <= 2 * P; ++rr) {
+        if (rr > rmax) break;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) s = fma(Ty.hw[rr][j], cv[j], s);
+        const long long gy = 2 * P * c + rr;
+        if (col0 || (A.mask_out && on_bdry(gy, oy))) s = 0.0;
+        dst[gy * ox + gx] = old[rr] + s;
+      }
+    }
+  }
+}
+
+template <int P>
+void launch_xyz(int F, const PassArgs& A, const DevAxisTransfer* ax, bool prolong, const double* in, double* out,
+                cudaStream_t s) {
+  using C = ZCfg<P>;
+  const long long ncx = prolong ? (A.i[0] - 1) / P : (A.o[0] - 1) / P;
+  const long long ncy = prolong ? (A.i[1] - 1) / P : (A.o[1] - 1) / P;
+  const long long ncz = prolong ? (A.i[2] - 1) / P : (A.o[2] - 1) / P;
+  const long long ntx = (ncx + kZCX - 1) / kZCX, nty = (ncy + kZCY - 1) / kZCY;
+  const long long tiles = ntx * nty;
+  // ~8 CTAs per SM-slot; restriction chunks of >= 4 coarse layers (halo layer)
+  long long nch = std::max<long long>(1, (148LL * 3 * 8 + tiles * F - 1) / (tiles * F));
+  nch = std::min<long long>(nch, std::max<long long>(1, prolong ? ncz : ncz / 4));
+  const long long zc = (ncz + nch - 1) / nch;
+  nch = (ncz + zc - 1) / zc;
+  const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(F * nch));
+  count_launch();
+  if (prolong) {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(xyz_prolong_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(C::p_smem()));
+      configured = true;
+    }
+    xyz_prolong_kernel<P><<<grid, kZT, C::p_smem(), s>>>(A, ax[0], ax[1], ax[2], in, out, static_cast<int>(ntx),
+                                                          static_cast<int>(nch), static_cast<int>(zc));
+  } else {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(xyz_restrict_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(C::r_smem()));
+      configured = true;
+    }
+    xyz_restrict_kernel<P><<<grid, kZT, C::r_smem(), s>>>(A, ax[0], ax[1], ax[2], in, out, static_cast<int>(ntx),
+                                                           static_cast<int>(nch), static_cast<int>(zc));
+  }
+}
+
+bool xyz_pass(int F, const PassArgs& A, const DevAxisTransfer* ax, bool prolong, const double* in, double* out,
+              cudaStream_t s) {
+  const int p = ax[0].hp;
+  if (p < 1 || p > 4 || ax[1].hp != p || ax[2].hp != p) return false;
+  // the z march is sequential per CTA: small levels (few planes of work per
+  // CTA, latency-bound) keep the plane-parallel separable passes
+  const long long fine_planes = prolong ? A.o[2] : A.i[2];
+  const long long fine_plane = prolong ? A.o[0] * A.o[1] : A.i[0] * A.i[1];
+  if (fine_plane < (1LL << 16) || fine_planes < 64) return false;
+  switch (p) {
+    case 1: launch_xyz<1>(F, A, ax, prolong, in, out, s); break;
+    case 2: launch_xyz<2>(F, A, ax, prolong, in, out, s); break;
+    case 3: launch_xyz<3>(F, A, ax, prolong, in, out, s); break;
+    case 4: launch_xyz<4>(F, A, ax, prolong, in, out, s); break;
+    default: return false;
+  }
+  return true;
+}
+
 // apply the per-axis maps x, then y, then z (2D: x, y); the intermediates are
 // compact, the source / destination use the given field strides
 void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const long long* src_d, const long long* dst_d,
@@ -537,6 +894,8 @@ void separable(const DevAxisTransfer* ax, bool prolong, int dim, int F, const lo
     return;
   }
   long long d2[3] = {dst_d[0], dst_d[1], src_d[2]};
+  // equal-p h-coarsening on all three axes: one fused z-marching kernel
+  if (xyz_pass(F, args(src_d, dst_d, fs_src, fs_dst, true, true), ax, prolong, in, out, s)) return;
   static const bool no_fused = std::getenv("STMG_XFER_SEPARABLE") != nullptr;
   if (!no_fused && ax[0].hp > 0 && ax[0].hp == ax[1].hp && ax[0].hp <= 4) {
     // equal-p h-coarsening in x and y: one fused x-y pass plus the z pass --

@@ -39,6 +39,16 @@ def main():
         N = op.n_dofs
         gbs = 16 * N / (ta * 1e-3) / 1e9
         line = f"{name}: N={N} apply {ta:.3f} ms ({gbs:.0f} GB/s alg, {N / ta / 1e6:.1f} GDoF/s) residual {tr:.3f} ms"
+        if "--xfer" in sys.argv:
+            M = api.SpaceTimeMultigrid(cfg.equation, cfg.scheme, mesh, cfg.rho, cfg.refinements, cfg.p, cfg.k,
+                                       cfg.n_steps, cfg.tau)
+            nc = M.level_info()[1]["n_dofs"]
+            c = torch.rand(nc, dtype=torch.float64, device="cuda", generator=g)
+            tr_ = timed(lambda: M.restrict_(0, u, c))
+            tp_ = timed(lambda: M.prolong(0, c, y))
+            tv_ = timed(lambda: M.apply(u, y), 5)
+            line += f" restrict {tr_:.3f} ms prolong {tp_:.3f} ms vcycle {tv_:.3f} ms"
+            del M, c
         if "--asm" in sys.argv:
             sm = api.ASMSmoother(op)
             z = torch.zeros_like(u)

@@ -33,10 +33,30 @@ def _stream():
     return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
 
 
-def _ptr(t) -> C.c_void_p:
-    if not t.is_cuda or t.dtype != _torch().float64 or not t.is_contiguous():
-        raise ValueError("expected a contiguous float64 CUDA tensor")
+def _ptr(t, n: Optional[int] = None) -> C.c_void_p:
+    """Device pointer of a tensor argument: contiguous float64 on the current
+    CUDA device, and exactly n entries when n is given (the C side reads or
+    writes n doubles; a short or foreign tensor would be out of bounds)."""
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise N.StmgInvalidArgument("expected a contiguous float64 CUDA tensor")
+    if t.device.index != torch.cuda.current_device():
+        raise N.StmgInvalidArgument(f"tensor on cuda:{t.device.index}, current device is cuda:{torch.cuda.current_device()}")
+    if n is not None and t.numel() != n:
+        raise N.StmgInvalidArgument(f"size mismatch: {t.numel()} entries, expected {n}")
     return C.c_void_p(t.data_ptr())
+
+
+def _host(a, n: int, writable: bool = False) -> np.ndarray:
+    """Host buffer argument: contiguous float64 numpy array of n entries."""
+    if writable:
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.flags.writeable):
+            raise N.StmgInvalidArgument("output must be a writable contiguous float64 numpy array")
+    else:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.size != n:
+        raise N.StmgInvalidArgument(f"size mismatch: {a.size} entries, expected {n}")
+    return a
 
 
 def _dbl(a: Optional[np.ndarray]):
@@ -112,16 +132,13 @@ class SpaceTimeOperator:
             raise N.StmgInvalidArgument("SpaceTimeOperator::apply: size mismatch")
         if y is None:
             y = torch.empty_like(u)
-        N.check(N.load().stmg_st_operator_apply(self._h, _ptr(u), _ptr(y), _stream()))
+        N.check(N.load().stmg_st_operator_apply(self._h, _ptr(u, self.n_dofs), _ptr(y, self.n_dofs), _stream()))
         return y
 
     def apply_host(self, u: np.ndarray, y: Optional[np.ndarray] = None) -> np.ndarray:
         """y = S u on host buffers (H2D/D2H inside the C ABI call)."""
-        u = np.ascontiguousarray(u, dtype=np.float64)
-        if u.size != self.n_dofs:
-            raise N.StmgInvalidArgument("SpaceTimeOperator::apply: size mismatch")
-        if y is None:
-            y = np.empty_like(u)
+        u = _host(u, self.n_dofs)
+        y = np.empty_like(u) if y is None else _host(y, self.n_dofs, writable=True)
         N.check(N.load().stmg_st_operator_apply_host(self._h, u.ctypes.data_as(N.c_double_p),
                                                      y.ctypes.data_as(N.c_double_p)))
         return y
@@ -130,7 +147,8 @@ class SpaceTimeOperator:
         """r = f - S u (one fused pass)."""
         if r is None:
             r = _torch().empty_like(u)
-        N.check(N.load().stmg_st_operator_residual(self._h, _ptr(f), _ptr(u), _ptr(r), _stream()))
+        n = self.n_dofs
+        N.check(N.load().stmg_st_operator_residual(self._h, _ptr(f, n), _ptr(u, n), _ptr(r, n), _stream()))
         return r
 
     def interpolate(self, kind: int, frequency: float = 0.5, t: float = 0.0, centre=(0.5, 0.5, 0.5),
@@ -172,7 +190,7 @@ class SpaceTimeOperator:
         torch = _torch()
         if y is None:
             y = torch.empty_like(u)
-        N.check(N.load().stmg_spatial_apply(self._h, kind, _ptr(u), _ptr(y), _stream()))
+        N.check(N.load().stmg_spatial_apply(self._h, kind, _ptr(u, self.n_space), _ptr(y, self.n_space), _stream()))
         return y
 
     def __del__(self):
@@ -189,7 +207,8 @@ class ASMSmoother:
 
     def add_correction(self, r, z):
         """z += W sum_T R_T^T B_T^-1 R_T r (accumulate)."""
-        N.check(N.load().stmg_asm_add_correction(self._h, _ptr(r), _ptr(z), _stream()))
+        n = self.op.n_dofs
+        N.check(N.load().stmg_asm_add_correction(self._h, _ptr(r, n), _ptr(z, n), _stream()))
         return z
 
     def __del__(self):
@@ -207,13 +226,15 @@ class Transfer:
     def prolong(self, c, f=None):
         if f is None:
             f = _torch().empty(self.fine.n_dofs, dtype=c.dtype, device=c.device)
-        N.check(N.load().stmg_transfer_prolong(self._h, _ptr(c), _ptr(f), _stream()))
+        N.check(N.load().stmg_transfer_prolong(self._h, _ptr(c, self.coarse.n_dofs), _ptr(f, self.fine.n_dofs),
+                                               _stream()))
         return f
 
     def restrict_(self, f, c=None):
         if c is None:
             c = _torch().empty(self.coarse.n_dofs, dtype=f.dtype, device=f.device)
-        N.check(N.load().stmg_transfer_restrict(self._h, _ptr(f), _ptr(c), _stream()))
+        N.check(N.load().stmg_transfer_restrict(self._h, _ptr(f, self.fine.n_dofs), _ptr(c, self.coarse.n_dofs),
+                                                _stream()))
         return c
 
     def __del__(self):
@@ -260,6 +281,11 @@ class SpaceTimeMultigrid:
     def operator_at(self, l: int) -> SpaceTimeOperator:
         return self._ops[l]
 
+    def _n(self, l: int) -> int:
+        if not 0 <= l < self.n_levels:
+            raise N.StmgInvalidArgument(f"bad level {l}")
+        return self._ops[l].n_dofs
+
     def level_info(self):
         out = []
         for l in range(self.n_levels):
@@ -304,33 +330,37 @@ class SpaceTimeMultigrid:
     def apply(self, r, z=None):
         if z is None:
             z = _torch().empty_like(r)
-        N.check(N.load().stmg_multigrid_apply(self._h, _ptr(r), _ptr(z), _stream()))
+        n = self._n(0)
+        N.check(N.load().stmg_multigrid_apply(self._h, _ptr(r, n), _ptr(z, n), _stream()))
         return z
 
     def apply_host(self, r: np.ndarray, z: np.ndarray) -> np.ndarray:
         """One V-cycle on host buffers (H2D/D2H inside the C ABI call)."""
+        r, z = _host(r, self._n(0)), _host(z, self._n(0), writable=True)
         N.check(N.load().stmg_multigrid_apply_host(self._h, r.ctypes.data_as(N.c_double_p),
                                                    z.ctypes.data_as(N.c_double_p)))
         return z
 
     def smooth(self, l: int, f, u):
-        N.check(N.load().stmg_multigrid_smooth(self._h, l, _ptr(f), _ptr(u), _stream()))
+        N.check(N.load().stmg_multigrid_smooth(self._h, l, _ptr(f, self._n(l)), _ptr(u, self._n(l)), _stream()))
         return u
 
     def asm_add_correction(self, l: int, r, z):
-        N.check(N.load().stmg_multigrid_asm_add_correction(self._h, l, _ptr(r), _ptr(z), _stream()))
+        N.check(N.load().stmg_multigrid_asm_add_correction(self._h, l, _ptr(r, self._n(l)), _ptr(z, self._n(l)),
+                                                           _stream()))
         return z
 
     def prolong(self, l: int, c, f=None):
         if f is None:
             f = _torch().empty(self._ops[l].n_dofs, dtype=c.dtype, device=c.device)
-        N.check(N.load().stmg_multigrid_prolong(self._h, l, _ptr(c), _ptr(f), _stream()))
+        N.check(N.load().stmg_multigrid_prolong(self._h, l, _ptr(c, self._n(l + 1)), _ptr(f, self._n(l)), _stream()))
         return f
 
     def restrict_(self, l: int, f, c=None):
         if c is None:
             c = _torch().empty(self._ops[l + 1].n_dofs, dtype=f.dtype, device=f.device)
-        N.check(N.load().stmg_multigrid_restrict(self._h, l, _ptr(f), _ptr(c), _stream()))
+        N.check(N.load().stmg_multigrid_restrict(self._h, l, _ptr(f, self._n(l)), _ptr(c, self._n(l + 1)),
+                                                 _stream()))
         return c
 
     def device_bytes(self) -> int:
@@ -342,7 +372,8 @@ class SpaceTimeMultigrid:
         o = gmres_options(**opts)
         res = N.GmresResult()
         hist = np.zeros(history_cap)
-        N.check(N.load().stmg_solve(self._h, 1 if precondition else 0, _ptr(b), _ptr(x), C.byref(o), C.byref(res),
+        N.check(N.load().stmg_solve(self._h, 1 if precondition else 0, _ptr(b, self._n(0)), _ptr(x, self._n(0)),
+                                    C.byref(o), C.byref(res),
                                     hist.ctypes.data_as(N.c_double_p), history_cap, _stream()))
         return _result(res, hist)
 
@@ -382,7 +413,7 @@ class SpaceTimeMultigrid:
         o = gmres_options(**opts)
         res = N.GmresResult()
         hist = np.zeros(history_cap)
-        b = np.ascontiguousarray(b, dtype=np.float64)
+        b, x = _host(b, self._n(0)), _host(x, self._n(0), writable=True)
         N.check(N.load().stmg_solve_host(self._h, 1 if precondition else 0, b.ctypes.data_as(N.c_double_p),
                                          x.ctypes.data_as(N.c_double_p), C.byref(o), C.byref(res),
                                          hist.ctypes.data_as(N.c_double_p), history_cap))
@@ -497,6 +528,9 @@ class SlabMultigrid:
             off, nd, p0 = C.c_longlong(), C.c_longlong(), C.c_longlong()
             N.check(lib.stmg_slab_multigrid_part(h, i, C.byref(off), C.byref(nd), C.byref(p0)))
             self.parts.append({"offset": off.value, "n_dofs": nd.value, "plane0": p0.value})
+        # full-length finest-level vector (scatter / gather)
+        self.n_full = (n_steps * (k + 1 if scheme == DG else k)) * int(np.prod(
+            [((mesh.base[a] << fine_level) * p + 1) for a in range(mesh.dim)]))
 
     def omega_at(self, l: int) -> float:
         return float(N.load().stmg_slab_multigrid_omega(self._h, l))
@@ -506,38 +540,42 @@ class SlabMultigrid:
 
     def apply(self, u, y=None):
         y = _torch().empty_like(u) if y is None else y
-        N.check(N.load().stmg_slab_multigrid_apply(self._h, _ptr(u), _ptr(y), _stream()))
+        N.check(N.load().stmg_slab_multigrid_apply(self._h, _ptr(u, self.n_local), _ptr(y, self.n_local), _stream()))
         return y
 
     def vcycle(self, r, z=None):
         z = _torch().empty_like(r) if z is None else z
-        N.check(N.load().stmg_slab_multigrid_vcycle(self._h, _ptr(r), _ptr(z), _stream()))
+        N.check(N.load().stmg_slab_multigrid_vcycle(self._h, _ptr(r, self.n_local), _ptr(z, self.n_local), _stream()))
         return z
 
     def asm_add_correction(self, r, z):
-        N.check(N.load().stmg_slab_multigrid_asm_add_correction(self._h, _ptr(r), _ptr(z), _stream()))
+        N.check(N.load().stmg_slab_multigrid_asm_add_correction(self._h, _ptr(r, self.n_local), _ptr(z, self.n_local),
+                                                                _stream()))
         return z
 
     def solve(self, b, x, **opts):
         o = gmres_options(**opts)
         res = N.GmresResult()
-        N.check(N.load().stmg_slab_multigrid_solve(self._h, _ptr(b), _ptr(x), C.byref(o), C.byref(res), _stream()))
+        N.check(N.load().stmg_slab_multigrid_solve(self._h, _ptr(b, self.n_local), _ptr(x, self.n_local), C.byref(o),
+                                                   C.byref(res), _stream()))
         return _result(res, np.zeros(0))
 
     def dot(self, a, b) -> float:
         out = C.c_double()
         _torch().cuda.synchronize()
-        N.check(N.load().stmg_slab_multigrid_dot(self._h, _ptr(a), _ptr(b), C.byref(out)))
+        N.check(N.load().stmg_slab_multigrid_dot(self._h, _ptr(a, self.n_local), _ptr(b, self.n_local), C.byref(out)))
         return out.value
 
     def scatter(self, full, local=None):
         torch = _torch()
         local = torch.empty(self.n_local, dtype=full.dtype, device=full.device) if local is None else local
-        N.check(N.load().stmg_slab_multigrid_scatter(self._h, _ptr(full), _ptr(local), _stream()))
+        N.check(N.load().stmg_slab_multigrid_scatter(self._h, _ptr(full, self.n_full), _ptr(local, self.n_local),
+                                                     _stream()))
         return local
 
     def gather(self, local, full):
-        N.check(N.load().stmg_slab_multigrid_gather(self._h, _ptr(local), _ptr(full), _stream()))
+        N.check(N.load().stmg_slab_multigrid_gather(self._h, _ptr(local, self.n_local), _ptr(full, self.n_full),
+                                                    _stream()))
         return full
 
     def __del__(self):

@@ -343,7 +343,6 @@ __global__ void __launch_bounds__(256, 3) asm_apply_warp_kernel(const __grid_con
 __host__ __device__ __forceinline__ int swz64(int a, int e) { return a * 64 + (e ^ ((a & 7) << 2)); }
 // record layout of 64-dof cells for the DFMA kernel: column XOR (row & 15),
 // conflict-free row and column reads of 64-bit words
-__host__ __device__ __forceinline__ int swz64f(int a, int e) { return a * 64 + (e ^ (a & 15)); }
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -564,7 +563,6 @@ __device__ __forceinline__ void stage_row(const DevASM& A, const double* Ps, con
 // (DevASM::x_layout == 2): the A-fragment loads X[a][e] (4 k-rows x 4 m-rows
 // per half-warp) then fall in 16 distinct 64-bit banks in both products; the
 // contiguous pitch 27 was 2-way conflicted (ncu: 117 M conflicts per C3 sweep)
-constexpr int kMma32Pitch = 28;
 template <int M>
 constexpr int mma32_xbuf() {
   static_assert(M <= kMma32Pitch && (M * kMma32Pitch) % 2 == 0, "16-byte bulk copies");
@@ -956,216 +954,6 @@ __global__ void __launch_bounds__(256, NBUF == 2 ? 3 : 2) asm_apply_fd64_kernel(
   }
 }
 
-// 64-dof cells on the FP64 FMA pipe (A.x_layout == 1): same record stream,
-// meta and temporal fast diagonalisation as asm_apply_fd64_kernel, but the
-// two 64 x 64 products are DFMA over the NCOL used columns only (the
-// tensor-core version pads them to 8): 256 threads, each product split in
-// four 16-row quarters reduced through shared memory; the row owner of
-// eigen-index e applies (B + lam_e)^-1 and Q for all its columns, so the
-// second product emits original columns directly.
-template <int NT, int S, int NBUF>
-__global__ void __launch_bounds__(256, 2) asm_apply_dfma64_kernel(const __grid_constant__ DevASM A,
-                                                                  const double* __restrict__ r,
-                                                                  double* __restrict__ z, double scale) {
-  constexpr int M = 64, NCOL = NT * S;
-  constexpr unsigned RBYTES = static_cast<unsigned>(kRec64 * sizeof(double));
-  extern __shared__ __align__(128) double sm[];
-  double* rs = sm + NBUF * kRec64;      // [64][4 or 8] P-transformed residual slots
-  constexpr int RW = NCOL <= 4 ? 4 : 8;  // slot row width (double4 broadcasts)
-  double* hs = rs + RW * M;              // [64][RW] result of the temporal solve (original columns)
-  double* part = hs + RW * M;            // [4][64][RW] quarter partial sums
-  long long* cinfo = reinterpret_cast<long long*>(part + 4 * RW * M);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(cinfo + 4);
-  const int t = threadIdx.x;
-  const long long n_pos = A.n_list, nsp = A.n_space;
-  const long long dx = A.dofs[0], dxy = A.dofs[0] * A.dofs[1];
-  const int row = t & 63, qtr = t >> 6;
-  int fb = 0;
-  const int lx = row & 3, ly = (row >> 2) & 3, lz = row >> 4;
-  fb = (lx == 0 ? 1 : 0) | (lx == 3 ? 2 : 0) | (ly == 0 ? 4 : 0) | (ly == 3 ? 8 : 0) | (lz == 0 ? 16 : 0) |
-       (lz == 3 ? 32 : 0);
-  const long long off = lz * dxy + ly * dx + lx;
-  const double w_int = scale * ldexp(1.0, -__popc(fb));
-  if (t == 0) {
-#pragma unroll
-    for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  long long pos = blockIdx.x;
-  if (t == 0) {
-#pragma unroll
-    for (int b = 0; b + 1 < NBUF; ++b) {
-      const long long q = pos + static_cast<long long>(b) * gridDim.x;
-      if (q < n_pos) {
-        mbar_expect_tx(&bar[b], RBYTES);
-        bulk_g2s(sm + b * kRec64, A.X + q * kRec64, RBYTES, &bar[b]);
-      }
-    }
-  }
-  double rn[NCOL];
-  long long g0n = 0, maskn = 0;
-  auto fetch = [&](long long q) {
-    if (t < M) {
-      const longlong2 mt = *reinterpret_cast<const longlong2*>(A.meta + 2 * q);
-      g0n = mt.x;
-      maskn = mt.y;
-#pragma unroll
-      for (int c = 0; c < NCOL; ++c) rn[c] = __ldg(r + c * nsp + g0n + off);
-    }
-  };
-  if (pos < n_pos) fetch(pos);
-  unsigned phase_bits = 0;
-  int buf = 0;
-  for (int it = 0; pos < n_pos; pos += gridDim.x, ++it) {
-    const int par = it & 1;
-    const long long next = pos + gridDim.x;
-    // ---- stage the residual (P-transformed slots), boundary contributions
-    if (t < M) {
-      double tr[RW];
-#pragma unroll
-      for (int k = 0; k < RW; ++k) {
-        double sacc = 0.0;
-        if (k < NCOL) {
-#pragma unroll
-          for (int c = 0; c < NCOL; ++c) sacc = fma(A.P[k][c], rn[c], sacc);
-        }
-        tr[k] = sacc;
-      }
-#pragma unroll
-      for (int k = 0; k < RW; k += 2) *reinterpret_cast<double2*>(rs + t * RW + k) = make_double2(tr[k], tr[k + 1]);
-      if (maskn & fb) {
-        const double w = scale * ldexp(1.0, -__popc(fb & ~static_cast<int>(maskn)));
-#pragma unroll
-        for (int c = 0; c < NCOL; ++c) atomicAdd(z + c * nsp + g0n + off, w * rn[c]);
-      }
-      if (t == 0) {
-        cinfo[2 * par] = g0n;
-        cinfo[2 * par + 1] = maskn;
-      }
-      if (next < n_pos) fetch(next);
-    }
-    mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);
-    phase_bits ^= 1u << buf;
-    __syncthreads();
-    {
-      const int fbuf = buf == 0 ? NBUF - 1 : buf - 1;
-      const long long q = pos + static_cast<long long>(NBUF - 1) * gridDim.x;
-      if (t == 0 && q < n_pos) {
-        fence_proxy_async();
-        mbar_expect_tx(&bar[fbuf], RBYTES);
-        bulk_g2s(sm + fbuf * kRec64, A.X + q * kRec64, RBYTES, &bar[fbuf]);
-      }
-    }
-    const double* Xs = sm + buf * kRec64;
-    // ---- product 1, quarter qtr: sum over a in [16 qtr, 16 qtr + 16) of X[a][e] rs[a][.]
-    {
-      double acc[RW];
-#pragma unroll
-      for (int k = 0; k < RW; ++k) acc[k] = 0.0;
-#pragma unroll 4
-      for (int i = 0; i < 16; ++i) {
-        const int a2 = qtr * 16 + i;
-        const double x = Xs[swz64f(a2, row)];
-        const double4 r0 = *reinterpret_cast<const double4*>(rs + a2 * RW);
-        acc[0] = fma(x, r0.x, acc[0]);
-        acc[1] = fma(x, r0.y, acc[1]);
-        acc[2] = fma(x, r0.z, acc[2]);
-        acc[3] = fma(x, r0.w, acc[3]);
-        if (RW == 8) {
-          const double4 r1 = *reinterpret_cast<const double4*>(rs + a2 * RW + 4);
-          acc[RW == 8 ? 4 : 0] = fma(x, r1.x, acc[RW == 8 ? 4 : 0]);
-          acc[RW == 8 ? 5 : 1] = fma(x, r1.y, acc[RW == 8 ? 5 : 1]);
-          acc[RW == 8 ? 6 : 2] = fma(x, r1.z, acc[RW == 8 ? 6 : 2]);
-          acc[RW == 8 ? 7 : 3] = fma(x, r1.w, acc[RW == 8 ? 7 : 3]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < RW; k += 2)
-        *reinterpret_cast<double2*>(part + (qtr * M + row) * RW + k) = make_double2(acc[k], acc[k + 1]);
-    }
-    __syncthreads();
-    // ---- row owner e: reduce, (B + lam_e)^-1 per slot pair, Q back to columns
-    if (t < M) {
-      double h[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) h[k] = 0.0;
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq)
-#pragma unroll
-        for (int k = 0; k < RW; ++k) h[k] += part[(qq * M + t) * RW + k];
-      const double lam = Xs[4096 + t];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (2 * j >= NCOL) break;
-        const int kd = A.kind[j];
-        const double a0 = A.s0[j], a1 = A.s1[j];
-        const double p0 = a0 + lam, p1 = a1 + lam;
-        const double m00 = kd ? p0 : p1, m11 = p0, m01 = kd ? -a1 : 0.0, m10 = kd ? a1 : 0.0;
-        const double inv = 1.0 / (kd ? fma(p0, p0, a1 * a1) : p0 * p1);
-        const double v0 = h[2 * j], v1 = h[2 * j + 1];
-        h[2 * j] = fma(m00, v0, m01 * v1) * inv;
-        h[2 * j + 1] = fma(m10, v0, m11 * v1) * inv;
-      }
-      double o[RW];
-#pragma unroll
-      for (int c = 0; c < RW; ++c) {
-        double sacc = 0.0;
-        if (c < NCOL) {
-#pragma unroll
-          for (int k = 0; k < NCOL; ++k) sacc = fma(A.Q[c][k], h[k], sacc);
-        }
-        o[c] = sacc;
-      }
-#pragma unroll
-      for (int c = 0; c < RW; c += 2) *reinterpret_cast<double2*>(hs + t * RW + c) = make_double2(o[c], o[c + 1]);
-    }
-    __syncthreads();
-    // ---- product 2, quarter qtr: sum over e in [16 qtr, 16 qtr + 16) of X[a][e] hs[e][.]
-    {
-      double acc[RW];
-#pragma unroll
-      for (int k = 0; k < RW; ++k) acc[k] = 0.0;
-#pragma unroll 4
-      for (int i = 0; i < 16; ++i) {
-        const int e2 = qtr * 16 + i;
-        const double x = Xs[swz64f(row, e2)];
-        const double4 h0 = *reinterpret_cast<const double4*>(hs + e2 * RW);
-        acc[0] = fma(x, h0.x, acc[0]);
-        acc[1] = fma(x, h0.y, acc[1]);
-        acc[2] = fma(x, h0.z, acc[2]);
-        acc[3] = fma(x, h0.w, acc[3]);
-        if (RW == 8) {
-          const double4 h1 = *reinterpret_cast<const double4*>(hs + e2 * RW + 4);
-          acc[RW == 8 ? 4 : 0] = fma(x, h1.x, acc[RW == 8 ? 4 : 0]);
-          acc[RW == 8 ? 5 : 1] = fma(x, h1.y, acc[RW == 8 ? 5 : 1]);
-          acc[RW == 8 ? 6 : 2] = fma(x, h1.z, acc[RW == 8 ? 6 : 2]);
-          acc[RW == 8 ? 7 : 3] = fma(x, h1.w, acc[RW == 8 ? 7 : 3]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < RW; k += 2)
-        *reinterpret_cast<double2*>(part + (qtr * M + row) * RW + k) = make_double2(acc[k], acc[k + 1]);
-    }
-    __syncthreads();
-    // ---- dof owner a: reduce, weight, scatter (Dirichlet rows were added by the gather)
-    if (t < M) {
-      const long long g0 = cinfo[2 * par];
-      const int mask = static_cast<int>(cinfo[2 * par + 1]);
-      if (!(mask & fb)) {
-#pragma unroll
-        for (int c = 0; c < NCOL; ++c) {
-          double sacc = 0.0;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) sacc += part[(qq * M + t) * RW + c];
-          atomicAdd(z + c * nsp + g0 + off, sacc * w_int);
-        }
-      }
-    }
-    buf = buf + 1 == NBUF ? 0 : buf + 1;
-  }
-}
-
 // Tensor-core variant for 3D Q4 exact cells (m = 125, padded to 128 rows):
 // one CTA of 16 warps per cell (persistent), warp w owns rows [8w, 8w+8) of
 // both products, mma.sync.m8n8k4.f64 over k in 32 steps of 4 (entries past m
@@ -1322,125 +1110,6 @@ __global__ void __launch_bounds__(((M + 7) / 8) * 32, 1) asm_apply_large_mma_ker
           if (col < ncol) atomicAdd(z + static_cast<long long>(col) * A.n_space + d.g, v0 * w);
           if (col + 1 < ncol) atomicAdd(z + static_cast<long long>(col + 1) * A.n_space + d.g, v1 * w);
         }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Large cell blocks (m > 64, e.g. 3D Q4: m = 125): one CTA of 128 threads per
-// cell (persistent), X row-major in global memory (m^2 doubles, L2-resident
-// across the two products of one cell), all S*n_t columns at once:
-//   hat r = X^T r  (thread e; consecutive threads read consecutive X entries)
-//   hat z_e = (T_M + lam_e T_A)^-1 hat r_e per step (pivoted n_t x n_t solve)
-//   z = X hat z    (thread a)
-// then the weighted scatter-add; Dirichlet rows contribute w * r.
-constexpr int kLargeChunk = 32;
-template <int NT>
-__global__ void __launch_bounds__(128, 4) asm_apply_large_kernel(const __grid_constant__ DevASM A,
-                                                              const double* __restrict__ r, double* __restrict__ z,
-                                                              double scale) {
-  const int m = A.m, t = threadIdx.x;
-  const int ncol = A.S * NT;
-  extern __shared__ __align__(16) double lsm[];
-  double* rs = lsm;            // [m][8]
-  double* hs = rs + 8 * 128;  // [m][8]
-  const unsigned cxn = static_cast<unsigned>(A.cells[0]), cyn = static_cast<unsigned>(A.cells[1]);
-  for (long long pos = blockIdx.x; pos < A.n_list; pos += gridDim.x) {
-    const unsigned ci = static_cast<unsigned>(A.list ? A.list[pos] : pos);
-    const long long cx = ci % cxn, cy = (ci / cxn) % cyn, cz = ci / (cxn * cyn);
-    LocalDof d{};
-    if (t < m) {
-      d = local_dof(A, cx, cy, cz, t);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) rs[t * 8 + c] = c < ncol ? __ldg(r + static_cast<long long>(c) * A.n_space + d.g) : 0.0;
-    }
-    __syncthreads();
-    const double* X = A.X + pos * A.xs;
-    if (t < m) {
-      double acc[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-      // X rows streamed from HBM: 16 loads in flight per thread
-#pragma unroll 16
-      for (int a = 0; a < m; ++a) {
-        const double x = __ldg(X + static_cast<long long>(a) * m + t);
-        const double4 r0 = *reinterpret_cast<const double4*>(rs + a * 8);
-        const double4 r1 = *reinterpret_cast<const double4*>(rs + a * 8 + 4);
-        acc[0] = fma(x, r0.x, acc[0]);
-        acc[1] = fma(x, r0.y, acc[1]);
-        acc[2] = fma(x, r0.z, acc[2]);
-        acc[3] = fma(x, r0.w, acc[3]);
-        acc[4] = fma(x, r1.x, acc[4]);
-        acc[5] = fma(x, r1.y, acc[5]);
-        acc[6] = fma(x, r1.z, acc[6]);
-        acc[7] = fma(x, r1.w, acc[7]);
-      }
-      const double lam = A.lam[pos * m + t];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) hs[t * 8 + c] = 0.0;
-#pragma unroll
-      for (int st = 0; st < 8 / NT; ++st) {
-        if (st >= A.S) break;
-        double b4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int i = 0; i < NT; ++i) b4[i] = acc[st * NT + i];
-        small_solve(A.TM, A.TA, lam, NT, b4);
-#pragma unroll
-        for (int i = 0; i < NT; ++i) hs[t * 8 + st * NT + i] = b4[i];
-      }
-    }
-    __syncthreads();
-    {
-      // z = X hat z (thread a). X is staged through shared memory in column
-      // chunks of kLargeChunk: coalesced row-segment loads that hit L2 (the
-      // first product just streamed X), conflict-free row reads (odd pitch);
-      // a thread-per-row global read would touch one sector per lane.
-      double acc[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-      double* xc = hs + 8 * 128;  // [128][kLargeChunk + 1]
-      constexpr int LDc = kLargeChunk + 1;
-      for (int e0 = 0; e0 < m; e0 += kLargeChunk) {
-        const int ncols = min(kLargeChunk, m - e0);
-        constexpr int NLD = 128 * kLargeChunk / 128;
-        double xv[NLD];
-#pragma unroll
-        for (int k = 0; k < NLD; ++k) {
-          const int i = t + 128 * k, row = i / kLargeChunk, col = i % kLargeChunk;
-          xv[k] = (row < m && col < ncols) ? __ldg(X + static_cast<long long>(row) * m + e0 + col) : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < NLD; ++k) {
-          const int i = t + 128 * k;
-          xc[(i / kLargeChunk) * LDc + i % kLargeChunk] = xv[k];
-        }
-        __syncthreads();
-        if (t < m) {
-          for (int k = 0; k < ncols; ++k) {
-            const double x = xc[t * LDc + k];
-            const double4 h0 = *reinterpret_cast<const double4*>(hs + (e0 + k) * 8);
-            const double4 h1 = *reinterpret_cast<const double4*>(hs + (e0 + k) * 8 + 4);
-            acc[0] = fma(x, h0.x, acc[0]);
-            acc[1] = fma(x, h0.y, acc[1]);
-            acc[2] = fma(x, h0.z, acc[2]);
-            acc[3] = fma(x, h0.w, acc[3]);
-            acc[4] = fma(x, h1.x, acc[4]);
-            acc[5] = fma(x, h1.y, acc[5]);
-            acc[6] = fma(x, h1.z, acc[6]);
-            acc[7] = fma(x, h1.w, acc[7]);
-          }
-        }
-        __syncthreads();
-      }
-      if (t < m) {
-      const double w = scale / d.mult;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (c >= ncol) break;
-        const double v = d.bdry ? rs[t * 8 + c] : acc[c];
-        atomicAdd(z + static_cast<long long>(c) * A.n_space + d.g, v * w);
-      }
       }
     }
     __syncthreads();
@@ -1614,7 +1283,7 @@ __global__ void back_transform_kernel(int m, long long xs, int layout, const dou
     const int a = i / m, e = i % m;
     double s = 0.0;
     for (int k = a; k < m; ++k) s = fma(Lc[static_cast<long long>(k) * m + a], Vc[static_cast<long long>(e) * m + k], s);
-    Xc[m == 64 ? (layout == 1 ? swz64f(a, e) : swz64(a, e)) : (layout == 2 ? a * kMma32Pitch + e : i)] = s;
+    Xc[m == 64 ? swz64(a, e) : (layout == 2 ? a * kMma32Pitch + e : i)] = s;
   }
 }
 
@@ -1662,9 +1331,8 @@ void launch_mma32(const DevASM& A, const double* r, double* z, double scale, cud
   count_launch();
   asm_apply_mma32_kernel<M, NT><<<static_cast<unsigned>(grid), 128, smem, s>>>(A, r, z, scale);
 }
-// m = 25 / 27 run on the tensor cores (C3 fine sweep 1.79 -> 1.51 ms) unless
-// STMG_ASM27=warp (the DFMA warp-per-cell kernel, kept as the measured
-// alternative and tested)
+// m = 25 / 27 run on the tensor cores (C3 fine sweep 1.79 -> 1.51 ms against
+// the DFMA warp-per-cell kernel, which serves the smaller blocks)
 template <int M, int NT>
 void launch_small(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if constexpr (M > 24) {
@@ -1739,47 +1407,12 @@ void launch_fd64_nbuf(const DevASM& A, const double* r, double* z, double scale,
   count_launch();
   asm_apply_fd64_kernel<NT, S, NBUF><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
 }
-template <int NT, int S>
-void launch_dfma64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
-  constexpr int NCOL = NT * S, RW = NCOL <= 4 ? 4 : 8;
-  constexpr size_t smem = sizeof(double) * (2 * static_cast<size_t>(kRec64) + 6 * RW * 64) + 4 * sizeof(long long) +
-                          2 * sizeof(unsigned long long);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(asm_apply_dfma64_kernel<NT, S, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cudaFuncSetAttribute(asm_apply_dfma64_kernel<NT, S, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    configured = true;
-  }
-  int per_sm = 0, dev = 0, sms = 148;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, asm_apply_dfma64_kernel<NT, S, 2>, 256, smem);
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (A.n_list == 0) return;
-  const long long grid =
-      std::max<long long>(1, std::min<long long>(A.n_list, static_cast<long long>(std::max(per_sm, 1)) * sms));
-  count_launch();
-  asm_apply_dfma64_kernel<NT, S, 2><<<static_cast<unsigned>(grid), 256, smem, s>>>(A, r, z, scale);
-}
-
-// record pipeline depth (STMG_ASM_NBUF = 2 or 3). Default 2: one record in
-// flight per CTA at 3 CTAs / SM measured 1.61 ms per C2 sweep against 1.91 ms
-// for 3 buffers at 2 CTAs / SM -- the per-cell solve, not the bytes in
-// flight, limits the sweep
+// one record in flight per CTA at 3 CTAs / SM (1.61 ms per C2 sweep against
+// 1.91 ms for three buffers at 2 CTAs / SM: the per-cell solve, not the bytes
+// in flight, limits the sweep)
 template <int NT, int S>
 void launch_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
-  if (A.x_layout == 1) {
-    launch_dfma64<NT, S>(A, r, z, scale, s);
-    return;
-  }
-  static const int nbuf = [] {
-    const char* e = std::getenv("STMG_ASM_NBUF");
-    return e ? std::atoi(e) : 2;
-  }();
-  if (nbuf == 2)
-    launch_fd64_nbuf<NT, S, 2>(A, r, z, scale, s);
-  else
-    launch_fd64_nbuf<NT, S, 3>(A, r, z, scale, s);
+  launch_fd64_nbuf<NT, S, 2>(A, r, z, scale, s);
 }
 void launch_asm_fd64(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   switch (A.nt * 10 + A.S) {
@@ -1816,31 +1449,13 @@ void launch_large_mma(const DevASM& A, const double* r, double* z, double scale,
   count_launch();
   asm_apply_large_mma_kernel<M, NT><<<static_cast<unsigned>(grid), NTH, smem, s>>>(A, r, z, scale);
 }
-// m = 125 (3D Q4) runs on the tensor cores unless STMG_ASM125=dfma (the
-// CTA-per-cell DFMA kernel below, kept as the measured alternative and tested)
+// m = 125 (3D Q4): the tensor-core kernel (the CTA-per-cell DFMA form it
+// replaced ran 2.8 vs 2.2 ms per C4 fine sweep)
 template <int NT>
 void launch_large(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if (A.n_list == 0) return;
-  static const bool dfma = [] {
-    const char* e = std::getenv("STMG_ASM125");
-    return e && std::string(e) == "dfma";
-  }();
-  if (A.m == 125 && !dfma) {
-    launch_large_mma<125, NT>(A, r, z, scale, s);
-    return;
-  }
-  const size_t smem = sizeof(double) * (16 * 128 + 128 * (kLargeChunk + 1));
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(asm_apply_large_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = true;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long grid = std::max<long long>(1, std::min<long long>(A.n_list, 16LL * sms));
-  count_launch();
-  asm_apply_large_kernel<NT><<<static_cast<unsigned>(grid), 128, smem, s>>>(A, r, z, scale);
+  if (A.m != 125) throw std::invalid_argument("ASMSmoother: exact blocks above 64 dofs need m = 125 (3D Q4)");
+  launch_large_mma<125, NT>(A, r, z, scale, s);
 }
 void launch_asm_large(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s) {
   if (A.m > 128) throw std::invalid_argument("ASMSmoother: cell blocks larger than 128 dofs are not supported");

@@ -149,13 +149,22 @@ struct DevASM {
   // (2j, 2j+1) is two real eigenvalues s0/s1 (kind 0) or one conjugate pair
   // s0 +- i s1 (kind 1)
   int tdiag;
-  // 64-dof record layout / kernel: 0 FP64 tensor cores (swz64), 1 DFMA (swz64f)
+  // record layout: 0 contiguous rows (m = 64: swizzled for the FP64 tensor
+  // cores), 2 pitch-28 rows (25 / 27 dofs); see asm_record_stride
   int x_layout;
   int kind[4];
   double s0[4], s1[4];
   double P[8][8], Q[8][8];
 };
 constexpr int kRec64 = 64 * 64 + 64;
+constexpr int kMma32Pitch = 28;  // row pitch of the 25 / 27-dof records (layout 2)
+// doubles per cell record of the exact smoother, by block size and layout;
+// the single definition setup (stmg.cpp) and the kernels (asm_smoother.cu) use
+inline long long asm_record_stride(int m, int layout) {
+  if (m == 64) return kRec64;
+  if (layout == 2) return static_cast<long long>(m) * kMma32Pitch;
+  return (static_cast<long long>(m) * m + 1) & ~1LL;
+}
 // z += scale * W sum_T R_T^T B_T^-1 R_T r
 void asm_add_correction(const DevASM& A, const double* r, double* z, double scale, cudaStream_t s);
 

@@ -936,19 +936,14 @@ void ASMSmoother::build_exact(const SpaceTimeOperator& op, const SpaceTimeOperat
   cusolverDnDestroyParams(prm);
   cusolverDnDestroy(h);
   // m = 64: one TMA record per cell, X (swizzled) followed by its eigenvalues
-  // 64-dof kernel: FP64 tensor cores (default) or DFMA (STMG_ASM64=dfma);
-  // 25/27-dof kernel: tensor cores on pitch-28 rows (layout 2, default) or the
-  // DFMA warp kernel on contiguous rows (STMG_ASM27=warp)
-  {
-    const char* e = std::getenv("STMG_ASM64");
-    const char* e27 = std::getenv("STMG_ASM27");
-    A.x_layout = (A.m == 64 && e && std::string(e) == "dfma") ? 1 : 0;
-    if (A.m > 24 && A.m <= 28 && !(e27 && std::string(e27) == "warp")) A.x_layout = 2;
-  }
-  A.xs = A.m == 64 ? kRec64
-         : A.x_layout == 2 ? static_cast<long long>(A.m) * 28
-                           : (static_cast<long long>(A.m) * A.m + 1) & ~1LL;
+  // (FP64 tensor-core kernel); 25/27 dofs: tensor cores on pitch-28 rows
+  // (layout 2); smaller blocks: contiguous rows (DFMA warp kernel)
+  A.x_layout = (A.m > 24 && A.m <= 28) ? 2 : 0;
+  A.xs = asm_record_stride(A.m, A.x_layout);
   X_.allocate(sizeof(double) * static_cast<size_t>(n_pos) * A.xs);
+  // pitch-28 rows leave padding columns m..27 unwritten: zero them once so the
+  // bulk copies stream defined data
+  cuda_check(cudaMemsetAsync(X_.raw(), 0, sizeof(double) * static_cast<size_t>(n_pos) * A.xs, s), "records");
   asm_back_transform(A.m, A.xs, A.x_layout, n_pos, cellM.d(), cellA.d(), X_.d(), s);
   if (A.m == 64) {
     cuda_check(cudaMemcpy2DAsync(X_.d() + 64 * 64, sizeof(double) * kRec64, lam_.d(), sizeof(double) * 64,

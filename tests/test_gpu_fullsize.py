@@ -8,7 +8,7 @@ GPU output is reduced the same way and compared:
     to a local error anywhere) and 4096 block norms: relative <= 1e-12
     against the block norm (signed dots) / 1e-12 (norms),
   * 20000 seeded sample entries: relative L2 <= 1e-12,
-  * the global norm: <= 1e-13.
+  * the global norm: <= 1e-12.
 The north_star bar is relative L2 <= 1e-12."""
 import os
 
@@ -52,6 +52,7 @@ def test_fullsize_vmult_fingerprint(cuda, name):
     got = y[idx].cpu().numpy()
     want = fx["sample_val"]
     assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-12
-    assert abs(float(y.norm()) - float(fx["norm"])) <= 1e-13 * float(fx["norm"])
+    # the global norm sums 5.4e8 squares in different orders on the two sides
+    assert abs(float(y.norm()) - float(fx["norm"])) <= 1e-12 * float(fx["norm"])
     del y
     cuda.cuda.empty_cache()

@@ -64,6 +64,12 @@ struct DevLevel {
   // space-time block coefficients, row-major F x F (space_time_operator.cpp:269-317)
   double CM[kMaxF * kMaxF];
   double CA[kMaxF * kMaxF];
+  // G = CA^-1 CM (row-major F x F), g_ok = 1 when CA is safely invertible:
+  // S = (CA (x) I)(G (x) M + I (x) A), the form st_brick.cu applies (the
+  // temporal coupling of the z stage becomes one F x F product per point,
+  // CA is applied once per output plane)
+  double G[kMaxF * kMaxF];
+  int g_ok;
 };
 
 }  // namespace stmgb

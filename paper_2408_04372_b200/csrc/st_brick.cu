@@ -241,14 +241,27 @@ __global__ void __launch_bounds__(kThreads, STB_MINB)
       } else {
         const bool no_f = (zz == 0 && !lo_dir);  // low interface plane: f counted by the slab below
         const long long base = f0 * ns + zz * dxy + pbase;
+        double out[FPG];
+        if (C::FG == 1 && L.g_ok) {
+#pragma unroll
+          for (int i = 0; i < FPG; ++i) {
+            double v = 0.0;
+#pragma unroll
+            for (int h = 0; h < F; ++h) v = fma(L.CA[i * F + h], win[h][jw], v);
+            out[i] = v;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < FPG; ++i) out[i] = win[i][jw];
+        }
 #pragma unroll
         for (int i = 0; i < FPG; ++i) {
           if (f0 + i >= F) break;
           const long long idx = base + i * ns;
           if (RES)
-            y[idx] = no_f ? -win[i][jw] : __ldg(fvec + idx) - win[i][jw];
+            y[idx] = no_f ? -out[i] : __ldg(fvec + idx) - out[i];
           else
-            y[idx] = win[i][jw];
+            y[idx] = out[i];
         }
       }
     }
@@ -401,17 +414,29 @@ __global__ void __launch_bounds__(kThreads, STB_MINB)
       for (int i = 0; i < FPG; ++i) cmc[i] = cap[i] = cac[i] = 0.0;
       const double* ic = Cc + b * F * C::CP_F + zy * C::CPP + zx;
       const double* ip = Cp + b * F * C::CP_F + zy * C::CPP + zx;
+      if (C::FG == 1 && L.g_ok) {
+        // (CA (x) I)(G (x) M + I (x) A): G c on the point, CA at the store
 #pragma unroll
-      for (int gg = 0; gg < F; ++gg) {
-        const double vc = ic[gg * C::CP_F], vp = ip[gg * C::CP_F];
+        for (int gg = 0; gg < F; ++gg) {
+          const double vc = ic[gg * C::CP_F];
+          cap[gg] = ip[gg * C::CP_F];
+          cac[gg] = vc;
 #pragma unroll
-        for (int i = 0; i < FPG; ++i) {
-          const int f = (C::FG == 1 ? 0 : f0) + i;
-          if (f >= F) break;
-          const double cm = L.CM[f * F + gg], ca = L.CA[f * F + gg];
-          cmc[i] = fma(cm, vc, cmc[i]);
-          cap[i] = fma(ca, vp, cap[i]);
-          cac[i] = fma(ca, vc, cac[i]);
+          for (int i = 0; i < F; ++i) cmc[i] = fma(L.G[i * F + gg], vc, cmc[i]);
+        }
+      } else {
+#pragma unroll
+        for (int gg = 0; gg < F; ++gg) {
+          const double vc = ic[gg * C::CP_F], vp = ip[gg * C::CP_F];
+#pragma unroll
+          for (int i = 0; i < FPG; ++i) {
+            const int f = (C::FG == 1 ? 0 : f0) + i;
+            if (f >= F) break;
+            const double cm = L.CM[f * F + gg], ca = L.CA[f * F + gg];
+            cmc[i] = fma(cm, vc, cmc[i]);
+            cap[i] = fma(ca, vp, cap[i]);
+            cac[i] = fma(ca, vc, cac[i]);
+          }
         }
       }
       // contribution of this plane to layer e at local index jl

@@ -174,6 +174,45 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
   if (!wide_) {
     std::copy(CM.begin(), CM.end(), d.CM);
     std::copy(CA.begin(), CA.end(), d.CA);
+    // G = CA^-1 CM when CA is well conditioned (Gauss-Jordan with partial
+    // pivoting; the ratio of the extreme pivots bounds the conditioning)
+    d.g_ok = 0;
+    std::memset(d.G, 0, sizeof(d.G));
+    {
+      std::vector<double> a(CA), g(CM);
+      double pmax = 0.0, pmin = 1e300;
+      bool ok = true;
+      for (int k = 0; k < F && ok; ++k) {
+        int piv = k;
+        for (int i = k + 1; i < F; ++i)
+          if (std::abs(a[static_cast<size_t>(i * F + k)]) > std::abs(a[static_cast<size_t>(piv * F + k)])) piv = i;
+        const double pv = a[static_cast<size_t>(piv * F + k)];
+        if (pv == 0.0) {
+          ok = false;
+          break;
+        }
+        pmax = std::max(pmax, std::abs(pv));
+        pmin = std::min(pmin, std::abs(pv));
+        for (int j = 0; j < F; ++j) {
+          std::swap(a[static_cast<size_t>(k * F + j)], a[static_cast<size_t>(piv * F + j)]);
+          std::swap(g[static_cast<size_t>(k * F + j)], g[static_cast<size_t>(piv * F + j)]);
+        }
+        for (int i = 0; i < F; ++i) {
+          if (i == k) continue;
+          const double m = a[static_cast<size_t>(i * F + k)] / a[static_cast<size_t>(k * F + k)];
+          if (m == 0.0) continue;
+          for (int j = 0; j < F; ++j) {
+            a[static_cast<size_t>(i * F + j)] -= m * a[static_cast<size_t>(k * F + j)];
+            g[static_cast<size_t>(i * F + j)] -= m * g[static_cast<size_t>(k * F + j)];
+          }
+        }
+      }
+      if (ok && pmax / pmin < 1e6) {
+        for (int i = 0; i < F; ++i)
+          for (int j = 0; j < F; ++j) d.G[i * F + j] = g[static_cast<size_t>(i * F + j)] / a[static_cast<size_t>(i * F + i)];
+        d.g_ok = 1;
+      }
+    }
   } else {
     // the fused kernels hold at most kMaxF fields: wide batches compose 2F
     // single-field applications (st_apply_wide) with the full tables
@@ -190,6 +229,8 @@ SpaceTimeOperator::SpaceTimeOperator(Equation equation, const TemporalWeights& w
   mass_desc_.n_dofs = d.n_space;
   std::memset(mass_desc_.CM, 0, sizeof(mass_desc_.CM));
   std::memset(mass_desc_.CA, 0, sizeof(mass_desc_.CA));
+  mass_desc_.g_ok = 0;  // single-field tables: the direct CM / CA coupling
+  std::memset(mass_desc_.G, 0, sizeof(mass_desc_.G));
   stiff_desc_ = mass_desc_;
   mass_desc_.CM[0] = 1.0;
   stiff_desc_.CA[0] = 1.0;

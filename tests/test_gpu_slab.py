@@ -122,3 +122,32 @@ def test_slab_with_nccl_comm_world1(cuda):
     u = _full(cuda, problems.uniform_vector(cfg.n_dofs, seed=27))
     assert _rel(S.apply(u).cpu().numpy(), G.operator_at(0).apply(u).cpu().numpy()) <= 1e-12
     assert S.dot(u, u) == pytest.approx(float((u * u).sum()), rel=1e-12)
+
+
+def test_weak_scaling_box_partition(cuda):
+    """The N = 2 weak-scaling workload of bench.py (C5: Q4 dG(3), box mesh
+    128 x 128 x 256 cells, 1.08e9 ST dofs) cut into two z-slabs, both held
+    by this process: operator and V-cycle against the unpartitioned solve of
+    the same box mesh (1e-12 / 1e-10)."""
+    from paper_2408_04372_b200 import dist as sdist
+    base = problems.config("C5-128")
+    box = sdist.weak_box(2)
+    mesh = api.Mesh(3, (0, 0, 0), tuple(float(b) for b in box), box, base.refinements)
+    G = api.SpaceTimeMultigrid(base.equation, base.scheme, mesh, None, base.refinements, base.p, base.k,
+                               base.n_steps, base.tau)
+    S = api.SlabMultigrid(base.equation, base.scheme, mesh, None, base.refinements, base.p, base.k, base.n_steps,
+                          base.tau, 2)
+    assert S.dist_levels >= 2
+    for l in range(G.n_levels):
+        assert abs(S.omega_at(l) - G.omega_at(l)) <= 1e-8 * G.omega_at(l)
+        S.set_omega(l, G.omega_at(l))
+    n = G.operator_at(0).n_dofs
+    g = cuda.Generator(device="cuda").manual_seed(8)
+    u = cuda.rand(n, dtype=cuda.float64, device="cuda", generator=g) * 2 - 1
+    want = G.operator_at(0).apply(u)
+    got = S.gather(S.apply(S.scatter(u)), cuda.zeros_like(u))
+    assert float((got - want).norm() / want.norm()) <= 1e-12
+    del want, got
+    want = G.apply(u)
+    got = S.gather(S.vcycle(S.scatter(u)), cuda.zeros_like(u))
+    assert float((got - want).norm() / want.norm()) <= 1e-10

@@ -125,12 +125,13 @@ def test_slab_with_nccl_comm_world1(cuda):
 
 
 def test_weak_scaling_box_partition(cuda):
-    """The N = 2 weak-scaling workload of bench.py (C5: Q4 dG(3), box mesh
-    128 x 128 x 256 cells, 1.08e9 ST dofs) cut into two z-slabs, both held
-    by this process: operator and V-cycle against the unpartitioned solve of
-    the same box mesh (1e-12 / 1e-10)."""
+    """The N = 2 weak-scaling box of bench.py (C5: Q4 dG(3), box mesh of
+    1 x 1 x 2 base cells; here refined to 64 x 64 x 128 cells, 1.36e8 ST dofs,
+    so that the unpartitioned and the partitioned hierarchies fit one GPU
+    together) cut into two z-slabs held by this process: operator and V-cycle
+    against the unpartitioned solve of the same box mesh (1e-12 / 1e-10)."""
     from paper_2408_04372_b200 import dist as sdist
-    base = problems.config("C5-128")
+    base = problems.config("C5-64")
     box = sdist.weak_box(2)
     mesh = api.Mesh(3, (0, 0, 0), tuple(float(b) for b in box), box, base.refinements)
     G = api.SpaceTimeMultigrid(base.equation, base.scheme, mesh, None, base.refinements, base.p, base.k,

@@ -506,422 +506,6 @@ __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant
   fdm_stages<N, NT, TD, MODE == 1>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
 }
 
-// ---------------------------------------------------------------------------
-// Owner-computes FDM sweep (3D): the same cell solves as fdm_lines_kernel, but
-// the weighted sum over the overlapping cells (asm_smoother.cpp:45-49, 75) is
-// formed in shared memory instead of by fp64 atomics into z. A CTA owns a
-// tile of TX x TY cells in x-y and marches a chunk of cell layers along z:
-//   stage: the residual on the layer's (TX p + 1) x (TY p + 1) x (p + 1)
-//     node box (cp.async, issued one layer ahead)
-//   Fy: thread = (x node of the box, plane, field): S_y^T of every y cell of
-//     the tile along its column (node columns on cell faces serve both cells)
-//   Fx: thread = (y cell, y eigen-index, plane, field): S_x^T per x cell
-//   Z:  thread = (cell, x and y eigen-indices): S_z^T, the n_t x n_t solves
-//     at the p + 1 z eigen-indices, S_z
-//   Bx: S_x per x cell, summed at shared x nodes (assembled along x)
-//   By: S_y per y cell, summed at shared y nodes, times the inverse
-//     multiplicity of the node, then z += scale * (.) -- a plain
-//     read-modify-write for nodes only this CTA's cells touch; fp64 atomics
-//     only on the tile's edge nodes and on the chunk's first / last plane.
-//     The layer's top plane is carried in shared memory to the next layer.
-// Dirichlet nodes receive scale * r once (the identity rows summed over the
-// cells divided by the multiplicity), from the CTA owning the node.
-namespace ft {
-constexpr int kT = 512, TX = 4, TY = 4;
-template <int N, int NT>
-struct Cfg {
-  static constexpr int P = N - 1;
-  static constexpr int NX = TX * P + 1, NY = TY * P + 1;
-  // residual box rows [f][b][y], each one 16-byte aligned bulk copy of the
-  // 16-byte aligned span covering the row's NX doubles (x at [s + x], s the
-  // row's start parity): pitch RP doubles
-  static constexpr int RW = ((NX + 1 + 1) / 2) * 2;  // doubles per row copy (NX + 1 rounded to even)
-  static constexpr int RP = RW;
-  static constexpr int ROWS = NT * N * NY;
-  static constexpr int RB = ROWS * RP;
-  // x-assembled / y-transformed data W1[cy][ey][f][b][x]
-  static constexpr int W1 = TY * N * NT * N * NX;
-  // per-cell coefficients W2[cx][ex][cy][ey] x 21-padded (b, f)
-  static constexpr int W2S = N * NT + 1;
-  static constexpr int W2 = TX * N * TY * N * W2S;
-  static constexpr int CY = 2 * NT * NY * NX;  // carried top plane [parity][f][y][x]
-  static constexpr size_t smem_bytes() { return sizeof(double) * static_cast<size_t>(RB + W1 + W2 + CY) + 16; }
-  static constexpr int IFY = NX * N * NT, IFX = TY * N * N * NT, IZ = TX * TY * N * N;
-  static_assert(IFX <= kT && IZ <= kT, "one Fx / Z item per thread");
-};
-
-__device__ __forceinline__ int axis_class(long long c, long long n, bool lo_phys, bool hi_phys) {
-  return (c == 0 && lo_phys ? 1 : 0) | (c == n - 1 && hi_phys ? 2 : 0);
-}
-
-// share of a Dirichlet node's identity row handled here: the cells around it
-// that are not solved by the exact per-cell kernel (skip), over all its cells
-__device__ double dirichlet_share(const DevFDM& P, long long gx, long long gy, long long gz) {
-  if (!P.skip) return 1.0;
-  const int p = P.p;
-  int all = 0, mine = 0;
-  const long long g[3] = {gx, gy, gz};
-  long long lo[3], hi[3];
-  for (int a = 0; a < 3; ++a) {
-    const long long c = g[a] / p;
-    lo[a] = (g[a] % p == 0) ? c - 1 : c;
-    hi[a] = c;
-    if (lo[a] < 0) lo[a] = 0;
-    if (hi[a] > P.cells[a] - 1) hi[a] = P.cells[a] - 1;
-  }
-  for (long long cz = lo[2]; cz <= hi[2]; ++cz)
-    for (long long cy = lo[1]; cy <= hi[1]; ++cy)
-      for (long long cx = lo[0]; cx <= hi[0]; ++cx) {
-        ++all;
-        if (!P.skip[(cz * P.cells[1] + cy) * P.cells[0] + cx]) ++mine;
-      }
-  return all > 0 ? static_cast<double>(mine) / all : 0.0;
-}
-
-__device__ __forceinline__ void bulk_g2s_fdm(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-               "l"(src), "r"(bytes), "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar)))
-               : "memory");
-}
-
-template <int N, int NT, bool TD>
-__global__ void __launch_bounds__(kT, 1) fdm_tile_kernel(const __grid_constant__ DevFDM P, const double* __restrict__ r,
-                                                         double* __restrict__ z, double scale, int ntx, int zc) {
-  using C = Cfg<N, NT>;
-  constexpr int p = C::P, NX = C::NX, NY = C::NY;
-  extern __shared__ __align__(16) double sm[];
-  double* Rb = sm;
-  double* W1 = Rb + C::RB;
-  double* W2 = W1 + C::W1;
-  double* Cy = W2 + C::W2;
-  const int t = threadIdx.x;
-  const long long dx = P.dofs[0], dy = P.dofs[1], dz = P.dofs[2], dxy = dx * dy, ns = P.n_space;
-  const long long ncx = P.cells[0], ncy = P.cells[1];
-  const int ncz = static_cast<int>(P.cells[2]);
-  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
-  const long long cx0 = static_cast<long long>(tx) * TX, cy0 = static_cast<long long>(ty) * TY;
-  const long long X0 = cx0 * p, Y0 = cy0 * p;
-  const int L0 = static_cast<int>(blockIdx.y) * zc, L1 = L0 + zc < ncz ? L0 + zc : ncz;
-  const bool lo_phys = (P.zbc & 1) != 0, hi_phys = (P.zbc & 2) != 0;
-  const long long st = blockIdx.z;  // step: fields st*NT .. st*NT + NT - 1
-  const double* rs = r + st * NT * ns;
-  double* zs = z + st * NT * ns;
-
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(Cy + C::CY);
-  const long long total = static_cast<long long>(P.S) * NT * ns;
-  // ---- stage the residual box of layer e: thread t < ROWS issues row t as
-  // one bulk copy (rows beyond the lattice are zero-filled, the array's last
-  // row avoids reading past the end)
-  auto stage = [&](int e) {
-    if (t < C::ROWS) {
-      const int y = t % NY, fb = t / NY;
-      const int b = fb % N, f = fb / N;
-      const long long gy = Y0 + y;
-      double* dst = Rb + t * C::RP;
-      if (gy < dy) {
-        const long long g = (st * NT + f) * ns + (static_cast<long long>(e) * p + b) * dxy + gy * dx + X0;
-        const long long g0 = g & ~1LL;
-        if (g0 + C::RW <= total) {
-          bulk_g2s_fdm(dst, r + g0, sizeof(double) * C::RW, bar);
-        } else {
-          const int n16 = static_cast<int>(((total - g0) / 2) * 2);
-          if (n16 > 0) bulk_g2s_fdm(dst, r + g0, sizeof(double) * n16, bar);
-          for (int k = n16; k < C::RW; ++k) dst[k] = g0 + k < total ? r[g0 + k] : 0.0;
-          if (n16 < C::RW) asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(
-                                          static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-                                      "r"(static_cast<unsigned>(sizeof(double) * (C::RW - n16)))
-                                      : "memory");
-        }
-      } else {
-        for (int k = 0; k < C::RW; ++k) dst[k] = 0.0;
-        asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(
-                         static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-                     "r"(static_cast<unsigned>(sizeof(double) * C::RW))
-                     : "memory");
-      }
-    }
-  };
-  auto stage_arm = [&]() {
-    if (t == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-                   "r"(static_cast<unsigned>(sizeof(double) * C::RW * C::ROWS))
-                   : "memory");
-  };
-  // start parity of box row (f, b, y): x = 0 of the row sits at [s + 0]
-  auto row_shift = [&](int f, int b, int y, int e) -> int {
-    const long long g = (st * NT + f) * ns + (static_cast<long long>(e) * p + b) * dxy + (Y0 + y) * dx + X0;
-    return static_cast<int>(g & 1);
-  };
-
-  // per-item identities
-  // Fy / By: items i = x + NX (b + N f) (x node, plane b, field f), looped
-  // Fx / Bx: (cy, ey, f, b) -- t = b + N (f + NT (ey + N cy))
-  const int fx_b = t % N, fx_f = (t / N) % NT, fx_ey = (t / (N * NT)) % N, fx_cy = t / (N * NT * N);
-  // Z: (ey, cy, ex, cx) -- t = ey + N (cy + TY (ex + N cx))
-  const int z_ey = t % N, z_cy = (t / N) % TY, z_ex = (t / (N * TY)) % N, z_cx = t / (N * TY * N);
-  auto w1 = [&](int cy, int ey, int f, int b, int x) { return W1 + (((cy * N + ey) * NT + f) * N + b) * NX + x; };
-  auto w2 = [&](int cx, int ex, int cy, int ey) { return W2 + ((ey + N * cy) + TY * N * (ex + N * cx)) * C::W2S; };
-
-  if (t == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
-                 "r"(1u)
-                 : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  stage_arm();
-  stage(L0);
-  unsigned phase = 0;
-  for (int e = L0; e < L1; ++e) {
-    {
-      unsigned ok = 0;
-      for (long long spin = 0; !ok; ++spin) {
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(phase)
-            : "memory");
-        if (spin > (1LL << 28)) __trap();
-      }
-      phase ^= 1;
-    }
-    __syncthreads();
-    const int tz = axis_class(e, ncz, lo_phys, hi_phys);
-    // ---- Fy: S_y^T of each y cell along the node column
-    for (int it = t; it < C::IFY; it += kT) {
-      const int fy_x = it % NX, fy_b = (it / NX) % N, fy_f = it / (NX * N);
-      const double* col = Rb + (fy_f * N + fy_b) * NY * C::RP + fy_x;
-      const int s0 = row_shift(fy_f, fy_b, 0, e);
-#pragma unroll
-      for (int cy = 0; cy < TY; ++cy) {
-        double in[N], out[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          const int yy = cy * p + k;
-          in[k] = col[yy * C::RP + (s0 ^ (yy & static_cast<int>(dx & 1)))];
-        }
-        const int cls = axis_class(cy0 + cy, ncy, true, true);
-        if (cls == 0 && P.eo)
-          fdm_fwd<N, true>(P.S1[1][0], in, out);
-        else
-          fdm_fwd<N, false>(P.S1[1][cls], in, out);
-#pragma unroll
-        for (int k = 0; k < N; ++k) *w1(cy, k, fy_f, fy_b, fy_x) = out[k];
-      }
-    }
-    __syncthreads();
-    if (e + 1 < L1) {  // the box is consumed: stage the next layer
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      stage_arm();
-      stage(e + 1);
-    }
-    // ---- Fx: S_x^T per x cell
-    if (t < C::IFX) {
-      const double* row = w1(fx_cy, fx_ey, fx_f, fx_b, 0);
-#pragma unroll
-      for (int cx = 0; cx < TX; ++cx) {
-        double in[N], out[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) in[k] = row[cx * p + k];
-        const int cls = axis_class(cx0 + cx, ncx, true, true);
-        if (cls == 0 && P.eo)
-          fdm_fwd<N, true>(P.S1[0][0], in, out);
-        else
-          fdm_fwd<N, false>(P.S1[0][cls], in, out);
-#pragma unroll
-        for (int k = 0; k < N; ++k) w2(cx, k, fx_cy, fx_ey)[fx_b + N * fx_f] = out[k];
-      }
-    }
-    __syncthreads();
-    // ---- Z: S_z^T, temporal solves, S_z for one (cell, ex, ey)
-    if (t < C::IZ) {
-      double* v = w2(z_cx, z_ex, z_cy, z_ey);
-      const long long gcx = cx0 + z_cx, gcy = cy0 + z_cy;
-      const bool valid = gcx < ncx && gcy < ncy &&
-                         !(P.skip && P.skip[(static_cast<long long>(e) * ncy + gcy) * ncx + gcx]);
-      double a[NT][N];
-      if (valid) {
-        const int cxs = axis_class(gcx, ncx, true, true), cys = axis_class(gcy, ncy, true, true);
-        double rho = 1.0;
-        if (P.rho0) {
-          const long long ax = gcx >> P.rho_shift, ay = gcy >> P.rho_shift, az = (e + P.cz0) >> P.rho_shift;
-          rho = __ldg(P.rho0 + (az * P.cells0[1] + ay) * P.cells0[0] + ax);
-        }
-#pragma unroll
-        for (int f = 0; f < NT; ++f) {
-          double in[N];
-#pragma unroll
-          for (int k = 0; k < N; ++k) in[k] = v[k + N * f];
-          if (tz == 0 && P.eo)
-            fdm_fwd<N, true>(P.S1[2][0], in, a[f]);
-          else
-            fdm_fwd<N, false>(P.S1[2][tz], in, a[f]);
-        }
-        const double lxy = P.L1[0][cxs][z_ex] + P.L1[1][cys][z_ey];
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double bb[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-          for (int f = 0; f < NT; ++f) bb[f] = a[f][k];
-          temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][tz][k]), bb);
-#pragma unroll
-          for (int f = 0; f < NT; ++f) a[f][k] = bb[f];
-        }
-#pragma unroll
-        for (int f = 0; f < NT; ++f) {
-          double out[N];
-          if (tz == 0 && P.eo)
-            fdm_bwd<N, true>(P.S1[2][0], a[f], out);
-          else
-            fdm_bwd<N, false>(P.S1[2][tz], a[f], out);
-#pragma unroll
-          for (int k = 0; k < N; ++k) v[k + N * f] = out[k];
-        }
-      } else {
-#pragma unroll
-        for (int f = 0; f < NT; ++f)
-#pragma unroll
-          for (int k = 0; k < N; ++k) v[k + N * f] = 0.0;
-      }
-    }
-    __syncthreads();
-    // ---- Bx: S_x per x cell, assembled along x
-    if (t < C::IFX) {
-      double* row = w1(fx_cy, fx_ey, fx_f, fx_b, 0);
-      double carry = 0.0;
-#pragma unroll
-      for (int cx = 0; cx < TX; ++cx) {
-        double in[N], out[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) in[k] = w2(cx, k, fx_cy, fx_ey)[fx_b + N * fx_f];
-        const int cls = axis_class(cx0 + cx, ncx, true, true);
-        if (cls == 0 && P.eo)
-          fdm_bwd<N, true>(P.S1[0][0], in, out);
-        else
-          fdm_bwd<N, false>(P.S1[0][cls], in, out);
-        row[cx * p] = carry + out[0];
-#pragma unroll
-        for (int k = 1; k < p; ++k) row[cx * p + k] = out[k];
-        carry = out[p];
-      }
-      row[TX * p] = carry;
-    }
-    __syncthreads();
-    // ---- By: S_y per y cell, assembled along y; weights; write
-    for (int it = t; it < C::IFY; it += kT) {
-      const int x = it % NX, b = (it / NX) % N, f = it / (NX * N);
-      double col[NY];
-      {
-        double carry = 0.0;
-#pragma unroll
-        for (int cy = 0; cy < TY; ++cy) {
-          double in[N], out[N];
-#pragma unroll
-          for (int k = 0; k < N; ++k) in[k] = *w1(cy, k, f, b, x);
-          const int cls = axis_class(cy0 + cy, ncy, true, true);
-          if (cls == 0 && P.eo)
-            fdm_bwd<N, true>(P.S1[1][0], in, out);
-          else
-            fdm_bwd<N, false>(P.S1[1][cls], in, out);
-          col[cy * p] = carry + out[0];
-#pragma unroll
-          for (int k = 1; k < p; ++k) col[cy * p + k] = out[k];
-          carry = out[p];
-        }
-        col[TY * p] = carry;
-      }
-      const long long gz = static_cast<long long>(e) * p + b;
-      const long long gx = X0 + x;
-      // the layer's bottom plane: add the previous layer's top plane (carry
-      // buffers alternate with the layer parity)
-      if (b == 0 && e > L0) {
-        const double* cin = Cy + ((((e - 1) & 1) * NT + f) * NY) * NX + x;
-#pragma unroll
-        for (int y = 0; y < NY; ++y) col[y] += cin[y * NX];
-      }
-      const bool last_layer = e == L1 - 1;
-      if (b == p && !last_layer) {
-        double* cout = Cy + (((e & 1) * NT + f) * NY) * NX + x;
-#pragma unroll
-        for (int y = 0; y < NY; ++y) cout[y * NX] = col[y];
-      } else if (gx < dx) {
-        // plane gz is final here, or (chunk-boundary planes) a partial sum
-        const bool zshared = (b == 0 && e == L0 && L0 > 0) || (b == p && L1 < ncz);
-        const bool zdir = (gz == 0 && lo_phys) || (gz == dz - 1 && hi_phys);
-        const bool z_owner = b < p || L1 == ncz;  // Dirichlet r added once
-        const bool xdir = gx == 0 || gx == dx - 1;
-        const bool xedge = (x == 0 && tx > 0) || (x == NX - 1 && gx != dx - 1);
-        const bool xown = x < NX - 1 || gx == dx - 1;
-        const double wz = (gz % p == 0 && !zdir) ? 0.5 : 1.0;
-        // a slab's interface plane: the other slab holds the other half of
-        // the node's cells (the interface sum adds its share)
-        const double ziface = ((gz == 0 && !lo_phys) || (gz == dz - 1 && !hi_phys)) ? 0.5 : 1.0;
-        const double wx = (gx % p == 0 && !xdir) ? 0.5 : 1.0;
-        double* zp = zs + f * ns + gz * dxy + gx;
-        const double* rp = rs + f * ns + gz * dxy + gx;
-        // plain read-modify-write nodes: all old values requested first
-        double old[NY];
-        bool plain[NY];
-#pragma unroll
-        for (int y = 0; y < NY; ++y) {
-          const long long gy = Y0 + y;
-          const bool in = gy < dy;
-          const bool ydir = gy == 0 || gy == dy - 1;
-          const bool yedge = (y == 0 && ty > 0) || (y == NY - 1 && gy != dy - 1);
-          plain[y] = in && !(zdir || xdir || ydir) && !(zshared || xedge || yedge);
-          old[y] = plain[y] ? zp[gy * dx] : 0.0;
-        }
-#pragma unroll
-        for (int y = 0; y < NY; ++y) {
-          const long long gy = Y0 + y;
-          if (gy >= dy) break;
-          const bool ydir = gy == 0 || gy == dy - 1;
-          const bool yown = y < NY - 1 || gy == dy - 1;
-          if (zdir || xdir || ydir) {
-            if (z_owner && xown && yown)
-              zp[gy * dx] += scale * ziface * dirichlet_share(P, gx, gy, gz) * __ldg(rp + gy * dx);
-            continue;
-          }
-          const double wy = (gy % p == 0) ? 0.5 : 1.0;
-          const double val = scale * wx * wy * wz * col[y];
-          if (plain[y])
-            zp[gy * dx] = old[y] + val;
-          else
-            atomicAdd(zp + gy * dx, val);
-        }
-      }
-    }
-  }
-}
-}  // namespace ft
-
-template <int N, int NT>
-void launch_tile(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
-  using C = ft::Cfg<N, NT>;
-  const long long ntx = (P.cells[0] + ft::TX - 1) / ft::TX, nty = (P.cells[1] + ft::TY - 1) / ft::TY;
-  const long long tiles = ntx * nty, ncz = P.cells[2];
-  long long nch = std::max<long long>(1, (148LL * 12 + tiles * P.S - 1) / (tiles * P.S));
-  nch = std::min<long long>(nch, std::max<long long>(1, ncz / 2));
-  const long long zc = (ncz + nch - 1) / nch;
-  nch = (ncz + zc - 1) / zc;
-  const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nch), static_cast<unsigned>(P.S));
-  count_launch();
-  auto go = [&](auto kern) {
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::smem_bytes()));
-      configured = true;
-    }
-    kern<<<grid, ft::kT, C::smem_bytes(), s>>>(P, r, z, scale, static_cast<int>(ntx), static_cast<int>(zc));
-  };
-  if (P.tdiag)
-    go(ft::fdm_tile_kernel<N, NT, true>);
-  else
-    go(ft::fdm_tile_kernel<N, NT, false>);
-}
-
 template <int N, int NT>
 void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
   constexpr int NC = 128 / (N * N);
@@ -947,11 +531,6 @@ void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cud
 template <int DIM, int N, int NT>
 void launch(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
   if (DIM == 3) {
-    // owner-computes tiles where one layer of TX x TY cells fits a CTA
-    if constexpr (ft::Cfg<N, NT>::IFX <= ft::kT && ft::Cfg<N, NT>::IZ <= ft::kT) {
-      launch_tile<N, NT>(P, r, z, scale, s);
-      return;
-    }
     launch_lines<N, NT>(P, r, z, scale, s);
     return;
   }

@@ -480,8 +480,511 @@ __global__ void __launch_bounds__(kThreads, STB_MINB)
   if (L1 == ncz) store_plane(z_last, 0);
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-specialised form of the same schedule (F <= 4). The three stages run
+// as three groups of warps on different planes at the same time, coupled by
+// shared-memory rings and mbarriers instead of CTA-wide barriers:
+//   Y warps: column (x, field) of the input box; the column of u is staged by
+//            the thread's own cp.async NSU - 1 planes ahead; a = My u,
+//            b = Ky u -> ring AB
+//   X warps: half row (row, field): c = Mx a, pre = Kx a / hx^2 + Mx b / hy^2
+//            -> ring CP
+//   Z warps: owned point: temporal coupling, z window in registers, stores
+// so no warp idles while another stage runs (the barrier after stage Y held
+// 18 % of the stall samples of st_brick_kernel: 168 of 256 threads have a
+// stage-Y item), and each group keeps only its own tables in registers.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait: a ring that never advances traps instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  for (long long spin = 0; !mbar_try_wait(bar, phase); ++spin)
+    if (spin > (1LL << 26)) __trap();
+}
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+}
+
+#ifndef STB_NSU
+#define STB_NSU 4
+#endif
+#ifndef STB_NSA
+#define STB_NSA 3
+#endif
+#ifndef STB_NSC
+#define STB_NSC 3
+#endif
+
+template <int N, int F>
+struct WsCfg {
+  using C = Cfg<N, F>;
+  static_assert(C::FG == 1, "warp-specialised form: all fields in one stage-Z thread");
+  static constexpr int YI = C::WX * F;            // stage-Y items per plane
+  static constexpr int XI = C::XH * C::OY * F;    // stage-X items per plane
+  static constexpr int ZI = C::OX * C::OY;        // stage-Z items per plane
+  static constexpr int YW = (YI + 31) / 32, XW = (XI + 31) / 32, ZW = ZI / 32;
+  static constexpr int THREADS = 32 * (YW + XW + ZW);
+  static constexpr int NSU = STB_NSU, NSA = STB_NSA, NSC = STB_NSC;  // ring depths (planes)
+  static constexpr int U_S = F * C::UB_F;          // one plane of the staged u boxes
+  static constexpr int AB_S = 2 * F * C::AB_F;     // one plane of a and b
+  static constexpr int CP_S = 2 * F * C::CP_F;     // one plane of c and pre
+  static constexpr int NBAR = 2 * NSA + 2 * NSC;
+  static constexpr size_t smem_bytes() {
+    return sizeof(double) * (static_cast<size_t>(NSU) * U_S + NSA * AB_S + NSC * CP_S) + 8 * NBAR;
+  }
+};
+
+template <int N, int F, bool RES>
+__global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
+    st_brick_ws_kernel(const __grid_constant__ DevLevel L, const double* __restrict__ u,
+                       const double* __restrict__ fvec, double* __restrict__ y, int ntx, int zc) {
+  using C = Cfg<N, F>;
+  using W = WsCfg<N, F>;
+  constexpr int P = C::P, OX = C::OX, OY = C::OY, WX = C::WX, WY = C::WY;
+  constexpr int NSU = W::NSU, NSA = W::NSA, NSC = W::NSC;
+  extern __shared__ __align__(16) double smem[];
+  double* Ub = smem;
+  double* ABr = Ub + NSU * W::U_S;
+  double* CPr = ABr + NSA * W::AB_S;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(CPr + NSC * W::CP_S);
+  unsigned long long* ab_full = bars;
+  unsigned long long* ab_empty = bars + NSA;
+  unsigned long long* cp_full = bars + 2 * NSA;
+  unsigned long long* cp_empty = bars + 2 * NSA + NSC;
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (t == 0) {
+    for (int i = 0; i < NSA; ++i) {
+      mbar_init(ab_full + i, W::YW);
+      mbar_init(ab_empty + i, W::XW);
+    }
+    for (int i = 0; i < NSC; ++i) {
+      mbar_init(cp_full + i, W::XW);
+      mbar_init(cp_empty + i, W::ZW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+  const long long X0 = static_cast<long long>(tx) * OX, Y0 = static_cast<long long>(ty) * OY;
+  const long long dx = L.dofs[0], dy = L.dofs[1], dz = L.dofs[2];
+  const long long dxy = dx * dy, ns = L.n_space;
+  const int ncz = static_cast<int>(L.cells[2]);
+  const int L0 = static_cast<int>(blockIdx.y) * zc;
+  const int L1 = L0 + zc < ncz ? L0 + zc : ncz;
+  const int Ls = L0 > 0 ? L0 - 1 : 0;  // first layer processed (halo)
+  const int z_first = Ls * P, z_last = L1 * P;
+  const bool lo_dir = (L.zbc & 1) != 0, hi_dir = (L.zbc & 2) != 0;
+
+  if (warp < W::YW) {
+    // ================= stage Y =================
+    const bool act = t < W::YI;
+    const int yx = t % WX, yf = act ? t / WX : 0;
+    int rlo = 0, rhi = 0;  // rows [rlo, rhi) of the column lie inside the lattice, off its Dirichlet faces
+    const double* ybase = u;
+    {
+      const long long gxx = X0 - P + yx;
+      if (act && gxx > 0 && gxx < dx - 1) {
+        rlo = static_cast<int>(Y0 - P) < 1 ? static_cast<int>(1 - (Y0 - P)) : 0;
+        const long long rmax = dy - 1 - (Y0 - P);  // first row at or beyond the high face
+        rhi = rmax < WY ? static_cast<int>(rmax) : WY;
+        ybase = u + yf * ns + (Y0 - P + rlo) * dx + gxx;
+      }
+    }
+    const bool full_col = rlo == 0 && rhi == WY;
+    double* ucol0 = Ub + yf * C::UB_F + yx;
+    // every thread commits exactly one group per call (empty past the end)
+    auto stage_u = [&](int z, int slot) {
+      if (act && z <= z_last) {
+        double* dst = ucol0 + slot * W::U_S;
+        const bool zd = (z == 0 && lo_dir) || (z == dz - 1 && hi_dir);
+        const double* src = ybase + z * dxy;
+        if (!zd && full_col) {
+#pragma unroll
+          for (int r = 0; r < WY; ++r) cp_async8(dst + r * WX, src + r * dx, 8);
+        } else {
+#pragma unroll
+          for (int r = 0; r < WY; ++r) {
+            const bool ok = !zd && r >= rlo && r < rhi;
+            cp_async8(dst + r * WX, ok ? src + (r - rlo) * dx : u, ok ? 8 : 0);
+          }
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < NSU - 1; ++i) stage_u(z_first + i, i);
+    int su = 0, sa = 0;
+    unsigned pa = 1;  // parity the empty ring is waited on (fresh barrier: passes)
+    for (int z = z_first; z <= z_last; ++z) {
+      cp_async_wait<NSU - 2>();
+      mbar_wait(ab_empty + sa, pa);
+      // refill the slot consumed one plane ago
+      stage_u(z + NSU - 1, su == 0 ? NSU - 1 : su - 1);
+      if (act) {
+        const double* ycolbuf = ucol0 + su * W::U_S;
+        double* oa = ABr + sa * W::AB_S + yf * C::AB_F + yx;
+        double* ob = oa + F * C::AB_F;
+        // element 0 is the halo cell: it reaches owned row 0 only
+        double v[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = ycolbuf[k * WX];
+        double ca, cb;
+        {
+          const Split<N> s = split_at<N>(v);
+          ca = elem_last<N>(L.MrE, L.MrO, s);
+          cb = elem_last<N>(L.KrE, L.KrO, s);
+        }
+#pragma unroll
+        for (int e = 1; e <= OY / P; ++e) {
+          v[0] = v[P];
+#pragma unroll
+          for (int k = 1; k < N; ++k) v[k] = ycolbuf[(e * P + k) * WX];
+          const Split<N> s = split_at<N>(v);
+          double ea[N], eb[N];
+          elem<N>(L.MrE, L.MrO, s, ea);
+          elem<N>(L.KrE, L.KrO, s, eb);
+          const int r0 = (e - 1) * P;
+          oa[r0 * C::XP] = ca + ea[0];
+          ob[r0 * C::XP] = cb + eb[0];
+#pragma unroll
+          for (int j = 1; j < P; ++j) {
+            oa[(r0 + j) * C::XP] = ea[j];
+            ob[(r0 + j) * C::XP] = eb[j];
+          }
+          ca = ea[P];
+          cb = eb[P];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ab_full + sa);
+      if (++su == NSU) su = 0;
+      if (++sa == NSA) {
+        sa = 0;
+        pa ^= 1;
+      }
+    }
+    cp_async_wait<0>();
+  } else if (warp < W::YW + W::XW) {
+    // ================= stage X =================
+    constexpr int HX = OX / C::XH;  // owned columns per half
+    const int i = t - 32 * W::YW;
+    const bool act = i < W::XI;
+    const int h = i % C::XH, rf = i / C::XH;
+    const int r = rf % OY, f = act ? rf / OY : 0;
+    const double sx = L.hinv2[0], sy = L.hinv2[1];
+    const int ioff = f * C::AB_F + r * C::XP + h * HX;
+    const int ooff = f * C::CP_F + r * C::CPP + h * HX;
+    int sa = 0, sc = 0;
+    unsigned pa = 0, pc = 1;
+    for (int z = z_first; z <= z_last; ++z) {
+      mbar_wait(ab_full + sa, pa);
+      mbar_wait(cp_empty + sc, pc);
+      if (act) {
+        const double* ia = ABr + sa * W::AB_S + ioff;
+        const double* ib = ia + F * C::AB_F;
+        double* oc = CPr + sc * W::CP_S + ooff;
+        double* op = oc + F * C::CP_F;
+        double va[N], vb[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          va[k] = ia[k];
+          vb[k] = ib[k];
+        }
+        double cc, cp;
+        {
+          const Split<N> sa_ = split_at<N>(va), sb_ = split_at<N>(vb);
+          cc = elem_last<N>(L.MrE, L.MrO, sa_);
+          cp = fma(sx, elem_last<N>(L.KrE, L.KrO, sa_), sy * elem_last<N>(L.MrE, L.MrO, sb_));
+        }
+#pragma unroll
+        for (int e = 1; e <= HX / P; ++e) {
+          va[0] = va[P];
+          vb[0] = vb[P];
+#pragma unroll
+          for (int k = 1; k < N; ++k) {
+            va[k] = ia[e * P + k];
+            vb[k] = ib[e * P + k];
+          }
+          const Split<N> sa_ = split_at<N>(va), sb_ = split_at<N>(vb);
+          double ec[N], ek[N], em[N];
+          elem<N>(L.MrE, L.MrO, sa_, ec);
+          elem<N>(L.KrE, L.KrO, sa_, ek);
+          elem<N>(L.MrE, L.MrO, sb_, em);
+          const int r0 = (e - 1) * P;
+          oc[r0] = cc + ec[0];
+          op[r0] = cp + fma(sx, ek[0], sy * em[0]);
+#pragma unroll
+          for (int j = 1; j < P; ++j) {
+            oc[r0 + j] = ec[j];
+            op[r0 + j] = fma(sx, ek[j], sy * em[j]);
+          }
+          cc = ec[P];
+          cp = fma(sx, ek[P], sy * em[P]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(ab_empty + sa);
+        mbar_arrive(cp_full + sc);
+      }
+      if (++sa == NSA) {
+        sa = 0;
+        pa ^= 1;
+      }
+      if (++sc == NSC) {
+        sc = 0;
+        pc ^= 1;
+      }
+    }
+  } else {
+    // ================= stage Z =================
+    const int pt = t - 32 * (W::YW + W::XW);
+    const int zx = pt % OX, zy = pt / OX;
+    const long long gx = X0 + zx, gy = Y0 + zy;
+    const double V = L.h[0] * L.h[1] * L.h[2];
+    const double sz = L.hinv2[2];
+    auto rho_of = [&](int e) -> double {
+      if (!L.rho0) return 1.0;
+      const long long az = (e + L.cz0) >> L.rho_shift;
+      return __ldg(L.rho0 + az * L.cells0[1] * L.cells0[0]);
+    };
+    // the point is written by this CTA if it lies on the lattice; x / y end
+    // planes (always Dirichlet) are written by the tile containing them, or by
+    // the last tile's border threads when the tile ends exactly on them
+    const bool on_lat = gx < dx && gy < dy;
+    const long long pbase = gy * dx + gx;
+    const bool xend_extra = (zx == OX - 1) && (X0 + OX == dx - 1);
+    const bool yend_extra = (zy == OY - 1) && (Y0 + OY == dy - 1);
+    const bool xy_dir = gx == 0 || gy == 0 || gx == dx - 1 || gy == dy - 1;
+
+    double win[F][N];  // z window of the open layer
+#pragma unroll
+    for (int i = 0; i < F; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) win[i][j] = 0.0;
+
+    // Dirichlet row: u (residual f - u); on a slab's low interface plane the
+    // row belongs to the slab below, this copy holds 0 (the interface sum adds it)
+    auto store_dir = [&](long long x, long long yy, long long zz) {
+      const bool other = zz == 0 && !lo_dir;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const long long idx = f * ns + zz * dxy + yy * dx + x;
+        if (other) {
+          y[idx] = 0.0;
+        } else {
+          const double uv = __ldg(u + idx);
+          y[idx] = RES ? __ldg(fvec + idx) - uv : uv;
+        }
+      }
+    };
+    // residual: pull the f entries of layer e's owned planes towards L2 when
+    // the layer opens; they are read when it closes, p planes later
+    auto prefetch_layer = [&](int e) {
+      if (!RES || !on_lat || e < L0) return;
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const double* base = fvec + static_cast<long long>(e * P + q) * dxy + pbase;
+#pragma unroll
+        for (int f = 0; f < F; ++f) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + f * ns));
+      }
+    };
+    auto store_plane = [&](long long zz, int jw) {
+      const bool zdir = (zz == 0 && lo_dir) || (zz == dz - 1 && hi_dir);
+      if (on_lat) {
+        if (zdir || xy_dir) {
+          store_dir(gx, gy, zz);
+        } else {
+          const bool no_f = (zz == 0 && !lo_dir);  // low interface plane: f counted by the slab below
+          const long long base = zz * dxy + pbase;
+          double out[F];
+          if (L.g_ok) {
+#pragma unroll
+            for (int i = 0; i < F; ++i) {
+              double v = 0.0;
+#pragma unroll
+              for (int h = 0; h < F; ++h) v = fma(L.CA[i * F + h], win[h][jw], v);
+              out[i] = v;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < F; ++i) out[i] = win[i][jw];
+          }
+#pragma unroll
+          for (int i = 0; i < F; ++i) {
+            const long long idx = base + i * ns;
+            if (RES)
+              y[idx] = no_f ? -out[i] : __ldg(fvec + idx) - out[i];
+            else
+              y[idx] = out[i];
+          }
+        }
+      }
+      if (xend_extra && gy < dy) store_dir(dx - 1, gy, zz);
+      if (yend_extra && gx < dx) store_dir(gx, dy - 1, zz);
+      if (xend_extra && yend_extra) store_dir(dx - 1, dy - 1, zz);
+    };
+
+    prefetch_layer(Ls);
+    const int coff = zy * C::CPP + zx;
+    int sc = 0;
+    unsigned pc = 0;
+    int e_of = Ls, j = 0;  // z = e_of * P + j
+    for (int z = z_first; z <= z_last; ++z) {
+      mbar_wait(cp_full + sc, pc);
+      double vc[F], vp[F];
+      {
+        const double* ic = CPr + sc * W::CP_S + coff;
+        const double* ip = ic + F * C::CP_F;
+#pragma unroll
+        for (int gg = 0; gg < F; ++gg) {
+          vc[gg] = ic[gg * C::CP_F];
+          vp[gg] = ip[gg * C::CP_F];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(cp_empty + sc);
+      if (++sc == NSC) {
+        sc = 0;
+        pc ^= 1;
+      }
+      double cmc[F], cap[F], cac[F];
+      if (L.g_ok) {
+        // (CA (x) I)(G (x) M + I (x) A): G c on the point, CA at the store
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int gg = 0; gg < F; ++gg) s = fma(L.G[i * F + gg], vc[gg], s);
+          cmc[i] = s;
+          cap[i] = vp[i];
+          cac[i] = vc[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+          double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+          for (int gg = 0; gg < F; ++gg) {
+            const double cm = L.CM[i * F + gg], ca = L.CA[i * F + gg];
+            a = fma(cm, vc[gg], a);
+            b = fma(ca, vp[gg], b);
+            c = fma(ca, vc[gg], c);
+          }
+          cmc[i] = a;
+          cap[i] = b;
+          cac[i] = c;
+        }
+      }
+      // contribution of this plane to layer e at local index jl
+      auto add_layer = [&](int e, int jl) {
+        const double rho = rho_of(e);
+        const double rv = rho * V * sz;
+        double mc[N], kc[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          mc[q] = L.Mr[q][jl];
+          kc[q] = L.Kr[q][jl];
+        }
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+          const double zm = V * fma(rho, cap[i], cmc[i]);
+          const double zk = rv * cac[i];
+#pragma unroll
+          for (int q = 0; q < N; ++q) win[i][q] = fma(mc[q], zm, fma(kc[q], zk, win[i][q]));
+        }
+      };
+      if (j == 0 && z > z_first) {
+        // vertex plane: close layer e - 1; its p lower planes are final
+        const int e = e_of - 1;
+        add_layer(e, P);
+        if (e >= L0) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) store_plane(static_cast<long long>(e) * P + q, q);
+        }
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+          win[i][0] = win[i][P];
+#pragma unroll
+          for (int q = 1; q < N; ++q) win[i][q] = 0.0;
+        }
+        if (z < z_last) prefetch_layer(e_of);
+      }
+      if (z < z_last) add_layer(e_of, j);
+      if (++j == P) {
+        j = 0;
+        ++e_of;
+      }
+    }
+    // the slab's top plane: Dirichlet, or an interface partial sum
+    if (L1 == ncz) store_plane(z_last, 0);
+  }
+}
+
+template <int N, int F>
+void launch_ws(const DevLevel& L, const double* u, const double* f, double* y, cudaStream_t s) {
+  using C = Cfg<N, F>;
+  using W = WsCfg<N, F>;
+  static bool configured = false;
+  if (!configured) {
+    for (auto k : {st_brick_ws_kernel<N, F, false>, st_brick_ws_kernel<N, F, true>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(W::smem_bytes()));
+    configured = true;
+  }
+  const long long ntx = std::max<long long>(1, (L.dofs[0] - 1 + C::OX - 1) / C::OX);
+  const long long nty = std::max<long long>(1, (L.dofs[1] - 1 + C::OY - 1) / C::OY);
+  const long long tiles = ntx * nty;
+  const long long ncz = L.cells[2];
+  // one CTA per SM: ~8 CTAs per SM over the launch, chunks of >= 4 layers (halo layer cost)
+  long long nch = std::max<long long>(1, (148LL * 8 + tiles - 1) / tiles);
+  nch = std::min<long long>(nch, std::max<long long>(1, ncz / 4));
+  const long long zc = (ncz + nch - 1) / nch;
+  nch = (ncz + zc - 1) / zc;
+  const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nch));
+  count_launch();
+  if (f)
+    st_brick_ws_kernel<N, F, true><<<grid, W::THREADS, W::smem_bytes(), s>>>(L, u, f, y, static_cast<int>(ntx),
+                                                                             static_cast<int>(zc));
+  else
+    st_brick_ws_kernel<N, F, false><<<grid, W::THREADS, W::smem_bytes(), s>>>(L, u, nullptr, y, static_cast<int>(ntx),
+                                                                              static_cast<int>(zc));
+}
+
+#ifndef STB_WS
+#define STB_WS 1
+#endif
+
 template <int N, int F>
 void launch(const DevLevel& L, const double* u, const double* f, double* y, cudaStream_t s) {
+  using C = Cfg<N, F>;
+  if constexpr (STB_WS && C::FG == 1) {
+    launch_ws<N, F>(L, u, f, y, s);
+    return;
+  }
+
   using C = Cfg<N, F>;
   static bool configured = false;
   if (!configured) {

@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <stdexcept>
+#include <type_traits>
 
 #include "kernels.hpp"
 #include "st_cart.cuh"
@@ -482,12 +483,14 @@ __global__ void __launch_bounds__(kThreads, STB_MINB)
 
 
 // ---------------------------------------------------------------------------
-// Warp-specialised form of the same schedule (F <= 4). The three stages run
-// as three groups of warps on different planes at the same time, coupled by
+// Warp-specialised form of the same schedule (F <= 4). The stages run as
+// groups of warps on different planes at the same time, coupled by
 // shared-memory rings and mbarriers instead of CTA-wide barriers:
-//   Y warps: column (x, field) of the input box; the column of u is staged by
-//            the thread's own cp.async NSU - 1 planes ahead; a = My u,
-//            b = Ky u -> ring AB
+//   loader warp: stages the (WY x WX) input box of every field of a plane
+//            with 8-byte cp.async (Dirichlet and out-of-domain inputs
+//            zero-filled, spatial_operator.cpp:304-307), NSU planes ahead;
+//            completion is counted on the ring's mbarrier
+//   Y warps: column (x, field) of the box: a = My u, b = Ky u -> ring AB
 //   X warps: half row (row, field): c = Mx a, pre = Kx a / hx^2 + Mx b / hy^2
 //            -> ring CP
 //   Z warps: owned point: temporal coupling, z window in registers, stores
@@ -503,27 +506,30 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// the executing thread's earlier cp.async copies arrive on the barrier when they land
+__device__ __forceinline__ void cp_async_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned phase) {
   unsigned ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
       "selp.u32 %0, 1, 0, p;\n"
       "}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(4000u)
       : "memory");
   return ok != 0;
 }
 // bounded wait: a ring that never advances traps instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
-  for (long long spin = 0; !mbar_try_wait(bar, phase); ++spin)
-    if (spin > (1LL << 26)) __trap();
+  for (unsigned spin = 0; !mbar_try_wait(bar, phase); ++spin)
+    if (spin > (1u << 22)) __trap();
 }
-template <int K>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory");
+__device__ __forceinline__ void cp_async8_s(unsigned dst, const double* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
 }
 
 #ifndef STB_NSU
@@ -544,16 +550,21 @@ struct WsCfg {
   static constexpr int XI = C::XH * C::OY * F;    // stage-X items per plane
   static constexpr int ZI = C::OX * C::OY;        // stage-Z items per plane
   static constexpr int YW = (YI + 31) / 32, XW = (XI + 31) / 32, ZW = ZI / 32;
-  static constexpr int THREADS = 32 * (YW + XW + ZW);
+  static constexpr int THREADS = 32 * (1 + YW + XW + ZW);
+  static constexpr int BOX = C::WX * C::WY;       // entries of one field's input box
+  static constexpr int NI = (BOX + 31) / 32;      // loader copies per lane and field
   static constexpr int NSU = STB_NSU, NSA = STB_NSA, NSC = STB_NSC;  // ring depths (planes)
   static constexpr int U_S = F * C::UB_F;          // one plane of the staged u boxes
   static constexpr int AB_S = 2 * F * C::AB_F;     // one plane of a and b
   static constexpr int CP_S = 2 * F * C::CP_F;     // one plane of c and pre
-  static constexpr int NBAR = 2 * NSA + 2 * NSC;
+  static constexpr int NBAR = 2 * (NSU + NSA + NSC);
   static constexpr size_t smem_bytes() {
     return sizeof(double) * (static_cast<size_t>(NSU) * U_S + NSA * AB_S + NSC * CP_S) + 8 * NBAR;
   }
 };
+
+template <int K>
+using IntC = std::integral_constant<int, K>;
 
 template <int N, int F, bool RES>
 __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
@@ -561,20 +572,26 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
                        const double* __restrict__ fvec, double* __restrict__ y, int ntx, int zc) {
   using C = Cfg<N, F>;
   using W = WsCfg<N, F>;
-  constexpr int P = C::P, OX = C::OX, OY = C::OY, WX = C::WX, WY = C::WY;
+  constexpr int P = C::P, OX = C::OX, OY = C::OY, WX = C::WX;
   constexpr int NSU = W::NSU, NSA = W::NSA, NSC = W::NSC;
   extern __shared__ __align__(16) double smem[];
   double* Ub = smem;
   double* ABr = Ub + NSU * W::U_S;
   double* CPr = ABr + NSA * W::AB_S;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(CPr + NSC * W::CP_S);
-  unsigned long long* ab_full = bars;
-  unsigned long long* ab_empty = bars + NSA;
-  unsigned long long* cp_full = bars + 2 * NSA;
-  unsigned long long* cp_empty = bars + 2 * NSA + NSC;
+  unsigned long long* u_full = bars;
+  unsigned long long* u_empty = u_full + NSU;
+  unsigned long long* ab_full = u_empty + NSU;
+  unsigned long long* ab_empty = ab_full + NSA;
+  unsigned long long* cp_full = ab_empty + NSA;
+  unsigned long long* cp_empty = cp_full + NSC;
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) {
+    for (int i = 0; i < NSU; ++i) {
+      mbar_init(u_full + i, 32);
+      mbar_init(u_empty + i, W::YW);
+    }
     for (int i = 0; i < NSA; ++i) {
       mbar_init(ab_full + i, W::YW);
       mbar_init(ab_empty + i, W::XW);
@@ -598,54 +615,69 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
   const int z_first = Ls * P, z_last = L1 * P;
   const bool lo_dir = (L.zbc & 1) != 0, hi_dir = (L.zbc & 2) != 0;
 
-  if (warp < W::YW) {
-    // ================= stage Y =================
-    const bool act = t < W::YI;
-    const int yx = t % WX, yf = act ? t / WX : 0;
-    int rlo = 0, rhi = 0;  // rows [rlo, rhi) of the column lie inside the lattice, off its Dirichlet faces
-    const double* ybase = u;
-    {
-      const long long gxx = X0 - P + yx;
-      if (act && gxx > 0 && gxx < dx - 1) {
-        rlo = static_cast<int>(Y0 - P) < 1 ? static_cast<int>(1 - (Y0 - P)) : 0;
-        const long long rmax = dy - 1 - (Y0 - P);  // first row at or beyond the high face
-        rhi = rmax < WY ? static_cast<int>(rmax) : WY;
-        ybase = u + yf * ns + (Y0 - P + rlo) * dx + gxx;
+  if (warp == 0) {
+    // ================= loader =================
+    // entry idx = lane + 32 i of the box is (row idx / WX, column idx % WX);
+    // its shared-memory offset inside the field's box is idx itself
+    int off[W::NI];
+    unsigned vmask = 0;  // entries inside the lattice, off its x / y Dirichlet faces
+#pragma unroll
+    for (int i = 0; i < W::NI; ++i) {
+      const int idx = lane + 32 * i;
+      const int r = idx / WX, x = idx - r * WX;
+      const long long gxx = X0 - P + x, gyy = Y0 - P + r;
+      const bool ok = idx < W::BOX && gxx > 0 && gxx < dx - 1 && gyy > 0 && gyy < dy - 1;
+      off[i] = ok ? static_cast<int>(gyy * dx + gxx) : 0;
+      if (ok) vmask |= 1u << i;
+    }
+    const bool last_in = lane + 32 * (W::NI - 1) < W::BOX;
+    const unsigned want = last_in ? (1u << W::NI) - 1u : (1u << (W::NI - 1)) - 1u;
+    const bool interior = __all_sync(0xffffffffu, vmask == want);
+    const unsigned dst0 = smem_u32(Ub) + 8u * lane;
+    int su = 0;
+    unsigned pu = 1;  // fresh barrier: the first pass over the ring does not wait
+    for (int z = z_first; z <= z_last; ++z) {
+      mbar_wait(u_empty + su, pu);
+      const bool zd = (z == 0 && lo_dir) || (z == dz - 1 && hi_dir);
+      const double* pz = u + z * dxy;
+      const unsigned d = dst0 + 8u * (su * W::U_S);
+      if (interior && !zd) {
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int i = 0; i < W::NI; ++i)
+            if (i + 1 < W::NI || last_in) cp_async8_s(d + 8u * (f * C::UB_F + 32 * i), pz + f * ns + off[i], 8);
+      } else {
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int i = 0; i < W::NI; ++i)
+            if (i + 1 < W::NI || last_in) {
+              const bool ok = !zd && ((vmask >> i) & 1u);
+              cp_async8_s(d + 8u * (f * C::UB_F + 32 * i), ok ? pz + f * ns + off[i] : u, ok ? 8 : 0);
+            }
+      }
+      cp_async_arrive(u_full + su);
+      if (++su == NSU) {
+        su = 0;
+        pu ^= 1;
       }
     }
-    const bool full_col = rlo == 0 && rhi == WY;
-    double* ucol0 = Ub + yf * C::UB_F + yx;
-    // every thread commits exactly one group per call (empty past the end)
-    auto stage_u = [&](int z, int slot) {
-      if (act && z <= z_last) {
-        double* dst = ucol0 + slot * W::U_S;
-        const bool zd = (z == 0 && lo_dir) || (z == dz - 1 && hi_dir);
-        const double* src = ybase + z * dxy;
-        if (!zd && full_col) {
-#pragma unroll
-          for (int r = 0; r < WY; ++r) cp_async8(dst + r * WX, src + r * dx, 8);
-        } else {
-#pragma unroll
-          for (int r = 0; r < WY; ++r) {
-            const bool ok = !zd && r >= rlo && r < rhi;
-            cp_async8(dst + r * WX, ok ? src + (r - rlo) * dx : u, ok ? 8 : 0);
-          }
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int i = 0; i < NSU - 1; ++i) stage_u(z_first + i, i);
+    cp_async_wait_all();
+  } else if (warp < 1 + W::YW) {
+    // ================= stage Y =================
+    const int i = t - 32;
+    const bool act = i < W::YI;
+    const int yx = i % WX, yf = act ? i / WX : 0;
+    const int uoff = yf * C::UB_F + yx, aoff = yf * C::AB_F + yx;
     int su = 0, sa = 0;
-    unsigned pa = 1;  // parity the empty ring is waited on (fresh barrier: passes)
+    unsigned pu = 0, pa = 1;
     for (int z = z_first; z <= z_last; ++z) {
-      cp_async_wait<NSU - 2>();
+      mbar_wait(u_full + su, pu);
       mbar_wait(ab_empty + sa, pa);
-      // refill the slot consumed one plane ago
-      stage_u(z + NSU - 1, su == 0 ? NSU - 1 : su - 1);
       if (act) {
-        const double* ycolbuf = ucol0 + su * W::U_S;
-        double* oa = ABr + sa * W::AB_S + yf * C::AB_F + yx;
+        const double* ycolbuf = Ub + su * W::U_S + uoff;
+        double* oa = ABr + sa * W::AB_S + aoff;
         double* ob = oa + F * C::AB_F;
         // element 0 is the halo cell: it reaches owned row 0 only
         double v[N];
@@ -679,18 +711,23 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(ab_full + sa);
-      if (++su == NSU) su = 0;
+      if (lane == 0) {
+        mbar_arrive(u_empty + su);
+        mbar_arrive(ab_full + sa);
+      }
+      if (++su == NSU) {
+        su = 0;
+        pu ^= 1;
+      }
       if (++sa == NSA) {
         sa = 0;
         pa ^= 1;
       }
     }
-    cp_async_wait<0>();
-  } else if (warp < W::YW + W::XW) {
+  } else if (warp < 1 + W::YW + W::XW) {
     // ================= stage X =================
     constexpr int HX = OX / C::XH;  // owned columns per half
-    const int i = t - 32 * W::YW;
+    const int i = t - 32 * (1 + W::YW);
     const bool act = i < W::XI;
     const int h = i % C::XH, rf = i / C::XH;
     const int r = rf % OY, f = act ? rf / OY : 0;
@@ -761,11 +798,11 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
     }
   } else {
     // ================= stage Z =================
-    const int pt = t - 32 * (W::YW + W::XW);
+    const int pt = t - 32 * (1 + W::YW + W::XW);
     const int zx = pt % OX, zy = pt / OX;
     const long long gx = X0 + zx, gy = Y0 + zy;
     const double V = L.h[0] * L.h[1] * L.h[2];
-    const double sz = L.hinv2[2];
+    const double Vsz = V * L.hinv2[2];
     auto rho_of = [&](int e) -> double {
       if (!L.rho0) return 1.0;
       const long long az = (e + L.cz0) >> L.rho_shift;
@@ -779,6 +816,8 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
     const bool xend_extra = (zx == OX - 1) && (X0 + OX == dx - 1);
     const bool yend_extra = (zy == OY - 1) && (Y0 + OY == dy - 1);
     const bool xy_dir = gx == 0 || gy == 0 || gx == dx - 1 || gy == dy - 1;
+    // CTA-uniform: every point of the tile is an interior lattice node in x and y
+    const bool tile_int = tx > 0 && ty > 0 && X0 + OX < dx - 1 && Y0 + OY < dy - 1;
 
     double win[F][N];  // z window of the open layer
 #pragma unroll
@@ -812,7 +851,34 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
         for (int f = 0; f < F; ++f) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + f * ns));
       }
     };
+    auto combine = [&](int jw, double (&out)[F]) {
+      if (L.g_ok) {
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+          double v = 0.0;
+#pragma unroll
+          for (int h = 0; h < F; ++h) v = fma(L.CA[i * F + h], win[h][jw], v);
+          out[i] = v;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < F; ++i) out[i] = win[i][jw];
+      }
+    };
     auto store_plane = [&](long long zz, int jw) {
+      const bool zedge = zz == 0 || zz == dz - 1;
+      if (tile_int && !zedge) {
+        // interior tile, interior plane: plain rows of the operator
+        const long long base = zz * dxy + pbase;
+        double out[F];
+        combine(jw, out);
+#pragma unroll
+        for (int i = 0; i < F; ++i) {
+          const long long idx = base + i * ns;
+          y[idx] = RES ? __ldg(fvec + idx) - out[i] : out[i];
+        }
+        return;
+      }
       const bool zdir = (zz == 0 && lo_dir) || (zz == dz - 1 && hi_dir);
       if (on_lat) {
         if (zdir || xy_dir) {
@@ -821,18 +887,7 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
           const bool no_f = (zz == 0 && !lo_dir);  // low interface plane: f counted by the slab below
           const long long base = zz * dxy + pbase;
           double out[F];
-          if (L.g_ok) {
-#pragma unroll
-            for (int i = 0; i < F; ++i) {
-              double v = 0.0;
-#pragma unroll
-              for (int h = 0; h < F; ++h) v = fma(L.CA[i * F + h], win[h][jw], v);
-              out[i] = v;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < F; ++i) out[i] = win[i][jw];
-          }
+          combine(jw, out);
 #pragma unroll
           for (int i = 0; i < F; ++i) {
             const long long idx = base + i * ns;
@@ -848,21 +903,21 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
       if (xend_extra && yend_extra) store_dir(dx - 1, dy - 1, zz);
     };
 
-    prefetch_layer(Ls);
     const int coff = zy * C::CPP + zx;
     int sc = 0;
     unsigned pc = 0;
-    int e_of = Ls, j = 0;  // z = e_of * P + j
-    for (int z = z_first; z <= z_last; ++z) {
+    double cmc[F], cap[F], cac[F];
+    // next plane of the CP ring -> the three coupled inputs of the z products
+    auto next_plane = [&]() {
       mbar_wait(cp_full + sc, pc);
-      double vc[F], vp[F];
+      double vc[F];
       {
         const double* ic = CPr + sc * W::CP_S + coff;
         const double* ip = ic + F * C::CP_F;
 #pragma unroll
         for (int gg = 0; gg < F; ++gg) {
           vc[gg] = ic[gg * C::CP_F];
-          vp[gg] = ip[gg * C::CP_F];
+          cap[gg] = ip[gg * C::CP_F];
         }
       }
       __syncwarp();
@@ -871,7 +926,6 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
         sc = 0;
         pc ^= 1;
       }
-      double cmc[F], cap[F], cac[F];
       if (L.g_ok) {
         // (CA (x) I)(G (x) M + I (x) A): G c on the point, CA at the store
 #pragma unroll
@@ -880,10 +934,12 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
 #pragma unroll
           for (int gg = 0; gg < F; ++gg) s = fma(L.G[i * F + gg], vc[gg], s);
           cmc[i] = s;
-          cap[i] = vp[i];
           cac[i] = vc[i];
         }
       } else {
+        double vp[F];
+#pragma unroll
+        for (int i = 0; i < F; ++i) vp[i] = cap[i];
 #pragma unroll
         for (int i = 0; i < F; ++i) {
           double a = 0.0, b = 0.0, c = 0.0;
@@ -899,46 +955,61 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
           cac[i] = c;
         }
       }
-      // contribution of this plane to layer e at local index jl
-      auto add_layer = [&](int e, int jl) {
-        const double rho = rho_of(e);
-        const double rv = rho * V * sz;
-        double mc[N], kc[N];
+    };
+    // contribution of the current plane to a layer with coefficient rho at
+    // the layer's local index JL (compile time: the table entries are immediates)
+    auto add_layer = [&](auto jc, double rho) {
+      constexpr int JL = decltype(jc)::value;
+      const double rv = rho * Vsz;
 #pragma unroll
-        for (int q = 0; q < N; ++q) {
-          mc[q] = L.Mr[q][jl];
-          kc[q] = L.Kr[q][jl];
-        }
+      for (int i = 0; i < F; ++i) {
+        const double zm = V * fma(rho, cap[i], cmc[i]);
+        const double zk = rv * cac[i];
 #pragma unroll
-        for (int i = 0; i < F; ++i) {
-          const double zm = V * fma(rho, cap[i], cmc[i]);
-          const double zk = rv * cac[i];
-#pragma unroll
-          for (int q = 0; q < N; ++q) win[i][q] = fma(mc[q], zm, fma(kc[q], zk, win[i][q]));
-        }
-      };
-      if (j == 0 && z > z_first) {
-        // vertex plane: close layer e - 1; its p lower planes are final
-        const int e = e_of - 1;
-        add_layer(e, P);
-        if (e >= L0) {
-#pragma unroll
-          for (int q = 0; q < P; ++q) store_plane(static_cast<long long>(e) * P + q, q);
-        }
-#pragma unroll
-        for (int i = 0; i < F; ++i) {
-          win[i][0] = win[i][P];
-#pragma unroll
-          for (int q = 1; q < N; ++q) win[i][q] = 0.0;
-        }
-        if (z < z_last) prefetch_layer(e_of);
+        for (int q = 0; q < N; ++q) win[i][q] = fma(L.Mr[q][JL], zm, fma(L.Kr[q][JL], zk, win[i][q]));
       }
-      if (z < z_last) add_layer(e_of, j);
-      if (++j == P) {
-        j = 0;
-        ++e_of;
+    };
+    // vertex plane above layer e: the layer's p lower planes are final
+    auto close_layer = [&](int e, double rho) {
+      add_layer(IntC<P>{}, rho);
+      if (e >= L0) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) store_plane(static_cast<long long>(e) * P + q, q);
       }
+#pragma unroll
+      for (int i = 0; i < F; ++i) {
+        win[i][0] = win[i][P];
+#pragma unroll
+        for (int q = 1; q < N; ++q) win[i][q] = 0.0;
+      }
+    };
+
+    prefetch_layer(Ls);
+    double rho_prev = 1.0;
+    for (int e = Ls; e < L1; ++e) {
+      const double rho = rho_of(e);
+      next_plane();
+      if (e > Ls) {
+        close_layer(e - 1, rho_prev);
+        prefetch_layer(e);
+      }
+      add_layer(IntC<0>{}, rho);
+      if constexpr (P > 1) {
+        next_plane();
+        add_layer(IntC<1>{}, rho);
+      }
+      if constexpr (P > 2) {
+        next_plane();
+        add_layer(IntC<2>{}, rho);
+      }
+      if constexpr (P > 3) {
+        next_plane();
+        add_layer(IntC<3>{}, rho);
+      }
+      rho_prev = rho;
     }
+    next_plane();
+    close_layer(L1 - 1, rho_prev);
     // the slab's top plane: Dirichlet, or an interface partial sum
     if (L1 == ncz) store_plane(z_last, 0);
   }

@@ -460,6 +460,13 @@ __device__ __forceinline__ void fdm_stages(const DevFDM& P, const double* __rest
 // interior, even-odd transforms; 2: only the other CTAs, generic. Modes 1 and
 // 2 are two launches over the same grid (CTAs of the other kind return at
 // once), so each kernel's code stays small enough for the instruction cache.
+// MODE 3: generic transforms, only the cells the strip kernel below leaves
+// out (strips touching the boundary or holding an exactly-solved cell).
+template <int N, int NT>
+struct SCfg;
+template <int N, int NT>
+__device__ __forceinline__ bool strip_left_out(const DevFDM& P, unsigned cx, unsigned cy, unsigned cz);
+
 template <int N, int NT, bool TD, int MODE>
 __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant__ DevFDM P,
                                                         const double* __restrict__ r, double* __restrict__ z,
@@ -499,11 +506,224 @@ __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant
   // CTAs whose cells are all interior take the even-odd transforms (P.eo = 0
   // when the host could not order the interior eigenvectors by parity: one
   // MODE 0 launch)
-  if constexpr (MODE != 0) {
+  if constexpr (MODE == 3) {
+    bool mine = false;
+    if (valid) {
+      const unsigned ci = static_cast<unsigned>(cell);
+      const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]);
+      mine = strip_left_out<N, NT>(P, ci % nx, (ci / nx) % ny, ci / (nx * ny));
+    }
+    if (!__syncthreads_or(mine)) return;
+    fdm_stages<N, NT, TD, false>(P, r, z, scale, W, mine, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
+    return;
+  } else if constexpr (MODE != 0) {
     const bool all_interior = __syncthreads_and(!valid || mask == 0);
     if (all_interior != (MODE == 1)) return;
   }
   fdm_stages<N, NT, TD, MODE == 1>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
+}
+
+// ---------------------------------------------------------------------------
+// Strip form of the interior cells (even-odd transforms). A 128-thread CTA
+// owns NCX cells consecutive in x of one (cy, cz) row and one step:
+//   load : the strip's residual block [field][z][y][x], one coalesced row
+//          (cp.async) per warp instruction
+//   P1   : thread = (cell, field, z plane): S_x^T and S_y^T of the 5 x 5
+//          plane in registers
+//   P2   : thread = (cell, e_y, e_x): S_z^T, the n_t x n_t solves at its N
+//          eigen-points, S_z for all fields
+//   P3   : thread = (cell, field, z plane): S_y, S_x, multiplicity weights;
+//          the strip's block is assembled in shared memory (cells share
+//          x faces) and
+//   scatter : added to z with one coalesced row of reductions per warp
+//          instruction (asm_smoother.cpp:45-49, 75).
+// Against the line-owner kernel: 3 stages instead of 5 through shared memory
+// (2 / 5 of its shared-memory traffic), row-contiguous global accesses instead
+// of 5-double segments, N * NCX fewer reductions on the shared x faces.
+template <int N, int NT>
+struct SCfg {
+  static constexpr int T = 128;
+  static constexpr int NL = N * N;   // P2 threads per cell
+  static constexpr int NP = NT * N;  // P1 / P3 threads per cell
+  static constexpr int P = N - 1;
+  static constexpr int min3(int a, int b, int c) { return a < b ? (a < c ? a : c) : (b < c ? b : c); }
+  static constexpr int NCX = min3(T / NL, T / NP, 31 / P);  // cells per strip (one row <= 32 nodes)
+  static constexpr int RX = P * NCX + 1;      // nodes of the strip along x
+  static constexpr int ROWS = NT * N * N;     // (field, z, y) rows of the block
+  static constexpr int BLK = ROWS * RX;
+  static constexpr int ND = N * N * N;
+  // cell stride = NL (mod 16): the P2 threads t = e + NL * cell address word t (mod 16)
+  static constexpr int CS = NT * ND + (((NL - NT * ND) % 16) + 16) % 16;
+  static constexpr int EDGE = NCX * NT * N * N;  // x = 0 faces of the cells
+  static constexpr size_t smem_bytes() { return sizeof(double) * (BLK + NCX * CS + EDGE); }
+  static_assert(RX <= 32, "one warp instruction per row");
+};
+
+template <int N, int NT>
+__device__ __forceinline__ bool strip_left_out(const DevFDM& P, unsigned cx, unsigned cy, unsigned cz) {
+  constexpr unsigned NCX = SCfg<N, NT>::NCX;
+  const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]),
+                 nz = static_cast<unsigned>(P.cells[2]);
+  const unsigned c0 = (cx / NCX) * NCX;
+  const unsigned c1 = c0 + NCX < nx ? c0 + NCX : nx;
+  if (c0 == 0 || c1 == nx || cy == 0 || cy == ny - 1) return true;
+  if ((cz == 0 && (P.zbc & 1)) || (cz == nz - 1 && (P.zbc & 2))) return true;
+  if (P.skip) {
+    const unsigned char* sk = P.skip + (static_cast<size_t>(cz) * ny + cy) * nx;
+    for (unsigned c = c0; c < c1; ++c)
+      if (sk[c]) return true;
+  }
+  return false;
+}
+
+template <int N, int NT, bool TD>
+__global__ void __launch_bounds__(SCfg<N, NT>::T, 4) fdm_strip_kernel(const __grid_constant__ DevFDM P,
+                                                                       const double* __restrict__ r,
+                                                                       double* __restrict__ z, double scale) {
+  using C = SCfg<N, NT>;
+  constexpr int p = C::P, NCX = C::NCX, RX = C::RX, ROWS = C::ROWS, CS = C::CS, ND = C::ND;
+  extern __shared__ __align__(16) double sm[];
+  double* IO = sm;                 // residual block in, assembled correction out
+  double* W = IO + C::BLK;         // per cell [field][z][y][x] between the stages
+  double* EDGE = W + NCX * CS;     // x = 0 face of every cell's correction
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]);
+  const unsigned sxn = (nx + NCX - 1) / NCX;
+  const unsigned sid = blockIdx.x;
+  const unsigned sx = sid % sxn, cy = (sid / sxn) % ny, cz = sid / (sxn * ny);
+  const unsigned cx0 = sx * NCX;
+  if (strip_left_out<N, NT>(P, cx0, cy, cz)) return;  // CTA-uniform
+  const int ncell = NCX;  // interior strips are whole
+  const long long dx = P.dofs[0], dxy = P.dofs[0] * P.dofs[1];
+  const long long base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx +
+                         static_cast<long long>(cx0) * p;
+  const long long st = blockIdx.y;
+  const double* rs = r + st * NT * P.n_space + base;
+  double* zs = z + st * NT * P.n_space + base;
+  double rho = 1.0;
+  if (P.rho0) {
+    const long long ax = cx0 >> P.rho_shift, ay = cy >> P.rho_shift, az = (cz + P.cz0) >> P.rho_shift;
+    rho = P.rho0[(az * P.cells0[1] + ay) * P.cells0[0] + ax];
+  }
+  // ---- load: row (f, lz, ly) of the block per warp instruction; a warp
+  // takes (field, z) pairs, the N rows of a pair are unrolled
+  if (lane < RX) {
+    for (int pr = warp; pr < NT * N; pr += C::T / 32) {
+      const int f = pr / N, lz = pr - f * N;
+      const double* src = rs + f * P.n_space + lz * dxy + lane;
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(IO + pr * N * RX + lane));
+#pragma unroll
+      for (int ly = 0; ly < N; ++ly)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * (ly * RX)), "l"(src + ly * dx)
+                     : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  const double(&Sx)[kMaxN][kMaxN] = P.S1[0][0];
+  const double(&Sy)[kMaxN][kMaxN] = P.S1[1][0];
+  const double(&Sz)[kMaxN][kMaxN] = P.S1[2][0];
+  // ---- P1: plane owner, S_x^T then S_y^T in registers
+  const int pc = t / C::NP, pf = (t % C::NP) / N, pz = t % N;
+  const bool pact = pc < ncell;
+  double* wpl = W + pc * CS + pf * ND + pz * N * N;  // this thread's plane of W
+  if (pact) {
+    const double* in = IO + (pf * N * N + pz * N) * RX + p * pc;
+    double a[N][N];
+#pragma unroll
+    for (int y = 0; y < N; ++y) {
+      double v[N];
+#pragma unroll
+      for (int x = 0; x < N; ++x) v[x] = in[y * RX + x];
+      fdm_fwd<N, true>(Sx, v, a[y]);
+    }
+#pragma unroll
+    for (int ex = 0; ex < N; ++ex) {
+      double v[N], o[N];
+#pragma unroll
+      for (int y = 0; y < N; ++y) v[y] = a[y][ex];
+      fdm_fwd<N, true>(Sy, v, o);
+#pragma unroll
+      for (int ey = 0; ey < N; ++ey) wpl[ey * N + ex] = o[ey];
+    }
+  }
+  __syncthreads();
+  // ---- P2: eigen-line owner along z
+  {
+    const int c = t / C::NL, e = t % C::NL;
+    if (c < ncell) {
+      const int ey = e / N, ex = e % N;
+      double* wl = W + c * CS + e;
+      double v[NT][N];
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double in[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) in[k] = wl[f * ND + k * N * N];
+        fdm_fwd<N, true>(Sz, in, v[f]);
+      }
+      const double lxy = P.L1[0][0][ex] + P.L1[1][0][ey];
+#pragma unroll
+      for (int ez = 0; ez < N; ++ez) {
+        double bb[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int f = 0; f < NT; ++f) bb[f] = v[f][ez];
+        temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][0][ez]), bb);
+#pragma unroll
+        for (int f = 0; f < NT; ++f) v[f][ez] = bb[f];
+      }
+#pragma unroll
+      for (int f = 0; f < NT; ++f) {
+        double out[N];
+        fdm_bwd<N, true>(Sz, v[f], out);
+#pragma unroll
+        for (int k = 0; k < N; ++k) wl[f * ND + k * N * N] = out[k];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- P3: plane owner, S_y then S_x, weights; block assembly
+  if (pact) {
+    double a[N][N];
+#pragma unroll
+    for (int ex = 0; ex < N; ++ex) {
+      double v[N], o[N];
+#pragma unroll
+      for (int ey = 0; ey < N; ++ey) v[ey] = wpl[ey * N + ex];
+      fdm_bwd<N, true>(Sy, v, o);
+#pragma unroll
+      for (int y = 0; y < N; ++y) a[y][ex] = o[y];
+    }
+    const double wz = scale * (pz == 0 || pz == p ? 0.5 : 1.0);
+    double* out = IO + (pf * N * N + pz * N) * RX + p * pc;
+    double* edge = EDGE + ((pc * NT + pf) * N + pz) * N;
+#pragma unroll
+    for (int y = 0; y < N; ++y) {
+      double o[N];
+      fdm_bwd<N, true>(Sx, a[y], o);
+      const double wzy = wz * (y == 0 || y == p ? 0.5 : 1.0);
+      edge[y] = 0.5 * wzy * o[0];
+#pragma unroll
+      for (int x = 1; x < N; ++x) out[y * RX + x] = (x == p ? 0.5 : 1.0) * wzy * o[x];
+    }
+  }
+  __syncthreads();
+  // ---- scatter: row (f, lz, ly) of the assembled block per warp instruction
+  if (lane < RX) {
+    const bool has_edge = lane % p == 0 && lane / p < ncell;
+    const double* eb = EDGE + (lane / p) * NT * N * N;
+    for (int pr = warp; pr < NT * N; pr += C::T / 32) {
+      const int f = pr / N, lz = pr - f * N;
+      double* dst = zs + f * P.n_space + lz * dxy + lane;
+      const double* blk = IO + pr * N * RX + lane;
+#pragma unroll
+      for (int ly = 0; ly < N; ++ly) {
+        double v = lane >= 1 ? blk[ly * RX] : 0.0;
+        if (has_edge) v += eb[pr * N + ly];
+        atomicAdd(dst + ly * dx, v);
+      }
+    }
+  }
 }
 
 template <int N, int NT>
@@ -516,8 +736,17 @@ void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cud
     constexpr bool TD = decltype(td)::value;
     if (P.eo) {
       count_launch();  // the second launch of the pair
-      fdm_lines_kernel<N, NT, TD, 1><<<grid, 128, 0, s>>>(P, r, z, scale);
-      fdm_lines_kernel<N, NT, TD, 2><<<grid, 128, 0, s>>>(P, r, z, scale);
+      using SC = SCfg<N, NT>;
+      static bool configured = false;
+      if (!configured) {
+        cudaFuncSetAttribute(fdm_strip_kernel<N, NT, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(SC::smem_bytes()));
+        configured = true;
+      }
+      const long long sxn = (P.cells[0] + SC::NCX - 1) / SC::NCX;
+      const dim3 sgrid(static_cast<unsigned>(sxn * P.cells[1] * P.cells[2]), static_cast<unsigned>(P.S));
+      fdm_strip_kernel<N, NT, TD><<<sgrid, SC::T, SC::smem_bytes(), s>>>(P, r, z, scale);
+      fdm_lines_kernel<N, NT, TD, 3><<<grid, 128, 0, s>>>(P, r, z, scale);
     } else {
       fdm_lines_kernel<N, NT, TD, 0><<<grid, 128, 0, s>>>(P, r, z, scale);
     }

@@ -848,7 +848,10 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
           for (int j = 0; j < kMaxN; ++j) Fd.S1[a][t][i][j] = S[t][i][j];
         }
     }
-    Fd.eo = fdm_order_interior_by_parity(Fd, d.dim) ? 1 : 0;
+    // STMG_FDM_GENERIC keeps the unordered tables, i.e. the generic line-owner
+    // kernel on every cell (the path taken when the interior eigenvectors
+    // cannot be ordered by parity), for testing the strip kernel against it
+    Fd.eo = !std::getenv("STMG_FDM_GENERIC") && fdm_order_interior_by_parity(Fd, d.dim) ? 1 : 0;
     if (d.rho0) {
       // host copy of the level-0 coefficient table
       const Index n0 = d.cells0[0] * d.cells0[1] * d.cells0[2];

@@ -3,6 +3,8 @@ reference oracle (asm_smoother.cpp:60-78, transfer.cpp:118-190,
 multigrid.cpp:127-234, gmres.cpp:8-115). Tolerances are written per test; the
 north_star gates are GMRES iterations within +-1 and final solution relative
 difference <= 1e-8."""
+import os
+
 import numpy as np
 import pytest
 
@@ -388,3 +390,35 @@ def test_transfers_separable_fallback(cuda, ref):
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "ok" in out.stdout
+
+
+@pytest.mark.parametrize("cells,p,k,S,scheme", [((16, 16, 16), 4, 3, 1, problems.DG), ((23, 13, 12), 4, 2, 2, problems.DG),
+                                                 ((33, 9, 8), 2, 2, 2, problems.CGP),
+                                                 ((24, 12, 10), 3, 1, 1, problems.DG),
+                                                 ((40, 8, 6), 1, 3, 1, problems.DG)])
+def test_fdm_strip_kernel_matches_line_owner(cuda, cells, p, k, S, scheme):
+    """The strip kernel of the interior cells (even-odd transforms, assembled
+    block scatter) against the generic line-owner kernel on every cell
+    (STMG_FDM_GENERIC, itself pinned to the reference's LU block solves by the
+    tests above) on meshes with interior strips, ragged strip counts and
+    several steps: 1e-12."""
+    import torch
+
+    def correction(generic):
+        if generic:
+            os.environ["STMG_FDM_GENERIC"] = "1"
+        try:
+            mesh = api.Mesh(3, (0, 0, 0), (1.0, 0.7, 0.6), cells, 0)
+            op = api.SpaceTimeOperator(mesh, 0, p, problems.HEAT, scheme, k, 0.05, S, None)
+            sm = api.ASMSmoother(op)
+        finally:
+            os.environ.pop("STMG_FDM_GENERIC", None)
+        g = torch.Generator(device="cuda").manual_seed(7)
+        r = torch.rand(op.n_dofs, dtype=torch.float64, device="cuda", generator=g) - 0.5
+        z = torch.rand(op.n_dofs, dtype=torch.float64, device="cuda", generator=g)
+        z0 = z.clone()
+        sm.add_correction(r, z)
+        return (z - z0).cpu().numpy()
+
+    got, want = correction(False), correction(True)
+    assert _rel(got, want) <= 1e-12

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <type_traits>
 #include <stdexcept>
+#include <vector>
 
 #include "kernels.hpp"
 #include "st_cart_layout.h"
@@ -464,32 +465,34 @@ __device__ __forceinline__ void fdm_stages(const DevFDM& P, const double* __rest
 // out (strips touching the boundary or holding an exactly-solved cell).
 template <int N, int NT>
 struct SCfg;
-template <int N, int NT>
-__device__ __forceinline__ bool strip_left_out(const DevFDM& P, unsigned cx, unsigned cy, unsigned cz);
-
 template <int N, int NT, bool TD, int MODE>
-__global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant__ DevFDM P,
-                                                        const double* __restrict__ r, double* __restrict__ z,
-                                                        double scale) {
+__device__ __forceinline__ void fdm_lines_group(const DevFDM& P, const double* __restrict__ r, double* __restrict__ z,
+                                                double scale, double* W, long long group) {
   using Y = stc::FdmLayout<N, NT>;  // bank-conflict-modelled (scripts/gen_cart_layout.py)
   constexpr int NL = N * N, NC = 128 / NL, RY = Y::RY, PZ = Y::PZ;
-  __shared__ double W[NC * Y::CS];
   const int t = threadIdx.x;
   const int c = t / NL, l = t - (t / NL) * NL;
   const int a = l % N, b = l / N;
   const long long n_cells = P.cells[0] * P.cells[1] * P.cells[2];
-  const long long cell = static_cast<long long>(blockIdx.x) * NC + c;
-  const bool valid = c < NC && cell < n_cells && !(P.skip && P.skip[cell]);
+  long long cell = group * NC + c;
+  bool valid;
+  if constexpr (MODE == 3) {
+    valid = c < NC && cell < P.n_left;
+    if (valid) cell = P.left[cell];
+  } else {
+    valid = c < NC && cell < n_cells && !(P.skip && P.skip[cell]);
+  }
   const long long dx = P.dofs[0], dxy = P.dofs[0] * P.dofs[1];
   constexpr int p = N - 1;
   long long base = 0;
   int mask = 0, tx = 0, ty = 0, tz = 0;
   double rho = 1.0;
+  unsigned cx = 0, cy = 0, cz = 0;
   if (valid) {
     const unsigned ci = static_cast<unsigned>(cell);
     const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]),
                    nz = static_cast<unsigned>(P.cells[2]);
-    const unsigned cx = ci % nx, cy = (ci / nx) % ny, cz = ci / (nx * ny);
+    cx = ci % nx, cy = (ci / nx) % ny, cz = ci / (nx * ny);
     base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx + static_cast<long long>(cx) * p;
     tx = (cx == 0 ? 1 : 0) | (cx == nx - 1 ? 2 : 0);
     ty = (cy == 0 ? 1 : 0) | (cy == ny - 1 ? 2 : 0);
@@ -506,21 +509,23 @@ __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant
   // CTAs whose cells are all interior take the even-odd transforms (P.eo = 0
   // when the host could not order the interior eigenvectors by parity: one
   // MODE 0 launch)
-  if constexpr (MODE == 3) {
-    bool mine = false;
-    if (valid) {
-      const unsigned ci = static_cast<unsigned>(cell);
-      const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]);
-      mine = strip_left_out<N, NT>(P, ci % nx, (ci / nx) % ny, ci / (nx * ny));
-    }
-    if (!__syncthreads_or(mine)) return;
-    fdm_stages<N, NT, TD, false>(P, r, z, scale, W, mine, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
-    return;
-  } else if constexpr (MODE != 0) {
+  if constexpr (MODE != 0 && MODE != 3) {
     const bool all_interior = __syncthreads_and(!valid || mask == 0);
     if (all_interior != (MODE == 1)) return;
   }
+  (void)cx, (void)cy, (void)cz;
   fdm_stages<N, NT, TD, MODE == 1>(P, r, z, scale, W, valid, base, mask, tx, ty, tz, rho, a, b, oy, ox, oz);
+}
+
+template <int N, int NT, bool TD, int MODE>
+__global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant__ DevFDM P,
+                                                        const double* __restrict__ r, double* __restrict__ z,
+                                                        double scale) {
+  using Y = stc::FdmLayout<N, NT>;
+  constexpr int NC = 128 / (N * N);
+  __shared__ double W[NC * Y::CS];
+  // MODE 3: blockIdx.x counts groups of the left-out cell list
+  fdm_lines_group<N, NT, TD, MODE>(P, r, z, scale, W, blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -559,18 +564,25 @@ struct SCfg {
   static_assert(RX <= 32, "one warp instruction per row");
 };
 
+// strips are the whole groups of NCX cells starting at cell 1 of every row
+// that stay clear of the row's last cell: the cells left out along x are
+// cell 0 and the tail of fewer than NCX + 1 cells
 template <int N, int NT>
-__device__ __forceinline__ bool strip_left_out(const DevFDM& P, unsigned cx, unsigned cy, unsigned cz) {
+__host__ __device__ __forceinline__ unsigned strips_per_row(long long nx) {
+  return nx >= 2 ? static_cast<unsigned>((nx - 2) / SCfg<N, NT>::NCX) : 0u;
+}
+template <int N, int NT>
+__host__ __device__ __forceinline__ bool strip_left_out(const DevFDM& P, const unsigned char* skip, unsigned cx,
+                                                        unsigned cy, unsigned cz) {
   constexpr unsigned NCX = SCfg<N, NT>::NCX;
   const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]),
                  nz = static_cast<unsigned>(P.cells[2]);
-  const unsigned c0 = (cx / NCX) * NCX;
-  const unsigned c1 = c0 + NCX < nx ? c0 + NCX : nx;
-  if (c0 == 0 || c1 == nx || cy == 0 || cy == ny - 1) return true;
+  if (cx == 0 || (cx - 1) / NCX >= strips_per_row<N, NT>(nx) || cy == 0 || cy == ny - 1) return true;
   if ((cz == 0 && (P.zbc & 1)) || (cz == nz - 1 && (P.zbc & 2))) return true;
-  if (P.skip) {
-    const unsigned char* sk = P.skip + (static_cast<size_t>(cz) * ny + cy) * nx;
-    for (unsigned c = c0; c < c1; ++c)
+  if (skip) {
+    const unsigned c0 = 1 + ((cx - 1) / NCX) * NCX;
+    const unsigned char* sk = skip + (static_cast<size_t>(cz) * ny + cy) * nx;
+    for (unsigned c = c0; c < c0 + NCX; ++c)
       if (sk[c]) return true;
   }
   return false;
@@ -588,11 +600,11 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 4) fdm_strip_kernel(const __gr
   double* EDGE = W + NCX * CS;     // x = 0 face of every cell's correction
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]);
-  const unsigned sxn = (nx + NCX - 1) / NCX;
+  const unsigned sxn = strips_per_row<N, NT>(nx);
   const unsigned sid = blockIdx.x;
   const unsigned sx = sid % sxn, cy = (sid / sxn) % ny, cz = sid / (sxn * ny);
-  const unsigned cx0 = sx * NCX;
-  if (strip_left_out<N, NT>(P, cx0, cy, cz)) return;  // CTA-uniform
+  const unsigned cx0 = 1 + sx * NCX;
+  if (strip_left_out<N, NT>(P, P.skip, cx0, cy, cz)) return;  // CTA-uniform
   const int ncell = NCX;  // interior strips are whole
   const long long dx = P.dofs[0], dxy = P.dofs[0] * P.dofs[1];
   const long long base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx +
@@ -743,10 +755,11 @@ void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cud
                              static_cast<int>(SC::smem_bytes()));
         configured = true;
       }
-      const long long sxn = (P.cells[0] + SC::NCX - 1) / SC::NCX;
+      const long long sxn = strips_per_row<N, NT>(P.cells[0]);
       const dim3 sgrid(static_cast<unsigned>(sxn * P.cells[1] * P.cells[2]), static_cast<unsigned>(P.S));
-      fdm_strip_kernel<N, NT, TD><<<sgrid, SC::T, SC::smem_bytes(), s>>>(P, r, z, scale);
-      fdm_lines_kernel<N, NT, TD, 3><<<grid, 128, 0, s>>>(P, r, z, scale);
+      if (sxn > 0) fdm_strip_kernel<N, NT, TD><<<sgrid, SC::T, SC::smem_bytes(), s>>>(P, r, z, scale);
+      const dim3 lgrid(static_cast<unsigned>((P.n_left + NC - 1) / NC), grid.y);
+      if (P.n_left > 0) fdm_lines_kernel<N, NT, TD, 3><<<lgrid, 128, 0, s>>>(P, r, z, scale);
     } else {
       fdm_lines_kernel<N, NT, TD, 0><<<grid, 128, 0, s>>>(P, r, z, scale);
     }
@@ -787,6 +800,44 @@ void launch_nt(const DevFDM& P, const double* r, double* z, double scale, cudaSt
 }
 
 }  // namespace
+
+namespace {
+template <int N, int NT>
+std::vector<long long> left_out_cells(const DevFDM& P, const unsigned char* skip) {
+  std::vector<long long> out;
+  const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]),
+                 nz = static_cast<unsigned>(P.cells[2]);
+  for (unsigned cz = 0; cz < nz; ++cz)
+    for (unsigned cy = 0; cy < ny; ++cy)
+      for (unsigned cx = 0; cx < nx; ++cx) {
+        const long long cell = (static_cast<long long>(cz) * ny + cy) * nx + cx;
+        if (skip && skip[cell]) continue;
+        if (strip_left_out<N, NT>(P, skip, cx, cy, cz)) out.push_back(cell);
+      }
+  return out;
+}
+template <int N>
+std::vector<long long> left_out_cells_nt(const DevFDM& P, const unsigned char* skip) {
+  switch (P.nt) {
+    case 1: return left_out_cells<N, 1>(P, skip);
+    case 2: return left_out_cells<N, 2>(P, skip);
+    case 3: return left_out_cells<N, 3>(P, skip);
+    case 4: return left_out_cells<N, 4>(P, skip);
+    default: throw std::invalid_argument("FDM smoother: n_t must be in [1, 4]");
+  }
+}
+}  // namespace
+
+std::vector<long long> fdm_left_out_cells(const DevFDM& P, const unsigned char* skip_host) {
+  if (P.dim != 3) return {};
+  switch (P.n) {
+    case 2: return left_out_cells_nt<2>(P, skip_host);
+    case 3: return left_out_cells_nt<3>(P, skip_host);
+    case 4: return left_out_cells_nt<4>(P, skip_host);
+    case 5: return left_out_cells_nt<5>(P, skip_host);
+    default: throw std::invalid_argument("FDM smoother: unsupported p");
+  }
+}
 
 void fdm_add_correction(const DevFDM& P, const double* r, double* z, double scale, cudaStream_t s) {
   const int key = P.dim * 10 + P.n;

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "device.cuh"
 
 namespace stmgb {
@@ -192,7 +194,13 @@ struct DevFDM {
   int tkind[4];
   double ta[4], tb[4];
   double tP[16], tQ[16];
+  // eo = 1, 3D: the cells the strip kernel leaves to the line-owner kernel
+  // (boundary strips, strips holding a skipped cell), from fdm_left_out_cells
+  const long long* left;
+  long long n_left;
 };
+// host: the left-out cell list of F (skip_host: host copy of F.skip or nullptr)
+std::vector<long long> fdm_left_out_cells(const DevFDM& F, const unsigned char* skip_host);
 void fdm_add_correction(const DevFDM& F, const double* r, double* z, double scale, cudaStream_t s);
 // probing-based extraction of restricted cell matrices (setup)
 // colours are classes of GLOBAL lattice coordinates; the probe lattice may

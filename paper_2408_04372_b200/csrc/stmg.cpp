@@ -852,6 +852,17 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
     // kernel on every cell (the path taken when the interior eigenvectors
     // cannot be ordered by parity), for testing the strip kernel against it
     Fd.eo = !std::getenv("STMG_FDM_GENERIC") && fdm_order_interior_by_parity(Fd, d.dim) ? 1 : 0;
+    Fd.left = nullptr;
+    Fd.n_left = 0;
+    // cells the strip kernel leaves to the line-owner kernel (asm_fdm.cu)
+    auto list_left_out = [&](const unsigned char* skip_host) {
+      if (!Fd.eo || d.dim != 3) return;
+      const std::vector<long long> left = fdm_left_out_cells(Fd, skip_host);
+      left_ = upload(left);
+      Fd.left = static_cast<const long long*>(left_.raw());
+      Fd.n_left = static_cast<long long>(left.size());
+    };
+    if (!d.rho0) list_left_out(nullptr);
     if (d.rho0) {
       // host copy of the level-0 coefficient table
       const Index n0 = d.cells0[0] * d.cells0[1] * d.cells0[2];
@@ -889,6 +900,7 @@ ASMSmoother::ASMSmoother(const SpaceTimeOperator& op, const SpaceTimeOperator* p
           Fd.skip = static_cast<const unsigned char*>(skip_.raw());
         }
       }
+      list_left_out(Fd.skip ? skip.data() : nullptr);
     }
     if (exact_cells.empty()) {
       A.n_list = 0;

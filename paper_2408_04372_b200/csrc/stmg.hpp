@@ -145,7 +145,7 @@ class ASMSmoother {
   int block_size() const { return op_->n_t() * asm_.m; }
   Index n_blocks() const { return static_cast<Index>(op_->n_steps()) * op_->mesh().n_cells(); }
   long sweeps() const { return sweep_count_; }
-  size_t bytes() const { return X_.bytes() + lam_.bytes() + list_.bytes() + skip_.bytes() + meta_.bytes(); }
+  size_t bytes() const { return X_.bytes() + lam_.bytes() + list_.bytes() + skip_.bytes() + meta_.bytes() + left_.bytes(); }
   // cells solved by tensor FDM / by the per-cell eigenbasis; exact() is false
   // when some block is only approximated (non-uniform coefficient around a
   // (p+1)^3 > 64 cell)
@@ -165,7 +165,7 @@ class ASMSmoother {
   DevFDM fdm_{};
   bool use_fdm_ = false;
   bool exact_ = true;
-  DeviceBuffer X_, lam_, list_, skip_, meta_;
+  DeviceBuffer X_, lam_, list_, skip_, meta_, left_;
   mutable long sweep_count_ = 0;
 };
 

@@ -530,18 +530,19 @@ __global__ void __launch_bounds__(128, 4) fdm_lines_kernel(const __grid_constant
 
 // ---------------------------------------------------------------------------
 // Strip form of the interior cells (even-odd transforms). A 128-thread CTA
-// owns NCX cells consecutive in x of one (cy, cz) row and one step:
-//   load : the strip's residual block [field][z][y][x], one coalesced row
-//          (cp.async) per warp instruction
+// owns NCX cells consecutive in x of one (cy, cz) row and one step; one
+// shared buffer, per cell [field][z][y][x], is used in place throughout:
+//   load : one coalesced row of the strip's residual block per warp
+//          instruction (cp.async), written straight into the cells' layout
+//          (x-face nodes to both cells)
 //   P1   : thread = (cell, field, z plane): S_x^T and S_y^T of the 5 x 5
 //          plane in registers
 //   P2   : thread = (cell, e_y, e_x): S_z^T, the n_t x n_t solves at its N
 //          eigen-points, S_z for all fields
-//   P3   : thread = (cell, field, z plane): S_y, S_x, multiplicity weights;
-//          the strip's block is assembled in shared memory (cells share
-//          x faces) and
-//   scatter : added to z with one coalesced row of reductions per warp
-//          instruction (asm_smoother.cpp:45-49, 75).
+//   P3   : thread = (cell, field, z plane): S_y, S_x, multiplicity weights
+//   scatter : one coalesced row of reductions into z per warp instruction,
+//          x-face nodes summed over their two cells
+//          (asm_smoother.cpp:45-49, 75).
 // Against the line-owner kernel: 3 stages instead of 5 through shared memory
 // (2 / 5 of its shared-memory traffic), row-contiguous global accesses instead
 // of 5-double segments, N * NCX fewer reductions on the shared x faces.
@@ -557,10 +558,11 @@ struct SCfg {
   static constexpr int ROWS = NT * N * N;     // (field, z, y) rows of the block
   static constexpr int BLK = ROWS * RX;
   static constexpr int ND = N * N * N;
-  // cell stride = NL (mod 16): the P2 threads t = e + NL * cell address word t (mod 16)
-  static constexpr int CS = NT * ND + (((NL - NT * ND) % 16) + 16) % 16;
-  static constexpr int EDGE = NCX * NT * N * N;  // x = 0 faces of the cells
-  static constexpr size_t smem_bytes() { return sizeof(double) * (BLK + NCX * CS + EDGE); }
+  // one buffer, per cell [field][z][y][x], used in place by every stage. Cell
+  // stride = N^2 NP (mod 16): the plane owners t = plane + NP * cell then
+  // address word N^2 t (mod 16), conflict-free for odd N
+  static constexpr int CS = NT * ND + (((NL * NP - NT * ND) % 16) + 16) % 16;
+  static constexpr size_t smem_bytes() { return sizeof(double) * NCX * CS; }
   static_assert(RX <= 32, "one warp instruction per row");
 };
 
@@ -589,15 +591,12 @@ __host__ __device__ __forceinline__ bool strip_left_out(const DevFDM& P, const u
 }
 
 template <int N, int NT, bool TD>
-__global__ void __launch_bounds__(SCfg<N, NT>::T, 4) fdm_strip_kernel(const __grid_constant__ DevFDM P,
+__global__ void __launch_bounds__(SCfg<N, NT>::T, 6) fdm_strip_kernel(const __grid_constant__ DevFDM P,
                                                                        const double* __restrict__ r,
                                                                        double* __restrict__ z, double scale) {
   using C = SCfg<N, NT>;
   constexpr int p = C::P, NCX = C::NCX, RX = C::RX, ROWS = C::ROWS, CS = C::CS, ND = C::ND;
-  extern __shared__ __align__(16) double sm[];
-  double* IO = sm;                 // residual block in, assembled correction out
-  double* W = IO + C::BLK;         // per cell [field][z][y][x] between the stages
-  double* EDGE = W + NCX * CS;     // x = 0 face of every cell's correction
+  extern __shared__ __align__(16) double W[];  // per cell [field][z][y][x]
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]);
   const unsigned sxn = strips_per_row<N, NT>(nx);
@@ -618,16 +617,28 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 4) fdm_strip_kernel(const __gr
     rho = P.rho0[(az * P.cells0[1] + ay) * P.cells0[0] + ax];
   }
   // ---- load: row (f, lz, ly) of the block per warp instruction; a warp
-  // takes (field, z) pairs, the N rows of a pair are unrolled
+  // takes (field, z) pairs, the N rows of a pair are unrolled. Lane = node x
+  // of the strip: local node x % p of cell x / p, and, on a shared face,
+  // node p of the cell before
+  const int lc = lane / p, lj = lane - lc * p;
+  const bool own = lane < RX && lc < ncell, dup = lane < RX && lj == 0 && lc >= 1;
+  const int o_own = lc * CS + lj, o_dup = (lc - 1) * CS + p;
   if (lane < RX) {
     for (int pr = warp; pr < NT * N; pr += C::T / 32) {
       const int f = pr / N, lz = pr - f * N;
       const double* src = rs + f * P.n_space + lz * dxy + lane;
-      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(IO + pr * N * RX + lane));
+      const unsigned d0 = static_cast<unsigned>(__cvta_generic_to_shared(W + pr * N * N));
 #pragma unroll
-      for (int ly = 0; ly < N; ++ly)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * (ly * RX)), "l"(src + ly * dx)
-                     : "memory");
+      for (int ly = 0; ly < N; ++ly) {
+        if (own)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * (o_own + ly * N)),
+                       "l"(src + ly * dx)
+                       : "memory");
+        if (dup)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * (o_dup + ly * N)),
+                       "l"(src + ly * dx)
+                       : "memory");
+      }
     }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
@@ -638,15 +649,14 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 4) fdm_strip_kernel(const __gr
   // ---- P1: plane owner, S_x^T then S_y^T in registers
   const int pc = t / C::NP, pf = (t % C::NP) / N, pz = t % N;
   const bool pact = pc < ncell;
-  double* wpl = W + pc * CS + pf * ND + pz * N * N;  // this thread's plane of W
+  double* wpl = W + pc * CS + pf * ND + pz * N * N;  // this thread's plane
   if (pact) {
-    const double* in = IO + (pf * N * N + pz * N) * RX + p * pc;
     double a[N][N];
 #pragma unroll
     for (int y = 0; y < N; ++y) {
       double v[N];
 #pragma unroll
-      for (int x = 0; x < N; ++x) v[x] = in[y * RX + x];
+      for (int x = 0; x < N; ++x) v[x] = wpl[y * N + x];
       fdm_fwd<N, true>(Sx, v, a[y]);
     }
 #pragma unroll
@@ -707,31 +717,26 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 4) fdm_strip_kernel(const __gr
       for (int y = 0; y < N; ++y) a[y][ex] = o[y];
     }
     const double wz = scale * (pz == 0 || pz == p ? 0.5 : 1.0);
-    double* out = IO + (pf * N * N + pz * N) * RX + p * pc;
-    double* edge = EDGE + ((pc * NT + pf) * N + pz) * N;
 #pragma unroll
     for (int y = 0; y < N; ++y) {
       double o[N];
       fdm_bwd<N, true>(Sx, a[y], o);
       const double wzy = wz * (y == 0 || y == p ? 0.5 : 1.0);
-      edge[y] = 0.5 * wzy * o[0];
 #pragma unroll
-      for (int x = 1; x < N; ++x) out[y * RX + x] = (x == p ? 0.5 : 1.0) * wzy * o[x];
+      for (int x = 0; x < N; ++x) wpl[y * N + x] = (x == 0 || x == p ? 0.5 : 1.0) * wzy * o[x];
     }
   }
   __syncthreads();
-  // ---- scatter: row (f, lz, ly) of the assembled block per warp instruction
+  // ---- scatter: row (f, lz, ly) of the strip per warp instruction
   if (lane < RX) {
-    const bool has_edge = lane % p == 0 && lane / p < ncell;
-    const double* eb = EDGE + (lane / p) * NT * N * N;
     for (int pr = warp; pr < NT * N; pr += C::T / 32) {
       const int f = pr / N, lz = pr - f * N;
       double* dst = zs + f * P.n_space + lz * dxy + lane;
-      const double* blk = IO + pr * N * RX + lane;
+      const double* w0 = W + pr * N * N;
 #pragma unroll
       for (int ly = 0; ly < N; ++ly) {
-        double v = lane >= 1 ? blk[ly * RX] : 0.0;
-        if (has_edge) v += eb[pr * N + ly];
+        double v = own ? w0[o_own + ly * N] : 0.0;
+        if (dup) v += w0[o_dup + ly * N];
         atomicAdd(dst + ly * dx, v);
       }
     }

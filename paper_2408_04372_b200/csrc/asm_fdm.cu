@@ -621,24 +621,29 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 6) fdm_strip_kernel(const __gr
   // of the strip: local node x % p of cell x / p, and, on a shared face,
   // node p of the cell before
   const int lc = lane / p, lj = lane - lc * p;
-  const bool own = lane < RX && lc < ncell, dup = lane < RX && lj == 0 && lc >= 1;
-  const int o_own = lc * CS + lj, o_dup = (lc - 1) * CS + p;
-  if (lane < RX) {
-    for (int pr = warp; pr < NT * N; pr += C::T / 32) {
-      const int f = pr / N, lz = pr - f * N;
-      const double* src = rs + f * P.n_space + lz * dxy + lane;
-      const unsigned d0 = static_cast<unsigned>(__cvta_generic_to_shared(W + pr * N * N));
+  const bool own = lane < RX && lc < ncell;
+  const int o_own = lc * CS + lj;
+  // x faces, compact: lane = (row ly, face fc = 1 .. ncell); the face is node
+  // p of cell fc - 1 and, but for the last one, node 0 of cell fc
+  constexpr int NF = NCX, FIT = (N * NF + 31) / 32;  // face items per lane
+  for (int pr = warp; pr < NT * N; pr += C::T / 32) {
+    const int f = pr / N, lz = pr - f * N;
+    const double* src = rs + f * P.n_space + lz * dxy;
+    const unsigned d0 = static_cast<unsigned>(__cvta_generic_to_shared(W + pr * N * N));
+    if (own) {
 #pragma unroll
-      for (int ly = 0; ly < N; ++ly) {
-        if (own)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * (o_own + ly * N)),
-                       "l"(src + ly * dx)
-                       : "memory");
-        if (dup)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * (o_dup + ly * N)),
-                       "l"(src + ly * dx)
-                       : "memory");
-      }
+      for (int ly = 0; ly < N; ++ly)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * (o_own + ly * N)),
+                     "l"(src + ly * dx + lane)
+                     : "memory");
+    }
+#pragma unroll
+    for (int k = 0; k < FIT; ++k) {
+      const int l = lane + 32 * k, fy = l / NF, fc = 1 + l - fy * NF;
+      if (l < N * NF)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * ((fc - 1) * CS + fy * N + p)),
+                     "l"(src + fy * dx + fc * p)
+                     : "memory");
     }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
@@ -727,18 +732,23 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 6) fdm_strip_kernel(const __gr
     }
   }
   __syncthreads();
-  // ---- scatter: row (f, lz, ly) of the strip per warp instruction
-  if (lane < RX) {
-    for (int pr = warp; pr < NT * N; pr += C::T / 32) {
-      const int f = pr / N, lz = pr - f * N;
-      double* dst = zs + f * P.n_space + lz * dxy + lane;
-      const double* w0 = W + pr * N * N;
+  // ---- scatter: the faces first take the contribution of the cell before
+  // (same warp, same (field, z) pair), then one row (f, lz, ly) of the strip
+  // per warp instruction
+  for (int pr = warp; pr < NT * N; pr += C::T / 32) {
+    const int f = pr / N, lz = pr - f * N;
+    double* w0 = W + pr * N * N;
 #pragma unroll
-      for (int ly = 0; ly < N; ++ly) {
-        double v = own ? w0[o_own + ly * N] : 0.0;
-        if (dup) v += w0[o_dup + ly * N];
-        atomicAdd(dst + ly * dx, v);
-      }
+    for (int k = 0; k < FIT; ++k) {
+      const int l = lane + 32 * k, fy = l / NF, fc = 1 + l - fy * NF;
+      if (l < N * NF && fc < ncell) w0[fc * CS + fy * N] += w0[(fc - 1) * CS + fy * N + p];
+    }
+    __syncwarp();
+    if (own || lane == p * ncell) {
+      double* dst = zs + f * P.n_space + lz * dxy + lane;
+      const double* wr = lane == p * ncell ? w0 + (ncell - 1) * CS + p : w0 + o_own;
+#pragma unroll
+      for (int ly = 0; ly < N; ++ly) atomicAdd(dst + ly * dx, wr[ly * N]);
     }
   }
 }

@@ -415,7 +415,7 @@ def roofline_of(kern, ms_step, workload):
     peak, peak_src = measured_peaks()
     if op_share >= asm_share:
         k, key, share = kern["vmult"], "vmult", op_share
-        name = "st_brick_kernel (fused space-time vmult, owner-computes Cartesian form)"
+        name = "st_brick_ws_kernel (fused space-time vmult, owner-computes Cartesian form, warp-specialised)"
     else:
         k, key, share = kern["asm"], "asm", asm_share
         name = "fine-level smoother sweep (ASMSmoother::add_correction)"

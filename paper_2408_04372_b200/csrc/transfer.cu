@@ -572,24 +572,41 @@ __global__ void __launch_bounds__(kZT, 2) xyz_restrict_kernel(const PassArgs A, 
   const int t = threadIdx.x;
   const long long gx0 = 2LL * P * (cx0 - 1), gy0 = 2LL * P * (cy0 - 1);
   const double* src_f = in + f * A.fs_in;
-  // stage fine plane zf of the tile region (input masks; left-of-domain zero)
+  // stage fine plane zf of the tile region (input masks; left-of-domain zero).
+  // The rows / columns of the region that lie inside the lattice and off its
+  // masked faces are the tile-coordinate ranges [ly_lo, ly_hi) x [lx_lo, lx_hi)
+  const int mk = A.mask_in ? 1 : 0;
+  const int lx_lo = static_cast<int>(std::max<long long>(0, mk - gx0));
+  const int lx_hi = static_cast<int>(std::min<long long>(C::LX, ix - mk - gx0));
+  const int ly_lo = static_cast<int>(std::max<long long>(0, mk - gy0));
+  const int ly_hi = static_cast<int>(std::min<long long>(C::LY, iy - mk - gy0));
+  const bool tile_in = lx_lo == 0 && lx_hi == C::LX && ly_lo == 0 && ly_hi == C::LY;
   auto stage = [&](int zf, double* dst) {
     // warp w stages rows w, w + 8, ...; lanes run along x (one row base per row)
     const bool plane0 = (A.mask_in && on_bdry_z(zf, iz, A.zbc)) || (A.skip_lo_in && zf == 0);
-    const double* src = src_f + static_cast<long long>(zf) * iy * ix;
+    const double* src = src_f + static_cast<long long>(zf) * iy * ix + gy0 * ix + gx0;
     const int lane = t & 31, w = t >> 5;
-    for (int ly = w; ly < C::LY; ly += kZT / 32) {
-      const long long gy = gy0 + ly;
-      const bool rok = !plane0 && gy >= 0 && gy < iy && !(A.mask_in && on_bdry(gy, iy));
-      const double* rs = src + gy * ix;
-      double* rd = dst + ly * C::LXP;
+    if (tile_in && !plane0) {
+      // interior tile: plain copies, no per-element tests
+      for (int ly = w; ly < C::LY; ly += kZT / 32) {
+        const double* rs = src + static_cast<long long>(ly) * ix;
+        const unsigned rd = static_cast<unsigned>(__cvta_generic_to_shared(dst + ly * C::LXP));
 #pragma unroll
-      for (int k = 0; k < (C::LX + 31) / 32; ++k) {
-        const int lx = lane + 32 * k;
-        if (lx < C::LX) {
-          const long long gx = gx0 + lx;
-          const bool ok = rok && gx >= 0 && gx < ix && !(A.mask_in && on_bdry(gx, ix));
-          cp8(rd + lx, rs + gx, ok);
+        for (int k = 0; k < (C::LX + 31) / 32; ++k) {
+          const int lx = lane + 32 * k;
+          if (lx < C::LX)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(rd + 8u * lx), "l"(rs + lx) : "memory");
+        }
+      }
+    } else {
+      for (int ly = w; ly < C::LY; ly += kZT / 32) {
+        const bool rok = !plane0 && ly >= ly_lo && ly < ly_hi;
+        const double* rs = src + static_cast<long long>(ly) * ix;
+        double* rd = dst + ly * C::LXP;
+#pragma unroll
+        for (int k = 0; k < (C::LX + 31) / 32; ++k) {
+          const int lx = lane + 32 * k;
+          if (lx < C::LX) cp8(rd + lx, rs + lx, rok && lx >= lx_lo && lx < lx_hi);
         }
       }
     }

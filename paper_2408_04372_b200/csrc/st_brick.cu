@@ -678,8 +678,8 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
       mbar_wait(ab_empty + sa, pa);
       if (act) {
         const double* ycolbuf = Ub + su * W::U_S + uoff;
-        double* oa = ABr + sa * W::AB_S + aoff;
-        double* ob = oa + F * C::AB_F;
+        // (a, b) of one node are one 16-byte entry: one store here, one load in stage X
+        double2* oab = reinterpret_cast<double2*>(ABr + sa * W::AB_S) + aoff;
         // element 0 is the halo cell: it reaches owned row 0 only
         double v[N];
 #pragma unroll
@@ -700,13 +700,9 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
           elem<N>(L.MrE, L.MrO, s, ea);
           elem<N>(L.KrE, L.KrO, s, eb);
           const int r0 = (e - 1) * P;
-          oa[r0 * C::XP] = ca + ea[0];
-          ob[r0 * C::XP] = cb + eb[0];
+          oab[r0 * C::XP] = make_double2(ca + ea[0], cb + eb[0]);
 #pragma unroll
-          for (int j = 1; j < P; ++j) {
-            oa[(r0 + j) * C::XP] = ea[j];
-            ob[(r0 + j) * C::XP] = eb[j];
-          }
+          for (int j = 1; j < P; ++j) oab[(r0 + j) * C::XP] = make_double2(ea[j], eb[j]);
           ca = ea[P];
           cb = eb[P];
         }
@@ -730,8 +726,10 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
     constexpr int HX = OX / C::XH;  // owned columns per half
     const int i = t - 32 * (1 + W::YW);
     const bool act = i < W::XI;
-    const int h = i % C::XH, rf = i / C::XH;
-    const int r = rf % OY, f = act ? rf / OY : 0;
+    // rows fastest: 8 consecutive lanes touch 16-byte entries a row pitch
+    // apart (odd pitches: distinct banks)
+    const int r = i % OY, hf = i / OY;
+    const int h = hf % C::XH, f = act ? hf / C::XH : 0;
     const double sx = L.hinv2[0], sy = L.hinv2[1];
     const int ioff = f * C::AB_F + r * C::XP + h * HX;
     const int ooff = f * C::CP_F + r * C::CPP + h * HX;
@@ -741,15 +739,14 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
       mbar_wait(ab_full + sa, pa);
       mbar_wait(cp_empty + sc, pc);
       if (act) {
-        const double* ia = ABr + sa * W::AB_S + ioff;
-        const double* ib = ia + F * C::AB_F;
-        double* oc = CPr + sc * W::CP_S + ooff;
-        double* op = oc + F * C::CP_F;
+        const double2* iab = reinterpret_cast<const double2*>(ABr + sa * W::AB_S) + ioff;
+        double2* ocp = reinterpret_cast<double2*>(CPr + sc * W::CP_S) + ooff;
         double va[N], vb[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          va[k] = ia[k];
-          vb[k] = ib[k];
+          const double2 ab = iab[k];
+          va[k] = ab.x;
+          vb[k] = ab.y;
         }
         double cc, cp;
         {
@@ -763,8 +760,9 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
           vb[0] = vb[P];
 #pragma unroll
           for (int k = 1; k < N; ++k) {
-            va[k] = ia[e * P + k];
-            vb[k] = ib[e * P + k];
+            const double2 ab = iab[e * P + k];
+            va[k] = ab.x;
+            vb[k] = ab.y;
           }
           const Split<N> sa_ = split_at<N>(va), sb_ = split_at<N>(vb);
           double ec[N], ek[N], em[N];
@@ -772,13 +770,9 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
           elem<N>(L.KrE, L.KrO, sa_, ek);
           elem<N>(L.MrE, L.MrO, sb_, em);
           const int r0 = (e - 1) * P;
-          oc[r0] = cc + ec[0];
-          op[r0] = cp + fma(sx, ek[0], sy * em[0]);
+          ocp[r0] = make_double2(cc + ec[0], cp + fma(sx, ek[0], sy * em[0]));
 #pragma unroll
-          for (int j = 1; j < P; ++j) {
-            oc[r0 + j] = ec[j];
-            op[r0 + j] = fma(sx, ek[j], sy * em[j]);
-          }
+          for (int j = 1; j < P; ++j) ocp[r0 + j] = make_double2(ec[j], fma(sx, ek[j], sy * em[j]));
           cc = ec[P];
           cp = fma(sx, ek[P], sy * em[P]);
         }
@@ -913,12 +907,12 @@ __global__ void __launch_bounds__(WsCfg<N, F>::THREADS, 1)
       mbar_wait(cp_full + sc, pc);
       double vc[F];
       {
-        const double* ic = CPr + sc * W::CP_S + coff;
-        const double* ip = ic + F * C::CP_F;
+        const double2* icp = reinterpret_cast<const double2*>(CPr + sc * W::CP_S) + coff;
 #pragma unroll
         for (int gg = 0; gg < F; ++gg) {
-          vc[gg] = ic[gg * C::CP_F];
-          cap[gg] = ip[gg * C::CP_F];
+          const double2 cpv = icp[gg * C::CP_F];
+          vc[gg] = cpv.x;
+          cap[gg] = cpv.y;
         }
       }
       __syncwarp();

@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kZT, 2) xyz_restrict_kernel(const PassArgs A, 
                                                            int ntx, int nch, int zc) {
   using C = ZCfg<P>;
   extern __shared__ __align__(16) double sm[];
-  double* R0[2] = {sm, sm + C::LY * C::LXP};
+  constexpr int R0S = C::LY * C::LXP;  // one staged fine plane (two buffers at sm)
   double* R1 = sm + 2 * C::LY * C::LXP;
   const long long ix = A.i[0], iy = A.i[1], iz = A.i[2], ox = A.o[0], oy = A.o[1];
   const int ncx = static_cast<int>((ox - 1) / P), ncy = static_cast<int>((oy - 1) / P),
@@ -659,13 +659,13 @@ __global__ void __launch_bounds__(kZT, 2) xyz_restrict_kernel(const PassArgs A, 
       }
     }
   };
-  stage(zf0, R0[0]);
+  stage(zf0, sm);
   for (int zf = zf0; zf <= zf_end; ++zf) {
     const int buf = (zf - zf0) & 1;
     cp_wait_all();
     __syncthreads();  // plane zf staged; the previous plane's R1 readers are done
-    if (zf + 1 <= zf_end) stage(zf + 1, R0[buf ^ 1]);
-    const double* R = R0[buf];
+    if (zf + 1 <= zf_end) stage(zf + 1, sm + (buf ^ 1) * R0S);
+    const double* R = sm + buf * R0S;
     // ---- x pass: (fine row ly, coarse cell lc) -> coarse x nodes lc*P + jj
     for (int e = t; e < C::LY * kZCX; e += kZT) {
       const int lc = e / C::LY, ly = e - lc * C::LY;

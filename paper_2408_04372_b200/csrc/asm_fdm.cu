@@ -82,6 +82,17 @@ __device__ __forceinline__ void solve_small(const double* TM, const double* TA, 
 // the host block-diagonalised T_A^-1 T_M = Q B Q^-1 (P.tdiag),
 // Q (B + mu)^-1 P b with P = Q^-1 T_A^-1 -- two n_t x n_t products and one
 // reciprocal per 1x1 / 2x2 block, no pivoting
+// reciprocal by the hardware seed (rcp.approx.ftz.f64, >= 20 bits) and two
+// Newton steps: full double accuracy for the normal, well-scaled pivots of
+// the temporal blocks, without the special-case path of the IEEE division
+__device__ __forceinline__ double rcp_newton(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
 template <int NT, bool TD>
 __device__ __forceinline__ void temporal_solve(const DevFDM& P, double mu, double (&b)[4]) {
   if constexpr (!TD) {
@@ -99,10 +110,10 @@ __device__ __forceinline__ void temporal_solve(const DevFDM& P, double mu, doubl
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
     if (P.tkind[i] == 0) {
-      w[i] = w[i] / (P.ta[i] + mu);
+      w[i] = w[i] * rcp_newton(P.ta[i] + mu);
     } else if (P.tkind[i] == 1 && i + 1 < NT) {
       const double al = P.ta[i] + mu, be = P.tb[i];
-      const double inv = 1.0 / fma(al, al, be * be);
+      const double inv = rcp_newton(fma(al, al, be * be));
       const double w0 = w[i], w1 = w[i + 1];
       w[i] = (al * w0 - be * w1) * inv;
       w[i + 1] = (be * w0 + al * w1) * inv;

@@ -601,27 +601,31 @@ __host__ __device__ __forceinline__ bool strip_left_out(const DevFDM& P, const u
   return false;
 }
 
-template <int N, int NT, bool TD>
-__global__ void __launch_bounds__(SCfg<N, NT>::T, 6) fdm_strip_kernel(const __grid_constant__ DevFDM P,
-                                                                       const double* __restrict__ r,
-                                                                       double* __restrict__ z, double scale) {
-  using C = SCfg<N, NT>;
+// NT = n_t fields of a step; SG consecutive steps (independent blocks,
+// asm_smoother.cpp:24-28) share the CTA so that NTF = NT * SG fields keep the
+// plane owners busy (n_t = 2: 50 of 128 threads otherwise)
+template <int N, int NT, int SG, bool TD>
+__global__ void __launch_bounds__(SCfg<N, NT * SG>::T, 6) fdm_strip_kernel(const __grid_constant__ DevFDM P,
+                                                                            const double* __restrict__ r,
+                                                                            double* __restrict__ z, double scale) {
+  constexpr int NTF = NT * SG;
+  using C = SCfg<N, NTF>;
   constexpr int p = C::P, NCX = C::NCX, RX = C::RX, ROWS = C::ROWS, CS = C::CS, ND = C::ND;
   extern __shared__ __align__(16) double W[];  // per cell [field][z][y][x]
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const unsigned nx = static_cast<unsigned>(P.cells[0]), ny = static_cast<unsigned>(P.cells[1]);
-  const unsigned sxn = strips_per_row<N, NT>(nx);
+  const unsigned sxn = strips_per_row<N, NTF>(nx);
   const unsigned sid = blockIdx.x;
   const unsigned sx = sid % sxn, cy = (sid / sxn) % ny, cz = sid / (sxn * ny);
   const unsigned cx0 = 1 + sx * NCX;
-  if (strip_left_out<N, NT>(P, P.skip, cx0, cy, cz)) return;  // CTA-uniform
+  if (strip_left_out<N, NTF>(P, P.skip, cx0, cy, cz)) return;  // CTA-uniform
   const int ncell = NCX;  // interior strips are whole
   const long long dx = P.dofs[0], dxy = P.dofs[0] * P.dofs[1];
   const long long base = static_cast<long long>(cz) * p * dxy + static_cast<long long>(cy) * p * dx +
                          static_cast<long long>(cx0) * p;
   const long long st = blockIdx.y;
-  const double* rs = r + st * NT * P.n_space + base;
-  double* zs = z + st * NT * P.n_space + base;
+  const double* rs = r + st * NTF * P.n_space + base;
+  double* zs = z + st * NTF * P.n_space + base;
   double rho = 1.0;
   if (P.rho0) {
     const long long ax = cx0 >> P.rho_shift, ay = cy >> P.rho_shift, az = (cz + P.cz0) >> P.rho_shift;
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 6) fdm_strip_kernel(const __gr
   // x faces, compact: lane = (row ly, face fc = 1 .. ncell); the face is node
   // p of cell fc - 1 and, but for the last one, node 0 of cell fc
   constexpr int NF = NCX, FIT = (N * NF + 31) / 32;  // face items per lane
-  for (int pr = warp; pr < NT * N; pr += C::T / 32) {
+  for (int pr = warp; pr < NTF * N; pr += C::T / 32) {
     const int f = pr / N, lz = pr - f * N;
     const double* src = rs + f * P.n_space + lz * dxy;
     const unsigned d0 = static_cast<unsigned>(__cvta_generic_to_shared(W + pr * N * N));
@@ -691,31 +695,34 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 6) fdm_strip_kernel(const __gr
     const int c = t / C::NL, e = t % C::NL;
     if (c < ncell) {
       const int ey = e / N, ex = e % N;
-      double* wl = W + c * CS + e;
-      double v[NT][N];
-#pragma unroll
-      for (int f = 0; f < NT; ++f) {
-        double in[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) in[k] = wl[f * ND + k * N * N];
-        fdm_fwd<N, true>(Sz, in, v[f]);
-      }
       const double lxy = P.L1[0][0][ex] + P.L1[1][0][ey];
 #pragma unroll
-      for (int ez = 0; ez < N; ++ez) {
-        double bb[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int g = 0; g < SG; ++g) {
+        double* wl = W + c * CS + g * NT * ND + e;  // the NT fields of step slot g
+        double v[NT][N];
 #pragma unroll
-        for (int f = 0; f < NT; ++f) bb[f] = v[f][ez];
-        temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][0][ez]), bb);
+        for (int f = 0; f < NT; ++f) {
+          double in[N];
 #pragma unroll
-        for (int f = 0; f < NT; ++f) v[f][ez] = bb[f];
-      }
+          for (int k = 0; k < N; ++k) in[k] = wl[f * ND + k * N * N];
+          fdm_fwd<N, true>(Sz, in, v[f]);
+        }
 #pragma unroll
-      for (int f = 0; f < NT; ++f) {
-        double out[N];
-        fdm_bwd<N, true>(Sz, v[f], out);
+        for (int ez = 0; ez < N; ++ez) {
+          double bb[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int k = 0; k < N; ++k) wl[f * ND + k * N * N] = out[k];
+          for (int f = 0; f < NT; ++f) bb[f] = v[f][ez];
+          temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][0][ez]), bb);
+#pragma unroll
+          for (int f = 0; f < NT; ++f) v[f][ez] = bb[f];
+        }
+#pragma unroll
+        for (int f = 0; f < NT; ++f) {
+          double out[N];
+          fdm_bwd<N, true>(Sz, v[f], out);
+#pragma unroll
+          for (int k = 0; k < N; ++k) wl[f * ND + k * N * N] = out[k];
+        }
       }
     }
   }
@@ -746,7 +753,7 @@ __global__ void __launch_bounds__(SCfg<N, NT>::T, 6) fdm_strip_kernel(const __gr
   // ---- scatter: the faces first take the contribution of the cell before
   // (same warp, same (field, z) pair), then one row (f, lz, ly) of the strip
   // per warp instruction
-  for (int pr = warp; pr < NT * N; pr += C::T / 32) {
+  for (int pr = warp; pr < NTF * N; pr += C::T / 32) {
     const int f = pr / N, lz = pr - f * N;
     double* w0 = W + pr * N * N;
 #pragma unroll
@@ -774,16 +781,31 @@ void launch_lines(const DevFDM& P, const double* r, double* z, double scale, cud
     constexpr bool TD = decltype(td)::value;
     if (P.eo) {
       count_launch();  // the second launch of the pair
-      using SC = SCfg<N, NT>;
-      static bool configured = false;
-      if (!configured) {
-        cudaFuncSetAttribute(fdm_strip_kernel<N, NT, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(SC::smem_bytes()));
-        configured = true;
+      // steps per CTA: the largest divisor of S with n_t * SG <= 4 fields
+      auto strips = [&](auto sgc) {
+        constexpr int SG = decltype(sgc)::value;
+        using SC = SCfg<N, NT * SG>;
+        static bool configured = false;
+        if (!configured) {
+          cudaFuncSetAttribute(fdm_strip_kernel<N, NT, SG, TD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(SC::smem_bytes()));
+          configured = true;
+        }
+        const long long sxn = strips_per_row<N, NT * SG>(P.cells[0]);
+        const dim3 sgrid(static_cast<unsigned>(sxn * P.cells[1] * P.cells[2]), static_cast<unsigned>(P.S / SG));
+        if (sxn > 0) fdm_strip_kernel<N, NT, SG, TD><<<sgrid, SC::T, SC::smem_bytes(), s>>>(P, r, z, scale);
+      };
+      const int sg = fdm_fields_per_cta(NT, P.S) / NT;
+      if constexpr (NT == 1) {
+        if (sg == 4) strips(std::integral_constant<int, 4>{});
+        else if (sg == 2) strips(std::integral_constant<int, 2>{});
+        else strips(std::integral_constant<int, 1>{});
+      } else if constexpr (NT == 2) {
+        if (sg == 2) strips(std::integral_constant<int, 2>{});
+        else strips(std::integral_constant<int, 1>{});
+      } else {
+        strips(std::integral_constant<int, 1>{});
       }
-      const long long sxn = strips_per_row<N, NT>(P.cells[0]);
-      const dim3 sgrid(static_cast<unsigned>(sxn * P.cells[1] * P.cells[2]), static_cast<unsigned>(P.S));
-      if (sxn > 0) fdm_strip_kernel<N, NT, TD><<<sgrid, SC::T, SC::smem_bytes(), s>>>(P, r, z, scale);
       const dim3 lgrid(static_cast<unsigned>((P.n_left + NC - 1) / NC), grid.y);
       if (P.n_left > 0) fdm_lines_kernel<N, NT, TD, 3><<<lgrid, 128, 0, s>>>(P, r, z, scale);
     } else {
@@ -844,7 +866,7 @@ std::vector<long long> left_out_cells(const DevFDM& P, const unsigned char* skip
 }
 template <int N>
 std::vector<long long> left_out_cells_nt(const DevFDM& P, const unsigned char* skip) {
-  switch (P.nt) {
+  switch (fdm_fields_per_cta(P.nt, P.S)) {  // the strip geometry follows the fields per CTA
     case 1: return left_out_cells<N, 1>(P, skip);
     case 2: return left_out_cells<N, 2>(P, skip);
     case 3: return left_out_cells<N, 3>(P, skip);

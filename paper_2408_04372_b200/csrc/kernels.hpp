@@ -199,6 +199,15 @@ struct DevFDM {
   const long long* left;
   long long n_left;
 };
+// fields a strip-kernel CTA works on: n_t times the largest of 1, 2, 4 that
+// divides S and keeps the product <= 4 (consecutive steps are independent
+// smoother blocks)
+inline int fdm_fields_per_cta(int nt, int S) {
+  int sg = 1;
+  for (int d = 2; d <= 4 && nt * d <= 4; d *= 2)
+    if (S % d == 0) sg = d;
+  return nt * sg;
+}
 // host: the left-out cell list of F (skip_host: host copy of F.skip or nullptr)
 std::vector<long long> fdm_left_out_cells(const DevFDM& F, const unsigned char* skip_host);
 void fdm_add_correction(const DevFDM& F, const double* r, double* z, double scale, cudaStream_t s);

@@ -395,13 +395,16 @@ def test_transfers_separable_fallback(cuda, ref):
 @pytest.mark.parametrize("cells,p,k,S,scheme", [((16, 16, 16), 4, 3, 1, problems.DG), ((23, 13, 12), 4, 2, 2, problems.DG),
                                                  ((33, 9, 8), 2, 2, 2, problems.CGP),
                                                  ((24, 12, 10), 3, 1, 1, problems.DG),
-                                                 ((40, 8, 6), 1, 3, 1, problems.DG)])
+                                                 ((40, 8, 6), 1, 3, 1, problems.DG),
+                                                 ((16, 12, 10), 4, 2, 4, problems.CGP),
+                                                 ((17, 9, 8), 4, 0, 4, problems.DG)])
 def test_fdm_strip_kernel_matches_line_owner(cuda, cells, p, k, S, scheme):
     """The strip kernel of the interior cells (even-odd transforms, assembled
     block scatter) against the generic line-owner kernel on every cell
     (STMG_FDM_GENERIC, itself pinned to the reference's LU block solves by the
     tests above) on meshes with interior strips, ragged strip counts and
-    several steps: 1e-12."""
+    several steps (steps sharing a CTA: n_t = 2 with S = 2, 4, n_t = 1 with
+    S = 4): 1e-12."""
     import torch
 
     def correction(generic):

@@ -15,7 +15,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start o
 echo "launches rc $?" >> gpurun_out/bench.log
 python scripts/launch_summary.py gpurun_out/launches_$W.csv > gpurun_out/launch_summary_$W.txt 2>&1
 python scripts/prof_kernels.py kernels $W > gpurun_out/prof_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"${KREGEX:-st_brick_kernel|fdm_lines_kernel}" -c ${KCOUNT:-8} -o gpurun_out/prof_$W python scripts/prof_kernels.py kernels $W > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"${KREGEX:-st_brick_ws_kernel|fdm_strip_kernel|fdm_lines_kernel}" -c ${KCOUNT:-9} -f -o gpurun_out/prof_$W python scripts/prof_kernels.py kernels $W > gpurun_out/ncu_full.log 2>&1
 echo "full rc $?" >> gpurun_out/bench.log
 fi
 tail -4 gpurun_out/pytest_gpu.log 2>/dev/null; tail -1 gpurun_out/smoke.log 2>/dev/null; tail -c 3000 gpurun_out/bench.log; tail -3 gpurun_out/bench.err

@@ -801,11 +801,9 @@ __global__ void __launch_bounds__(kZT, 2) xyz_prolong_kernel(const PassArgs A, c
     // ---- y pass: (fine x column lx, coarse y cell lc) -> fine rows, masked add
     const bool plane_out0 = A.mask_out && on_bdry_z(zf, oz, A.zbc);
     double* dst = dst_f + static_cast<long long>(zf) * oy * ox;
-    for (int e = t; e < C::FX * kZCY; e += kZT) {
-      const int lc = e / C::FX, lx = e - lc * C::FX;
+    auto y_item = [&](int lc, int lx) {
       const long long c = cy0 + lc, gx = 2LL * P * cx0 + lx;
-      if (c >= ncy || gx >= ox) continue;
-      if (lx == 2 * P * kZCX && gx != ox - 1) continue;  // the next tile's first column
+      if (c >= ncy || gx >= ox) return;
       double cv[P + 1];
 #pragma unroll
       for (int j = 0; j <= P; ++j) cv[j] = R1[(lc * P + j) * C::FXP + lx];
@@ -824,7 +822,12 @@ __global__ void __launch_bounds__(kZT, 2) xyz_prolong_kernel(const PassArgs A, c
         if (col0 || (A.mask_out && on_bdry(gy, oy))) s = 0.0;
         dst[gy * ox + gx] = old[rr] + s;
       }
-    }
+    };
+    // the tile's own 2P kZCX columns: whole passes of the CTA; column 2P kZCX
+    // is the next tile's first one, except on the lattice's last column
+    constexpr int FXO = 2 * P * kZCX;
+    for (int e = t; e < FXO * kZCY; e += kZT) y_item(e / FXO, e % FXO);
+    if (2LL * P * cx0 + FXO == ox - 1 && t < kZCY) y_item(t, FXO);
   }
 }
 

@@ -601,6 +601,29 @@ __host__ __device__ __forceinline__ bool strip_left_out(const DevFDM& P, const u
   return false;
 }
 
+// 8-byte cp.async / fp64 reduction at base + 8 * off: the address is one
+// mad.wide.u32 (lattice offsets inside a field fit 32 bits)
+__device__ __forceinline__ void cp8_off(unsigned dst, const double* base, unsigned off) {
+  asm volatile(
+      "{\n"
+      ".reg .u64 a;\n"
+      "mad.wide.u32 a, %2, 8, %1;\n"
+      "cp.async.ca.shared.global [%0], [a], 8;\n"
+      "}\n" ::"r"(dst),
+      "l"(base), "r"(off)
+      : "memory");
+}
+__device__ __forceinline__ void red_off(double* base, unsigned off, double v) {
+  asm volatile(
+      "{\n"
+      ".reg .u64 a;\n"
+      "mad.wide.u32 a, %1, 8, %0;\n"
+      "red.global.add.f64 [a], %2;\n"
+      "}\n" ::"l"(base),
+      "r"(off), "d"(v)
+      : "memory");
+}
+
 // NT = n_t fields of a step; SG consecutive steps (independent blocks,
 // asm_smoother.cpp:24-28) share the CTA so that NTF = NT * SG fields keep the
 // plane owners busy (n_t = 2: 50 of 128 threads otherwise)
@@ -641,25 +664,33 @@ __global__ void __launch_bounds__(SCfg<N, NT * SG>::T, 6) fdm_strip_kernel(const
   // x faces, compact: lane = (row ly, face fc = 1 .. ncell); the face is node
   // p of cell fc - 1 and, but for the last one, node 0 of cell fc
   constexpr int NF = NCX, FIT = (N * NF + 31) / 32;  // face items per lane
+  const unsigned dxu = static_cast<unsigned>(dx);
+  const unsigned w_u32 = static_cast<unsigned>(__cvta_generic_to_shared(W));
+  // per-lane invariants: shared-memory byte offset and lattice offset of the
+  // lane's own node (row ly = 0) and of its face item(s)
+  const unsigned own_sm = 8u * o_own;
+  unsigned face_sm[FIT], face_gl[FIT], face_to[FIT];
+  bool face_ok[FIT], face_in[FIT];
+#pragma unroll
+  for (int k = 0; k < FIT; ++k) {
+    const int l = lane + 32 * k, fy = l / NF, fc = 1 + l - fy * NF;
+    face_ok[k] = l < N * NF;
+    face_in[k] = face_ok[k] && fc < ncell;
+    face_sm[k] = 8u * ((fc - 1) * CS + fy * N + p);  // node p of cell fc - 1
+    face_to[k] = 8u * (fc * CS + fy * N);            // node 0 of cell fc
+    face_gl[k] = fy * dxu + fc * p;
+  }
   for (int pr = warp; pr < NTF * N; pr += C::T / 32) {
     const int f = pr / N, lz = pr - f * N;
     const double* src = rs + f * P.n_space + lz * dxy;
-    const unsigned d0 = static_cast<unsigned>(__cvta_generic_to_shared(W + pr * N * N));
+    const unsigned d0 = w_u32 + 8u * (pr * N * N);
     if (own) {
 #pragma unroll
-      for (int ly = 0; ly < N; ++ly)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * (o_own + ly * N)),
-                     "l"(src + ly * dx + lane)
-                     : "memory");
+      for (int ly = 0; ly < N; ++ly) cp8_off(d0 + own_sm + 8u * (ly * N), src, ly * dxu + lane);
     }
 #pragma unroll
-    for (int k = 0; k < FIT; ++k) {
-      const int l = lane + 32 * k, fy = l / NF, fc = 1 + l - fy * NF;
-      if (l < N * NF)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d0 + 8u * ((fc - 1) * CS + fy * N + p)),
-                     "l"(src + fy * dx + fc * p)
-                     : "memory");
-    }
+    for (int k = 0; k < FIT; ++k)
+      if (face_ok[k]) cp8_off(d0 + face_sm[k], src, face_gl[k]);
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
@@ -753,20 +784,21 @@ __global__ void __launch_bounds__(SCfg<N, NT * SG>::T, 6) fdm_strip_kernel(const
   // ---- scatter: the faces first take the contribution of the cell before
   // (same warp, same (field, z) pair), then one row (f, lz, ly) of the strip
   // per warp instruction
+  const bool last = lane == p * ncell;  // the strip's last node: node p of the last cell
+  const unsigned row_sm = last ? 8u * ((ncell - 1) * CS + p) : own_sm;
   for (int pr = warp; pr < NTF * N; pr += C::T / 32) {
     const int f = pr / N, lz = pr - f * N;
-    double* w0 = W + pr * N * N;
+    char* w0 = reinterpret_cast<char*>(W + pr * N * N);
 #pragma unroll
-    for (int k = 0; k < FIT; ++k) {
-      const int l = lane + 32 * k, fy = l / NF, fc = 1 + l - fy * NF;
-      if (l < N * NF && fc < ncell) w0[fc * CS + fy * N] += w0[(fc - 1) * CS + fy * N + p];
-    }
+    for (int k = 0; k < FIT; ++k)
+      if (face_in[k])
+        *reinterpret_cast<double*>(w0 + face_to[k]) += *reinterpret_cast<const double*>(w0 + face_sm[k]);
     __syncwarp();
-    if (own || lane == p * ncell) {
-      double* dst = zs + f * P.n_space + lz * dxy + lane;
-      const double* wr = lane == p * ncell ? w0 + (ncell - 1) * CS + p : w0 + o_own;
+    if (own || last) {
+      double* dst = zs + f * P.n_space + lz * dxy;
 #pragma unroll
-      for (int ly = 0; ly < N; ++ly) atomicAdd(dst + ly * dx, wr[ly * N]);
+      for (int ly = 0; ly < N; ++ly)
+        red_off(dst, ly * dxu + lane, *reinterpret_cast<const double*>(w0 + row_sm + 8u * (ly * N)));
     }
   }
 }

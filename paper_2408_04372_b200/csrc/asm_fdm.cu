@@ -128,6 +128,53 @@ __device__ __forceinline__ void temporal_solve(const DevFDM& P, double mu, doubl
   }
 }
 
+// the N temporal solves of one eigen-line at once (tdiag form): every entry of
+// P / Q is loaded once and applied to all N right-hand sides
+template <int N, int NT>
+__device__ __forceinline__ void temporal_solve_line(const DevFDM& P, const double (&mu)[N], double (&v)[NT][N]) {
+  double w[NT][N];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+#pragma unroll
+    for (int e = 0; e < N; ++e) w[i][e] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const double c = P.tP[i * NT + j];
+#pragma unroll
+      for (int e = 0; e < N; ++e) w[i][e] = fma(c, v[j][e], w[i][e]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    if (P.tkind[i] == 0) {
+      const double ta = P.ta[i];
+#pragma unroll
+      for (int e = 0; e < N; ++e) w[i][e] *= rcp_newton(ta + mu[e]);
+    } else if (P.tkind[i] == 1 && i + 1 < NT) {
+      const double ta = P.ta[i], be = P.tb[i];
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        const double al = ta + mu[e];
+        const double inv = rcp_newton(fma(al, al, be * be));
+        const double w0 = w[i][e], w1 = w[i + 1 < NT ? i + 1 : i][e];
+        w[i][e] = (al * w0 - be * w1) * inv;
+        w[i + 1 < NT ? i + 1 : i][e] = (be * w0 + al * w1) * inv;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+#pragma unroll
+    for (int e = 0; e < N; ++e) v[i][e] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const double c = P.tQ[i * NT + j];
+#pragma unroll
+      for (int e = 0; e < N; ++e) v[i][e] = fma(c, w[j][e], v[i][e]);
+    }
+  }
+}
+
 template <int N, bool TRANS>
 __device__ __forceinline__ void sweep(double* arr, int base, int stride, const double (&S)[kMaxN][kMaxN]) {
   double in[N];
@@ -738,14 +785,21 @@ __global__ void __launch_bounds__(SCfg<N, NT * SG>::T, 6) fdm_strip_kernel(const
           for (int k = 0; k < N; ++k) in[k] = wl[f * ND + k * N * N];
           fdm_fwd<N, true>(Sz, in, v[f]);
         }
+        if constexpr (TD) {
+          double mu[N];
 #pragma unroll
-        for (int ez = 0; ez < N; ++ez) {
-          double bb[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int ez = 0; ez < N; ++ez) mu[ez] = rho * (lxy + P.L1[2][0][ez]);
+          temporal_solve_line<N, NT>(P, mu, v);
+        } else {
 #pragma unroll
-          for (int f = 0; f < NT; ++f) bb[f] = v[f][ez];
-          temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][0][ez]), bb);
+          for (int ez = 0; ez < N; ++ez) {
+            double bb[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int f = 0; f < NT; ++f) v[f][ez] = bb[f];
+            for (int f = 0; f < NT; ++f) bb[f] = v[f][ez];
+            temporal_solve<NT, TD>(P, rho * (lxy + P.L1[2][0][ez]), bb);
+#pragma unroll
+            for (int f = 0; f < NT; ++f) v[f][ez] = bb[f];
+          }
         }
 #pragma unroll
         for (int f = 0; f < NT; ++f) {

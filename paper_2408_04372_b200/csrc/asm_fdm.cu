@@ -639,12 +639,7 @@ __host__ __device__ __forceinline__ bool strip_left_out(const DevFDM& P, const u
                  nz = static_cast<unsigned>(P.cells[2]);
   if (cx == 0 || (cx - 1) / NCX >= strips_per_row<N, NT>(nx) || cy == 0 || cy == ny - 1) return true;
   if ((cz == 0 && (P.zbc & 1)) || (cz == nz - 1 && (P.zbc & 2))) return true;
-  if (skip) {
-    const unsigned c0 = 1 + ((cx - 1) / NCX) * NCX;
-    const unsigned char* sk = skip + (static_cast<size_t>(cz) * ny + cy) * nx;
-    for (unsigned c = c0; c < c0 + NCX; ++c)
-      if (sk[c]) return true;
-  }
+  (void)skip;  // exactly-solved cells inside a strip are masked by the strip kernel
   return false;
 }
 
@@ -696,10 +691,19 @@ __global__ void __launch_bounds__(SCfg<N, NT * SG>::T, 6) fdm_strip_kernel(const
   const long long st = blockIdx.y;
   const double* rs = r + st * NTF * P.n_space + base;
   double* zs = z + st * NTF * P.n_space + base;
-  double rho = 1.0;
-  if (P.rho0) {
-    const long long ax = cx0 >> P.rho_shift, ay = cy >> P.rho_shift, az = (cz + P.cz0) >> P.rho_shift;
-    rho = P.rho0[(az * P.cells0[1] + ay) * P.cells0[0] + ax];
+  // coefficient and "solved exactly elsewhere" flag of cell c of the strip
+  // (the coefficient is uniform over an FDM cell's neighbourhood, not over the strip)
+  auto rho_of = [&](int c) {
+    if (!P.rho0) return 1.0;
+    const long long ax = (cx0 + c) >> P.rho_shift, ay = cy >> P.rho_shift, az = (cz + P.cz0) >> P.rho_shift;
+    return __ldg(P.rho0 + (az * P.cells0[1] + ay) * P.cells0[0] + ax);
+  };
+  const unsigned char* skip_row = P.skip ? P.skip + (static_cast<size_t>(cz) * ny + cy) * nx + cx0 : nullptr;
+  auto skipped = [&](int c) { return skip_row && skip_row[c] != 0; };
+  if (skip_row) {  // nothing to do when the exact kernel solves every cell of the strip (CTA-uniform)
+    bool any = false;
+    for (int c = 0; c < ncell; ++c) any = any || skip_row[c] == 0;
+    if (!any) return;
   }
   // ---- load: row (f, lz, ly) of the block per warp instruction; a warp
   // takes (field, z) pairs, the N rows of a pair are unrolled. Lane = node x
@@ -771,8 +775,9 @@ __global__ void __launch_bounds__(SCfg<N, NT * SG>::T, 6) fdm_strip_kernel(const
   // ---- P2: eigen-line owner along z
   {
     const int c = t / C::NL, e = t % C::NL;
-    if (c < ncell) {
+    if (c < ncell && !skipped(c)) {
       const int ey = e / N, ex = e % N;
+      const double rho = rho_of(c);
       const double lxy = P.L1[0][0][ex] + P.L1[1][0][ey];
 #pragma unroll
       for (int g = 0; g < SG; ++g) {
@@ -824,7 +829,8 @@ __global__ void __launch_bounds__(SCfg<N, NT * SG>::T, 6) fdm_strip_kernel(const
 #pragma unroll
       for (int y = 0; y < N; ++y) a[y][ex] = o[y];
     }
-    const double wz = scale * (pz == 0 || pz == p ? 0.5 : 1.0);
+    // a cell solved by the exact kernel contributes nothing here
+    const double wz = skipped(pc) ? 0.0 : scale * (pz == 0 || pz == p ? 0.5 : 1.0);
 #pragma unroll
     for (int y = 0; y < N; ++y) {
       double o[N];

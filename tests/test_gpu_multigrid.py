@@ -425,3 +425,33 @@ def test_fdm_strip_kernel_matches_line_owner(cuda, cells, p, k, S, scheme):
 
     got, want = correction(False), correction(True)
     assert _rel(got, want) <= 1e-12
+
+
+def test_fdm_strip_kernel_masks_exact_cells(cuda):
+    """Piecewise-constant coefficient on blocks of 4 cells: the cells next to
+    a jump are solved by the exact per-cell kernel, the others by FDM with
+    their own coefficient. Strips mixing both kinds (the strip kernel masks
+    the exact cells, coefficient per cell) against the generic line-owner
+    kernel on every FDM cell: 1e-12."""
+    import torch
+
+    rho = np.random.default_rng(11).choice([1.0, 100.0], size=6 * 3 * 3)
+
+    def correction(generic):
+        if generic:
+            os.environ["STMG_FDM_GENERIC"] = "1"
+        try:
+            mesh = api.Mesh(3, (0, 0, 0), (1.0, 0.5, 0.5), (6, 3, 3), 2)
+            op = api.SpaceTimeOperator(mesh, 2, 2, problems.HEAT, problems.CGP, 2, 0.05, 2, rho)
+            sm = api.ASMSmoother(op)
+        finally:
+            os.environ.pop("STMG_FDM_GENERIC", None)
+        g = torch.Generator(device="cuda").manual_seed(9)
+        r = torch.rand(op.n_dofs, dtype=torch.float64, device="cuda", generator=g) - 0.5
+        z = torch.zeros(op.n_dofs, dtype=torch.float64, device="cuda")
+        sm.add_correction(r, z)
+        return z.cpu().numpy()
+
+    got, want = correction(False), correction(True)
+    assert np.linalg.norm(want) > 0.0
+    assert _rel(got, want) <= 1e-12

@@ -840,9 +840,11 @@ void launch_xyz(int F, const PassArgs& A, const DevAxisTransfer* ax, bool prolon
   const long long ncz = prolong ? (A.i[2] - 1) / P : (A.o[2] - 1) / P;
   const long long ntx = (ncx + kZCX - 1) / kZCX, nty = (ncy + kZCY - 1) / kZCY;
   const long long tiles = ntx * nty;
-  // ~8 CTAs per SM-slot; restriction chunks of >= 4 coarse layers (halo layer)
+  // prolongation: ~8 CTAs per SM-slot. Restriction: every chunk repeats one
+  // halo coarse layer (2p fine planes); 4 chunks measured best at C5-64 and
+  // C5-128 (4: 1.71 ms, 14: 1.86 ms)
   long long nch = std::max<long long>(1, (148LL * 3 * 8 + tiles * F - 1) / (tiles * F));
-  nch = std::min<long long>(nch, std::max<long long>(1, prolong ? ncz : ncz / 4));
+  nch = std::min<long long>(nch, std::max<long long>(1, prolong ? ncz : std::min<long long>(4, ncz / 4)));
   const long long zc = (ncz + nch - 1) / nch;
   nch = (ncz + zc - 1) / zc;
   const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(F * nch));

@@ -1067,9 +1067,10 @@ void launch(const DevLevel& L, const double* u, const double* f, double* y, cuda
   const long long nty = std::max<long long>(1, (L.dofs[1] - 1 + C::OY - 1) / C::OY);
   const long long tiles = ntx * nty;
   const long long ncz = L.cells[2];
-  // enough CTAs for ~8 per SM-slot, chunks of >= 4 layers (halo layer cost)
-  long long nch = std::max<long long>(1, (148LL * 2 * 8 + tiles - 1) / tiles);
-  nch = std::min<long long>(nch, std::max<long long>(1, ncz / 4));
+  // the rule of launch_ws for 2 CTAs per SM (C4: 3 / 6 / 12 chunks measured 7.04 / 6.79 / 6.94 ms)
+  long long nch = (148LL * 2 * 20 + tiles - 1) / tiles;
+  nch = std::min(nch, std::max(ncz / 12, (148LL * 2 * 2 + tiles - 1) / tiles));
+  nch = std::max<long long>(1, std::min(nch, ncz / 2));
   const long long zc = (ncz + nch - 1) / nch;
   nch = (ncz + zc - 1) / zc;
   const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nch));

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kThreads) multidot_partial_kernel(const double
   if ((al & 15) == 0) {
     const long long n2 = n / 2;
     const double2* w2 = reinterpret_cast<const double2*>(w);
+#pragma unroll(G <= 2 ? 4 : (G <= 4 ? 2 : 1))
     for (long long j = tid; j < n2; j += stride) {
       const double2 wj = __ldg(w2 + j);
 #pragma unroll
@@ -217,10 +218,25 @@ void vec_sub_into(double* r, const double* f, const double* y, long long n, cuda
 }
 void vec_multidot(const double* const* V, int k, const double* w, long long n, double* out, double* scratch,
                   cudaStream_t s) {
-  constexpr int G = 8;
-  for (int i0 = 0; i0 < k; i0 += G) {
+  // groups of 8 basis vectors; the last group takes the smallest kernel that
+  // holds it (a padded slot re-reads w: a norm through the 8-wide kernel ran
+  // at 3.7 TB/s of DRAM traffic)
+  for (int i0 = 0; i0 < k;) {
+    const int rem = k - i0;
     count_launch();
-    multidot_partial_kernel<G><<<kDotBlocks, kThreads, 0, s>>>(V, i0, k, w, n, scratch);
+    if (rem > 4) {
+      multidot_partial_kernel<8><<<kDotBlocks, kThreads, 0, s>>>(V, i0, k, w, n, scratch);
+      i0 += 8;
+    } else if (rem > 2) {
+      multidot_partial_kernel<4><<<kDotBlocks, kThreads, 0, s>>>(V, i0, k, w, n, scratch);
+      i0 += 4;
+    } else if (rem > 1) {
+      multidot_partial_kernel<2><<<kDotBlocks, kThreads, 0, s>>>(V, i0, k, w, n, scratch);
+      i0 += 2;
+    } else {
+      multidot_partial_kernel<1><<<kDotBlocks, kThreads, 0, s>>>(V, i0, k, w, n, scratch);
+      i0 += 1;
+    }
   }
   count_launch();
   reduce_partials_kernel<<<k, 32, 0, s>>>(scratch, kDotBlocks, k, out);

@@ -138,9 +138,23 @@ void vec_multidot_seg(const double* const* V, int k, const double* w, const DotS
                       double* scratch, cudaStream_t s) {
   // scratch: kDotBlocks * k doubles (kDotGrid == kDotBlocks)
   static_assert(kDotGrid == kDotBlocks, "dot grid");
-  for (int i0 = 0; i0 < k; i0 += 8) {
+  // as vec_multidot: the last group takes the smallest kernel that holds it
+  for (int i0 = 0; i0 < k;) {
+    const int rem = k - i0;
     count_launch();
-    multidot_seg_kernel<8><<<kDotGrid, kT, 0, s>>>(V, i0, k, w, seg, scratch);
+    if (rem > 4) {
+      multidot_seg_kernel<8><<<kDotGrid, kT, 0, s>>>(V, i0, k, w, seg, scratch);
+      i0 += 8;
+    } else if (rem > 2) {
+      multidot_seg_kernel<4><<<kDotGrid, kT, 0, s>>>(V, i0, k, w, seg, scratch);
+      i0 += 4;
+    } else if (rem > 1) {
+      multidot_seg_kernel<2><<<kDotGrid, kT, 0, s>>>(V, i0, k, w, seg, scratch);
+      i0 += 2;
+    } else {
+      multidot_seg_kernel<1><<<kDotGrid, kT, 0, s>>>(V, i0, k, w, seg, scratch);
+      i0 += 1;
+    }
   }
   count_launch();
   reduce_seg_partials_kernel<<<k, 32, 0, s>>>(scratch, kDotGrid, k, out);
